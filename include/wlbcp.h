@@ -1,0 +1,122 @@
+/* wlbcp.h -- C ABI of the B200-native WLB-LLM context-parallel hot path.
+ *
+ * One shared library, `paper_2503_17924_b200/libwlbcp.so`, built for sm_100a.
+ * Plain pointers and sizes only (no torch types).  Pointers documented as
+ * "device" must be CUDA device memory; `stream` is a cudaStream_t (may be 0).
+ * Every entry point returns WLB_OK or an error code; wlb_last_error() gives
+ * the message.  All device work is stream-ordered and asynchronous.
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/pkg/src/balsim/...).  The reference's FFI boundary is the
+ * `balsim._kernels` module (_kernels/__init__.py:35-61), which the drop-in
+ * Python layer (paper_2503_17924_b200/_native.py) binds with ctypes.
+ */
+#ifndef WLBCP_H
+#define WLBCP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WLB_OK 0
+#define WLB_EINVAL 22      /* bad argument: maps to Python ValueError */
+#define WLB_ENODEV 19      /* no usable sm_100 device */
+#define WLB_ECUDA 1000     /* CUDA runtime / driver failure */
+
+#define WLB_STRATEGY_PER_SEQUENCE 0
+#define WLB_STRATEGY_PER_DOCUMENT 1
+#define WLB_POLICY_ADAPTIVE 2
+
+int32_t wlb_abi_version(void);
+const char* wlb_last_error(void);
+/* 0 when a compute-capability-10.x device is visible, else WLB_ENODEV. */
+int wlb_device_check(void);
+
+/* ---------------------------------------------------------------- host ---
+ * Longest-first min-W bin placement (bit-identical fp64 expression order).
+ * Replaces _kernels.heuristic_fill (_kernels/__init__.py:53-61,
+ * _compiled.pyx:50-86).  lengths host [n], sorted descending; out host [n],
+ * bin index or -1 for "fits nowhere under l_max". */
+int wlb_heuristic_fill(const int64_t* lengths, int64_t n, int32_t n_mb, int64_t l_max,
+                       double attn_coeff, double linear_coeff, int32_t* out);
+
+/* -------------------------------------------------------------- device ---
+ * Batched CP shard builder + adaptive selector.  Replaces
+ * sharding.per_sequence_shard / per_document_shard / strategy_latencies /
+ * adaptive_select (sharding.py:86-188) and _kernels.kernel_latency_sum
+ * (_kernels/__init__.py:45-50) for n_mb micro-batches in ONE launch.
+ *
+ * Inputs (device): mb_doc_off[n_mb+1] doc offsets, doc_len[mb_doc_off[n_mb]],
+ *   mb_tok_off[n_mb+1] token offsets, curve_q[n_curve], curve_v[n_curve].
+ * policy: WLB_STRATEGY_PER_SEQUENCE / _PER_DOCUMENT / WLB_POLICY_ADAPTIVE.
+ * Outputs (device):
+ *   choice[n_mb]               strategy used (0 seq, 1 doc); -1 if T % 2cp != 0
+ *   rank_latency[n_mb][2][cp]  fp64 model latency per strategy and rank,
+ *                              bit-identical to worker_attention_latency
+ *   rank_pairs[n_mb][cp]       causal pairs per rank (chosen strategy)
+ *   seg_count[n_mb][2][cp]     canonical range count per strategy and rank
+ *   segs[n_mb][2][cp][max_segs][3]  (doc pos, start, end), canonical order
+ *   rowset_off[n_mb][cp][max_docs+1] local row offset of each doc (chosen)
+ *   gather_index[mb_tok_off[n_mb]], positions[...] (may be NULL): for rank r
+ *     of micro-batch b, local row i lives at mb_tok_off[b] + r*T_b/cp + i and
+ *     holds the micro-batch-global token index / in-document position.
+ * max_segs must be >= 4*max_docs+2; max_docs >= docs of any micro-batch. */
+int wlb_shard_plan(int32_t n_mb, const int32_t* mb_doc_off, const int64_t* doc_len,
+                   const int64_t* mb_tok_off, int32_t cp, int32_t policy,
+                   int64_t tile, const int64_t* curve_q, const double* curve_v,
+                   int32_t n_curve, double op_scale, int32_t max_segs, int32_t max_docs,
+                   int32_t* choice, double* rank_latency, int64_t* rank_pairs,
+                   int32_t* seg_count, int32_t* segs, int32_t* rowset_off,
+                   int32_t* gather_index, int32_t* positions, void* stream);
+
+/* Tile-padded model latency of arbitrary (q, kv) ranges, summed in order
+ * (replaces _kernels.kernel_latency_sum, _compiled.pyx:30-47).  All device;
+ * out[0] receives the fp64 sum. */
+int wlb_kernel_latency_sum(const int64_t* q_lens, const int64_t* kv_lens, int64_t n,
+                           int64_t tile, const int64_t* curve_q, const double* curve_v,
+                           int32_t n_curve, double op_scale, double* out, void* stream);
+
+/* Attention work list for one rank: query tiles of <= block_m rows cut from
+ * each (rank, doc) row-set, back-aligned (optimal for the doc-prefix cost),
+ * sorted by descending KV extent.  rowset_off[n_docs+1], positions[rows] and
+ * doc_start[n_docs+1] (global KV offsets) are device arrays.
+ * tiles[max_tiles][4] = {row0, nrows, kv_begin, kv_end}; n_tiles[0] = count. */
+int wlb_attn_tiles(int32_t n_docs, const int32_t* rowset_off, const int32_t* positions,
+                   const int32_t* doc_start, int32_t block_m, int32_t max_tiles,
+                   int32_t* tiles, int32_t* n_tiles, void* stream);
+
+/* Document-prefix causal attention forward, tcgen05/TMEM/TMA on sm_100a.
+ * q[Tl][Hq][D], k/v[T][Hkv][D] bf16 (document order), o[Tl][Hq][D] bf16,
+ * lse[Hq][Tl] fp32 (natural-log logsumexp of scaled scores).
+ * Row i attends keys [kv_begin, kv_begin + positions[i] + 1) of its tile.
+ * D in {64, 128}; Hq % Hkv == 0. */
+int wlb_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
+                 const int32_t* tiles, const int32_t* n_tiles, int32_t max_tiles,
+                 const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq,
+                 int32_t Hkv, int32_t D, float scale, void* stream);
+
+/* Backward.  do_[Tl][Hq][D] bf16, o, lse from forward.  Writes
+ * dq[Tl][Hq][D] bf16, and dk/dv partials for the full sequence
+ * [T][Hkv][D] (fp32) -- summed over ranks by the CP reduce-scatter.
+ * ws: device workspace of wlb_attn_bwd_workspace() bytes. */
+size_t wlb_attn_bwd_workspace(int32_t Tl, int32_t T, int32_t Hq, int32_t Hkv, int32_t D);
+int wlb_attn_bwd(const void* q, const void* k, const void* v, const void* o,
+                 const void* do_, const float* lse, void* dq, float* dk, float* dv,
+                 const int32_t* tiles, const int32_t* n_tiles, int32_t max_tiles,
+                 const int32_t* rowset_off, const int32_t* doc_start, int32_t n_docs,
+                 const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq,
+                 int32_t Hkv, int32_t D, float scale, void* ws, void* stream);
+
+/* Row permutations for the CP exchange (rows of row_bytes, 16-B aligned).
+ * scatter: dst[index[i]] = src[i];  gather: dst[i] = src[index[i]]. */
+int wlb_rows_scatter(const void* src, void* dst, const int32_t* index, int64_t n_rows,
+                     int64_t row_bytes, void* stream);
+int wlb_rows_gather(const void* src, void* dst, const int32_t* index, int64_t n_rows,
+                    int64_t row_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WLBCP_H */

@@ -1,0 +1,88 @@
+"""ctypes binding of libwlbcp.so, the C ABI declared in include/wlbcp.h.
+
+This replaces the reference's `balsim._kernels` dispatch module
+(`_kernels/__init__.py:1-61`): there is exactly ONE backend (sm_100a), no pure
+fallback and no environment switch.  If the library is missing, or no
+compute-capability-10 device is visible, compute entry points raise
+`NativeError` -- they never fall back to the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .errors import NativeError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libwlbcp.so")
+
+WLB_OK, WLB_EINVAL, WLB_ENODEV, WLB_ECUDA = 0, 22, 19, 1000
+
+_p, _i32, _i64, _f64, _f32, _sz = C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_float, C.c_size_t
+
+# name -> (restype, argtypes); must match include/wlbcp.h
+SIGNATURES = {
+    "wlb_abi_version": (_i32, []),
+    "wlb_last_error": (C.c_char_p, []),
+    "wlb_device_check": (C.c_int, []),
+    "wlb_heuristic_fill": (C.c_int, [_p, _i64, _i32, _i64, _f64, _f64, _p]),
+    "wlb_shard_plan": (C.c_int, [_i32, _p, _p, _p, _i32, _i32, _i64, _p, _p, _i32, _f64, _i32,
+                                 _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "wlb_kernel_latency_sum": (C.c_int, [_p, _p, _i64, _i64, _p, _p, _i32, _f64, _p, _p]),
+    "wlb_attn_tiles": (C.c_int, [_i32, _p, _p, _p, _i32, _i32, _p, _p, _p]),
+    "wlb_attn_fwd": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, _i32, _p, _i32, _i32, _i32, _i32,
+                               _i32, _f32, _p]),
+    "wlb_attn_bwd_workspace": (_sz, [_i32, _i32, _i32, _i32, _i32]),
+    "wlb_attn_bwd": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i32, _p, _p, _i32,
+                               _p, _i32, _i32, _i32, _i32, _i32, _f32, _p, _p]),
+    "wlb_rows_scatter": (C.c_int, [_p, _p, _p, _i64, _i64, _p]),
+    "wlb_rows_gather": (C.c_int, [_p, _p, _p, _i64, _i64, _p]),
+}
+
+_lib = None
+_device_ok = None
+
+
+def lib():
+    """Load the library once (host entry points work without a GPU)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NativeError(f"{LIB_PATH} is missing: run `python -m paper_2503_17924_b200.build`")
+        handle = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype, fn.argtypes = res, args
+        _lib = handle
+    return _lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc == WLB_OK:
+        return
+    msg = lib().wlb_last_error().decode(errors="replace")
+    if rc == WLB_EINVAL:
+        raise ValueError(f"{what}: {msg}")
+    raise NativeError(f"{what} failed ({rc}): {msg}")
+
+
+def require_device() -> None:
+    """Raise NativeError unless an sm_100 device is usable from torch and the library."""
+    global _device_ok
+    if _device_ok is None:
+        import torch
+        if not torch.cuda.is_available():
+            raise NativeError("no CUDA device: the sm_100a path has no CPU fallback")
+        torch.cuda.init()
+        check(lib().wlb_device_check(), "wlb_device_check")
+        _device_ok = True
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()

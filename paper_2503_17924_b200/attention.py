@@ -1,0 +1,121 @@
+"""Document-prefix causal attention on sm_100a (forward + backward).
+
+Host-side orchestration of the tcgen05 kernels in `csrc/attn_fwd.cu` and
+`csrc/attn_bwd.cu`.  The computation is the one the reference prices but
+never runs (`sharding.py:19-21`): a query row at in-document position t of
+document p attends keys [doc_start_p, doc_start_p + t + 1) of the
+document-ordered K/V.  All tensors are THD ([tokens, heads, dim]) bf16.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _native
+
+BLOCK_M = 128
+
+
+@dataclass
+class AttnTiles:
+    """Query-tile work list of one rank (device)."""
+
+    tiles: torch.Tensor       # [2*max_tiles, 4] int32 (second half is scratch)
+    n_tiles: torch.Tensor     # [1] int32
+    max_tiles: int
+    positions: torch.Tensor   # [Tl] int32
+    rowset_off: torch.Tensor  # [n_docs+1] int32
+    doc_start: torch.Tensor   # [n_docs+1] int32
+    n_docs: int
+    T: int                    # full (global) token count of the micro-batch
+
+
+def build_tiles(rowset_off: torch.Tensor, positions: torch.Tensor, doc_lengths,
+                block_m: int = BLOCK_M) -> AttnTiles:
+    """Cut one rank's (rank, document) row-sets into query tiles on the GPU."""
+    _native.require_device()
+    dev = positions.device
+    n_docs = len(doc_lengths)
+    starts = [0]
+    for x in doc_lengths:
+        starts.append(starts[-1] + int(x))
+    doc_start = torch.tensor(starts, dtype=torch.int32, device=dev)
+    tl = positions.numel()
+    max_tiles = tl // block_m + n_docs + 1
+    tiles = torch.empty((2 * max_tiles, 4), dtype=torch.int32, device=dev)
+    n_tiles = torch.empty(1, dtype=torch.int32, device=dev)
+    p = _native.ptr
+    _native.check(_native.lib().wlb_attn_tiles(
+        n_docs, p(rowset_off), p(positions), p(doc_start), block_m, max_tiles, p(tiles),
+        p(n_tiles), _native.stream_ptr()), "wlb_attn_tiles")
+    return AttnTiles(tiles, n_tiles, max_tiles, positions, rowset_off, doc_start, n_docs,
+                     starts[-1])
+
+
+def _check_inputs(q, k, v):
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous() or t.dim() != 3:
+            raise ValueError(f"{name} must be a contiguous CUDA bf16 [tokens, heads, dim] tensor")
+    if q.shape[2] != k.shape[2] or k.shape != v.shape or q.shape[1] % k.shape[1]:
+        raise ValueError("shape mismatch between q, k, v")
+
+
+def attn_forward(q, k, v, tiles: AttnTiles, scale: float | None = None):
+    """O [Tl,Hq,D] bf16 and LSE [Hq,Tl] fp32 for one rank's local queries."""
+    _check_inputs(q, k, v)
+    tl, hq, d = q.shape
+    scale = 1.0 / math.sqrt(d) if scale is None else scale
+    o = torch.empty_like(q)
+    lse = torch.empty((hq, tl), dtype=torch.float32, device=q.device)
+    p = _native.ptr
+    _native.check(_native.lib().wlb_attn_fwd(
+        p(q), p(k), p(v), p(o), p(lse), p(tiles.tiles), p(tiles.n_tiles), tiles.max_tiles,
+        p(tiles.positions), tl, k.shape[0], hq, k.shape[1], d, scale, _native.stream_ptr()),
+        "wlb_attn_fwd")
+    return o, lse
+
+
+def attn_backward(q, k, v, o, lse, do, tiles: AttnTiles, scale: float | None = None):
+    """dQ [Tl,Hq,D] bf16 and fp32 dK/dV partials over the full sequence."""
+    _check_inputs(q, k, v)
+    tl, hq, d = q.shape
+    T, hkv = k.shape[0], k.shape[1]
+    scale = 1.0 / math.sqrt(d) if scale is None else scale
+    do = do.contiguous()
+    dq = torch.empty_like(q)
+    dk = torch.empty((T, hkv, d), dtype=torch.float32, device=q.device)
+    dv = torch.empty((T, hkv, d), dtype=torch.float32, device=q.device)
+    lib = _native.lib()
+    ws = torch.empty(lib.wlb_attn_bwd_workspace(tl, T, hq, hkv, d), dtype=torch.uint8,
+                     device=q.device)
+    p = _native.ptr
+    _native.check(lib.wlb_attn_bwd(
+        p(q), p(k), p(v), p(o), p(do), p(lse), p(dq), p(dk), p(dv), p(tiles.tiles),
+        p(tiles.n_tiles), tiles.max_tiles, p(tiles.rowset_off), p(tiles.doc_start),
+        tiles.n_docs, p(tiles.positions), tl, T, hq, hkv, d, scale, p(ws),
+        _native.stream_ptr()), "wlb_attn_bwd")
+    return dq, dk, dv
+
+
+class DocPrefixAttention(torch.autograd.Function):
+    """Single-rank (CP=1 or pre-gathered KV) autograd wrapper."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, tiles: AttnTiles, scale):
+        o, lse = attn_forward(q, k, v, tiles, scale)
+        ctx.save_for_backward(q, k, v, o, lse)
+        ctx.tiles, ctx.scale = tiles, scale
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v, o, lse = ctx.saved_tensors
+        dq, dk, dv = attn_backward(q, k, v, o, lse, do, ctx.tiles, ctx.scale)
+        return dq, dk.to(k.dtype), dv.to(v.dtype), None, None
+
+
+def doc_prefix_attention(q, k, v, tiles: AttnTiles, scale: float | None = None):
+    return DocPrefixAttention.apply(q, k, v, tiles, scale)

@@ -1,0 +1,67 @@
+// Shared helpers for the wlbcp sm_100a library: error state, launch checks and
+// block-wide scans.  PTX wrappers for TMA / mbarrier / tcgen05 live in sm100.cuh.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/wlbcp.h"
+
+namespace wlb {
+
+// Last error message (per host thread).
+void set_error(const char* fmt, ...);
+
+#define WLB_CUDA_TRY(expr)                                                        \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess) {                                                      \
+      ::wlb::set_error("%s failed at %s:%d: %s", #expr, __FILE__, __LINE__,       \
+                       cudaGetErrorString(_e));                                   \
+      return WLB_ECUDA;                                                           \
+    }                                                                             \
+  } while (0)
+
+#define WLB_LAUNCH_CHECK() WLB_CUDA_TRY(cudaGetLastError())
+
+#define WLB_REQUIRE(cond, ...)                                                    \
+  do {                                                                            \
+    if (!(cond)) {                                                                \
+      ::wlb::set_error(__VA_ARGS__);                                              \
+      return WLB_EINVAL;                                                          \
+    }                                                                             \
+  } while (0)
+
+// Block-wide exclusive scan of one int64 per thread.  `warp_tot` must hold
+// blockDim.x/32 + 1 entries of shared memory.  Returns the exclusive prefix and
+// writes the block total to *total (all threads).
+__device__ __forceinline__ long long block_exclusive_scan(long long v, long long* warp_tot,
+                                                          long long* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    long long t = lane < nwarp ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      long long y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < nwarp) warp_tot[lane] = t;           // inclusive warp prefix
+    if (lane == nwarp - 1) warp_tot[nwarp] = t;     // block total
+  }
+  __syncthreads();
+  long long base = warp ? warp_tot[warp - 1] : 0;
+  long long res = base + x - v;
+  *total = warp_tot[nwarp];
+  __syncthreads();
+  return res;
+}
+
+}  // namespace wlb

@@ -1,0 +1,84 @@
+"""tcgen05 doc-prefix attention vs the fp32 CPU oracle.
+
+Tolerance (north star): max abs err <= 2e-2 and rel (max err / max |ref|)
+<= 1e-2 for O, dQ, dK, dV, on bf16 inputs drawn N(0, 1).
+"""
+
+import math
+
+import pytest
+import torch
+
+import paper_2503_17924_b200 as wl
+from paper_2503_17924_b200.attention import attn_backward, attn_forward, build_tiles
+from oracle import attention_oracle as ao
+from oracle import shard_oracle as so
+
+pytestmark = pytest.mark.gpu
+
+ATOL, RTOL = 2e-2, 1e-2
+
+
+def _close(got, ref, name):
+    got, ref = got.float().cpu(), ref.float().cpu()
+    err = (got - ref).abs().max().item()
+    scale = ref.abs().max().item()
+    assert err <= ATOL, f"{name}: max abs err {err:.3e}"
+    assert err <= RTOL * max(scale, 1.0), f"{name}: rel err {err / max(scale, 1e-9):.3e}"
+
+
+def _inputs(T, tl, hq, hkv, d, seed):
+    g = torch.Generator().manual_seed(seed)
+    mk = lambda *s: torch.randn(*s, generator=g).to(torch.bfloat16)
+    return mk(T, hq, d), mk(T, hkv, d), mk(T, hkv, d), mk(T, hq, d)
+
+
+def _rank_case(lengths, cp, policy, hq, hkv, d, seed=0, with_bwd=False):
+    lengths = so.pad_lengths_for_cp(lengths, cp)
+    T = sum(lengths)
+    q, k, v, do = _inputs(T, T // cp, hq, hkv, d, seed)
+    plan = wl.build_shard_plan([lengths], cp, policy)
+    a = plan.assignment(0)
+    ranges = [[(p, r.start, r.end) for p, r in w] for w in a.workers]
+    dev = torch.device("cuda")
+    kd, vd = k.to(dev), v.to(dev)
+    for w in range(cp):
+        gidx, pos, ro = plan.rank_local(0, w)
+        idx = gidx.long().cpu()
+        ql = q[idx].contiguous()
+        tiles = build_tiles(ro, pos, lengths)
+        o, lse = attn_forward(ql.to(dev), kd, vd, tiles)
+        if with_bwd:
+            ro_, rl, rdq, rdk, rdv = ao.segment_attention_fwd_bwd(ql, k, v, do[idx], lengths, ranges[w])
+            dq, dk, dv = attn_backward(ql.to(dev), kd, vd, o, lse, do[idx].contiguous().to(dev), tiles)
+            _close(dq, rdq, "dq")
+            _close(dk, rdk, "dk")
+            _close(dv, rdv, "dv")
+        else:
+            ro_, rl = ao.segment_attention(ql, k, v, lengths, ranges[w])
+        _close(o, ro_, "o")
+        assert (lse.cpu() - rl).abs().max().item() < 1e-2
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_fwd_single_doc_cp1(d):
+    _rank_case([512], 1, "per_document", 2, 2, d)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_fwd_multi_doc_cp1(d):
+    _rank_case([300, 17, 1, 640, 129, 2], 1, "per_document", 4, 4, d, seed=1)
+
+
+def test_fwd_gqa():
+    _rank_case([400, 260, 77], 1, "per_document", 8, 2, 128, seed=2)
+
+
+@pytest.mark.parametrize("policy", ["per_document", "per_sequence"])
+@pytest.mark.parametrize("cp", [2, 4])
+def test_fwd_cp_ranks(policy, cp):
+    _rank_case([1000, 3, 250, 777, 40], cp, policy, 4, 2, 64, seed=cp)
+
+
+def test_fwd_long_doc():
+    _rank_case([4096], 2, "per_document", 2, 1, 128, seed=5)

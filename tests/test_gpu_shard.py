@@ -1,0 +1,133 @@
+"""GPU shard builder + selector: bit-exact against the reference's outputs."""
+
+import pytest
+import torch
+
+from conftest import load_golden, to_workers
+import paper_2503_17924_b200 as wl
+from oracle import shard_oracle as so
+
+pytestmark = pytest.mark.gpu
+
+PROFILE = wl.CostProfile()
+
+
+def _mb(lengths):
+    return wl.MicroBatch([wl.Document(i, x) for i, x in enumerate(lengths)])
+
+
+@pytest.mark.parametrize("name", ["sharding_random.json.gz", "sharding_synthetic.json.gz"])
+def test_batched_plan_bit_exact(name):
+    """All golden cases, grouped by cp, each group in ONE batched launch."""
+    cases = load_golden(name)["cases"]
+    for cp in (1, 2, 4, 8):
+        group = [c for c in cases if c["cp"] == cp]
+        if not group:
+            continue
+        plan = wl.build_shard_plan([c["lengths"] for c in group], cp, "adaptive", PROFILE)
+        lat = plan.rank_latency.cpu()
+        for b, c in enumerate(group):
+            assert to_workers(plan.assignment(b, wl.ShardStrategy.PER_SEQUENCE)) == c["per_sequence"]
+            assert to_workers(plan.assignment(b, wl.ShardStrategy.PER_DOCUMENT)) == c["per_document"]
+            assert [x.hex() for x in lat[b, 0].tolist()] == c["lat_seq"]
+            assert [x.hex() for x in lat[b, 1].tolist()] == c["lat_doc"]
+            assert plan.strategy(b).value == c["adaptive"]
+
+
+def test_token_layout_and_pairs_match_oracle():
+    cases = load_golden("sharding_random.json.gz")["cases"][:120]
+    for cp in (1, 2, 4, 8):
+        group = [c for c in cases if c["cp"] == cp]
+        for policy in ("per_sequence", "per_document"):
+            plan = wl.build_shard_plan([c["lengths"] for c in group], cp, policy)
+            pairs = plan.rank_pairs.cpu()
+            for b, c in enumerate(group):
+                a = so.shard(c["lengths"], cp, so.SEQ if policy == "per_sequence" else so.DOC)
+                for w in range(cp):
+                    g, p, ro = plan.rank_local(b, w)
+                    eg, ep = so.local_layout(c["lengths"], a[w])
+                    assert g.tolist() == eg and p.tolist() == ep
+                    assert int(pairs[b, w]) == so.worker_pairs(a[w])
+                    # row-set offsets: tokens of each doc on this rank, in doc order
+                    counts = [0] * len(c["lengths"])
+                    for pos, s, e in a[w]:
+                        counts[pos] += e - s
+                    exp = [0]
+                    for x in counts:
+                        exp.append(exp[-1] + x)
+                    assert ro.tolist() == exp
+
+
+def test_reference_api_hand_examples():
+    """test_sharding.py:69-145,152-216 of the reference, through the drop-in API."""
+    a = wl.per_sequence_shard(_mb([16]), 2)
+    assert a.workers[0] == [(0, wl.TokenRange(0, 4)), (0, wl.TokenRange(12, 16))]
+    assert a.workers[1] == [(0, wl.TokenRange(4, 12))]
+    a = wl.per_document_shard(_mb([10, 6]), 2)
+    assert a.workers[0] == [(0, wl.TokenRange(0, 2)), (0, wl.TokenRange(6, 9)),
+                            (1, wl.TokenRange(0, 1)), (1, wl.TokenRange(3, 5))]
+    assert a.workers[1] == [(0, wl.TokenRange(2, 6)), (0, wl.TokenRange(9, 10)),
+                            (1, wl.TokenRange(1, 3)), (1, wl.TokenRange(5, 6))]
+    assert wl.per_document_shard(_mb([1, 1, 1, 1]), 2).worker_token_count(0) == 2
+    with pytest.raises(ValueError):
+        wl.per_sequence_shard(_mb([10]), 2)
+    with pytest.raises(ValueError):
+        wl.per_document_shard(_mb([8]), 0)
+    a = wl.per_sequence_shard(_mb([16]), 2)
+    assert wl.worker_attention_latency(a, 1, PROFILE) == wl.attention_kernel_latency(8, 12, PROFILE)
+    a.workers[1] = []
+    assert wl.worker_attention_latency(a, 1, PROFILE) == 0.0
+    assert wl.adaptive_select(_mb([128 * 1024]), 4, PROFILE).strategy is wl.ShardStrategy.PER_SEQUENCE
+    assert wl.adaptive_select(_mb([128] * 64), 4, PROFILE).strategy is wl.ShardStrategy.PER_SEQUENCE
+    assert wl.adaptive_select(_mb([96 * 1024] + [1024] * 32), 4, PROFILE).strategy \
+        is wl.ShardStrategy.PER_DOCUMENT
+    assert wl.shard(_mb([32]), 2, "per_document", PROFILE).strategy is wl.ShardStrategy.PER_DOCUMENT
+    with pytest.raises(ValueError):
+        wl.shard(_mb([32]), 2, "bogus", PROFILE)
+
+
+def test_worker_latency_bit_exact_random(rng):
+    for _ in range(50):
+        cp = int(rng.choice([2, 4, 8]))
+        k = int(rng.integers(1, 30))
+        lengths = [int(x) for x in rng.integers(1, 9000, size=k)]
+        lengths = so.pad_lengths_for_cp(lengths, cp)
+        a = wl.per_document_shard(_mb(lengths), cp)
+        ref = so.per_document(lengths, cp)
+        for w in range(cp):
+            got = wl.worker_attention_latency(a, w, PROFILE)
+            assert got == so.worker_latency(ref[w], 128, [0, 256], [3.5e11, 7e11], 70.0)
+        lats = wl.strategy_latencies(_mb(lengths), cp, PROFILE)
+        exp = so.strategy_latencies(lengths, cp, 128, [0, 256], [3.5e11, 7e11], 70.0)
+        assert lats[wl.ShardStrategy.PER_SEQUENCE] == exp[so.SEQ]
+        assert lats[wl.ShardStrategy.PER_DOCUMENT] == exp[so.DOC]
+
+
+def test_config5_selection_matches_reference():
+    """64 packed micro-batches per step, padded for cp=8, one batched launch."""
+    g = load_golden("packer_config5.json.gz")["iterations"]
+    for it in g:
+        mbs = [m for m in it["microbatches"] if m["lengths"]]
+        plan = wl.build_shard_plan([m["lengths"] for m in mbs], 8, "adaptive", PROFILE)
+        assert [plan.strategy(b).value for b in range(len(mbs))] == [m["choice"] for m in mbs]
+
+
+def test_attention_tiles_cover_rows_once():
+    from paper_2503_17924_b200.attention import build_tiles
+    lengths = so.pad_lengths_for_cp([700, 3, 129, 2000, 1, 257], 4)
+    plan = wl.build_shard_plan([lengths], 4, "per_document")
+    for w in range(4):
+        g, pos, ro = plan.rank_local(0, w)
+        t = build_tiles(ro, pos, lengths)
+        n = int(t.n_tiles.item())
+        tiles = t.tiles[:n].cpu().tolist()
+        seen = torch.zeros(pos.numel(), dtype=torch.int32)
+        ext = []
+        for row0, nrows, kvb, kve in tiles:
+            assert 1 <= nrows <= 128
+            seen[row0:row0 + nrows] += 1
+            p = pos[row0 + nrows - 1].item()
+            assert kve - kvb == p + 1
+            ext.append((kve - kvb + 127) // 128)
+        assert bool((seen == 1).all())
+        assert ext == sorted(ext, reverse=True)   # longest first
