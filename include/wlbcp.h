@@ -82,7 +82,8 @@ int wlb_kernel_latency_sum(const int64_t* q_lens, const int64_t* kv_lens, int64_
  * each (rank, doc) row-set, back-aligned (optimal for the doc-prefix cost),
  * sorted by descending KV extent.  rowset_off[n_docs+1], positions[rows] and
  * doc_start[n_docs+1] (global KV offsets) are device arrays.
- * tiles[max_tiles][4] = {row0, nrows, kv_begin, kv_end}; n_tiles[0] = count. */
+ * tiles[2*max_tiles][4]: the first n_tiles[0] rows receive {row0, nrows,
+ * kv_begin, kv_end}; the second half is scratch. */
 int wlb_attn_tiles(int32_t n_docs, const int32_t* rowset_off, const int32_t* positions,
                    const int32_t* doc_start, int32_t block_m, int32_t max_tiles,
                    int32_t* tiles, int32_t* n_tiles, void* stream);
@@ -97,14 +98,16 @@ int wlb_attn_fwd(const void* q, const void* k, const void* v, void* o, float* ls
                  const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq,
                  int32_t Hkv, int32_t D, float scale, void* stream);
 
-/* Backward.  do_[Tl][Hq][D] bf16, o, lse from forward.  Writes
- * dq[Tl][Hq][D] bf16, and dk/dv partials for the full sequence
- * [T][Hkv][D] (fp32) -- summed over ranks by the CP reduce-scatter.
+/* Backward.  do_[Tl][Hq][D] bf16, o and lse from the forward.  Writes
+ * dq[Tl][Hq][D] bf16 and dK/dV partials over the full document-ordered
+ * sequence, dk/dv[T][Hkv][D] fp32 (summed over ranks by the CP
+ * reduce-scatter).  rowset_off[n_docs+1] / positions[Tl] as produced by
+ * wlb_shard_plan for this rank, doc_start[n_docs+1] global KV offsets.
  * ws: device workspace of wlb_attn_bwd_workspace() bytes. */
-size_t wlb_attn_bwd_workspace(int32_t Tl, int32_t T, int32_t Hq, int32_t Hkv, int32_t D);
+size_t wlb_attn_bwd_workspace(int32_t Tl, int32_t T, int32_t Hq, int32_t Hkv, int32_t D,
+                              int32_t n_docs);
 int wlb_attn_bwd(const void* q, const void* k, const void* v, const void* o,
                  const void* do_, const float* lse, void* dq, float* dk, float* dv,
-                 const int32_t* tiles, const int32_t* n_tiles, int32_t max_tiles,
                  const int32_t* rowset_off, const int32_t* doc_start, int32_t n_docs,
                  const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq,
                  int32_t Hkv, int32_t D, float scale, void* ws, void* stream);

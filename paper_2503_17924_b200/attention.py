@@ -89,13 +89,12 @@ def attn_backward(q, k, v, o, lse, do, tiles: AttnTiles, scale: float | None = N
     dk = torch.empty((T, hkv, d), dtype=torch.float32, device=q.device)
     dv = torch.empty((T, hkv, d), dtype=torch.float32, device=q.device)
     lib = _native.lib()
-    ws = torch.empty(lib.wlb_attn_bwd_workspace(tl, T, hq, hkv, d), dtype=torch.uint8,
-                     device=q.device)
+    ws = torch.empty(lib.wlb_attn_bwd_workspace(tl, T, hq, hkv, d, tiles.n_docs),
+                     dtype=torch.uint8, device=q.device)
     p = _native.ptr
     _native.check(lib.wlb_attn_bwd(
-        p(q), p(k), p(v), p(o), p(do), p(lse), p(dq), p(dk), p(dv), p(tiles.tiles),
-        p(tiles.n_tiles), tiles.max_tiles, p(tiles.rowset_off), p(tiles.doc_start),
-        tiles.n_docs, p(tiles.positions), tl, T, hq, hkv, d, scale, p(ws),
+        p(q), p(k), p(v), p(o), p(do), p(lse), p(dq), p(dk), p(dv), p(tiles.rowset_off),
+        p(tiles.doc_start), tiles.n_docs, p(tiles.positions), tl, T, hq, hkv, d, scale, p(ws),
         _native.stream_ptr()), "wlb_attn_bwd")
     return dq, dk, dv
 

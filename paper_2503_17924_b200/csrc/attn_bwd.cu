@@ -1,14 +1,476 @@
-// Placeholder until the tcgen05 backward lands (next milestone).
+// Document-prefix causal attention, backward, on sm_100a tensor cores.
+//
+// Work item = (KV tile, KV head g): 128 consecutive keys of ONE document
+// (positions [k0, k0+128) of doc p) and every local query row of the
+// (rank, doc p) row-set that can see them (in-document position >= k0 -- a
+// suffix of the row-set, found by binary search), for every query head of
+// the GQA group.  Per query tile (<= 128 rows, one head):
+//
+//   S^T  = K Q^T          (TMEM, lanes = keys)        tcgen05 SS
+//   dP^T = V dO^T         (TMEM, lanes = keys)        tcgen05 SS
+//   P^T  = exp2(S^T*scale*log2e - LSE2[q]),  dS^T = P^T (dP^T - Delta[q])
+//          (compute warps, one key row per thread; P^T, dS^T -> SMEM bf16)
+//   dV  += P^T dO         (TMEM accumulator)          A K-major, B MN-major
+//   dK  += dS^T Q         (TMEM accumulator)
+//   dQ   = dS K           (TMEM, aliases S^T)         A MN-major (dS^T read
+//          transposed), B MN-major; drained by the compute warps into an
+//          fp32 accumulator with vector atomics.
+//
+// dK/dV are written once per work item (fp32 partials over the full
+// document-ordered sequence; the CP reduce-scatter sums them over ranks).
+// A preprocessing kernel computes Delta = rowsum(dO * O); a final kernel
+// converts the fp32 dQ accumulator to bf16.
 #include "common.cuh"
+#include "sm100.cuh"
+#include "tmap.cuh"
 
-extern "C" size_t wlb_attn_bwd_workspace(int32_t Tl, int32_t T, int32_t Hq, int32_t Hkv, int32_t D) {
-  return (size_t)Tl * Hq * D * 4 + (size_t)Hq * Tl * 4;
+#include <algorithm>
+
+namespace wlb {
+using namespace sm100;
+
+template <int D>
+struct BwdCfg {
+  static constexpr int BM = 128, BN = 128;   // queries per tile, keys per tile
+  static constexpr int SLABS = D / 64;
+  static constexpr int KV_BYTES = BN * D * 2;
+  static constexpr int Q_BYTES = BM * D * 2;
+  static constexpr int T_BYTES = BN * BM * 2;   // P^T / dS^T tiles
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = OFF_K + KV_BYTES;
+  static constexpr int OFF_Q = OFF_V + KV_BYTES;
+  static constexpr int OFF_DO = OFF_Q + Q_BYTES;
+  static constexpr int OFF_P = OFF_DO + Q_BYTES;
+  static constexpr int OFF_DS = OFF_P + T_BYTES;
+  static constexpr int OFF_VEC = OFF_DS + T_BYTES;          // 2 x {lse2, delta, pos}[BM]
+  static constexpr int OFF_BAR = OFF_VEC + 2 * 3 * BM * 4;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr uint32_t TMEM_COLS = 512;
+  static constexpr uint32_t COL_S = 0;          // S^T, later dQ
+  static constexpr uint32_t COL_DP = 128;
+  static constexpr uint32_t COL_DV = 256;
+  static constexpr uint32_t COL_DK = 256 + D;
+  static constexpr uint32_t IDESC_ST = idesc_bf16(BN, BM, 0, 0);
+  static constexpr uint32_t IDESC_ACC = idesc_bf16(BN, D, 0, 1);   // dV, dK
+  static constexpr uint32_t IDESC_DQ = idesc_bf16(BM, D, 1, 1);    // dQ
+};
+
+struct BwdBars {
+  uint64_t kv_full, q_full, q_empty, s_full, p_full, mma2_done, tmem_free;
+  uint32_t tmem_base;
+};
+
+// kv_tiles[2i] = {kv_begin (global), kv_len, row_first, row_end}, kv_tiles[2i+1].x = k0
+template <int D>
+__global__ void __launch_bounds__(256, 1)
+attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                const float* __restrict__ lse, const float* __restrict__ delta,
+                float* __restrict__ dq_acc, float* __restrict__ dk, float* __restrict__ dv,
+                const int4* __restrict__ kv_tiles, const int* __restrict__ n_kv_tiles,
+                const int* __restrict__ positions, int Tl, int Hq, int Hkv, float scale,
+                float scale_log2) {
+  using C = BwdCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  const int item = blockIdx.x / Hkv, g = blockIdx.x % Hkv;
+  if (item >= n_kv_tiles[0]) return;
+  const int4 kt = kv_tiles[2 * item];
+  const int k0 = kv_tiles[2 * item + 1].x;   // in-document position of the first key
+  const int group = Hq / Hkv;
+  const int q_tiles_per_head = (kt.w - kt.z + C::BM - 1) / C::BM;
+  const int n_iter = q_tiles_per_head * group;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  BwdBars* bars = reinterpret_cast<BwdBars*>(smem + C::OFF_BAR);
+  uint8_t* sK = smem + C::OFF_K;
+  uint8_t* sV = smem + C::OFF_V;
+  uint8_t* sQ = smem + C::OFF_Q;
+  uint8_t* sDO = smem + C::OFF_DO;
+  uint8_t* sP = smem + C::OFF_P;
+  uint8_t* sDS = smem + C::OFF_DS;
+  float* sVec = reinterpret_cast<float*>(smem + C::OFF_VEC);
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars->kv_full, 1);
+    mbar_init(&bars->q_full, 1);
+    mbar_init(&bars->q_empty, 1);
+    mbar_init(&bars->s_full, 1);
+    mbar_init(&bars->p_full, 128);
+    mbar_init(&bars->mma2_done, 1);
+    mbar_init(&bars->tmem_free, 128);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(&bars->tmem_base, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer --
+    if (lane == 0) {
+      tma_prefetch(&tmQ);
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmV);
+      tma_prefetch(&tmDO);
+      mbar_expect_tx(&bars->kv_full, 2 * C::KV_BYTES);
+      for (int s = 0; s < C::SLABS; ++s) {
+        tma_load_3d(sK + s * C::BN * 128, &tmK, &bars->kv_full, s * 64, g, kt.x);
+        tma_load_3d(sV + s * C::BN * 128, &tmV, &bars->kv_full, s * 64, g, kt.x);
+      }
+      for (int i = 0; i < n_iter; ++i) {
+        const int h = g * group + i / q_tiles_per_head;
+        const int row = kt.z + (i % q_tiles_per_head) * C::BM;
+        mbar_wait(&bars->q_empty, (i & 1) ^ 1);
+        mbar_expect_tx(&bars->q_full, 2 * C::Q_BYTES);
+        for (int s = 0; s < C::SLABS; ++s) {
+          tma_load_3d(sQ + s * C::BM * 128, &tmQ, &bars->q_full, s * 64, h, row);
+          tma_load_3d(sDO + s * C::BM * 128, &tmDO, &bars->q_full, s * 64, h, row);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer --
+    if (lane == 0) {
+      const uint32_t k_b = smem_u32(sK), v_b = smem_u32(sV), q_b = smem_u32(sQ),
+                     do_b = smem_u32(sDO), p_b = smem_u32(sP), ds_b = smem_u32(sDS);
+      mbar_wait(&bars->kv_full, 0);
+      for (int i = 0; i < n_iter; ++i) {
+        mbar_wait(&bars->q_full, i & 1);
+        if (i > 0) mbar_wait(&bars->tmem_free, (i - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {   // contraction over D: K-major both
+          const uint32_t ko = (kk >> 2) * C::BN * 128 + (kk & 3) * 32;
+          const uint32_t qo = (kk >> 2) * C::BM * 128 + (kk & 3) * 32;
+          mma_ss(tmem + C::COL_S, sdesc_sw128(k_b + ko, 16, 1024), sdesc_sw128(q_b + qo, 16, 1024),
+                 C::IDESC_ST, kk > 0);
+          mma_ss(tmem + C::COL_DP, sdesc_sw128(v_b + ko, 16, 1024),
+                 sdesc_sw128(do_b + qo, 16, 1024), C::IDESC_ST, kk > 0);
+        }
+        mma_commit(&bars->s_full);
+        mbar_wait(&bars->p_full, i & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < C::BM / 16; ++kk) {   // contraction over queries
+          const uint32_t to = (kk >> 2) * C::BN * 128 + (kk & 3) * 32;   // P^T / dS^T K-major
+          const uint32_t mo = kk * 16 * 128;                             // Q / dO MN-major
+          const uint32_t acc = (i > 0) || (kk > 0);
+          mma_ss(tmem + C::COL_DV, sdesc_sw128(p_b + to, 16, 1024),
+                 sdesc_sw128(do_b + mo, C::BM * 128, 1024), C::IDESC_ACC, acc);
+          mma_ss(tmem + C::COL_DK, sdesc_sw128(ds_b + to, 16, 1024),
+                 sdesc_sw128(q_b + mo, C::BM * 128, 1024), C::IDESC_ACC, acc);
+        }
+#pragma unroll
+        for (int kk = 0; kk < C::BN / 16; ++kk) {   // contraction over keys
+          const uint32_t o = kk * 16 * 128;
+          mma_ss(tmem + C::COL_S, sdesc_sw128(ds_b + o, C::BN * 128, 1024),
+                 sdesc_sw128(k_b + o, C::BN * 128, 1024), C::IDESC_DQ, kk > 0);
+        }
+        mma_commit(&bars->mma2_done);
+        mma_commit(&bars->q_empty);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------- compute --
+    const int wq = warp & 3;
+    const int t = wq * 32 + lane;                 // key row (S^T lanes) / query row (dQ lanes)
+    const uint32_t lane_base = tmem + ((uint32_t)(wq * 32) << 16);
+    const bool key_ok = t < kt.y;                 // key t of the tile lies inside the document
+    for (int i = 0; i < n_iter; ++i) {
+      const int h = g * group + i / q_tiles_per_head;
+      const int row0 = kt.z + (i % q_tiles_per_head) * C::BM;
+      float* vec = sVec + (i & 1) * 3 * C::BM;
+      {
+        const int row = row0 + t;
+        const bool ok = row < kt.w;
+        vec[t] = ok ? lse[(size_t)h * Tl + row] * 1.4426950408889634f : 0.f;
+        vec[C::BM + t] = ok ? delta[(size_t)h * Tl + row] : 0.f;
+        reinterpret_cast<int*>(vec)[2 * C::BM + t] = ok ? positions[row] - k0 : -1;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      mbar_wait(&bars->s_full, i & 1);
+      tc_fence_after();
+      const float* vl = vec;
+      const float* vd = vec + C::BM;
+      const int* vp = reinterpret_cast<const int*>(vec + 2 * C::BM);
+      uint32_t pk[C::BM / 2], dk2[C::BM / 2];
+#pragma unroll
+      for (int c = 0; c < C::BM / 32; ++c) {
+        uint32_t us[32], ud[32];
+        tmem_ld32(lane_base + C::COL_S + c * 32, us);
+        tmem_ld32(lane_base + C::COL_DP + c * 32, ud);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          float pp[2], dd[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int q = c * 32 + e + u;
+            const bool allowed = key_ok && vp[q] >= t;   // key pos k0+t <= query pos
+            const float p = allowed ? ex2(__uint_as_float(us[e + u]) * scale_log2 - vl[q]) : 0.f;
+            pp[u] = p;
+            dd[u] = p * (__uint_as_float(ud[e + u]) - vd[q]);
+          }
+          pk[(c * 32 + e) / 2] = pack_bf16(pp[0], pp[1]);
+          dk2[(c * 32 + e) / 2] = pack_bf16(dd[0], dd[1]);
+        }
+      }
+      // previous MMA group (readers of sP / sdS) completed before the dQ drain of i-1
+      uint8_t* prow = sP + t * 128;
+      uint8_t* drow = sDS + t * 128;
+#pragma unroll
+      for (int c = 0; c < C::BM / 8; ++c) {
+        const int slab = c >> 3, cc = c & 7;
+        const int off = slab * C::BN * 128 + ((cc ^ (t & 7)) << 4);
+        *reinterpret_cast<uint4*>(prow + off) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        *reinterpret_cast<uint4*>(drow + off) = make_uint4(dk2[4 * c], dk2[4 * c + 1], dk2[4 * c + 2], dk2[4 * c + 3]);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&bars->p_full);
+      // drain dQ (lanes = query rows of this tile)
+      mbar_wait(&bars->mma2_done, i & 1);
+      tc_fence_after();
+      const int qrow = row0 + t;
+      const bool q_ok = qrow < kt.w;
+      float4* dst = reinterpret_cast<float4*>(dq_acc + ((size_t)qrow * Hq + h) * D);
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t u[32];
+        tmem_ld32(lane_base + C::COL_S + c * 32, u);
+        tmem_ld_wait();
+        if (q_ok) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            atomicAdd(dst + c * 8 + e,
+                      make_float4(__uint_as_float(u[4 * e]) * scale, __uint_as_float(u[4 * e + 1]) * scale,
+                                  __uint_as_float(u[4 * e + 2]) * scale, __uint_as_float(u[4 * e + 3]) * scale));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bars->tmem_free);
+    }
+    // ------------------------------------------------------------ epilogue --
+    // TMEM loads are warp-collective (.sync.aligned): issue them converged and
+    // predicate only the global stores on the key lying inside the document.
+    float* dvr = dv + ((size_t)(kt.x + t) * Hkv + g) * D;
+    float* dkr = dk + ((size_t)(kt.x + t) * Hkv + g) * D;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t a[32], b[32];
+      tmem_ld32(lane_base + C::COL_DV + c * 32, a);
+      tmem_ld32(lane_base + C::COL_DK + c * 32, b);
+      tmem_ld_wait();
+      if (key_ok) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          reinterpret_cast<float4*>(dvr + c * 32)[e] =
+              make_float4(__uint_as_float(a[4 * e]), __uint_as_float(a[4 * e + 1]),
+                          __uint_as_float(a[4 * e + 2]), __uint_as_float(a[4 * e + 3]));
+          reinterpret_cast<float4*>(dkr + c * 32)[e] =
+              make_float4(__uint_as_float(b[4 * e]) * scale, __uint_as_float(b[4 * e + 1]) * scale,
+                          __uint_as_float(b[4 * e + 2]) * scale, __uint_as_float(b[4 * e + 3]) * scale);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
-extern "C" int wlb_attn_bwd(const void*, const void*, const void*, const void*, const void*,
-                            const float*, void*, float*, float*, const int32_t*, const int32_t*,
-                            int32_t, const int32_t*, const int32_t*, int32_t, const int32_t*,
-                            int32_t, int32_t, int32_t, int32_t, int32_t, float, void*, void*) {
-  wlb::set_error("wlb_attn_bwd: not built yet");
-  return WLB_EINVAL;
+// Delta[h][i] = sum_d dO[i,h,d] * O[i,h,d] (fp32).  One warp per (row, head).
+template <int D>
+__global__ void bwd_delta_kernel(const __nv_bfloat16* __restrict__ o,
+                                 const __nv_bfloat16* __restrict__ dout, float* __restrict__ delta,
+                                 int Tl, int Hq) {
+  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= (long long)Tl * Hq) return;
+  const int lane = threadIdx.x & 31;
+  const int row = (int)(w / Hq), h = (int)(w % Hq);
+  constexpr int PER = D / 32;   // 2 or 4 elements per lane
+  const __nv_bfloat16* a = o + w * D + lane * PER;
+  const __nv_bfloat16* b = dout + w * D + lane * PER;
+  float s = 0.f;
+#pragma unroll
+  for (int e = 0; e < PER; ++e) s += __bfloat162float(a[e]) * __bfloat162float(b[e]);
+#pragma unroll
+  for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) delta[(size_t)h * Tl + row] = s;
+}
+
+__global__ void dq_convert_kernel(const float4* __restrict__ acc, __nv_bfloat162* __restrict__ dq,
+                                  long long n4) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    float4 v = acc[i];
+    dq[2 * i] = __floats2bfloat162_rn(v.x, v.y);
+    dq[2 * i + 1] = __floats2bfloat162_rn(v.z, v.w);
+  }
+}
+
+// KV-tile work list: for each document with local rows, 128-key tiles up to the
+// largest local position; the query rows of a tile are the row-set suffix with
+// position >= k0 (binary search).  Sorted by descending query-row count.
+constexpr int kKvThreads = 1024;
+constexpr int kKvBins = 2048;
+__global__ void __launch_bounds__(kKvThreads)
+bwd_kv_tiles_kernel(int nd, const int* __restrict__ rowset_off, const int* __restrict__ positions,
+                    const int* __restrict__ doc_start, int max_items, int4* __restrict__ out,
+                    int* __restrict__ n_out, int4* __restrict__ scratch) {
+  __shared__ long long warp_tot[kKvThreads / 32 + 1];
+  __shared__ int hist[kKvBins];
+  __shared__ int maxkey_s;
+  long long carry = 0;
+  for (int base = 0; base < nd; base += blockDim.x) {
+    const int p = base + threadIdx.x;
+    int nt = 0, r0 = 0, r1 = 0;
+    if (p < nd) {
+      r0 = rowset_off[p];
+      r1 = rowset_off[p + 1];
+      if (r1 > r0) nt = (positions[r1 - 1] + 128) / 128;
+    }
+    long long tot;
+    const long long off = carry + block_exclusive_scan(nt, warp_tot, &tot);
+    for (int t = 0; t < nt; ++t) {
+      const int k0 = t * 128;
+      int lo = r0, hi = r1;   // first row with position >= k0
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (positions[mid] >= k0) hi = mid;
+        else lo = mid + 1;
+      }
+      const int len = doc_start[p + 1] - doc_start[p] - k0;
+      if (off + t < max_items) {
+        scratch[2 * (off + t)] = make_int4(doc_start[p] + k0, len < 128 ? len : 128, lo, r1);
+        scratch[2 * (off + t) + 1] = make_int4(k0, p, 0, 0);
+      }
+    }
+    carry += tot;
+  }
+  const int total = carry < max_items ? (int)carry : max_items;
+  int mk = 0;
+  for (int i = threadIdx.x; i < total; i += blockDim.x)
+    mk = max(mk, (scratch[2 * i].w - scratch[2 * i].z + 127) >> 7);
+  for (int o = 16; o; o >>= 1) mk = max(mk, __shfl_xor_sync(0xffffffffu, mk, o));
+  if (threadIdx.x == 0) maxkey_s = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) atomicMax(&maxkey_s, mk);
+  __syncthreads();
+  int shift = 0;
+  while ((maxkey_s >> shift) >= kKvBins) ++shift;
+  for (int i = threadIdx.x; i < kKvBins; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < total; i += blockDim.x)
+    atomicAdd(&hist[kKvBins - 1 - (((scratch[2 * i].w - scratch[2 * i].z + 127) >> 7) >> shift)], 1);
+  __syncthreads();
+  const long long a0 = hist[2 * threadIdx.x], a1 = hist[2 * threadIdx.x + 1];
+  long long tot;
+  const long long ex = block_exclusive_scan(a0 + a1, warp_tot, &tot);
+  hist[2 * threadIdx.x] = (int)ex;
+  hist[2 * threadIdx.x + 1] = (int)(ex + a0);
+  __syncthreads();
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    const int key = kKvBins - 1 - (((scratch[2 * i].w - scratch[2 * i].z + 127) >> 7) >> shift);
+    const int slot = atomicAdd(&hist[key], 1);
+    out[2 * slot] = scratch[2 * i];
+    out[2 * slot + 1] = scratch[2 * i + 1];
+  }
+  if (threadIdx.x == 0) n_out[0] = total;
+}
+
+struct BwdWorkspace {
+  float* dq_acc;
+  float* delta;
+  int4* kv_tiles;   // [2*max_items] sorted + [2*max_items] scratch
+  int* n_kv;
+  size_t bytes;
+};
+
+static BwdWorkspace carve(void* base, int Tl, int T, int Hq, int D, int n_docs) {
+  BwdWorkspace w;
+  const size_t max_items = (size_t)T / 128 + n_docs + 1;
+  uint8_t* p = (uint8_t*)base;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    uint8_t* r = p ? p + off : nullptr;
+    off += (bytes + 255) & ~(size_t)255;
+    return r;
+  };
+  w.dq_acc = (float*)take((size_t)Tl * Hq * D * 4);
+  w.delta = (float*)take((size_t)Hq * Tl * 4);
+  w.kv_tiles = (int4*)take(4 * max_items * sizeof(int4));
+  w.n_kv = (int*)take(16);
+  w.bytes = off;
+  return w;
+}
+
+template <int D>
+static int launch_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                      const float* lse, void* dq, float* dk, float* dv, const int32_t* rowset_off,
+                      const int32_t* doc_start, int32_t n_docs, const int32_t* positions,
+                      int32_t Tl, int32_t T, int32_t Hq, int32_t Hkv, float scale, void* ws,
+                      cudaStream_t stream) {
+  using C = BwdCfg<D>;
+  BwdWorkspace w = carve(ws, Tl, T, Hq, D, n_docs);
+  const int max_items = T / 128 + n_docs + 1;
+  WLB_CUDA_TRY(cudaMemsetAsync(w.dq_acc, 0, (size_t)Tl * Hq * D * 4, stream));
+  WLB_CUDA_TRY(cudaMemsetAsync(dk, 0, (size_t)T * Hkv * D * 4, stream));
+  WLB_CUDA_TRY(cudaMemsetAsync(dv, 0, (size_t)T * Hkv * D * 4, stream));
+  {
+    const long long warps = (long long)Tl * Hq;
+    bwd_delta_kernel<D><<<(unsigned)((warps + 7) / 8), 256, 0, stream>>>(
+        (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, w.delta, Tl, Hq);
+    WLB_LAUNCH_CHECK();
+  }
+  bwd_kv_tiles_kernel<<<1, kKvThreads, 0, stream>>>(n_docs, rowset_off, positions, doc_start,
+                                                     max_items, w.kv_tiles, w.n_kv,
+                                                     w.kv_tiles + 2 * max_items);
+  WLB_LAUNCH_CHECK();
+  CUtensorMap tq, tk, tv, tdo;
+  int rc;
+  if ((rc = make_thd_tmap(&tq, q, Tl, Hq, D, C::BM))) return rc;
+  if ((rc = make_thd_tmap(&tdo, dout, Tl, Hq, D, C::BM))) return rc;
+  if ((rc = make_thd_tmap(&tk, k, T, Hkv, D, C::BN))) return rc;
+  if ((rc = make_thd_tmap(&tv, v, T, Hkv, D, C::BN))) return rc;
+  static bool attr = false;
+  if (!attr) {
+    WLB_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      C::SMEM));
+    attr = true;
+  }
+  attn_bwd_kernel<D><<<(unsigned)max_items * Hkv, 256, C::SMEM, stream>>>(
+      tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq, Hkv,
+      scale, scale * 1.4426950408889634f);
+  WLB_LAUNCH_CHECK();
+  const long long n4 = (long long)Tl * Hq * D / 4;
+  dq_convert_kernel<<<(unsigned)std::min<long long>((n4 + 255) / 256, 148 * 16), 256, 0, stream>>>(
+      (const float4*)w.dq_acc, (__nv_bfloat162*)dq, n4);
+  WLB_LAUNCH_CHECK();
+  return WLB_OK;
+}
+
+}  // namespace wlb
+
+extern "C" size_t wlb_attn_bwd_workspace(int32_t Tl, int32_t T, int32_t Hq, int32_t Hkv, int32_t D,
+                                         int32_t n_docs) {
+  (void)Hkv;
+  return wlb::carve(nullptr, Tl, T, Hq, D, n_docs).bytes;
+}
+
+extern "C" int wlb_attn_bwd(const void* q, const void* k, const void* v, const void* o,
+                            const void* do_, const float* lse, void* dq, float* dk, float* dv,
+                            const int32_t* rowset_off, const int32_t* doc_start, int32_t n_docs,
+                            const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq,
+                            int32_t Hkv, int32_t D, float scale, void* ws, void* stream) {
+  WLB_REQUIRE(D == 64 || D == 128, "head dim %d unsupported (64 or 128)", D);
+  WLB_REQUIRE(Hq > 0 && Hkv > 0 && Hq % Hkv == 0, "Hq must be a multiple of Hkv");
+  WLB_REQUIRE(Tl >= 0 && T > 0 && n_docs >= 0 && ws != nullptr, "bad sizes");
+  if (D == 64)
+    return wlb::launch_bwd<64>(q, k, v, o, do_, lse, dq, dk, dv, rowset_off, doc_start, n_docs,
+                               positions, Tl, T, Hq, Hkv, scale, ws, (cudaStream_t)stream);
+  return wlb::launch_bwd<128>(q, k, v, o, do_, lse, dq, dk, dv, rowset_off, doc_start, n_docs,
+                              positions, Tl, T, Hq, Hkv, scale, ws, (cudaStream_t)stream);
 }

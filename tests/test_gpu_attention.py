@@ -82,3 +82,22 @@ def test_fwd_cp_ranks(policy, cp):
 
 def test_fwd_long_doc():
     _rank_case([4096], 2, "per_document", 2, 1, 128, seed=5)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_bwd_single_doc_cp1(d):
+    _rank_case([384], 1, "per_document", 2, 2, d, seed=11, with_bwd=True)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_bwd_multi_doc(d):
+    _rank_case([300, 17, 1, 640, 129, 2], 1, "per_document", 2, 2, d, seed=12, with_bwd=True)
+
+
+def test_bwd_gqa():
+    _rank_case([400, 260, 77], 1, "per_document", 8, 2, 128, seed=13, with_bwd=True)
+
+
+@pytest.mark.parametrize("policy", ["per_document", "per_sequence"])
+def test_bwd_cp_ranks(policy):
+    _rank_case([1000, 3, 250, 777, 40], 4, policy, 4, 2, 64, seed=14, with_bwd=True)
