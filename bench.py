@@ -1,0 +1,361 @@
+"""Benchmark: document-masked CP attention fwd+bwd on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = the hot path over one synthetic global batch: the 8 long-tail
+sequences `generate_synthetic_stream(SyntheticSpec(T, T), seed=0, n_batches=8)`
+(BASELINE.md 3), each a micro-batch that is sharded + strategy-selected on
+the GPU (one batched `wlb_shard_plan` launch), then run through CP
+document-masked attention forward and backward (tcgen05 kernels, NCCL
+all-gather / reduce-scatter for N > 1).
+
+Workloads (BASELINE.json configs): N = 1 -> config 2, Llama-7B attention
+(32 q / 32 kv heads, d = 128), seq 32K, CP = 1.  N > 1 -> config 3 shape at
+seq 128K, CP = N (one process per GPU, torchrun).
+
+FLOPs are algorithmic and unmasked: 14 * D * Hq * pairs, pairs = sum over
+documents of L(L+1)/2 (`attention_workload`, workload.py:196-198).
+`value` = whole-job TFLOP/s = step FLOPs / max-over-ranks step time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import paper_2503_17924_b200 as wl  # noqa: E402
+from paper_2503_17924_b200.attention import attn_backward, attn_forward  # noqa: E402
+from paper_2503_17924_b200.cp import build_cp_shards, gather_kv, scatter_dkv  # noqa: E402
+
+N_SEQ = 8
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        p = json.load(open(path))
+        return p["bf16_tflops"], p.get("bf16_tflops_sustained"), "measured"
+    return 1590.0, 1400.0, "fallback"
+
+
+def _workload(n):
+    if n == 1:
+        return dict(name="llama7b-attn-32k-cp1", window=32768, hq=32, hkv=32, d=128, cp=1)
+    return dict(name=f"llama7b-attn-128k-cp{n}", window=131072, hq=32, hkv=32, d=128, cp=n)
+
+
+def _lengths(window):
+    spec = wl.SyntheticSpec(context_window=window, tokens_per_global_batch=window)
+    return [[d.length for d in b] for b in wl.generate_synthetic_stream(spec, 0, N_SEQ)]
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in getattr(self, "lines", []):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        busy = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _cpu_sample(lengths_list, hq_sample, d, budget_s, first=0):
+    """Oracle (torch-CPU fp32) fwd+bwd on head(s) of whole sequences, all host cores.
+    TEST/BASELINE ONLY: the checker is never the thing measured for `value`."""
+    from oracle import attention_oracle as ao
+    from oracle import shard_oracle as so
+    torch.set_num_threads(os.cpu_count())
+    flops = secs = 0.0
+    done = []
+    i = first
+    t_start = time.perf_counter()
+    while True:
+        lengths = lengths_list[i % len(lengths_list)]
+        g = torch.Generator().manual_seed(1000 + i)
+        T = sum(lengths)
+        q = torch.randn(T, hq_sample, d, generator=g)
+        k = torch.randn(T, hq_sample, d, generator=g)
+        v = torch.randn(T, hq_sample, d, generator=g)
+        do = torch.randn(T, hq_sample, d, generator=g)
+        t0 = time.perf_counter()
+        ranges = so.per_document(lengths, 1)[0]          # reference CP path (cp=1)
+        ao.segment_attention_fwd_bwd(q, k, v, do, lengths, ranges)
+        secs += time.perf_counter() - t0
+        flops += 14.0 * d * hq_sample * sum(x * (x + 1) // 2 for x in lengths)
+        done.append(i % len(lengths_list))
+        i += 1
+        if time.perf_counter() - t_start > budget_s or len(done) >= len(lengths_list):
+            break
+    return flops / secs / 1e12, done, secs
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference's CPU path (oracle port: the reference
+    computes no attention; its sharding is Python and cannot travel) on the
+    host cores, rank 0 only."""
+    if rank != 0:
+        return
+    wk = _workload(world)
+    lengths = _lengths(wk["window"])
+    vals = []
+    secs_tot = flops_tot = 0.0
+    for s in range(args.warmup + args.steps):
+        tflops, done, secs = _cpu_sample(lengths, 1, wk["d"], budget_s=0.0, first=s)
+        if s >= args.warmup:
+            vals.append(tflops)
+            secs_tot += secs
+            flops_tot += tflops * 1e12 * secs
+    value = flops_tot / secs_tot / 1e12
+    line = {
+        "impl": "reference", "metric": "doc-masked attn TFLOP/s/GPU & CP rank imbalance",
+        "value": round(value, 4), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(secs_tot / args.steps * 1e3, 1),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": wk["name"], "seq_len": wk["window"], "heads": [wk["hq"], wk["hkv"]],
+                   "head_dim": wk["d"], "cp": wk["cp"]},
+        "cpu_baseline": {"value": round(value, 4), "unit": "TFLOP/s", "cores": os.cpu_count(),
+                         "kind": "port",
+                         "sample": "per step: head 0 of one synthetic sequence (cycling the 8), "
+                                   "per_document shard + torch-CPU fp32 doc-prefix attention "
+                                   "fwd+bwd (oracle/attention_oracle.py)"},
+        "e2e": {"value": round(value, 4), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    group = None
+    wk = _workload(world)
+    cp, hq, hkv, d = wk["cp"], wk["hq"], wk["hkv"], wk["d"]
+    lengths = _lengths(wk["window"])
+    T = wk["window"]
+    tl = T // cp
+
+    # inputs resident in HBM: this rank's local tokens of every sequence
+    gen = torch.Generator(device=dev)
+    ins = []
+    for b in range(N_SEQ):
+        gen.manual_seed(1000 + 64 * b + rank)
+        mk = lambda h: torch.randn((tl, h, d), generator=gen, device=dev, dtype=torch.bfloat16)
+        ins.append((mk(hq), mk(hkv), mk(hkv), mk(hq)))
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    launches = [0]
+
+    def step(record=None, ios=None, outs_host=None):
+        shards = build_cp_shards(lengths, cp, rank, "adaptive")
+        launches[0] += 1 + N_SEQ                                    # plan + tiles
+        for b, sh in enumerate(shards):
+            q, k, v, do = ins[b]
+            if ios is not None:                                     # e2e: H2D this step's inputs
+                for dst, src in zip(ins[b], ios):
+                    dst.copy_(src, non_blocking=True)
+            k_full, v_full = gather_kv(k, v, sh, group)
+            e = [ev() for _ in range(4)] if record is not None else None
+            if e: e[0].record()
+            o, lse = attn_forward(q, k_full, v_full, sh.tiles)
+            if e: e[1].record()
+            if e: e[2].record()
+            dq, dk_full, dv_full = attn_backward(q, k_full, v_full, o, lse, do, sh.tiles)
+            if e: e[3].record()
+            dk, dv = scatter_dkv(dk_full, dv_full, sh, group)
+            launches[0] += 1 + 4 + (4 if cp > 1 else 0)
+            if record is not None:
+                record.append((e, sh))
+            if outs_host is not None:                               # e2e: D2H the results
+                for src, dst in zip((o, dq, dk, dv), outs_host):
+                    dst.copy_(src if src.dtype == torch.bfloat16 else src.to(torch.bfloat16),
+                              non_blocking=True)
+        return shards
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        shards = step()
+    barrier()
+
+    # ------------------------------------------------------------ timed loop --
+    launches[0] = 0
+    recs = []
+    t0, t1 = ev(), ev()
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        t0.record()
+        for _ in range(args.steps):
+            shards = step(record=recs)
+        t1.record()
+        barrier()
+    my_ms = t0.elapsed_time(t1)
+    fwd_ms = sum(e[0].elapsed_time(e[1]) for e, _ in recs)
+    bwd_ms = sum(e[2].elapsed_time(e[3]) for e, _ in recs)
+    my_pairs = sum(sh.pairs for sh in shards)
+    total_pairs = sum(sum(x * (x + 1) // 2 for x in ls) for ls in lengths)
+    step_flops = 14.0 * d * hq * total_pairs
+    kern_ms = fwd_ms + bwd_ms
+    stats = torch.tensor([my_ms, kern_ms, fwd_ms, bwd_ms, float(my_pairs)], device=dev,
+                         dtype=torch.float64)
+    if world > 1:
+        allv = [torch.empty_like(stats) for _ in range(world)]
+        dist.all_gather(allv, stats)
+        allv = torch.stack(allv).cpu()
+    else:
+        allv = stats.cpu()[None]
+    max_ms = float(allv[:, 0].max())
+    ms_step = max_ms / args.steps
+    value = step_flops * args.steps / (max_ms / 1e3) / 1e12
+    kt = allv[:, 1]
+    imbalance = float(kt.max() / kt.mean())
+    pair_imb = float(allv[:, 4].max() / allv[:, 4].mean())
+    strategies = [sh.strategy.value for sh in shards]
+
+    # ------------------------------------------------------------------ e2e --
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t.cpu())
+        host_in = [pin(t) for t in ins[0]]
+        host_out = [torch.empty((tl, hq, d), dtype=torch.bfloat16, pin_memory=True)] * 2 + \
+                   [torch.empty((tl, hkv, d), dtype=torch.bfloat16, pin_memory=True)] * 2
+        step(ios=host_in, outs_host=host_out)
+        barrier()
+        a, b = ev(), ev()
+        n_e2e = max(1, min(args.steps, 3))
+        a.record()
+        for _ in range(n_e2e):
+            step(ios=host_in, outs_host=host_out)
+        b.record()
+        barrier()
+        e_ms = torch.tensor([a.elapsed_time(b)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        h2d = N_SEQ * sum(t.numel() * t.element_size() for t in host_in)
+        d2h = N_SEQ * sum(t.numel() * t.element_size() for t in host_out)
+        e2e = {"value": round(step_flops * n_e2e / (float(e_ms) / 1e3) / 1e12, 2),
+               "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "note": "per micro-batch: H2D q,k,v,dO from pinned host; D2H o,dq,dk,dv; "
+                       "shard plan + attention through the public API"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_sus, peak_kind = _peaks()
+    bwd_flops = 10.0 * d * hq * my_pairs * args.steps
+    fwd_flops = 4.0 * d * hq * my_pairs * args.steps
+    dom = ("attn_bwd", bwd_flops, bwd_ms) if bwd_ms >= fwd_ms else ("attn_fwd", fwd_flops, fwd_ms)
+    achieved = dom[1] / (dom[2] / 1e3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(wk["name"], {}).get(dom[0])
+    line = {
+        "metric": "doc-masked attn TFLOP/s/GPU & CP rank imbalance (max/mean) at CP=1/2/4/8",
+        "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": wk["name"], "seq_len": T, "sequences_per_step": N_SEQ,
+                   "heads": [hq, hkv], "head_dim": d, "cp": cp, "policy": "adaptive",
+                   "strategies": strategies, "l2": "inputs > L2 (256 MiB per tensor)",
+                   "parallelism": f"cp{cp}"},
+        "tflops_per_gpu": round(value / world, 2),
+        "frac_of_peak": round(value / world / peak, 4),
+        "imbalance": round(imbalance, 4),
+        "pair_imbalance": round(pair_imb, 5),
+        "rank_kernel_ms": [round(float(x), 3) for x in kt],
+        "fwd_ms": round(fwd_ms, 3), "bwd_ms": round(bwd_ms, 3),
+        "roofline": {"kernel": dom[0], "bound": "tensor", "achieved": round(achieved, 1),
+                     "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                     "peak_kind": f"{peak_kind} burst bf16 (sustained {peak_sus})",
+                     "traffic": traffic,
+                     "flops_basis": "10*D*Hq*pairs (bwd) / 4*D*Hq*pairs (fwd) per launch"},
+        "gpu_launches": launches[0],
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        tflops, done, secs = _cpu_sample(lengths, 1, d, budget_s=15.0)
+        line["cpu_baseline"] = {
+            "value": round(tflops, 4), "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"head 0 of synthetic sequences {done} ({secs:.1f} s): per_document shard "
+                      "+ torch-CPU fp32 doc-prefix attention fwd+bwd (oracle)"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

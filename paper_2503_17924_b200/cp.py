@@ -1,0 +1,132 @@
+"""Context-parallel document-masked attention across ranks (one process per GPU).
+
+The paper's CP exchange (`PAPER.md:102,425`; absent from the reference, which
+folds it into W_l, `SPEC.md:335`): each rank owns T/cp tokens chosen by the
+shard builder (per-sequence or per-document, selected per micro-batch).
+
+  forward : all-gather local K,V (bf16, NCCL over NVLink)  -> rank-contiguous
+            buffer -> scatter rows to document order (wlb_rows_scatter) ->
+            doc-prefix attention for the local queries.
+  backward: attention backward -> full-length fp32 dK/dV partials -> gather
+            rows to rank-contiguous order (wlb_rows_gather) -> NCCL
+            reduce-scatter (sum) -> local dK/dV.
+
+`gather_index` of the micro-batch (ranks concatenated) is exactly the
+all-gather output order, so one index serves both permutations.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from . import _native
+from .attention import AttnTiles, attn_backward, attn_forward, build_tiles
+from .sharding import ShardPlan, build_shard_plan
+from .workload import CostProfile
+
+
+@dataclass
+class CPShard:
+    """Everything one rank needs for one micro-batch."""
+
+    plan: ShardPlan
+    index: int             # micro-batch index inside the plan
+    rank: int
+    cp: int
+    tiles: AttnTiles
+    gather_all: torch.Tensor   # [T] int32: all ranks' local rows -> global token
+    gather_local: torch.Tensor  # [T/cp] int32
+    pairs: int             # causal pairs of this rank (FLOP basis)
+
+    @property
+    def strategy(self):
+        return self.plan.strategy(self.index)
+
+
+def shard_for_rank(plan: ShardPlan, index: int, rank: int) -> CPShard:
+    lengths = plan.lengths[index]
+    g, pos, ro = plan.rank_local(index, rank)
+    T = sum(lengths)
+    lo = plan.tok_off[index]
+    tiles = build_tiles(ro, pos, lengths)
+    return CPShard(plan=plan, index=index, rank=rank, cp=plan.cp, tiles=tiles,
+                   gather_all=plan.gather_index[lo:lo + T], gather_local=g,
+                   pairs=int(plan.host("rank_pairs")[index, rank]))
+
+
+def build_cp_shards(microbatches, cp: int, rank: int, policy: str = "adaptive",
+                    profile: CostProfile | None = None) -> list[CPShard]:
+    """Shard + select every micro-batch of a step in one GPU launch, then cut
+    this rank's attention tiles."""
+    plan = build_shard_plan(microbatches, cp, policy, profile)
+    return [shard_for_rank(plan, b, rank) for b in range(plan.n_mb)]
+
+
+def _rows(fn, src, dst, index):
+    row_bytes = src[0].numel() * src.element_size()
+    _native.check(getattr(_native.lib(), fn)(src.data_ptr(), dst.data_ptr(), index.data_ptr(),
+                                             index.numel(), row_bytes, _native.stream_ptr()), fn)
+
+
+def gather_kv(k_local, v_local, shard: CPShard, group=None):
+    """All-gather local K/V and return them in document order [T, Hkv, D]."""
+    if shard.cp == 1:
+        return k_local, v_local
+    T = shard.gather_all.numel()
+    kv = torch.stack((k_local, v_local))                       # [2, Tl, Hkv, D]
+    gathered = torch.empty((shard.cp,) + tuple(kv.shape), dtype=kv.dtype, device=kv.device)
+    dist.all_gather_into_tensor(gathered, kv, group=group)
+    outs = []
+    for i in range(2):
+        src = gathered[:, i].reshape(T, *k_local.shape[1:])
+        dst = torch.empty_like(src)
+        _rows("wlb_rows_scatter", src.contiguous(), dst, shard.gather_all)
+        outs.append(dst)
+    return outs[0], outs[1]
+
+
+def scatter_dkv(dk_full, dv_full, shard: CPShard, group=None):
+    """Sum full-length fp32 dK/dV partials over ranks; return this rank's rows."""
+    if shard.cp == 1:
+        return dk_full, dv_full
+    T = dk_full.shape[0]
+    tl = T // shard.cp
+    both = torch.empty((shard.cp, 2, tl) + tuple(dk_full.shape[1:]), dtype=dk_full.dtype,
+                       device=dk_full.device)
+    for i, full in enumerate((dk_full, dv_full)):
+        perm = torch.empty_like(full)
+        _rows("wlb_rows_gather", full, perm, shard.gather_all)
+        both[:, i] = perm.view(shard.cp, tl, *full.shape[1:])
+    out = torch.empty((2, tl) + tuple(dk_full.shape[1:]), dtype=dk_full.dtype, device=dk_full.device)
+    dist.reduce_scatter_tensor(out, both, group=group)
+    return out[0], out[1]
+
+
+class CPDocAttention(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, q, k, v, shard: CPShard, group, scale):
+        k_full, v_full = gather_kv(k, v, shard, group)
+        o, lse = attn_forward(q, k_full, v_full, shard.tiles, scale)
+        ctx.save_for_backward(q, k_full, v_full, o, lse)
+        ctx.shard, ctx.group, ctx.scale = shard, group, scale
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k_full, v_full, o, lse = ctx.saved_tensors
+        dq, dk_full, dv_full = attn_backward(q, k_full, v_full, o, lse, do, ctx.shard.tiles,
+                                             ctx.scale)
+        dk, dv = scatter_dkv(dk_full, dv_full, ctx.shard, ctx.group)
+        return dq, dk.to(torch.bfloat16), dv.to(torch.bfloat16), None, None, None
+
+
+def cp_doc_attention(q, k, v, shard: CPShard, group=None, scale=None):
+    """Document-masked causal attention of this rank's local tokens.
+
+    q [T/cp, Hq, D], k/v [T/cp, Hkv, D] bf16 in the rank's local order
+    (`shard.gather_local`); returns O [T/cp, Hq, D] bf16.  Differentiable.
+    """
+    return CPDocAttention.apply(q, k, v, shard, group, scale)
