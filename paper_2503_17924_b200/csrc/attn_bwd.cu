@@ -1,25 +1,24 @@
 // Document-prefix causal attention, backward, on sm_100a tensor cores.
 //
 // Work item = (KV tile, KV head g): 128 consecutive keys of ONE document
-// (positions [k0, k0+128) of doc p) and every local query row of the
-// (rank, doc p) row-set that can see them (in-document position >= k0 -- a
-// suffix of the row-set, found by binary search), for every query head of
-// the GQA group.  Per query tile (<= 128 rows, one head):
+// (in-document positions [k0, k0+128)) and every local query row of the
+// (rank, doc) row-set that can see them (position >= k0: a suffix of the
+// row-set, found by binary search), for every query head of the GQA group.
+// The rows are walked in query tiles of BM = 64; per tile i:
 //
-//   S^T  = K Q^T          (TMEM, lanes = keys)        tcgen05 SS
-//   dP^T = V dO^T         (TMEM, lanes = keys)        tcgen05 SS
-//   P^T  = exp2(S^T*scale*log2e - LSE2[q]),  dS^T = P^T (dP^T - Delta[q])
-//          (compute warps, one key row per thread; P^T, dS^T -> SMEM bf16)
-//   dV  += P^T dO         (TMEM accumulator)          A K-major, B MN-major
-//   dK  += dS^T Q         (TMEM accumulator)
-//   dQ   = dS K           (TMEM, aliases S^T)         A MN-major (dS^T read
-//          transposed), B MN-major; drained by the compute warps into an
-//          fp32 accumulator with vector atomics.
+//   S^T  = K Q^T,  dP^T = V dO^T     TMEM, lanes = keys, double-buffered
+//   P^T  = exp2(S^T*scale*log2e - LSE2[q]);  dS^T = P^T (dP^T - Delta[q])
+//          (8 compute warps: key row = TMEM lane, 32 query columns each;
+//           P^T / dS^T -> SMEM bf16, double-buffered)
+//   dV  += P^T dO,  dK += dS^T Q     TMEM accumulators (A K-major, B MN-major)
+//   dQ^T = K^T dS^T                  TMEM, aliases S^T of the same buffer;
+//          drained by the compute warps with warp-coalesced fp32 reductions
+//          (lane = head-dim index, so each red covers 128 contiguous bytes).
 //
-// dK/dV are written once per work item (fp32 partials over the full
-// document-ordered sequence; the CP reduce-scatter sums them over ranks).
-// A preprocessing kernel computes Delta = rowsum(dO * O); a final kernel
-// converts the fp32 dQ accumulator to bf16.
+// The MMA warp issues S/dP for tile i+1 before the dV/dK/dQ group of tile i,
+// so the tensor pipe runs while the compute warps work on the previous tile.
+// dK/dV are written once per work item as fp32 partials over the full
+// document-ordered sequence (the CP reduce-scatter sums them over ranks).
 #include "common.cuh"
 #include "sm100.cuh"
 #include "tmap.cuh"
@@ -29,40 +28,46 @@
 namespace wlb {
 using namespace sm100;
 
-template <int D>
+template <int D, int NCW = 2>
 struct BwdCfg {
-  static constexpr int BM = 128, BN = 128;   // queries per tile, keys per tile
+  static_assert(NCW == 2, "two compute warpgroups (one 32-query half each)");
+  static constexpr int BM = 64, BN = 128;   // queries per tile, keys per tile
   static constexpr int SLABS = D / 64;
   static constexpr int KV_BYTES = BN * D * 2;
   static constexpr int Q_BYTES = BM * D * 2;
-  static constexpr int T_BYTES = BN * BM * 2;   // P^T / dS^T tiles
+  static constexpr int T_BYTES = BN * BM * 2;   // P^T / dS^T tile: 128 rows x 128 B
+  static constexpr int Q_SLAB = BM * 128, KV_SLAB = BN * 128;
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = OFF_K + KV_BYTES;
-  static constexpr int OFF_Q = OFF_V + KV_BYTES;
-  static constexpr int OFF_DO = OFF_Q + Q_BYTES;
-  static constexpr int OFF_P = OFF_DO + Q_BYTES;
-  static constexpr int OFF_DS = OFF_P + T_BYTES;
-  static constexpr int OFF_VEC = OFF_DS + T_BYTES;          // 2 x {lse2, delta, pos}[BM]
+  static constexpr int OFF_Q = OFF_V + KV_BYTES;        // 2 stages
+  static constexpr int OFF_DO = OFF_Q + 2 * Q_BYTES;    // 2 stages
+  static constexpr int OFF_P = OFF_DO + 2 * Q_BYTES;    // 2 buffers
+  static constexpr int OFF_DS = OFF_P + 2 * T_BYTES;    // 2 buffers
+  static constexpr int OFF_VEC = OFF_DS + 2 * T_BYTES;  // 2 x {lse2, delta, pos-k0}[BM]
   static constexpr int OFF_BAR = OFF_VEC + 2 * 3 * BM * 4;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr uint32_t TMEM_COLS = 512;
-  static constexpr uint32_t COL_S = 0;          // S^T, later dQ
-  static constexpr uint32_t COL_DP = 128;
+  static constexpr uint32_t COL_S = 0;      // S^T[b] at b*64 (later dQ^T[b])
+  static constexpr uint32_t COL_DP = 128;   // dP^T[b] at 128 + b*64
   static constexpr uint32_t COL_DV = 256;
   static constexpr uint32_t COL_DK = 256 + D;
   static constexpr uint32_t IDESC_ST = idesc_bf16(BN, BM, 0, 0);
   static constexpr uint32_t IDESC_ACC = idesc_bf16(BN, D, 0, 1);   // dV, dK
-  static constexpr uint32_t IDESC_DQ = idesc_bf16(BM, D, 1, 1);    // dQ
+  static constexpr uint32_t IDESC_DQT = idesc_bf16(D, BM, 1, 1);   // dQ^T
+  static constexpr int THREADS = 128 + 128 * NCW;
 };
 
 struct BwdBars {
-  uint64_t kv_full, q_full, q_empty, s_full, p_full, mma2_done, tmem_free;
+  uint64_t kv_full;
+  uint64_t q_full[2], q_empty[2];
+  uint64_t s_full[2], p_full[2], mma2_done[2], s_free[2];
+  uint64_t vec_full[2], vec_empty[2];
   uint32_t tmem_base;
 };
 
 // kv_tiles[2i] = {kv_begin (global), kv_len, row_first, row_end}, kv_tiles[2i+1].x = k0
-template <int D>
-__global__ void __launch_bounds__(256, 1)
+template <int D, int NCW>
+__global__ void __launch_bounds__(128 + 128 * NCW, 1)
 attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                 const float* __restrict__ lse, const float* __restrict__ delta,
@@ -70,16 +75,16 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const int4* __restrict__ kv_tiles, const int* __restrict__ n_kv_tiles,
                 const int* __restrict__ positions, int Tl, int Hq, int Hkv, float scale,
                 float scale_log2) {
-  using C = BwdCfg<D>;
+  using C = BwdCfg<D, NCW>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int item = blockIdx.x / Hkv, g = blockIdx.x % Hkv;
   if (item >= n_kv_tiles[0]) return;
   const int4 kt = kv_tiles[2 * item];
-  const int k0 = kv_tiles[2 * item + 1].x;   // in-document position of the first key
+  const int k0 = kv_tiles[2 * item + 1].x;   // in-document position of key 0 of the tile
   const int group = Hq / Hkv;
-  const int q_tiles_per_head = (kt.w - kt.z + C::BM - 1) / C::BM;
-  const int n_iter = q_tiles_per_head * group;
+  const int qt_per_head = (kt.w - kt.z + C::BM - 1) / C::BM;
+  const int n_iter = qt_per_head * group;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   BwdBars* bars = reinterpret_cast<BwdBars*>(smem + C::OFF_BAR);
@@ -93,12 +98,16 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
 
   if (threadIdx.x == 0) {
     mbar_init(&bars->kv_full, 1);
-    mbar_init(&bars->q_full, 1);
-    mbar_init(&bars->q_empty, 1);
-    mbar_init(&bars->s_full, 1);
-    mbar_init(&bars->p_full, 128);
-    mbar_init(&bars->mma2_done, 1);
-    mbar_init(&bars->tmem_free, 128);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->q_full[i], 1);
+      mbar_init(&bars->q_empty[i], 1);
+      mbar_init(&bars->s_full[i], 1);
+      mbar_init(&bars->p_full[i], 128 * NCW);
+      mbar_init(&bars->mma2_done[i], 1);
+      mbar_init(&bars->s_free[i], 128 * NCW);
+      mbar_init(&bars->vec_full[i], 32);
+      mbar_init(&bars->vec_empty[i], 128 * NCW);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(&bars->tmem_base, C::TMEM_COLS);
@@ -116,17 +125,19 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       tma_prefetch(&tmDO);
       mbar_expect_tx(&bars->kv_full, 2 * C::KV_BYTES);
       for (int s = 0; s < C::SLABS; ++s) {
-        tma_load_3d(sK + s * C::BN * 128, &tmK, &bars->kv_full, s * 64, g, kt.x);
-        tma_load_3d(sV + s * C::BN * 128, &tmV, &bars->kv_full, s * 64, g, kt.x);
+        tma_load_3d(sK + s * C::KV_SLAB, &tmK, &bars->kv_full, s * 64, g, kt.x);
+        tma_load_3d(sV + s * C::KV_SLAB, &tmV, &bars->kv_full, s * 64, g, kt.x);
       }
       for (int i = 0; i < n_iter; ++i) {
-        const int h = g * group + i / q_tiles_per_head;
-        const int row = kt.z + (i % q_tiles_per_head) * C::BM;
-        mbar_wait(&bars->q_empty, (i & 1) ^ 1);
-        mbar_expect_tx(&bars->q_full, 2 * C::Q_BYTES);
+        const int st = i & 1;
+        const int h = g * group + i / qt_per_head;
+        const int row = kt.z + (i % qt_per_head) * C::BM;
+        mbar_wait(&bars->q_empty[st], ((i >> 1) & 1) ^ 1);
+        mbar_expect_tx(&bars->q_full[st], 2 * C::Q_BYTES);
         for (int s = 0; s < C::SLABS; ++s) {
-          tma_load_3d(sQ + s * C::BM * 128, &tmQ, &bars->q_full, s * 64, h, row);
-          tma_load_3d(sDO + s * C::BM * 128, &tmDO, &bars->q_full, s * 64, h, row);
+          tma_load_3d(sQ + st * C::Q_BYTES + s * C::Q_SLAB, &tmQ, &bars->q_full[st], s * 64, h, row);
+          tma_load_3d(sDO + st * C::Q_BYTES + s * C::Q_SLAB, &tmDO, &bars->q_full[st], s * 64, h,
+                      row);
         }
       }
     }
@@ -136,132 +147,149 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       const uint32_t k_b = smem_u32(sK), v_b = smem_u32(sV), q_b = smem_u32(sQ),
                      do_b = smem_u32(sDO), p_b = smem_u32(sP), ds_b = smem_u32(sDS);
       mbar_wait(&bars->kv_full, 0);
-      for (int i = 0; i < n_iter; ++i) {
-        mbar_wait(&bars->q_full, i & 1);
-        if (i > 0) mbar_wait(&bars->tmem_free, (i - 1) & 1);
-        tc_fence_after();
+      for (int i = 0; i <= n_iter; ++i) {
+        if (i < n_iter) {
+          const int b = i & 1;
+          mbar_wait(&bars->q_full[b], (i >> 1) & 1);
+          if (i >= 2) mbar_wait(&bars->s_free[b], ((i - 2) >> 1) & 1);
+          tc_fence_after();
+          const uint32_t qs = q_b + b * C::Q_BYTES, dos = do_b + b * C::Q_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {   // contraction over D: K-major both
-          const uint32_t ko = (kk >> 2) * C::BN * 128 + (kk & 3) * 32;
-          const uint32_t qo = (kk >> 2) * C::BM * 128 + (kk & 3) * 32;
-          mma_ss(tmem + C::COL_S, sdesc_sw128(k_b + ko, 16, 1024), sdesc_sw128(q_b + qo, 16, 1024),
-                 C::IDESC_ST, kk > 0);
-          mma_ss(tmem + C::COL_DP, sdesc_sw128(v_b + ko, 16, 1024),
-                 sdesc_sw128(do_b + qo, 16, 1024), C::IDESC_ST, kk > 0);
+          for (int kk = 0; kk < D / 16; ++kk) {   // contract over D: K-major both
+            const uint32_t ko = (kk >> 2) * C::KV_SLAB + (kk & 3) * 32;
+            const uint32_t qo = (kk >> 2) * C::Q_SLAB + (kk & 3) * 32;
+            mma_ss(tmem + C::COL_S + b * 64, sdesc_sw128(k_b + ko, 16, 1024),
+                   sdesc_sw128(qs + qo, 16, 1024), C::IDESC_ST, kk > 0);
+            mma_ss(tmem + C::COL_DP + b * 64, sdesc_sw128(v_b + ko, 16, 1024),
+                   sdesc_sw128(dos + qo, 16, 1024), C::IDESC_ST, kk > 0);
+          }
+          mma_commit(&bars->s_full[b]);
         }
-        mma_commit(&bars->s_full);
-        mbar_wait(&bars->p_full, i & 1);
-        tc_fence_after();
+        if (i >= 1) {
+          const int j = i - 1, b = j & 1;
+          mbar_wait(&bars->p_full[b], (j >> 1) & 1);
+          tc_fence_after();
+          const uint32_t qs = q_b + b * C::Q_BYTES, dos = do_b + b * C::Q_BYTES;
+          const uint32_t ps = p_b + b * C::T_BYTES, dss = ds_b + b * C::T_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < C::BM / 16; ++kk) {   // contraction over queries
-          const uint32_t to = (kk >> 2) * C::BN * 128 + (kk & 3) * 32;   // P^T / dS^T K-major
-          const uint32_t mo = kk * 16 * 128;                             // Q / dO MN-major
-          const uint32_t acc = (i > 0) || (kk > 0);
-          mma_ss(tmem + C::COL_DV, sdesc_sw128(p_b + to, 16, 1024),
-                 sdesc_sw128(do_b + mo, C::BM * 128, 1024), C::IDESC_ACC, acc);
-          mma_ss(tmem + C::COL_DK, sdesc_sw128(ds_b + to, 16, 1024),
-                 sdesc_sw128(q_b + mo, C::BM * 128, 1024), C::IDESC_ACC, acc);
-        }
+          for (int kk = 0; kk < C::BM / 16; ++kk) {   // contract over queries
+            const uint32_t acc = (j > 0) || (kk > 0);
+            mma_ss(tmem + C::COL_DV, sdesc_sw128(ps + kk * 32, 16, 1024),
+                   sdesc_sw128(dos + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
+            mma_ss(tmem + C::COL_DK, sdesc_sw128(dss + kk * 32, 16, 1024),
+                   sdesc_sw128(qs + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
+          }
 #pragma unroll
-        for (int kk = 0; kk < C::BN / 16; ++kk) {   // contraction over keys
-          const uint32_t o = kk * 16 * 128;
-          mma_ss(tmem + C::COL_S, sdesc_sw128(ds_b + o, C::BN * 128, 1024),
-                 sdesc_sw128(k_b + o, C::BN * 128, 1024), C::IDESC_DQ, kk > 0);
+          for (int kk = 0; kk < C::BN / 16; ++kk) {   // contract over keys
+            mma_ss(tmem + C::COL_S + b * 64, sdesc_sw128(k_b + kk * 2048, C::KV_SLAB, 1024),
+                   sdesc_sw128(dss + kk * 2048, C::KV_SLAB, 1024), C::IDESC_DQT, kk > 0);
+          }
+          mma_commit(&bars->mma2_done[b]);
+          mma_commit(&bars->q_empty[b]);
         }
-        mma_commit(&bars->mma2_done);
-        mma_commit(&bars->q_empty);
       }
+    }
+  } else if (warp == 3) {
+    // ------------------------------------------------- per-query vectors --
+    for (int i = 0; i < n_iter; ++i) {
+      const int b = i & 1;
+      const int h = g * group + i / qt_per_head;
+      const int row0 = kt.z + (i % qt_per_head) * C::BM;
+      mbar_wait(&bars->vec_empty[b], ((i >> 1) & 1) ^ 1);
+      float* vec = sVec + b * 3 * C::BM;
+#pragma unroll
+      for (int e = lane; e < C::BM; e += 32) {
+        const int row = row0 + e;
+        const bool ok = row < kt.w;
+        vec[e] = ok ? lse[(size_t)h * Tl + row] * 1.4426950408889634f : 0.f;
+        vec[C::BM + e] = ok ? delta[(size_t)h * Tl + row] : 0.f;
+        reinterpret_cast<int*>(vec)[2 * C::BM + e] = ok ? positions[row] - k0 : -1;
+      }
+      mbar_arrive(&bars->vec_full[b]);
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------- compute --
-    const int wq = warp & 3;
-    const int t = wq * 32 + lane;                 // key row (S^T lanes) / query row (dQ lanes)
-    const uint32_t lane_base = tmem + ((uint32_t)(wq * 32) << 16);
-    const bool key_ok = t < kt.y;                 // key t of the tile lies inside the document
-    for (int i = 0; i < n_iter; ++i) {
-      const int h = g * group + i / q_tiles_per_head;
-      const int row0 = kt.z + (i % q_tiles_per_head) * C::BM;
-      float* vec = sVec + (i & 1) * 3 * C::BM;
-      {
-        const int row = row0 + t;
-        const bool ok = row < kt.w;
-        vec[t] = ok ? lse[(size_t)h * Tl + row] * 1.4426950408889634f : 0.f;
-        vec[C::BM + t] = ok ? delta[(size_t)h * Tl + row] : 0.f;
-        reinterpret_cast<int*>(vec)[2 * C::BM + t] = ok ? positions[row] - k0 : -1;
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      mbar_wait(&bars->s_full, i & 1);
+    const int lg = warp & 3;                 // TMEM lane quarter
+    const int ch = (warp - 4) >> 2;          // which 32-column half of the 64 queries
+    const int t = lg * 32 + lane;            // key row in the tile
+    const bool key_ok = t < kt.y;
+    const uint32_t lane_base = tmem + ((uint32_t)(lg * 32) << 16);
+
+    auto drain = [&](int j) {                // dQ^T of tile j -> fp32 accumulator
+      const int b = j & 1;
+      const int h = g * group + j / qt_per_head;
+      const int row0 = kt.z + (j % qt_per_head) * C::BM + ch * 32;
+      mbar_wait(&bars->mma2_done[b], (j >> 1) & 1);
       tc_fence_after();
+      uint32_t u[32];
+      tmem_ld32(lane_base + C::COL_S + b * 64 + ch * 32, u);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&bars->s_free[b]);
+      // dQ^T lanes are head-dim rows: D=128 -> d = t; D=64 (M=64 layout) -> lanes 0-15 of each quarter
+      const int d = D == 128 ? t : lg * 16 + lane;
+      if (D == 128 || lane < 16) {
+        float* base = dq_acc + ((size_t)row0 * Hq + h) * D + d;
+        const int nvalid = min(32, kt.w - row0);
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          if (q < nvalid) atomicAdd(base + (size_t)q * Hq * D, __uint_as_float(u[q]) * scale);
+      }
+    };
+
+    for (int i = 0; i < n_iter; ++i) {
+      const int b = i & 1;
+      mbar_wait(&bars->vec_full[b], (i >> 1) & 1);
+      mbar_wait(&bars->s_full[b], (i >> 1) & 1);
+      tc_fence_after();
+      uint32_t us[32], ud[32];
+      tmem_ld32(lane_base + C::COL_S + b * 64 + ch * 32, us);
+      tmem_ld32(lane_base + C::COL_DP + b * 64 + ch * 32, ud);
+      const float* vec = sVec + b * 3 * C::BM + ch * 32;
       const float* vl = vec;
       const float* vd = vec + C::BM;
       const int* vp = reinterpret_cast<const int*>(vec + 2 * C::BM);
-      uint32_t pk[C::BM / 2], dk2[C::BM / 2];
+      tmem_ld_wait();
+      uint32_t pk[16], dk2[16];
 #pragma unroll
-      for (int c = 0; c < C::BM / 32; ++c) {
-        uint32_t us[32], ud[32];
-        tmem_ld32(lane_base + C::COL_S + c * 32, us);
-        tmem_ld32(lane_base + C::COL_DP + c * 32, ud);
-        tmem_ld_wait();
+      for (int e = 0; e < 32; e += 2) {
+        float pp[2], dd[2];
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float pp[2], dd[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int q = c * 32 + e + u;
-            const bool allowed = key_ok && vp[q] >= t;   // key pos k0+t <= query pos
-            const float p = allowed ? ex2(__uint_as_float(us[e + u]) * scale_log2 - vl[q]) : 0.f;
-            pp[u] = p;
-            dd[u] = p * (__uint_as_float(ud[e + u]) - vd[q]);
-          }
-          pk[(c * 32 + e) / 2] = pack_bf16(pp[0], pp[1]);
-          dk2[(c * 32 + e) / 2] = pack_bf16(dd[0], dd[1]);
+        for (int u = 0; u < 2; ++u) {
+          const int q = e + u;
+          const bool allowed = key_ok && vp[q] >= t;   // key position k0+t <= query position
+          const float p = allowed ? ex2(__uint_as_float(us[q]) * scale_log2 - vl[q]) : 0.f;
+          pp[u] = p;
+          dd[u] = p * (__uint_as_float(ud[q]) - vd[q]);
         }
+        pk[e / 2] = pack_bf16(pp[0], pp[1]);
+        dk2[e / 2] = pack_bf16(dd[0], dd[1]);
       }
-      // previous MMA group (readers of sP / sdS) completed before the dQ drain of i-1
-      uint8_t* prow = sP + t * 128;
-      uint8_t* drow = sDS + t * 128;
+      tc_fence_before();
+      mbar_arrive(&bars->vec_empty[b]);
+      // buffer b was last read by the MMA group of tile i-2, drained at i-1
+      uint8_t* prow = sP + b * C::T_BYTES + t * 128;
+      uint8_t* drow = sDS + b * C::T_BYTES + t * 128;
 #pragma unroll
-      for (int c = 0; c < C::BM / 8; ++c) {
-        const int slab = c >> 3, cc = c & 7;
-        const int off = slab * C::BN * 128 + ((cc ^ (t & 7)) << 4);
+      for (int c = 0; c < 4; ++c) {
+        const int off = (((ch * 4 + c) ^ (t & 7)) << 4);
         *reinterpret_cast<uint4*>(prow + off) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
         *reinterpret_cast<uint4*>(drow + off) = make_uint4(dk2[4 * c], dk2[4 * c + 1], dk2[4 * c + 2], dk2[4 * c + 3]);
       }
       fence_proxy_async_smem();
-      tc_fence_before();
-      mbar_arrive(&bars->p_full);
-      // drain dQ (lanes = query rows of this tile)
-      mbar_wait(&bars->mma2_done, i & 1);
-      tc_fence_after();
-      const int qrow = row0 + t;
-      const bool q_ok = qrow < kt.w;
-      float4* dst = reinterpret_cast<float4*>(dq_acc + ((size_t)qrow * Hq + h) * D);
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t u[32];
-        tmem_ld32(lane_base + C::COL_S + c * 32, u);
-        tmem_ld_wait();
-        if (q_ok) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            atomicAdd(dst + c * 8 + e,
-                      make_float4(__uint_as_float(u[4 * e]) * scale, __uint_as_float(u[4 * e + 1]) * scale,
-                                  __uint_as_float(u[4 * e + 2]) * scale, __uint_as_float(u[4 * e + 3]) * scale));
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&bars->tmem_free);
+      mbar_arrive(&bars->p_full[b]);
+      if (i >= 1) drain(i - 1);
     }
+    drain(n_iter - 1);
     // ------------------------------------------------------------ epilogue --
-    // TMEM loads are warp-collective (.sync.aligned): issue them converged and
-    // predicate only the global stores on the key lying inside the document.
-    float* dvr = dv + ((size_t)(kt.x + t) * Hkv + g) * D;
-    float* dkr = dk + ((size_t)(kt.x + t) * Hkv + g) * D;
+    // TMEM loads are warp-collective: issue converged, predicate the stores.
+    float* dvr = dv + ((size_t)(kt.x + t) * Hkv + g) * D + ch * (D / 2);
+    float* dkr = dk + ((size_t)(kt.x + t) * Hkv + g) * D + ch * (D / 2);
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t a[32], b[32];
-      tmem_ld32(lane_base + C::COL_DV + c * 32, a);
-      tmem_ld32(lane_base + C::COL_DK + c * 32, b);
+    for (int c = 0; c < D / 64; ++c) {
+      uint32_t a[32], bb[32];
+      tmem_ld32(lane_base + C::COL_DV + ch * (D / 2) + c * 32, a);
+      tmem_ld32(lane_base + C::COL_DK + ch * (D / 2) + c * 32, bb);
       tmem_ld_wait();
       if (key_ok) {
 #pragma unroll
@@ -270,8 +298,8 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
               make_float4(__uint_as_float(a[4 * e]), __uint_as_float(a[4 * e + 1]),
                           __uint_as_float(a[4 * e + 2]), __uint_as_float(a[4 * e + 3]));
           reinterpret_cast<float4*>(dkr + c * 32)[e] =
-              make_float4(__uint_as_float(b[4 * e]) * scale, __uint_as_float(b[4 * e + 1]) * scale,
-                          __uint_as_float(b[4 * e + 2]) * scale, __uint_as_float(b[4 * e + 3]) * scale);
+              make_float4(__uint_as_float(bb[4 * e]) * scale, __uint_as_float(bb[4 * e + 1]) * scale,
+                          __uint_as_float(bb[4 * e + 2]) * scale, __uint_as_float(bb[4 * e + 3]) * scale);
         }
       }
     }
@@ -437,11 +465,11 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   if ((rc = make_thd_tmap(&tv, v, T, Hkv, D, C::BN))) return rc;
   static bool attr = false;
   if (!attr) {
-    WLB_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    WLB_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       C::SMEM));
     attr = true;
   }
-  attn_bwd_kernel<D><<<(unsigned)max_items * Hkv, 256, C::SMEM, stream>>>(
+  attn_bwd_kernel<D, 2><<<(unsigned)max_items * Hkv, C::THREADS, C::SMEM, stream>>>(
       tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq, Hkv,
       scale, scale * 1.4426950408889634f);
   WLB_LAUNCH_CHECK();
