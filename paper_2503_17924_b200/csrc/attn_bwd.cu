@@ -229,11 +229,17 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       // dQ^T lanes are head-dim rows: D=128 -> d = t; D=64 (M=64 layout) -> lanes 0-15 of each quarter
       const int d = D == 128 ? t : lg * 16 + lane;
       if (D == 128 || lane < 16) {
-        float* base = dq_acc + ((size_t)row0 * Hq + h) * D + d;
+        float* ptr = dq_acc + ((size_t)row0 * Hq + h) * D + d;
+        const size_t stride = (size_t)Hq * D;
         const int nvalid = min(32, kt.w - row0);
+        if (nvalid == 32) {
 #pragma unroll
-        for (int q = 0; q < 32; ++q)
-          if (q < nvalid) atomicAdd(base + (size_t)q * Hq * D, __uint_as_float(u[q]) * scale);
+          for (int q = 0; q < 32; ++q, ptr += stride) atomicAdd(ptr, __uint_as_float(u[q]) * scale);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q, ptr += stride)
+            if (q < nvalid) atomicAdd(ptr, __uint_as_float(u[q]) * scale);
+        }
       }
     };
 
@@ -246,24 +252,40 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       tmem_ld32(lane_base + C::COL_S + b * 64 + ch * 32, us);
       tmem_ld32(lane_base + C::COL_DP + b * 64 + ch * 32, ud);
       const float* vec = sVec + b * 3 * C::BM + ch * 32;
-      const float* vl = vec;
-      const float* vd = vec + C::BM;
-      const int* vp = reinterpret_cast<const int*>(vec + 2 * C::BM);
+      const float4* vl4 = reinterpret_cast<const float4*>(vec);
+      const float4* vd4 = reinterpret_cast<const float4*>(vec + C::BM);
+      const int4* vp4 = reinterpret_cast<const int4*>(vec + 2 * C::BM);
+      // Unmasked fast path: every query of this half sees every key of the tile
+      // (rows are position-sorted, so the first and last columns bound them).
+      const bool full = kt.y == C::BN && vp4[0].x >= C::BN - 1 && vp4[7].w >= C::BN - 1;
       tmem_ld_wait();
       uint32_t pk[16], dk2[16];
 #pragma unroll
-      for (int e = 0; e < 32; e += 2) {
-        float pp[2], dd[2];
+      for (int e4 = 0; e4 < 8; ++e4) {
+        const float4 l4 = vl4[e4], d4 = vd4[e4];
+        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
+        float pp[4], dd[4];
+        if (full) {
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int q = e + u;
-          const bool allowed = key_ok && vp[q] >= t;   // key position k0+t <= query position
-          const float p = allowed ? ex2(__uint_as_float(us[q]) * scale_log2 - vl[q]) : 0.f;
-          pp[u] = p;
-          dd[u] = p * (__uint_as_float(ud[q]) - vd[q]);
+          for (int u = 0; u < 4; ++u) {
+            pp[u] = ex2(fmaf(__uint_as_float(us[4 * e4 + u]), scale_log2, -lv[u]));
+            dd[u] = pp[u] * (__uint_as_float(ud[4 * e4 + u]) - dv4[u]);
+          }
+        } else {
+          const int4 p4 = vp4[e4];
+          const int pv[4] = {p4.x, p4.y, p4.z, p4.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const bool allowed = key_ok && pv[u] >= t;   // key position k0+t <= query position
+            const float x = fmaf(__uint_as_float(us[4 * e4 + u]), scale_log2, -lv[u]);
+            pp[u] = allowed ? ex2(x) : 0.f;
+            dd[u] = pp[u] * (__uint_as_float(ud[4 * e4 + u]) - dv4[u]);
+          }
         }
-        pk[e / 2] = pack_bf16(pp[0], pp[1]);
-        dk2[e / 2] = pack_bf16(dd[0], dd[1]);
+        pk[2 * e4] = pack_bf16(pp[0], pp[1]);
+        pk[2 * e4 + 1] = pack_bf16(pp[2], pp[3]);
+        dk2[2 * e4] = pack_bf16(dd[0], dd[1]);
+        dk2[2 * e4 + 1] = pack_bf16(dd[2], dd[3]);
       }
       tc_fence_before();
       mbar_arrive(&bars->vec_empty[b]);

@@ -15,7 +15,7 @@ ap.add_argument("--batch", type=int, default=1)
 ap.add_argument("--hq", type=int, default=32)
 ap.add_argument("--hkv", type=int, default=32)
 ap.add_argument("--d", type=int, default=128)
-ap.add_argument("--iters", type=int, default=3)
+ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--single", action="store_true")
 a = ap.parse_args()
 lengths = [d.length for d in wl.generate_synthetic_stream(wl.SyntheticSpec(a.T, a.T), 0, a.batch + 1)[a.batch]]
@@ -30,6 +30,7 @@ k = torch.randn(a.T, a.hkv, a.d, device=dev, dtype=torch.bfloat16)
 v = torch.randn_like(k)
 do = torch.randn_like(q)
 pairs = sum(x * (x + 1) // 2 for x in lengths)
+fs, bs = [], []
 for it in range(a.iters):
     e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     e[0].record()
@@ -38,6 +39,9 @@ for it in range(a.iters):
     dq, dk, dv = attn_backward(q, k, v, o, lse, do, tiles)
     e[2].record()
     torch.cuda.synchronize()
-    f, b = e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2])
-    print(f"docs={len(lengths)} fwd {f:.3f} ms {4*a.d*a.hq*pairs/f/1e9:.0f} TF/s | "
-          f"bwd {b:.3f} ms {10*a.d*a.hq*pairs/b/1e9:.0f} TF/s")
+    fs.append(e[0].elapsed_time(e[1]))
+    bs.append(e[1].elapsed_time(e[2]))
+f, b = sorted(fs)[len(fs) // 2], sorted(bs)[len(bs) // 2]
+print(f"docs={len(lengths)} maxdoc={max(lengths)} median of {a.iters}: fwd {f:.3f} ms "
+      f"{4*a.d*a.hq*pairs/f/1e9:.0f} TF/s | bwd {b:.3f} ms {10*a.d*a.hq*pairs/b/1e9:.0f} TF/s "
+      f"(min {min(bs):.3f} max {max(bs):.3f})")
