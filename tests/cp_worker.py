@@ -1,0 +1,76 @@
+"""torchrun worker: CP document-masked attention fwd+bwd across ranks (NCCL) vs
+the unsharded fp32 oracle.  Launched by tests/test_cp_multi.py (or by hand):
+
+    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tests/cp_worker.py
+"""
+
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2503_17924_b200 as wl  # noqa: E402
+from paper_2503_17924_b200.cp import cp_doc_attention, shard_for_rank  # noqa: E402
+from oracle import attention_oracle as ao  # noqa: E402
+from oracle import shard_oracle as so  # noqa: E402
+
+
+def check(name, got, ref, atol=2e-2, rtol=1e-2):
+    """Elementwise |got - ref| <= atol + rtol*|ref| (see tests/test_gpu_attention.py)."""
+    got, ref = got.float().cpu(), ref.float()
+    err = (got - ref).abs()
+    ok = bool((err <= atol + rtol * ref.abs()).all())
+    return ok, f"{name}: max abs err {err.max().item():.3e} (ref max {ref.abs().max().item():.2f})"
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    failures = []
+    cases = [([700, 3, 129, 2000, 1, 257, 64], "per_document", 4, 2, 128),
+             ([700, 3, 129, 2000, 1, 257, 64], "per_sequence", 4, 4, 64),
+             ([1500, 500], "adaptive", 8, 2, 128)]
+    for lengths, policy, hq, hkv, d in cases:
+        lengths = so.pad_lengths_for_cp(lengths, world)
+        T = sum(lengths)
+        g = torch.Generator().manual_seed(7)
+        q = torch.randn(T, hq, d, generator=g).bfloat16()
+        k = torch.randn(T, hkv, d, generator=g).bfloat16()
+        v = torch.randn(T, hkv, d, generator=g).bfloat16()
+        do = torch.randn(T, hq, d, generator=g).bfloat16()
+        plan = wl.build_shard_plan([lengths], world, policy)
+        shard = shard_for_rank(plan, 0, rank)
+        idx = shard.gather_local.long().cpu()
+        ql = q[idx].to(dev).requires_grad_(True)
+        kl = k[idx].to(dev).requires_grad_(True)
+        vl = v[idx].to(dev).requires_grad_(True)
+        o = cp_doc_attention(ql, kl, vl, shard)
+        o.backward(do[idx].to(dev))
+        torch.cuda.synchronize()
+        full = [(p, 0, x) for p, x in enumerate(lengths)]
+        ro, _, rdq, rdk, rdv = ao.segment_attention_fwd_bwd(q, k, v, do, lengths, full)
+        for name, got, ref in (("o", o, ro[idx]), ("dq", ql.grad, rdq[idx]),
+                               ("dk", kl.grad, rdk[idx]), ("dv", vl.grad, rdv[idx])):
+            ok, msg = check(name, got, ref)
+            tag = f"[rank {rank} {policy} {shard.strategy.value} hq={hq} hkv={hkv} d={d}] {msg}"
+            print(tag, flush=True)
+            if not ok:
+                failures.append(tag)
+    dist.barrier()
+    dist.destroy_process_group()
+    if failures:
+        print("FAIL", failures, flush=True)
+        sys.exit(1)
+    print(f"rank {rank}: CP OK", flush=True)
+
+
+if __name__ == "__main__":
+    main()
