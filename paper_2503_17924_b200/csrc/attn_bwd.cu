@@ -39,13 +39,16 @@ struct BwdCfg {
   static constexpr int Q_SLAB = BM * 128, KV_SLAB = BN * 128;
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = OFF_K + KV_BYTES;
-  static constexpr int OFF_Q = OFF_V + KV_BYTES;        // 2 stages
-  static constexpr int OFF_DO = OFF_Q + 2 * Q_BYTES;    // 2 stages
-  static constexpr int OFF_P = OFF_DO + 2 * Q_BYTES;    // 2 buffers
+  static constexpr int QS = 3;                          // Q/dO + query-vector ring depth
+  static constexpr int OFF_Q = OFF_V + KV_BYTES;        // QS stages
+  static constexpr int OFF_DO = OFF_Q + QS * Q_BYTES;   // QS stages
+  static constexpr int OFF_P = OFF_DO + QS * Q_BYTES;   // 2 buffers
   static constexpr int OFF_DS = OFF_P + 2 * T_BYTES;    // 2 buffers
-  static constexpr int OFF_VEC = OFF_DS + 2 * T_BYTES;  // 2 x {lse2, delta, pos-k0}[BM]
-  static constexpr int OFF_BAR = OFF_VEC + 2 * 3 * BM * 4;
-  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr int OFF_VEC = OFF_DS + 2 * T_BYTES;  // QS x {lse2, delta, pos-k0}[BM]
+  static constexpr int OFF_BAR = OFF_VEC + QS * 3 * BM * 4;
+  // The dynamic-SMEM window starts 1024-B aligned on sm_100 (checked at run
+  // time), so no alignment slack is reserved: D = 128 uses 226.4 KB of 227.
+  static constexpr int SMEM = OFF_BAR + 256;
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr uint32_t COL_S = 0;      // S^T[b] at b*64 (later dQ^T[b])
   static constexpr uint32_t COL_DP = 128;   // dP^T[b] at 128 + b*64
@@ -57,11 +60,11 @@ struct BwdCfg {
   static constexpr int THREADS = 128 + 128 * NCW;
 };
 
-struct BwdBars {
+struct BwdBars {  // 172 bytes; OFF_BAR reserves 256
   uint64_t kv_full;
-  uint64_t q_full[2], q_empty[2];
+  uint64_t q_full[3], q_empty[3];
   uint64_t s_full[2], p_full[2], mma2_done[2], s_free[2];
-  uint64_t vec_full[2], vec_empty[2];
+  uint64_t vec_full[3], vec_empty[3];
   uint32_t tmem_base;
 };
 
@@ -77,7 +80,8 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 float scale_log2) {
   using C = BwdCfg<D, NCW>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  if (smem_u32(smem_raw) & 1023) __trap();   // SW128 tiles need 1024-B alignment
+  uint8_t* smem = smem_raw;
   const int item = blockIdx.x / Hkv, g = blockIdx.x % Hkv;
   if (item >= n_kv_tiles[0]) return;
   const int4 kt = kv_tiles[2 * item];
@@ -98,15 +102,17 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
 
   if (threadIdx.x == 0) {
     mbar_init(&bars->kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < C::QS; ++i) {
       mbar_init(&bars->q_full[i], 1);
       mbar_init(&bars->q_empty[i], 1);
+      mbar_init(&bars->vec_full[i], 32);
+      mbar_init(&bars->vec_empty[i], 128 * NCW);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->s_full[i], 1);
       mbar_init(&bars->p_full[i], 128 * NCW);
       mbar_init(&bars->mma2_done[i], 1);
       mbar_init(&bars->s_free[i], 128 * NCW);
-      mbar_init(&bars->vec_full[i], 32);
-      mbar_init(&bars->vec_empty[i], 128 * NCW);
     }
     fence_mbar_init();
   }
@@ -129,10 +135,10 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         tma_load_3d(sV + s * C::KV_SLAB, &tmV, &bars->kv_full, s * 64, g, kt.x);
       }
       for (int i = 0; i < n_iter; ++i) {
-        const int st = i & 1;
+        const int st = i % C::QS;
         const int h = g * group + i / qt_per_head;
         const int row = kt.z + (i % qt_per_head) * C::BM;
-        mbar_wait(&bars->q_empty[st], ((i >> 1) & 1) ^ 1);
+        mbar_wait(&bars->q_empty[st], ((i / C::QS) & 1) ^ 1);
         mbar_expect_tx(&bars->q_full[st], 2 * C::Q_BYTES);
         for (int s = 0; s < C::SLABS; ++s) {
           tma_load_3d(sQ + st * C::Q_BYTES + s * C::Q_SLAB, &tmQ, &bars->q_full[st], s * 64, h, row);
@@ -149,11 +155,11 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       mbar_wait(&bars->kv_full, 0);
       for (int i = 0; i <= n_iter; ++i) {
         if (i < n_iter) {
-          const int b = i & 1;
-          mbar_wait(&bars->q_full[b], (i >> 1) & 1);
+          const int b = i & 1, st = i % C::QS;
+          mbar_wait(&bars->q_full[st], (i / C::QS) & 1);
           if (i >= 2) mbar_wait(&bars->s_free[b], ((i - 2) >> 1) & 1);
           tc_fence_after();
-          const uint32_t qs = q_b + b * C::Q_BYTES, dos = do_b + b * C::Q_BYTES;
+          const uint32_t qs = q_b + st * C::Q_BYTES, dos = do_b + st * C::Q_BYTES;
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {   // contract over D: K-major both
             const uint32_t ko = (kk >> 2) * C::KV_SLAB + (kk & 3) * 32;
@@ -166,10 +172,10 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
           mma_commit(&bars->s_full[b]);
         }
         if (i >= 1) {
-          const int j = i - 1, b = j & 1;
+          const int j = i - 1, b = j & 1, st = j % C::QS;
           mbar_wait(&bars->p_full[b], (j >> 1) & 1);
           tc_fence_after();
-          const uint32_t qs = q_b + b * C::Q_BYTES, dos = do_b + b * C::Q_BYTES;
+          const uint32_t qs = q_b + st * C::Q_BYTES, dos = do_b + st * C::Q_BYTES;
           const uint32_t ps = p_b + b * C::T_BYTES, dss = ds_b + b * C::T_BYTES;
 #pragma unroll
           for (int kk = 0; kk < C::BM / 16; ++kk) {   // contract over queries
@@ -185,17 +191,17 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                    sdesc_sw128(dss + kk * 2048, C::KV_SLAB, 1024), C::IDESC_DQT, kk > 0);
           }
           mma_commit(&bars->mma2_done[b]);
-          mma_commit(&bars->q_empty[b]);
+          mma_commit(&bars->q_empty[st]);
         }
       }
     }
   } else if (warp == 3) {
     // ------------------------------------------------- per-query vectors --
     for (int i = 0; i < n_iter; ++i) {
-      const int b = i & 1;
+      const int b = i % C::QS;
       const int h = g * group + i / qt_per_head;
       const int row0 = kt.z + (i % qt_per_head) * C::BM;
-      mbar_wait(&bars->vec_empty[b], ((i >> 1) & 1) ^ 1);
+      mbar_wait(&bars->vec_empty[b], ((i / C::QS) & 1) ^ 1);
       float* vec = sVec + b * 3 * C::BM;
 #pragma unroll
       for (int e = lane; e < C::BM; e += 32) {
@@ -244,14 +250,14 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     };
 
     for (int i = 0; i < n_iter; ++i) {
-      const int b = i & 1;
-      mbar_wait(&bars->vec_full[b], (i >> 1) & 1);
+      const int b = i & 1, vb = i % C::QS;
+      mbar_wait(&bars->vec_full[vb], (i / C::QS) & 1);
       mbar_wait(&bars->s_full[b], (i >> 1) & 1);
       tc_fence_after();
       uint32_t us[32], ud[32];
       tmem_ld32(lane_base + C::COL_S + b * 64 + ch * 32, us);
       tmem_ld32(lane_base + C::COL_DP + b * 64 + ch * 32, ud);
-      const float* vec = sVec + b * 3 * C::BM + ch * 32;
+      const float* vec = sVec + vb * 3 * C::BM + ch * 32;
       const float4* vl4 = reinterpret_cast<const float4*>(vec);
       const float4* vd4 = reinterpret_cast<const float4*>(vec + C::BM);
       const int4* vp4 = reinterpret_cast<const int4*>(vec + 2 * C::BM);
@@ -288,7 +294,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         dk2[2 * e4 + 1] = pack_bf16(dd[2], dd[3]);
       }
       tc_fence_before();
-      mbar_arrive(&bars->vec_empty[b]);
+      mbar_arrive(&bars->vec_empty[vb]);
       // buffer b was last read by the MMA group of tile i-2, drained at i-1
       uint8_t* prow = sP + b * C::T_BYTES + t * 128;
       uint8_t* drow = sDS + b * C::T_BYTES + t * 128;
