@@ -57,7 +57,7 @@ struct BwdCfg {
   static constexpr uint32_t IDESC_ST = idesc_bf16(BN, BM, 0, 0);
   static constexpr uint32_t IDESC_ACC = idesc_bf16(BN, D, 0, 1);   // dV, dK
   static constexpr uint32_t IDESC_DQT = idesc_bf16(D, BM, 1, 1);   // dQ^T
-  static constexpr int THREADS = 128 + 128 * NCW;
+  static constexpr int THREADS = 128 + 128 * NCW + 128;   // + dQ drain warpgroup
 };
 
 struct BwdBars {  // 172 bytes; OFF_BAR reserves 256
@@ -70,7 +70,7 @@ struct BwdBars {  // 172 bytes; OFF_BAR reserves 256
 
 // kv_tiles[2i] = {kv_begin (global), kv_len, row_first, row_end}, kv_tiles[2i+1].x = k0
 template <int D, int NCW>
-__global__ void __launch_bounds__(128 + 128 * NCW, 1)
+__global__ void __launch_bounds__(256 + 128 * NCW, 1)
 attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                 const float* __restrict__ lse, const float* __restrict__ delta,
@@ -112,7 +112,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       mbar_init(&bars->s_full[i], 1);
       mbar_init(&bars->p_full[i], 128 * NCW);
       mbar_init(&bars->mma2_done[i], 1);
-      mbar_init(&bars->s_free[i], 128 * NCW);
+      mbar_init(&bars->s_free[i], 128);
     }
     fence_mbar_init();
   }
@@ -213,6 +213,41 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       }
       mbar_arrive(&bars->vec_full[b]);
     }
+  } else if (warp >= 4 + 4 * NCW) {
+    // ------------------------------------------------------------ dQ drain --
+    // dQ^T lanes are head-dim rows (lane = d for D = 128; for D = 64 the M=64
+    // accumulator uses lanes 0-15 of each quarter).  Each warp-wide RED covers
+    // 32 consecutive floats of one query row.  Kept off the compute warps so
+    // their proxy fences never wait on outstanding global reductions.
+    const int lg = warp & 3;
+    const uint32_t lane_base = tmem + ((uint32_t)(lg * 32) << 16);
+    const int d = D == 128 ? lg * 32 + lane : lg * 16 + lane;
+    const size_t stride = (size_t)Hq * D;
+    for (int j = 0; j < n_iter; ++j) {
+      const int b = j & 1;
+      const int h = g * group + j / qt_per_head;
+      const int row0 = kt.z + (j % qt_per_head) * C::BM;
+      mbar_wait(&bars->mma2_done[b], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t u[64];
+      tmem_ld32(lane_base + C::COL_S + b * 64, *reinterpret_cast<uint32_t(*)[32]>(u));
+      tmem_ld32(lane_base + C::COL_S + b * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&bars->s_free[b]);
+      if (D == 128 || lane < 16) {
+        float* ptr = dq_acc + ((size_t)row0 * Hq + h) * D + d;
+        const int nvalid = min(C::BM, kt.w - row0);
+        if (nvalid == C::BM) {
+#pragma unroll
+          for (int q = 0; q < C::BM; ++q, ptr += stride) atomicAdd(ptr, __uint_as_float(u[q]) * scale);
+        } else {
+#pragma unroll
+          for (int q = 0; q < C::BM; ++q, ptr += stride)
+            if (q < nvalid) atomicAdd(ptr, __uint_as_float(u[q]) * scale);
+        }
+      }
+    }
   } else if (warp >= 4) {
     // ------------------------------------------------------------- compute --
     const int lg = warp & 3;                 // TMEM lane quarter
@@ -220,34 +255,6 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     const int t = lg * 32 + lane;            // key row in the tile
     const bool key_ok = t < kt.y;
     const uint32_t lane_base = tmem + ((uint32_t)(lg * 32) << 16);
-
-    auto drain = [&](int j) {                // dQ^T of tile j -> fp32 accumulator
-      const int b = j & 1;
-      const int h = g * group + j / qt_per_head;
-      const int row0 = kt.z + (j % qt_per_head) * C::BM + ch * 32;
-      mbar_wait(&bars->mma2_done[b], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t u[32];
-      tmem_ld32(lane_base + C::COL_S + b * 64 + ch * 32, u);
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&bars->s_free[b]);
-      // dQ^T lanes are head-dim rows: D=128 -> d = t; D=64 (M=64 layout) -> lanes 0-15 of each quarter
-      const int d = D == 128 ? t : lg * 16 + lane;
-      if (D == 128 || lane < 16) {
-        float* ptr = dq_acc + ((size_t)row0 * Hq + h) * D + d;
-        const size_t stride = (size_t)Hq * D;
-        const int nvalid = min(32, kt.w - row0);
-        if (nvalid == 32) {
-#pragma unroll
-          for (int q = 0; q < 32; ++q, ptr += stride) atomicAdd(ptr, __uint_as_float(u[q]) * scale);
-        } else {
-#pragma unroll
-          for (int q = 0; q < 32; ++q, ptr += stride)
-            if (q < nvalid) atomicAdd(ptr, __uint_as_float(u[q]) * scale);
-        }
-      }
-    };
 
     for (int i = 0; i < n_iter; ++i) {
       const int b = i & 1, vb = i % C::QS;
@@ -306,9 +313,12 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       }
       fence_proxy_async_smem();
       mbar_arrive(&bars->p_full[b]);
-      if (i >= 1) drain(i - 1);
     }
-    drain(n_iter - 1);
+    {   // the last MMA group wrote the final dV / dK
+      const int j = n_iter - 1;
+      mbar_wait(&bars->mma2_done[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+    }
     // ------------------------------------------------------------ epilogue --
     // TMEM loads are warp-collective: issue converged, predicate the stores.
     float* dvr = dv + ((size_t)(kt.x + t) * Hkv + g) * D + ch * (D / 2);
