@@ -124,32 +124,32 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer --
-    if (lane == 0) {
+    {   // whole warp; one elected lane issues
       tma_prefetch(&tmQ);
       tma_prefetch(&tmK);
       tma_prefetch(&tmV);
       tma_prefetch(&tmDO);
-      mbar_expect_tx(&bars->kv_full, 2 * C::KV_BYTES);
+      mbar_expect_tx_w(&bars->kv_full, 2 * C::KV_BYTES);
       for (int s = 0; s < C::SLABS; ++s) {
-        tma_load_3d(sK + s * C::KV_SLAB, &tmK, &bars->kv_full, s * 64, g, kt.x);
-        tma_load_3d(sV + s * C::KV_SLAB, &tmV, &bars->kv_full, s * 64, g, kt.x);
+        tma_load_3d_w(sK + s * C::KV_SLAB, &tmK, &bars->kv_full, s * 64, g, kt.x);
+        tma_load_3d_w(sV + s * C::KV_SLAB, &tmV, &bars->kv_full, s * 64, g, kt.x);
       }
       for (int i = 0; i < n_iter; ++i) {
         const int st = i % C::QS;
         const int h = g * group + i / qt_per_head;
         const int row = kt.z + (i % qt_per_head) * C::BM;
         mbar_wait(&bars->q_empty[st], ((i / C::QS) & 1) ^ 1);
-        mbar_expect_tx(&bars->q_full[st], 2 * C::Q_BYTES);
+        mbar_expect_tx_w(&bars->q_full[st], 2 * C::Q_BYTES);
         for (int s = 0; s < C::SLABS; ++s) {
-          tma_load_3d(sQ + st * C::Q_BYTES + s * C::Q_SLAB, &tmQ, &bars->q_full[st], s * 64, h, row);
-          tma_load_3d(sDO + st * C::Q_BYTES + s * C::Q_SLAB, &tmDO, &bars->q_full[st], s * 64, h,
+          tma_load_3d_w(sQ + st * C::Q_BYTES + s * C::Q_SLAB, &tmQ, &bars->q_full[st], s * 64, h, row);
+          tma_load_3d_w(sDO + st * C::Q_BYTES + s * C::Q_SLAB, &tmDO, &bars->q_full[st], s * 64, h,
                       row);
         }
       }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer --
-    if (lane == 0) {
+    {   // whole warp; one elected lane issues
       const uint32_t k_b = smem_u32(sK), v_b = smem_u32(sV), q_b = smem_u32(sQ),
                      do_b = smem_u32(sDO), p_b = smem_u32(sP), ds_b = smem_u32(sDS);
       mbar_wait(&bars->kv_full, 0);
@@ -164,12 +164,12 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
           for (int kk = 0; kk < D / 16; ++kk) {   // contract over D: K-major both
             const uint32_t ko = (kk >> 2) * C::KV_SLAB + (kk & 3) * 32;
             const uint32_t qo = (kk >> 2) * C::Q_SLAB + (kk & 3) * 32;
-            mma_ss(tmem + C::COL_S + b * 64, sdesc_sw128(k_b + ko, 16, 1024),
+            mma_ss_w(tmem + C::COL_S + b * 64, sdesc_sw128(k_b + ko, 16, 1024),
                    sdesc_sw128(qs + qo, 16, 1024), C::IDESC_ST, kk > 0);
-            mma_ss(tmem + C::COL_DP + b * 64, sdesc_sw128(v_b + ko, 16, 1024),
+            mma_ss_w(tmem + C::COL_DP + b * 64, sdesc_sw128(v_b + ko, 16, 1024),
                    sdesc_sw128(dos + qo, 16, 1024), C::IDESC_ST, kk > 0);
           }
-          mma_commit(&bars->s_full[b]);
+          mma_commit_w(&bars->s_full[b]);
         }
         if (i >= 1) {
           const int j = i - 1, b = j & 1, st = j % C::QS;
@@ -180,18 +180,18 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
 #pragma unroll
           for (int kk = 0; kk < C::BM / 16; ++kk) {   // contract over queries
             const uint32_t acc = (j > 0) || (kk > 0);
-            mma_ss(tmem + C::COL_DV, sdesc_sw128(ps + kk * 32, 16, 1024),
+            mma_ss_w(tmem + C::COL_DV, sdesc_sw128(ps + kk * 32, 16, 1024),
                    sdesc_sw128(dos + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
-            mma_ss(tmem + C::COL_DK, sdesc_sw128(dss + kk * 32, 16, 1024),
+            mma_ss_w(tmem + C::COL_DK, sdesc_sw128(dss + kk * 32, 16, 1024),
                    sdesc_sw128(qs + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
           }
 #pragma unroll
           for (int kk = 0; kk < C::BN / 16; ++kk) {   // contract over keys
-            mma_ss(tmem + C::COL_S + b * 64, sdesc_sw128(k_b + kk * 2048, C::KV_SLAB, 1024),
+            mma_ss_w(tmem + C::COL_S + b * 64, sdesc_sw128(k_b + kk * 2048, C::KV_SLAB, 1024),
                    sdesc_sw128(dss + kk * 2048, C::KV_SLAB, 1024), C::IDESC_DQT, kk > 0);
           }
-          mma_commit(&bars->mma2_done[b]);
-          mma_commit(&bars->q_empty[st]);
+          mma_commit_w(&bars->mma2_done[b]);
+          mma_commit_w(&bars->q_empty[st]);
         }
       }
     }

@@ -98,32 +98,32 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer --
-    if (lane == 0) {
+    {   // whole warp; one elected lane issues
       tma_prefetch(&tmQ);
       tma_prefetch(&tmK);
       tma_prefetch(&tmV);
-      mbar_expect_tx(&bars->q_full, C::Q_BYTES);
+      mbar_expect_tx_w(&bars->q_full, C::Q_BYTES);
       for (int s = 0; s < C::SLABS; ++s)
-        tma_load_3d(sQ + s * C::BM * 128, &tmQ, &bars->q_full, s * 64, h, tile.x);
+        tma_load_3d_w(sQ + s * C::BM * 128, &tmQ, &bars->q_full, s * 64, h, tile.x);
       for (int j = 0; j < n_kv; ++j) {
         const int st = j % C::STAGES;
         const uint32_t ph = (j / C::STAGES) & 1;
         const int row = tile.z + j * C::BN;
         mbar_wait(&bars->k_empty[st], ph ^ 1);
-        mbar_expect_tx(&bars->k_full[st], C::KV_BYTES);
+        mbar_expect_tx_w(&bars->k_full[st], C::KV_BYTES);
         for (int s = 0; s < C::SLABS; ++s)
-          tma_load_3d(sK + st * C::KV_BYTES + s * C::BN * 128, &tmK, &bars->k_full[st], s * 64,
+          tma_load_3d_w(sK + st * C::KV_BYTES + s * C::BN * 128, &tmK, &bars->k_full[st], s * 64,
                       kvh, row);
         mbar_wait(&bars->v_empty[st], ph ^ 1);
-        mbar_expect_tx(&bars->v_full[st], C::KV_BYTES);
+        mbar_expect_tx_w(&bars->v_full[st], C::KV_BYTES);
         for (int s = 0; s < C::SLABS; ++s)
-          tma_load_3d(sV + st * C::KV_BYTES + s * C::BN * 128, &tmV, &bars->v_full[st], s * 64,
+          tma_load_3d_w(sV + st * C::KV_BYTES + s * C::BN * 128, &tmV, &bars->v_full[st], s * 64,
                       kvh, row);
       }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer --
-    if (lane == 0) {
+    {   // whole warp; one elected lane issues
       const uint32_t q_base = smem_u32(sQ), k_base = smem_u32(sK), v_base = smem_u32(sV),
                      p_base = smem_u32(sP);
       mbar_wait(&bars->q_full, 0);
@@ -138,11 +138,11 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t off = (kk >> 2) * C::BM * 128 + (kk & 3) * 32;
             const uint32_t koff = (kk >> 2) * C::BN * 128 + (kk & 3) * 32;
-            mma_ss(s_tmem, sdesc_sw128(q_base + off, 16, 1024),
+            mma_ss_w(s_tmem, sdesc_sw128(q_base + off, 16, 1024),
                    sdesc_sw128(k_base + st * C::KV_BYTES + koff, 16, 1024), C::IDESC_QK, kk > 0);
           }
-          mma_commit(&bars->s_full[j & 1]);
-          mma_commit(&bars->k_empty[st]);
+          mma_commit_w(&bars->s_full[j & 1]);
+          mma_commit_w(&bars->k_empty[st]);
         }
         if (j >= 1) {
           const int jj = j - 1, st = jj % C::STAGES;
@@ -153,11 +153,11 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
           for (int kk = 0; kk < C::BN / 16; ++kk) {
             const uint32_t poff = (kk >> 2) * C::BM * 128 + (kk & 3) * 32;
             const uint32_t voff = st * C::KV_BYTES + kk * 16 * 128;
-            mma_ss(tmem + C::COL_O, sdesc_sw128(p_base + poff, 16, 1024),
+            mma_ss_w(tmem + C::COL_O, sdesc_sw128(p_base + poff, 16, 1024),
                    sdesc_sw128(v_base + voff, C::BN * 128, 1024), C::IDESC_PV, (jj > 0) || (kk > 0));
           }
-          mma_commit(&bars->pv_done);
-          mma_commit(&bars->v_empty[st]);
+          mma_commit_w(&bars->pv_done);
+          mma_commit_w(&bars->v_empty[st]);
         }
       }
     }
