@@ -78,12 +78,15 @@ int wlb_kernel_latency_sum(const int64_t* q_lens, const int64_t* kv_lens, int64_
                            int64_t tile, const int64_t* curve_q, const double* curve_v,
                            int32_t n_curve, double op_scale, double* out, void* stream);
 
-/* Attention work list for one rank: query tiles of <= block_m rows cut from
- * each (rank, doc) row-set, back-aligned (optimal for the doc-prefix cost),
- * sorted by descending KV extent.  rowset_off[n_docs+1], positions[rows] and
+/* Attention work list for one rank: query tiles of <= 128 rows cut from each
+ * (rank, doc) row-set, back-aligned (optimal for the doc-prefix cost), paired
+ * from the end of the row-set (a pair shares K/V tiles) and sorted by
+ * descending KV extent.  rowset_off[n_docs+1], positions[rows] and
  * doc_start[n_docs+1] (global KV offsets) are device arrays.
- * tiles[2*max_tiles][4]: the first n_tiles[0] rows receive {row0, nrows,
- * kv_begin, kv_end}; the second half is scratch. */
+ * tiles[4*max_tiles][4] int32: item i occupies rows 2i, 2i+1 =
+ * {rowX0, nrowsX, kv_begin, kv_endX}, {rowY0, nrowsY, kv_endY, 0} (X is the
+ * later tile; nrowsY = 0 when unpaired); the second half is scratch.
+ * n_tiles[0] receives the item count.  block_m must be 128. */
 int wlb_attn_tiles(int32_t n_docs, const int32_t* rowset_off, const int32_t* positions,
                    const int32_t* doc_start, int32_t block_m, int32_t max_tiles,
                    int32_t* tiles, int32_t* n_tiles, void* stream);
@@ -91,7 +94,7 @@ int wlb_attn_tiles(int32_t n_docs, const int32_t* rowset_off, const int32_t* pos
 /* Document-prefix causal attention forward, tcgen05/TMEM/TMA on sm_100a.
  * q[Tl][Hq][D], k/v[T][Hkv][D] bf16 (document order), o[Tl][Hq][D] bf16,
  * lse[Hq][Tl] fp32 (natural-log logsumexp of scaled scores).
- * Row i attends keys [kv_begin, kv_begin + positions[i] + 1) of its tile.
+ * Row i attends keys [kv_begin, kv_begin + positions[i] + 1) of its item.
  * D in {64, 128}; Hq % Hkv == 0. */
 int wlb_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
                  const int32_t* tiles, const int32_t* n_tiles, int32_t max_tiles,

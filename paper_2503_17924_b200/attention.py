@@ -23,8 +23,8 @@ BLOCK_M = 128
 class AttnTiles:
     """Query-tile work list of one rank (device)."""
 
-    tiles: torch.Tensor       # [2*max_tiles, 4] int32 (second half is scratch)
-    n_tiles: torch.Tensor     # [1] int32
+    tiles: torch.Tensor       # [4*max_tiles, 4] int32: 2 rows per tile pair, then scratch
+    n_tiles: torch.Tensor     # [1] int32 (number of tile pairs)
     max_tiles: int
     positions: torch.Tensor   # [Tl] int32
     rowset_off: torch.Tensor  # [n_docs+1] int32
@@ -44,8 +44,8 @@ def build_tiles(rowset_off: torch.Tensor, positions: torch.Tensor, doc_lengths,
         starts.append(starts[-1] + int(x))
     doc_start = torch.tensor(starts, dtype=torch.int32, device=dev)
     tl = positions.numel()
-    max_tiles = tl // block_m + n_docs + 1
-    tiles = torch.empty((2 * max_tiles, 4), dtype=torch.int32, device=dev)
+    max_tiles = tl // (2 * block_m) + n_docs + 1
+    tiles = torch.empty((4 * max_tiles, 4), dtype=torch.int32, device=dev)
     n_tiles = torch.empty(1, dtype=torch.int32, device=dev)
     p = _native.ptr
     _native.check(_native.lib().wlb_attn_tiles(

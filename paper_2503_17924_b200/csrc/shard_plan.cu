@@ -253,46 +253,62 @@ __global__ void kernel_latency_sum_kernel(const long long* q, const long long* k
 }
 
 // ---------------------------------------------------------------------------
-// Attention tile list.  Row-set (rank, doc) rows are sorted by in-document
-// position; a tile's cost is its KV extent (last row position + 1).  Because
-// the optimal cost f(i) of tiling the first i rows is non-decreasing in i,
-// f(i) = f(i - BM) + cost(last tile): back-aligned tiling (partial tile first)
-// is optimal.  Tiles are then counting-sorted by descending KV extent so the
-// persistent attention kernels schedule longest-first (LPT).
+// Attention work list.  Row-set (rank, doc) rows are sorted by in-document
+// position; a query tile's cost is its KV extent (last row position + 1).
+// Because the optimal cost f(i) of tiling the first i rows is non-decreasing
+// in i, f(i) = f(i - BM) + cost(last tile): back-aligned tiling (partial tile
+// first) is optimal.  Adjacent tiles of a row-set are then paired from the
+// end -- a pair shares every K/V tile of the shorter member -- and the pairs
+// are counting-sorted by descending KV extent so the persistent-style grid
+// schedules longest-first (LPT).
+//   item[2i]   = {rowX0, nrowsX, kv_begin, kv_endX}   X = later tile (longer KV)
+//   item[2i+1] = {rowY0, nrowsY, kv_endY, 0}          Y = earlier tile, nrowsY may be 0
 constexpr int kTileThreads = 1024;
 constexpr int kTileBins = 2048;
 
 __global__ void __launch_bounds__(kTileThreads)
 attn_tiles_kernel(int nd, const int* __restrict__ rowset_off, const int* __restrict__ positions,
-                  const int* __restrict__ doc_start, int bm, int max_tiles, int4* __restrict__ tiles,
-                  int* __restrict__ n_tiles, int4* __restrict__ scratch) {
+                  const int* __restrict__ doc_start, int bm, int max_items, int4* __restrict__ items,
+                  int* __restrict__ n_items, int4* __restrict__ scratch) {
   __shared__ long long warp_tot[kTileThreads / 32 + 1];
   __shared__ int hist[kTileBins];
   __shared__ int kv_shift_s;
-  // pass 1: tile count per doc -> offsets; emit unsorted tiles into scratch
+  // pass 1: pair count per doc -> offsets; emit unsorted pairs into scratch
   long long carry = 0;
   for (int base = 0; base < nd; base += blockDim.x) {
     int p = base + threadIdx.x;
     int rows = p < nd ? rowset_off[p + 1] - rowset_off[p] : 0;
     int nt = (rows + bm - 1) / bm;
+    int npairs = (nt + 1) / 2;
     long long tot;
-    long long off = carry + block_exclusive_scan(nt, warp_tot, &tot);
+    long long off = carry + block_exclusive_scan(npairs, warp_tot, &tot);
     if (p < nd) {
       const int r0 = rowset_off[p], r1 = rowset_off[p + 1];
-      for (int t = 0; t < nt; ++t) {
-        int end = r1 - (nt - 1 - t) * bm;       // back-aligned
-        int beg = end - bm > r0 ? end - bm : r0;
-        int kv_end = doc_start[p] + positions[end - 1] + 1;
-        if (off + t < max_tiles) scratch[off + t] = make_int4(beg, end - beg, doc_start[p], kv_end);
+      for (int k = 0; k < npairs; ++k) {
+        // tiles counted from the end: X = tile nt-1-2k, Y = tile nt-2-2k (if any)
+        const int endX = r1 - 2 * k * bm;
+        const int begX = endX - bm > r0 ? endX - bm : r0;
+        const int kvX = doc_start[p] + positions[endX - 1] + 1;
+        int begY = begX, nY = 0, kvY = 0;
+        if (begX > r0) {
+          const int endY = begX;
+          begY = endY - bm > r0 ? endY - bm : r0;
+          nY = endY - begY;
+          kvY = doc_start[p] + positions[endY - 1] + 1;
+        }
+        if (off + k < max_items) {
+          scratch[2 * (off + k)] = make_int4(begX, endX - begX, doc_start[p], kvX);
+          scratch[2 * (off + k) + 1] = make_int4(begY, nY, kvY, 0);
+        }
       }
     }
     carry += tot;
   }
-  const int total = carry < max_tiles ? (int)carry : max_tiles;
+  const int total = carry < max_items ? (int)carry : max_items;
   // pass 2: counting sort by descending KV extent (in 128-key blocks)
   int max_ext = 0;
   for (int i = threadIdx.x; i < total; i += blockDim.x)
-    max_ext = max(max_ext, (scratch[i].w - scratch[i].z + 127) >> 7);
+    max_ext = max(max_ext, (scratch[2 * i].w - scratch[2 * i].z + 127) >> 7);
   for (int o = 16; o; o >>= 1) max_ext = max(max_ext, __shfl_xor_sync(0xffffffffu, max_ext, o));
   if (threadIdx.x == 0) kv_shift_s = 0;
   __syncthreads();
@@ -303,23 +319,22 @@ attn_tiles_kernel(int nd, const int* __restrict__ rowset_off, const int* __restr
   for (int i = threadIdx.x; i < kTileBins; i += blockDim.x) hist[i] = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < total; i += blockDim.x) {
-    int key = kTileBins - 1 - (((scratch[i].w - scratch[i].z + 127) >> 7) >> shift);
+    int key = kTileBins - 1 - (((scratch[2 * i].w - scratch[2 * i].z + 127) >> 7) >> shift);
     atomicAdd(&hist[key], 1);
   }
   __syncthreads();
-  // exclusive scan of the histogram (2 bins per thread)
   long long a0 = hist[2 * threadIdx.x], a1 = hist[2 * threadIdx.x + 1], tot;
   long long ex = block_exclusive_scan(a0 + a1, warp_tot, &tot);
   hist[2 * threadIdx.x] = (int)ex;
   hist[2 * threadIdx.x + 1] = (int)(ex + a0);
   __syncthreads();
-  // stable scatter: one thread walks each bin's members in order (bins are tiny)
   for (int i = threadIdx.x; i < total; i += blockDim.x) {
-    int key = kTileBins - 1 - (((scratch[i].w - scratch[i].z + 127) >> 7) >> shift);
+    int key = kTileBins - 1 - (((scratch[2 * i].w - scratch[2 * i].z + 127) >> 7) >> shift);
     int slot = atomicAdd(&hist[key], 1);
-    tiles[slot] = scratch[i];
+    items[2 * slot] = scratch[2 * i];
+    items[2 * slot + 1] = scratch[2 * i + 1];
   }
-  if (threadIdx.x == 0) n_tiles[0] = total;
+  if (threadIdx.x == 0) n_items[0] = total;
 }
 
 }  // namespace wlb
@@ -362,15 +377,15 @@ extern "C" int wlb_kernel_latency_sum(const int64_t* q_lens, const int64_t* kv_l
   return WLB_OK;
 }
 
-// Scratch for the unsorted tiles lives right after the sorted array.
+// Scratch for the unsorted items lives right after the sorted array.
 extern "C" int wlb_attn_tiles(int32_t n_docs, const int32_t* rowset_off, const int32_t* positions,
                               const int32_t* doc_start, int32_t block_m, int32_t max_tiles,
                               int32_t* tiles, int32_t* n_tiles, void* stream) {
-  WLB_REQUIRE(block_m == 64 || block_m == 128, "block_m must be 64 or 128");
+  WLB_REQUIRE(block_m == 128, "block_m must be 128");
   WLB_REQUIRE(n_docs >= 0 && max_tiles >= 1, "bad arguments");
   attn_tiles_kernel<<<1, kTileThreads, 0, (cudaStream_t)stream>>>(
       n_docs, rowset_off, positions, doc_start, block_m, max_tiles, (int4*)tiles, n_tiles,
-      (int4*)tiles + max_tiles);
+      (int4*)tiles + 2 * (size_t)max_tiles);
   WLB_LAUNCH_CHECK();
   return WLB_OK;
 }

@@ -120,14 +120,17 @@ def test_attention_tiles_cover_rows_once():
         g, pos, ro = plan.rank_local(0, w)
         t = build_tiles(ro, pos, lengths)
         n = int(t.n_tiles.item())
-        tiles = t.tiles[:n].cpu().tolist()
+        items = t.tiles[:2 * n].cpu().view(n, 8).tolist()
         seen = torch.zeros(pos.numel(), dtype=torch.int32)
         ext = []
-        for row0, nrows, kvb, kve in tiles:
-            assert 1 <= nrows <= 128
-            seen[row0:row0 + nrows] += 1
-            p = pos[row0 + nrows - 1].item()
-            assert kve - kvb == p + 1
-            ext.append((kve - kvb + 127) // 128)
+        for rx, nx, kvb, kvx, ry, ny, kvy, _ in items:
+            assert 1 <= nx <= 128 and 0 <= ny <= 128
+            seen[rx:rx + nx] += 1
+            assert kvx - kvb == pos[rx + nx - 1].item() + 1
+            if ny:
+                assert ry + ny == rx                      # Y is the tile just before X
+                seen[ry:ry + ny] += 1
+                assert kvy - kvb == pos[ry + ny - 1].item() + 1 and kvy <= kvx
+            ext.append((kvx - kvb + 127) // 128)
         assert bool((seen == 1).all())
         assert ext == sorted(ext, reverse=True)   # longest first
