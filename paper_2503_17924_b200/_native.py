@@ -14,7 +14,9 @@ import os
 
 from .errors import NativeError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libwlbcp.so")
+# WLB_LIB_PATH selects an alternative build of the SAME library (A/B experiments).
+LIB_PATH = os.environ.get("WLB_LIB_PATH",
+                          os.path.join(os.path.dirname(os.path.abspath(__file__)), "libwlbcp.so"))
 
 WLB_OK, WLB_EINVAL, WLB_ENODEV, WLB_ECUDA = 0, 22, 19, 1000
 

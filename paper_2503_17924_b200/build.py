@@ -8,11 +8,12 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libwlbcp.so")
+OUT = os.environ.get("WLB_LIB_OUT", os.path.join(HERE, "libwlbcp.so"))
 SOURCES = ["abi.cu", "shard_plan.cu", "attn_fwd.cu", "attn_bwd.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+FLAGS += os.environ.get("WLB_NVCC_EXTRA", "").split()   # experiment switches (e.g. -DWLB_FWD_POLY=4)
 
 
 def build(verbose: bool = False) -> str:
@@ -23,7 +24,7 @@ def build(verbose: bool = False) -> str:
         return OUT
     objs = []
     for s in srcs:
-        o = os.path.join(CSRC, os.path.basename(s) + ".o")
+        o = OUT + "." + os.path.basename(s) + ".o"
         cmd = [NVCC, *FLAGS, "-c", s, "-o", o]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or r.returncode:

@@ -28,6 +28,10 @@
 #include "sm100.cuh"
 #include "tmap.cuh"
 
+#ifndef WLB_FWD_POLY
+#define WLB_FWD_POLY 8   // 0: MUFU only; k: one column pair in k uses the polynomial
+#endif
+
 namespace wlb {
 using namespace sm100;
 
@@ -189,45 +193,61 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       for (int j = 0; j < nkv; ++j) {
         mbar_wait(&bars->s_full[t], j & 1);
         tc_fence_after();
-        float s[C::BN];
+        // all 128 scores of this row in registers (one TMEM wait per tile:
+        // a chunked two-pass variant re-reading S measured ~40% slower)
+        float sv[C::BN];
 #pragma unroll
         for (int c = 0; c < C::BN / 32; ++c) {
           uint32_t u[32];
           tmem_ld32(s_col + c * 32, u);
-          tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(u[i]);
+          for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(u[i]);
         }
+        tmem_ld_wait();
         const int lim = lim0 - j * C::BN;
+        const bool full = __all_sync(0xffffffffu, lim >= C::BN);
         float mt = -INFINITY;
-        if (__all_sync(0xffffffffu, lim >= C::BN)) {
+        if (full) {
 #pragma unroll
-          for (int c = 0; c < C::BN; ++c) mt = fmaxf(mt, s[c]);
+          for (int c = 0; c < C::BN; ++c) mt = fmaxf(mt, sv[c]);
         } else {
 #pragma unroll
           for (int c = 0; c < C::BN; ++c) {
-            s[c] = c < lim ? s[c] : -INFINITY;
-            mt = fmaxf(mt, s[c]);
+            sv[c] = c < lim ? sv[c] : -INFINITY;
+            mt = fmaxf(mt, sv[c]);
           }
         }
         const float m_new = fmaxf(m_run, mt * scale_log2);
         const bool rescale = __any_sync(0xffffffffu, m_new > m_run + 8.f);
         const float m_use = rescale ? m_new : m_run;
         const float alpha = ex2(m_run - m_use);
+        // P = exp2(S*scale - m), written back as packed bf16 over the first 64
+        // columns of S (P chunk c lands in S columns [16c, 16c+16), already
+        // consumed).  Optionally one column pair in WLB_FWD_POLY takes the
+        // polynomial exp2 to offload the MUFU.
         float lsum = 0.f;
-        uint32_t p[C::BN / 2];
 #pragma unroll
-        for (int c = 0; c < C::BN / 2; ++c) {
-          const float p0 = ex2(fmaf(s[2 * c], scale_log2, -m_use));
-          const float p1 = ex2(fmaf(s[2 * c + 1], scale_log2, -m_use));
-          lsum += p0 + p1;
-          p[c] = pack_bf16(p0, p1);
+        for (int c = 0; c < C::BN / 32; ++c) {
+          uint32_t p[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int col = c * 32 + 2 * i;
+            const float x0 = fmaf(sv[col], scale_log2, -m_use);
+            const float x1 = fmaf(sv[col + 1], scale_log2, -m_use);
+            float p0, p1;
+            if (WLB_FWD_POLY && (i % (WLB_FWD_POLY > 0 ? WLB_FWD_POLY : 1)) == WLB_FWD_POLY - 1) {
+              p0 = ex2_poly(x0);
+              p1 = ex2_poly(x1);
+            } else {
+              p0 = ex2(x0);
+              p1 = ex2(x1);
+            }
+            lsum += p0 + p1;
+            p[i] = pack_bf16(p0, p1);
+          }
+          tmem_st16(s_col + c * 16, p);
         }
         l_run = l_run * alpha + lsum;
-        // P over the first 64 columns of S (S already consumed into registers;
-        // PV(j-1) finished before QK(j) wrote S, so no reader is pending).
-        tmem_st32(s_col, *reinterpret_cast<uint32_t(*)[32]>(p));
-        tmem_st32(s_col + 32, *reinterpret_cast<uint32_t(*)[32]>(p + 32));
         if (rescale && j > 0) {                // PV(j-1) complete (ordered before QK(j))
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
