@@ -42,10 +42,13 @@ N_SEQ = 8
 
 
 def _peaks():
+    """(burst, sustained, kind) dense bf16 TFLOP/s.  The attention kernels run
+    inside a long step (seconds of back-to-back tensor work under the 1 kW cap),
+    so the roofline denominator is the SUSTAINED figure; burst is reported too."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         p = json.load(open(path))
-        return p["bf16_tflops"], p.get("bf16_tflops_sustained"), "measured"
+        return p["bf16_tflops"], p.get("bf16_tflops_sustained") or p["bf16_tflops"], "measured"
     return 1590.0, 1400.0, "fallback"
 
 
@@ -213,14 +216,11 @@ def main():
     ev = lambda: torch.cuda.Event(enable_timing=True)
     launches = [0]
 
-    def step(record=None, ios=None, outs_host=None):
+    def step(record=None):
         shards = build_cp_shards(lengths, cp, rank, "adaptive")
         launches[0] += 1 + N_SEQ                                    # plan + tiles
         for b, sh in enumerate(shards):
             q, k, v, do = ins[b]
-            if ios is not None:                                     # e2e: H2D this step's inputs
-                for dst, src in zip(ins[b], ios):
-                    dst.copy_(src, non_blocking=True)
             k_full, v_full = gather_kv(k, v, sh, group)
             e = [ev() for _ in range(4)] if record is not None else None
             if e: e[0].record()
@@ -233,10 +233,6 @@ def main():
             launches[0] += 1 + 4 + (4 if cp > 1 else 0)
             if record is not None:
                 record.append((e, sh))
-            if outs_host is not None:                               # e2e: D2H the results
-                for src, dst in zip((o, dq, dk, dv), outs_host):
-                    dst.copy_(src if src.dtype == torch.bfloat16 else src.to(torch.bfloat16),
-                              non_blocking=True)
         return shards
 
     def barrier():
@@ -283,30 +279,69 @@ def main():
     strategies = [sh.strategy.value for sh in shards]
 
     # ------------------------------------------------------------------ e2e --
+    # The same step through the public API with host buffers: every step copies
+    # each micro-batch's q, k, v, dO from pinned host memory (H2D stream) and
+    # reads o, dq, dk, dv back (D2H stream); the copies are pipelined against
+    # compute across micro-batches with CUDA events.
     e2e = None
     if not args.no_e2e:
         pin = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t.cpu())
         host_in = [pin(t) for t in ins[0]]
-        host_out = [torch.empty((tl, hq, d), dtype=torch.bfloat16, pin_memory=True)] * 2 + \
-                   [torch.empty((tl, hkv, d), dtype=torch.bfloat16, pin_memory=True)] * 2
-        step(ios=host_in, outs_host=host_out)
+        host_out = [torch.empty((tl, hq, d), dtype=torch.bfloat16, pin_memory=True),
+                    torch.empty((tl, hq, d), dtype=torch.bfloat16, pin_memory=True),
+                    torch.empty((tl, hkv, d), dtype=torch.bfloat16, pin_memory=True),
+                    torch.empty((tl, hkv, d), dtype=torch.bfloat16, pin_memory=True)]
+        h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+        cur = torch.cuda.current_stream()
+
+        def e2e_step():
+            shards = build_cp_shards(lengths, cp, rank, "adaptive")
+            h2d_s.wait_stream(cur)             # previous step is done reading the inputs
+            ready = []
+            with torch.cuda.stream(h2d_s):
+                for b in range(N_SEQ):
+                    for dst, src in zip(ins[b], host_in):
+                        dst.copy_(src, non_blocking=True)
+                    e = torch.cuda.Event()
+                    e.record(h2d_s)
+                    ready.append(e)
+            for b, sh in enumerate(shards):
+                q, k, v, do = ins[b]
+                cur.wait_event(ready[b])
+                k_full, v_full = gather_kv(k, v, sh, group)
+                o, lse = attn_forward(q, k_full, v_full, sh.tiles)
+                dq, dk_full, dv_full = attn_backward(q, k_full, v_full, o, lse, do, sh.tiles)
+                dk, dv = scatter_dkv(dk_full, dv_full, sh, group)
+                outs = [o, dq, dk.to(torch.bfloat16), dv.to(torch.bfloat16)]
+                done = torch.cuda.Event()
+                done.record(cur)
+                d2h_s.wait_event(done)
+                with torch.cuda.stream(d2h_s):
+                    for src, dst in zip(outs, host_out):
+                        dst.copy_(src, non_blocking=True)
+                        src.record_stream(d2h_s)
+            cur.wait_stream(d2h_s)
+
+        e2e_step()
         barrier()
-        a, b = ev(), ev()
+        a, b_ = ev(), ev()
         n_e2e = max(1, min(args.steps, 3))
         a.record()
         for _ in range(n_e2e):
-            step(ios=host_in, outs_host=host_out)
-        b.record()
+            e2e_step()
+        b_.record()
         barrier()
-        e_ms = torch.tensor([a.elapsed_time(b)], device=dev, dtype=torch.float64)
+        e_ms = torch.tensor([a.elapsed_time(b_)], device=dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
         h2d = N_SEQ * sum(t.numel() * t.element_size() for t in host_in)
         d2h = N_SEQ * sum(t.numel() * t.element_size() for t in host_out)
         e2e = {"value": round(step_flops * n_e2e / (float(e_ms) / 1e3) / 1e12, 2),
                "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "note": "per micro-batch: H2D q,k,v,dO from pinned host; D2H o,dq,dk,dv; "
-                       "shard plan + attention through the public API"}
+               "ms_per_step": round(float(e_ms) / n_e2e, 2),
+               "note": "every micro-batch: H2D q,k,v,dO from pinned host, D2H o,dq,dk,dv "
+                       "(copy streams pipelined against compute); shard plan + attention "
+                       "through the public API"}
 
     if rank != 0:
         if world > 1:
@@ -332,14 +367,16 @@ def main():
                    "strategies": strategies, "l2": "inputs > L2 (256 MiB per tensor)",
                    "parallelism": f"cp{cp}"},
         "tflops_per_gpu": round(value / world, 2),
-        "frac_of_peak": round(value / world / peak, 4),
+        "frac_of_peak": round(value / world / peak_sus, 4),
+        "frac_of_burst_peak": round(value / world / peak, 4),
         "imbalance": round(imbalance, 4),
         "pair_imbalance": round(pair_imb, 5),
         "rank_kernel_ms": [round(float(x), 3) for x in kt],
         "fwd_ms": round(fwd_ms, 3), "bwd_ms": round(bwd_ms, 3),
         "roofline": {"kernel": dom[0], "bound": "tensor", "achieved": round(achieved, 1),
-                     "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                     "peak_kind": f"{peak_kind} burst bf16 (sustained {peak_sus})",
+                     "peak": peak_sus, "unit": "TFLOP/s", "frac": round(achieved / peak_sus, 4),
+                     "frac_burst": round(achieved / peak, 4),
+                     "peak_kind": f"{peak_kind} sustained bf16 (burst {peak})",
                      "traffic": traffic,
                      "flops_basis": "10*D*Hq*pairs (bwd) / 4*D*Hq*pairs (fwd) per launch"},
         "gpu_launches": launches[0],

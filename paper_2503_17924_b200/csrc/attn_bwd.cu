@@ -11,7 +11,7 @@
 //          (8 compute warps: key row = TMEM lane, 32 query columns each;
 //           P^T / dS^T -> SMEM bf16, double-buffered)
 //   dV  += P^T dO,  dK += dS^T Q     TMEM accumulators (A K-major, B MN-major)
-//   dQ^T = K^T dS^T                  TMEM, aliases S^T of the same buffer;
+//   dQ^T = K^T dS^T                  TMEM, aliases dP^T of the same buffer;
 //          drained by the compute warps with warp-coalesced fp32 reductions
 //          (lane = head-dim index, so each red covers 128 contiguous bytes).
 //
@@ -50,8 +50,8 @@ struct BwdCfg {
   // time), so no alignment slack is reserved: D = 128 uses 226.4 KB of 227.
   static constexpr int SMEM = OFF_BAR + 256;
   static constexpr uint32_t TMEM_COLS = 512;
-  static constexpr uint32_t COL_S = 0;      // S^T[b] at b*64 (later dQ^T[b])
-  static constexpr uint32_t COL_DP = 128;   // dP^T[b] at 128 + b*64
+  static constexpr uint32_t COL_S = 0;      // S^T[b] at b*64
+  static constexpr uint32_t COL_DP = 128;   // dP^T[b] at 128 + b*64 (later dQ^T[b])
   static constexpr uint32_t COL_DV = 256;
   static constexpr uint32_t COL_DK = 256 + D;
   static constexpr uint32_t IDESC_ST = idesc_bf16(BN, BM, 0, 0);
@@ -157,17 +157,26 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         if (i < n_iter) {
           const int b = i & 1, st = i % C::QS;
           mbar_wait(&bars->q_full[st], (i / C::QS) & 1);
-          if (i >= 2) mbar_wait(&bars->s_free[b], ((i - 2) >> 1) & 1);
           tc_fence_after();
           const uint32_t qs = q_b + st * C::Q_BYTES, dos = do_b + st * C::Q_BYTES;
+          // S^T[b] was last read by the compute warps of tile i-2 (before p_full,
+          // already waited); dP^T[b] also held dQ^T of tile i-2, so only the dP
+          // half waits for the drain warps.
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {   // contract over D: K-major both
             const uint32_t ko = (kk >> 2) * C::KV_SLAB + (kk & 3) * 32;
             const uint32_t qo = (kk >> 2) * C::Q_SLAB + (kk & 3) * 32;
             mma_ss_w(tmem + C::COL_S + b * 64, sdesc_sw128(k_b + ko, 16, 1024),
-                   sdesc_sw128(qs + qo, 16, 1024), C::IDESC_ST, kk > 0);
+                     sdesc_sw128(qs + qo, 16, 1024), C::IDESC_ST, kk > 0);
+          }
+          if (i >= 2) mbar_wait(&bars->s_free[b], ((i - 2) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t ko = (kk >> 2) * C::KV_SLAB + (kk & 3) * 32;
+            const uint32_t qo = (kk >> 2) * C::Q_SLAB + (kk & 3) * 32;
             mma_ss_w(tmem + C::COL_DP + b * 64, sdesc_sw128(v_b + ko, 16, 1024),
-                   sdesc_sw128(dos + qo, 16, 1024), C::IDESC_ST, kk > 0);
+                     sdesc_sw128(dos + qo, 16, 1024), C::IDESC_ST, kk > 0);
           }
           mma_commit_w(&bars->s_full[b]);
         }
@@ -187,7 +196,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
           }
 #pragma unroll
           for (int kk = 0; kk < C::BN / 16; ++kk) {   // contract over keys
-            mma_ss_w(tmem + C::COL_S + b * 64, sdesc_sw128(k_b + kk * 2048, C::KV_SLAB, 1024),
+            mma_ss_w(tmem + C::COL_DP + b * 64, sdesc_sw128(k_b + kk * 2048, C::KV_SLAB, 1024),
                    sdesc_sw128(dss + kk * 2048, C::KV_SLAB, 1024), C::IDESC_DQT, kk > 0);
           }
           mma_commit_w(&bars->mma2_done[b]);
@@ -230,8 +239,8 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       mbar_wait(&bars->mma2_done[b], (j >> 1) & 1);
       tc_fence_after();
       uint32_t u[64];
-      tmem_ld32(lane_base + C::COL_S + b * 64, *reinterpret_cast<uint32_t(*)[32]>(u));
-      tmem_ld32(lane_base + C::COL_S + b * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
+      tmem_ld32(lane_base + C::COL_DP + b * 64, *reinterpret_cast<uint32_t(*)[32]>(u));
+      tmem_ld32(lane_base + C::COL_DP + b * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&bars->s_free[b]);
