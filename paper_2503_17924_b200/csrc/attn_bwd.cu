@@ -9,8 +9,8 @@
 //   S^T  = K Q^T,  dP^T = V dO^T     TMEM, lanes = keys, double-buffered
 //   P^T  = exp2(S^T*scale*log2e - LSE2[q]);  dS^T = P^T (dP^T - Delta[q])
 //          (8 compute warps: key row = TMEM lane, 32 query columns each;
-//           P^T / dS^T -> SMEM bf16, double-buffered)
-//   dV  += P^T dO,  dK += dS^T Q     TMEM accumulators (A K-major, B MN-major)
+//           P^T -> TMEM over S^T, dS^T -> TMEM over dP^T AND SMEM, bf16)
+//   dV  += P^T dO,  dK += dS^T Q     TS MMAs (A read from TMEM), TMEM accumulators
 //   dQ^T = K^T dS^T                  TMEM, aliases dP^T of the same buffer;
 //          drained by the compute warps with warp-coalesced fp32 reductions
 //          (lane = head-dim index, so each red covers 128 contiguous bytes).
@@ -42,8 +42,7 @@ struct BwdCfg {
   static constexpr int QS = 3;                          // Q/dO + query-vector ring depth
   static constexpr int OFF_Q = OFF_V + KV_BYTES;        // QS stages
   static constexpr int OFF_DO = OFF_Q + QS * Q_BYTES;   // QS stages
-  static constexpr int OFF_P = OFF_DO + QS * Q_BYTES;   // 2 buffers
-  static constexpr int OFF_DS = OFF_P + 2 * T_BYTES;    // 2 buffers
+  static constexpr int OFF_DS = OFF_DO + QS * Q_BYTES;  // 2 buffers (dS^T for the dQ MMA)
   static constexpr int OFF_VEC = OFF_DS + 2 * T_BYTES;  // QS x {lse2, delta, pos-k0}[BM]
   static constexpr int OFF_BAR = OFF_VEC + QS * 3 * BM * 4;
   // The dynamic-SMEM window starts 1024-B aligned on sm_100 (checked at run
@@ -96,7 +95,6 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
   uint8_t* sV = smem + C::OFF_V;
   uint8_t* sQ = smem + C::OFF_Q;
   uint8_t* sDO = smem + C::OFF_DO;
-  uint8_t* sP = smem + C::OFF_P;
   uint8_t* sDS = smem + C::OFF_DS;
   float* sVec = reinterpret_cast<float*>(smem + C::OFF_VEC);
 
@@ -151,7 +149,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     // ---------------------------------------------------------- MMA issuer --
     {   // whole warp; one elected lane issues
       const uint32_t k_b = smem_u32(sK), v_b = smem_u32(sV), q_b = smem_u32(sQ),
-                     do_b = smem_u32(sDO), p_b = smem_u32(sP), ds_b = smem_u32(sDS);
+                     do_b = smem_u32(sDO), ds_b = smem_u32(sDS);
       mbar_wait(&bars->kv_full, 0);
       for (int i = 0; i <= n_iter; ++i) {
         if (i < n_iter) {
@@ -185,14 +183,14 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
           mbar_wait(&bars->p_full[b], (j >> 1) & 1);
           tc_fence_after();
           const uint32_t qs = q_b + st * C::Q_BYTES, dos = do_b + st * C::Q_BYTES;
-          const uint32_t ps = p_b + b * C::T_BYTES, dss = ds_b + b * C::T_BYTES;
+          const uint32_t dss = ds_b + b * C::T_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < C::BM / 16; ++kk) {   // contract over queries
+          for (int kk = 0; kk < C::BM / 16; ++kk) {   // contract over queries (A from TMEM)
             const uint32_t acc = (j > 0) || (kk > 0);
-            mma_ss_w(tmem + C::COL_DV, sdesc_sw128(ps + kk * 32, 16, 1024),
-                   sdesc_sw128(dos + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
-            mma_ss_w(tmem + C::COL_DK, sdesc_sw128(dss + kk * 32, 16, 1024),
-                   sdesc_sw128(qs + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
+            mma_ts_w(tmem + C::COL_DV, tmem + C::COL_S + b * 64 + kk * 8,
+                     sdesc_sw128(dos + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
+            mma_ts_w(tmem + C::COL_DK, tmem + C::COL_DP + b * 64 + kk * 8,
+                     sdesc_sw128(qs + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
           }
 #pragma unroll
           for (int kk = 0; kk < C::BN / 16; ++kk) {   // contract over keys
@@ -311,16 +309,22 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       }
       tc_fence_before();
       mbar_arrive(&bars->vec_empty[vb]);
-      // buffer b was last read by the MMA group of tile i-2, drained at i-1
-      uint8_t* prow = sP + b * C::T_BYTES + t * 128;
+      // P^T (packed bf16) over this half's S^T columns and dS^T over its dP^T
+      // columns: A operands of the TS dV / dK MMAs.  S^T / dP^T of tile i are in
+      // registers already; the previous readers (dV/dK/dQ of tile i-2) finished
+      // before MMA1(i) (s_full implies it).  dS^T also goes to SMEM as the B
+      // operand of dQ^T = K^T dS^T.
+      tmem_st16(lane_base + C::COL_S + b * 64 + ch * 16, pk);
+      tmem_st16(lane_base + C::COL_DP + b * 64 + ch * 16, dk2);
       uint8_t* drow = sDS + b * C::T_BYTES + t * 128;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int off = (((ch * 4 + c) ^ (t & 7)) << 4);
-        *reinterpret_cast<uint4*>(prow + off) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
         *reinterpret_cast<uint4*>(drow + off) = make_uint4(dk2[4 * c], dk2[4 * c + 1], dk2[4 * c + 2], dk2[4 * c + 3]);
       }
       fence_proxy_async_smem();
+      tmem_st_wait();
+      tc_fence_before();
       mbar_arrive(&bars->p_full[b]);
     }
     {   // the last MMA group wrote the final dV / dK
