@@ -130,3 +130,82 @@ def cp_doc_attention(q, k, v, shard: CPShard, group=None, scale=None):
     (`shard.gather_local`); returns O [T/cp, Hq, D] bf16.  Differentiable.
     """
     return CPDocAttention.apply(q, k, v, shard, group, scale)
+
+
+class CPStepPipeline:
+    """CP attention over all micro-batches of a step with the exchange overlapped.
+
+    The K/V all-gather (+ document-order scatter) of micro-batch b+1 and the
+    dK/dV gather + reduce-scatter of micro-batch b-1 run on a dedicated
+    communication stream while micro-batch b's attention kernels run on the
+    compute stream; CUDA events order each exchange against its producer and
+    consumer.  Hooks:
+
+    * `ready[b]` (optional CUDA events): micro-batch b's inputs are valid once
+      they fire (e.g. H2D copies); by default inputs are taken as resident.
+    * `on_kernels(b, shard, fn)` wraps the attention kernels (e.g. CUDA events
+      for per-rank kernel time) without timing the exchange.
+    * `on_outputs(b, (o, dq, dk, dv), event)` is called as soon as micro-batch
+      b's outputs are enqueued; `event` fires when all four are complete.
+    """
+
+    def __init__(self, group=None):
+        self.group = group
+        self.comm = torch.cuda.Stream()
+
+    def _gather(self, k, v, shard, cur, ready):
+        if ready is None:
+            self.comm.wait_stream(cur)
+        else:
+            self.comm.wait_event(ready)
+        with torch.cuda.stream(self.comm):
+            k_full, v_full = gather_kv(k, v, shard, self.group)
+            ev = torch.cuda.Event()
+            ev.record(self.comm)
+        return k_full, v_full, ev
+
+    def run(self, shards, inputs, scale=None, ready=None, on_kernels=None, on_outputs=None):
+        """inputs[b] = (q, k, v, do) local bf16 tensors.  Returns per micro-batch
+        (o, dq, dk, dv) local tensors (dk/dv fp32), complete on the current stream."""
+        cur = torch.cuda.current_stream()
+        n = len(shards)
+        rdy = ready if ready is not None else [None] * n
+        outs = [None] * n
+        pend = {0: self._gather(inputs[0][1], inputs[0][2], shards[0], cur, rdy[0])}
+        tail = []
+        for b in range(n):
+            if b + 1 < n:
+                pend[b + 1] = self._gather(inputs[b + 1][1], inputs[b + 1][2], shards[b + 1], cur,
+                                           rdy[b + 1])
+            k_full, v_full, ev = pend.pop(b)
+            cur.wait_event(ev)
+            if rdy[b] is not None:
+                cur.wait_event(rdy[b])
+            q, _, _, do = inputs[b]
+
+            def kernels(q=q, do=do, k_full=k_full, v_full=v_full, sh=shards[b]):
+                o, lse = attn_forward(q, k_full, v_full, sh.tiles, scale)
+                dq, dkf, dvf = attn_backward(q, k_full, v_full, o, lse, do, sh.tiles, scale)
+                return o, dq, dkf, dvf
+
+            o, dq, dkf, dvf = on_kernels(b, shards[b], kernels) if on_kernels else kernels()
+            if shards[b].cp > 1:
+                for t in (k_full, v_full):
+                    t.record_stream(cur)
+            done = torch.cuda.Event()
+            done.record(cur)
+            self.comm.wait_event(done)
+            with torch.cuda.stream(self.comm):
+                dk, dv = scatter_dkv(dkf, dvf, shards[b], self.group)
+                if shards[b].cp > 1:
+                    for t in (dkf, dvf):
+                        t.record_stream(self.comm)
+                fin = torch.cuda.Event()
+                fin.record(self.comm)
+            tail.append(fin)
+            outs[b] = (o, dq, dk, dv)
+            if on_outputs is not None:
+                on_outputs(b, outs[b], fin)
+        for ev in tail:
+            cur.wait_event(ev)
+        return outs
