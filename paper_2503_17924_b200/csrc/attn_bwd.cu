@@ -514,6 +514,9 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   if ((rc = make_thd_tmap(&tdo, dout, Tl, Hq, D, C::BM))) return rc;
   if ((rc = make_thd_tmap(&tk, k, T, Hkv, D, C::BN))) return rc;
   if ((rc = make_thd_tmap(&tv, v, T, Hkv, D, C::BN))) return rc;
+  // (A 128-query, single-buffered variant with all-N=128 MMAs measured 1.5x
+  //  slower: the S/dP -> compute -> dV/dK/dQ serialisation costs more than the
+  //  SMEM bandwidth it saves.)
   static bool attr = false;
   if (!attr) {
     WLB_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
