@@ -402,34 +402,49 @@ bwd_kv_tiles_kernel(int nd, const int* __restrict__ rowset_off, const int* __res
   __shared__ long long warp_tot[kKvThreads / 32 + 1];
   __shared__ int hist[kKvBins];
   __shared__ int maxkey_s;
+  // pass 1 (parallel over documents): KV-tile count and item offset of each
+  // document (doc_base lives past the item scratch); pass 2 expands the items
+  // in parallel over items (a serial per-document loop cost ~250 us per call).
+  int* doc_base = reinterpret_cast<int*>(scratch + 2 * (size_t)max_items);   // [nd + 1]
   long long carry = 0;
   for (int base = 0; base < nd; base += blockDim.x) {
     const int p = base + threadIdx.x;
-    int nt = 0, r0 = 0, r1 = 0;
+    int nt = 0;
     if (p < nd) {
-      r0 = rowset_off[p];
-      r1 = rowset_off[p + 1];
+      const int r0 = rowset_off[p], r1 = rowset_off[p + 1];
       if (r1 > r0) nt = (positions[r1 - 1] + 128) / 128;
     }
     long long tot;
     const long long off = carry + block_exclusive_scan(nt, warp_tot, &tot);
-    for (int t = 0; t < nt; ++t) {
-      const int k0 = t * 128;
-      int lo = r0, hi = r1;   // first row with position >= k0
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (positions[mid] >= k0) hi = mid;
-        else lo = mid + 1;
-      }
-      const int len = doc_start[p + 1] - doc_start[p] - k0;
-      if (off + t < max_items) {
-        scratch[2 * (off + t)] = make_int4(doc_start[p] + k0, len < 128 ? len : 128, lo, r1);
-        scratch[2 * (off + t) + 1] = make_int4(k0, p, 0, 0);
-      }
-    }
+    if (p < nd) doc_base[p] = (int)off;
     carry += tot;
   }
-  const int total = carry < max_items ? (int)carry : max_items;
+  if (threadIdx.x == 0) doc_base[nd] = (int)carry;
+  __syncthreads();
+  const int n_items = carry < max_items ? (int)carry : max_items;
+  // pass 2 (parallel over items): owning document by binary search over the
+  // bases, first visible row by binary search over the row-set positions.
+  for (int it = threadIdx.x; it < n_items; it += blockDim.x) {
+    int lo = 0, hi = nd;                      // largest p with doc_base[p] <= it
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (doc_base[mid] <= it) lo = mid;
+      else hi = mid;
+    }
+    const int p = lo, t = it - doc_base[p], k0 = t * 128;
+    const int r0 = rowset_off[p], r1 = rowset_off[p + 1];
+    int a = r0, b = r1;                       // first row with position >= k0
+    while (a < b) {
+      const int mid = (a + b) >> 1;
+      if (positions[mid] >= k0) b = mid;
+      else a = mid + 1;
+    }
+    const int len = doc_start[p + 1] - doc_start[p] - k0;
+    scratch[2 * it] = make_int4(doc_start[p] + k0, len < 128 ? len : 128, a, r1);
+    scratch[2 * it + 1] = make_int4(k0, p, 0, 0);
+  }
+  __syncthreads();
+  const int total = n_items;
   int mk = 0;
   for (int i = threadIdx.x; i < total; i += blockDim.x)
     mk = max(mk, (scratch[2 * i].w - scratch[2 * i].z + 127) >> 7);
@@ -480,7 +495,7 @@ static BwdWorkspace carve(void* base, int Tl, int T, int Hq, int D, int n_docs) 
   };
   w.dq_acc = (float*)take((size_t)Tl * Hq * D * 4);
   w.delta = (float*)take((size_t)Hq * Tl * 4);
-  w.kv_tiles = (int4*)take(4 * max_items * sizeof(int4));
+  w.kv_tiles = (int4*)take(4 * max_items * sizeof(int4) + (n_docs + 1) * sizeof(int));
   w.n_kv = (int*)take(16);
   w.bytes = off;
   return w;
