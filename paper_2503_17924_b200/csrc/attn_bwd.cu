@@ -75,13 +75,14 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const float* __restrict__ lse, const float* __restrict__ delta,
                 float* __restrict__ dq_acc, float* __restrict__ dk, float* __restrict__ dv,
                 const int4* __restrict__ kv_tiles, const int* __restrict__ n_kv_tiles,
-                const int* __restrict__ positions, int Tl, int Hq, int Hkv, float scale,
-                float scale_log2) {
+                const int* __restrict__ positions, int Tl, int Hq, int Hkv, int n_slots,
+                float scale, float scale_log2) {
   using C = BwdCfg<D, NCW>;
   extern __shared__ uint8_t smem_raw[];
   if (smem_u32(smem_raw) & 1023) __trap();   // SW128 tiles need 1024-B alignment
   uint8_t* smem = smem_raw;
-  const int item = blockIdx.x / Hkv, g = blockIdx.x % Hkv;
+  // head-major order (LPT within a head): resident CTAs share one head's Q/dO/dQ in L2
+  const int item = blockIdx.x % n_slots, g = blockIdx.x / n_slots;
   if (item >= n_kv_tiles[0]) return;
   const int4 kt = kv_tiles[2 * item];
   const int k0 = kv_tiles[2 * item + 1].x;   // in-document position of key 0 of the tile
@@ -540,7 +541,7 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   }
   attn_bwd_kernel<D, 2><<<(unsigned)max_items * Hkv, C::THREADS, C::SMEM, stream>>>(
       tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq, Hkv,
-      scale, scale * 1.4426950408889634f);
+      max_items, scale, scale * 1.4426950408889634f);
   WLB_LAUNCH_CHECK();
   const long long n4 = (long long)Tl * Hq * D / 4;
   dq_convert_kernel<<<(unsigned)std::min<long long>((n4 + 255) / 256, 148 * 16), 256, 0, stream>>>(

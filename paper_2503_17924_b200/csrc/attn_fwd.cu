@@ -67,11 +67,12 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ out,
                 float* __restrict__ lse, const int4* __restrict__ items,
                 const int* __restrict__ n_items, const int* __restrict__ positions, int Tl,
-                int Hq, int Hkv, float scale_log2) {
+                int Hq, int Hkv, int n_slots, float scale_log2) {
   using C = FwdCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  const int item = blockIdx.x / Hq, h = blockIdx.x % Hq;
+  // head-major order (LPT within a head): resident CTAs share one head's K/V in L2
+  const int item = blockIdx.x % n_slots, h = blockIdx.x / n_slots;
   if (item >= n_items[0]) return;
   const int4 tx = items[2 * item], ty = items[2 * item + 1];
   // tile 0 = X {row0, nrows, kv_end}, tile 1 = Y
@@ -313,7 +314,7 @@ static int launch_fwd(const void* q, const void* k, const void* v, void* o, floa
   const float scale_log2 = scale * 1.4426950408889634f;
   attn_fwd_kernel<D><<<(unsigned)max_tiles * Hq, C::THREADS, C::SMEM, stream>>>(
       tq, tk, tv, (__nv_bfloat16*)o, lse, (const int4*)tiles, n_tiles, positions, Tl, Hq, Hkv,
-      scale_log2);
+      max_tiles, scale_log2);
   WLB_LAUNCH_CHECK();
   return WLB_OK;
 }
