@@ -70,15 +70,18 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index):
+    def __init__(self, index, period_ms=500):
         self.index = index
+        self.period_ms = period_ms
         self.proc = None
 
     def __enter__(self):
+        if self.period_ms <= 0:
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -186,6 +189,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--clock-ms", type=int, default=500,
+                    help="nvidia-smi sampling period during the timed region (0: off)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -232,8 +237,10 @@ def main():
             record.append((e, sh))
             return res
 
-        pipe.run(shards, ins, on_kernels=timed)   # outputs dropped here: holding a whole
-        return shards                             # step's outputs churns the allocator
+        # outputs are released micro-batch by micro-batch: holding a whole step's
+        # outputs (~20 GB) made the caching allocator free + re-malloc (device syncs)
+        pipe.run(shards, ins, on_kernels=timed, keep_outputs=False)
+        return shards
 
     def barrier():
         if world > 1:
@@ -248,7 +255,7 @@ def main():
     launches[0] = 0
     recs = []
     t0, t1 = ev(), ev()
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(local_rank, args.clock_ms) as clk:
         barrier()
         t0.record()
         for _ in range(args.steps):
@@ -256,6 +263,7 @@ def main():
         t1.record()
         barrier()
     my_ms = t0.elapsed_time(t1)
+    alloc_retries = torch.cuda.memory_stats(dev).get("num_alloc_retries", 0)
     kern_each = [e[0].elapsed_time(e[1]) for e, _ in recs]
     my_pairs = sum(sh.pairs for sh in shards)
     total_pairs = sum(sum(x * (x + 1) // 2 for x in ls) for ls in lengths)
@@ -312,7 +320,7 @@ def main():
                         dst.copy_(src, non_blocking=True)
                         src.record_stream(d2h_s)
 
-            pipe.run(shards, ins, ready=ready, on_outputs=d2h)
+            pipe.run(shards, ins, ready=ready, on_outputs=d2h, keep_outputs=False)
             cur.wait_stream(d2h_s)
 
         e2e_step()
@@ -373,6 +381,7 @@ def main():
                      "traffic": traffic,
                      "flops_basis": "14*D*Hq*pairs_rank per (fwd+bwd) launch pair"},
         "gpu_launches": launches[0],
+        "alloc_retries": alloc_retries,
         "clocks": clk.summary(),
         "e2e": e2e,
     }

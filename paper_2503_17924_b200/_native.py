@@ -86,5 +86,15 @@ def stream_ptr(stream=None) -> int:
     return s.cuda_stream
 
 
+def to_device(values, dtype, device):
+    """Host list -> device tensor WITHOUT a host sync (pinned staging + async
+    copy; torch's caching host allocator keeps the staging buffer alive until
+    the copy has run).  torch.tensor(..., device=cuda) would block the host
+    until all queued GPU work drained."""
+    import torch
+    host = torch.tensor(values, dtype=dtype, pin_memory=True)
+    return host.to(device, non_blocking=True)
+
+
 def ptr(t) -> int | None:
     return None if t is None else t.data_ptr()

@@ -42,7 +42,7 @@ def build_tiles(rowset_off: torch.Tensor, positions: torch.Tensor, doc_lengths,
     starts = [0]
     for x in doc_lengths:
         starts.append(starts[-1] + int(x))
-    doc_start = torch.tensor(starts, dtype=torch.int32, device=dev)
+    doc_start = _native.to_device(starts, torch.int32, dev)
     tl = positions.numel()
     max_tiles = tl // (2 * block_m) + n_docs + 1
     tiles = torch.empty((4 * max_tiles, 4), dtype=torch.int32, device=dev)

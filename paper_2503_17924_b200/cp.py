@@ -39,7 +39,11 @@ class CPShard:
     tiles: AttnTiles
     gather_all: torch.Tensor   # [T] int32: all ranks' local rows -> global token
     gather_local: torch.Tensor  # [T/cp] int32
-    pairs: int             # causal pairs of this rank (FLOP basis)
+
+    @property
+    def pairs(self) -> int:
+        """Causal pairs of this rank (FLOP basis); reading it syncs with the GPU."""
+        return int(self.plan.host("rank_pairs")[self.index, self.rank])
 
     @property
     def strategy(self):
@@ -53,8 +57,7 @@ def shard_for_rank(plan: ShardPlan, index: int, rank: int) -> CPShard:
     lo = plan.tok_off[index]
     tiles = build_tiles(ro, pos, lengths)
     return CPShard(plan=plan, index=index, rank=rank, cp=plan.cp, tiles=tiles,
-                   gather_all=plan.gather_index[lo:lo + T], gather_local=g,
-                   pairs=int(plan.host("rank_pairs")[index, rank]))
+                   gather_all=plan.gather_index[lo:lo + T], gather_local=g)
 
 
 def build_cp_shards(microbatches, cp: int, rank: int, policy: str = "adaptive",
@@ -164,9 +167,11 @@ class CPStepPipeline:
             ev.record(self.comm)
         return k_full, v_full, ev
 
-    def run(self, shards, inputs, scale=None, ready=None, on_kernels=None, on_outputs=None):
+    def run(self, shards, inputs, scale=None, ready=None, on_kernels=None, on_outputs=None,
+            keep_outputs=True):
         """inputs[b] = (q, k, v, do) local bf16 tensors.  Returns per micro-batch
-        (o, dq, dk, dv) local tensors (dk/dv fp32), complete on the current stream."""
+        (o, dq, dk, dv) local tensors (dk/dv fp32), complete on the current stream
+        (None entries when keep_outputs=False: consume them in on_outputs)."""
         cur = torch.cuda.current_stream()
         n = len(shards)
         rdy = ready if ready is not None else [None] * n
@@ -203,9 +208,15 @@ class CPStepPipeline:
                 fin = torch.cuda.Event()
                 fin.record(self.comm)
             tail.append(fin)
-            outs[b] = (o, dq, dk, dv)
             if on_outputs is not None:
-                on_outputs(b, outs[b], fin)
+                on_outputs(b, (o, dq, dk, dv), fin)
+            if keep_outputs:
+                outs[b] = (o, dq, dk, dv)
+            else:
+                for t in (o, dq, dk, dv):      # freed now; keep them valid for pending work
+                    t.record_stream(cur)
+                    if t.device.type == "cuda" and shards[b].cp > 1:
+                        t.record_stream(self.comm)
         for ev in tail:
             cur.wait_event(ev)
         return outs

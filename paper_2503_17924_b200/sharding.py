@@ -151,12 +151,13 @@ def build_shard_plan(microbatches, cp: int, policy: str = "adaptive",
         tok_off.append(tok_off[-1] + sum(ls))
     i32 = dict(dtype=torch.int32, device=dev)
     flat = [x for ls in lengths for x in ls] or [0]
-    d_doc_off = torch.tensor(doc_off, **i32)
-    d_len = torch.tensor(flat, dtype=torch.int64, device=dev)
-    d_tok = torch.tensor(tok_off, dtype=torch.int64, device=dev)
+    up = _native.to_device        # no host sync: the step can be enqueued ahead
+    d_doc_off = up(doc_off, torch.int32, dev)
+    d_len = up(flat, torch.int64, dev)
+    d_tok = up(tok_off, torch.int64, dev)
     cq, cv = profile.curve_arrays()
-    d_cq = torch.tensor(cq, dtype=torch.int64, device=dev)
-    d_cv = torch.tensor(cv, dtype=torch.float64, device=dev)
+    d_cq = up(cq, torch.int64, dev)
+    d_cv = up(cv, torch.float64, dev)
     choice = torch.empty(n_mb, **i32)
     lat = torch.empty((n_mb, 2, cp), dtype=torch.float64, device=dev)
     pairs = torch.empty((n_mb, cp), dtype=torch.int64, device=dev)
