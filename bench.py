@@ -115,8 +115,25 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def _cpu_sample(lengths_list, hq_sample, d, budget_s, first=0):
-    """Oracle (torch-CPU fp32) fwd+bwd on head(s) of whole sequences, all host cores.
+def _bounded(lengths, max_pairs):
+    """Documents in order, the last one cut to a prefix, so that the sample's
+    causal pairs stay <= max_pairs (a prefix of a document is exact
+    document-prefix attention of its own)."""
+    out, used = [], 0
+    for x in lengths:
+        room = max_pairs - used
+        if room <= 0:
+            break
+        if x * (x + 1) // 2 > room:
+            x = max(1, int(((8 * room + 1) ** 0.5 - 1) // 2))
+        out.append(x)
+        used += x * (x + 1) // 2
+    return out
+
+
+def _cpu_sample(lengths_list, hq_sample, d, budget_s, first=0, max_pairs=1_500_000_000):
+    """Oracle (torch-CPU fp32) fwd+bwd on head(s) of synthetic sequences, all host
+    cores, each sequence bounded to max_pairs causal pairs (~10-15 s of CPU).
     TEST/BASELINE ONLY: the checker is never the thing measured for `value`."""
     from oracle import attention_oracle as ao
     from oracle import shard_oracle as so
@@ -126,7 +143,7 @@ def _cpu_sample(lengths_list, hq_sample, d, budget_s, first=0):
     i = first
     t_start = time.perf_counter()
     while True:
-        lengths = lengths_list[i % len(lengths_list)]
+        lengths = so.pad_lengths_for_cp(_bounded(lengths_list[i % len(lengths_list)], max_pairs), 1)
         g = torch.Generator().manual_seed(1000 + i)
         T = sum(lengths)
         q = torch.randn(T, hq_sample, d, generator=g)
@@ -173,8 +190,9 @@ def run_reference(args, world, rank):
         "cpu_baseline": {"value": round(value, 4), "unit": "TFLOP/s", "cores": os.cpu_count(),
                          "kind": "port",
                          "sample": "per step: head 0 of one synthetic sequence (cycling the 8), "
-                                   "per_document shard + torch-CPU fp32 doc-prefix attention "
-                                   "fwd+bwd (oracle/attention_oracle.py)"},
+                                   "documents in order up to 1.5e9 causal pairs (last one "
+                                   "prefix-cut), per_document shard + torch-CPU fp32 "
+                                   "doc-prefix attention fwd+bwd (oracle/attention_oracle.py)"},
         "e2e": {"value": round(value, 4), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -389,8 +407,9 @@ def main():
         tflops, done, secs = _cpu_sample(lengths, 1, d, budget_s=15.0)
         line["cpu_baseline"] = {
             "value": round(tflops, 4), "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"head 0 of synthetic sequences {done} ({secs:.1f} s): per_document shard "
-                      "+ torch-CPU fp32 doc-prefix attention fwd+bwd (oracle)"}
+            "sample": f"head 0 of synthetic sequences {done}, each bounded to 1.5e9 causal "
+                      f"pairs ({secs:.1f} s): per_document shard + torch-CPU fp32 "
+                      "doc-prefix attention fwd+bwd (oracle)"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
