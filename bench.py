@@ -39,6 +39,7 @@ from paper_2503_17924_b200.attention import attn_backward, attn_forward  # noqa:
 from paper_2503_17924_b200.cp import CPStepPipeline, build_cp_shards  # noqa: E402
 
 N_SEQ = 8
+METRIC = "doc-masked attn TFLOP/s/GPU & CP rank imbalance (max/mean) at CP=1/2/4/8"
 
 
 def _peaks():
@@ -180,13 +181,14 @@ def run_reference(args, world, rank):
             flops_tot += tflops * 1e12 * secs
     value = flops_tot / secs_tot / 1e12
     line = {
-        "impl": "reference", "metric": "doc-masked attn TFLOP/s/GPU & CP rank imbalance",
+        "impl": "reference", "metric": METRIC,
         "value": round(value, 4), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(secs_tot / args.steps * 1e3, 1),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": wk["name"], "seq_len": wk["window"], "heads": [wk["hq"], wk["hkv"]],
-                   "head_dim": wk["d"], "cp": wk["cp"]},
+        "config": {"workload": wk["name"], "seq_len": wk["window"], "sequences_per_step": N_SEQ,
+                   "heads": [wk["hq"], wk["hkv"]], "head_dim": wk["d"], "cp": wk["cp"],
+                   "policy": "per_document (CPU sample)", "parallelism": f"cp{wk['cp']}"},
         "cpu_baseline": {"value": round(value, 4), "unit": "TFLOP/s", "cores": os.cpu_count(),
                          "kind": "port",
                          "sample": "per step: head 0 of one synthetic sequence (cycling the 8), "
@@ -377,7 +379,7 @@ def main():
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(wk["name"], {}).get(dom[0])
     line = {
-        "metric": "doc-masked attn TFLOP/s/GPU & CP rank imbalance (max/mean) at CP=1/2/4/8",
+        "metric": METRIC,
         "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
