@@ -176,12 +176,31 @@ def packer_config5(b):
     _dump("packer_config5.json.gz", {"iterations": iters})
 
 
+def records(b):
+    """Wire formats written by the reference itself (records.py:60-116)."""
+    from balsim import records as rec
+    from balsim.sharding import per_document_shard, per_sequence_shard
+    spec = b.SyntheticSpec(context_window=8192, tokens_per_global_batch=4 * 8192)
+    stream = b.generate_synthetic_stream(spec, seed=3, n_batches=3)
+    packer = b.HeuristicPacker(b.OutlierQueueSet((2048, 6144)), 4, 10240, b.CostProfile())
+    plans = [packer.feed(batch, it) for it, batch in enumerate(stream)] + packer.flush(3)
+    rec.write_plans(plans, os.path.join(HERE, "records_plans.jsonl"))
+    assigns = []
+    for lengths, cp in (([700, 3, 129, 2000, 1, 257, 6], 4), ([16], 2), ([10, 6], 2),
+                        ([5000, 3000, 120, 7, 1], 8)):
+        mb = b.MicroBatch([b.Document(100 + i, x) for i, x in enumerate(lengths)])
+        assigns += [per_sequence_shard(mb, cp), per_document_shard(mb, cp)]
+    rec.write_assignments(assigns, os.path.join(HERE, "records_shards.jsonl"))
+    print("wrote records_plans.jsonl, records_shards.jsonl")
+
+
 def main():
     b = _import_reference()
     sharding_random(b)
     synthetic_streams(b)
     kernels(b)
     packer_config5(b)
+    records(b)
 
 
 if __name__ == "__main__":
