@@ -122,6 +122,21 @@ int wlb_rows_scatter(const void* src, void* dst, const int32_t* index, int64_t n
 int wlb_rows_gather(const void* src, void* dst, const int32_t* index, int64_t n_rows,
                     int64_t row_bytes, void* stream);
 
+/* Fused CP exchange over NVLink peer memory (symmetric buffers; replaces NCCL
+ * all-gather + un-permute and permute + reduce-scatter).
+ * peer_bases: device array [cp] of peer-mapped base addresses (same layout on
+ * every rank).  kv_push stores local row i of K / V at row gather_local[i] of
+ * EVERY rank's document-ordered buffers (base + k_off / v_off).  dkv_pull
+ * writes dk[i] = sum_r partial_dk_r[gather_local[i]] (fp32, row_bytes per row),
+ * same for dv.  Cross-rank ordering is the caller's (symmetric-memory
+ * barriers on the same stream). */
+int wlb_cp_kv_push(const void* k_local, const void* v_local, const int32_t* gather_local,
+                   int64_t n_rows, int64_t row_bytes, const uint64_t* peer_bases,
+                   int64_t k_off, int64_t v_off, int32_t cp, void* stream);
+int wlb_cp_dkv_pull(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_off,
+                    const int32_t* gather_local, int64_t n_rows, int64_t row_bytes,
+                    float* dk, float* dv, int32_t cp, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

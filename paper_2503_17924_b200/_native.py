@@ -39,6 +39,8 @@ SIGNATURES = {
                                _i32, _i32, _i32, _f32, _p, _p]),
     "wlb_rows_scatter": (C.c_int, [_p, _p, _p, _i64, _i64, _p]),
     "wlb_rows_gather": (C.c_int, [_p, _p, _p, _i64, _i64, _p]),
+    "wlb_cp_kv_push": (C.c_int, [_p, _p, _p, _i64, _i64, _p, _i64, _i64, _i32, _p]),
+    "wlb_cp_dkv_pull": (C.c_int, [_p, _i64, _i64, _p, _i64, _i64, _p, _p, _i32, _p]),
 }
 
 _lib = None

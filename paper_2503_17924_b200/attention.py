@@ -78,16 +78,18 @@ def attn_forward(q, k, v, tiles: AttnTiles, scale: float | None = None):
     return o, lse
 
 
-def attn_backward(q, k, v, o, lse, do, tiles: AttnTiles, scale: float | None = None):
-    """dQ [Tl,Hq,D] bf16 and fp32 dK/dV partials over the full sequence."""
+def attn_backward(q, k, v, o, lse, do, tiles: AttnTiles, scale: float | None = None,
+                  dk_out=None, dv_out=None):
+    """dQ [Tl,Hq,D] bf16 and fp32 dK/dV partials over the full sequence
+    (written into dk_out / dv_out when given, e.g. symmetric exchange buffers)."""
     _check_inputs(q, k, v)
     tl, hq, d = q.shape
     T, hkv = k.shape[0], k.shape[1]
     scale = 1.0 / math.sqrt(d) if scale is None else scale
     do = do.contiguous()
     dq = torch.empty_like(q)
-    dk = torch.empty((T, hkv, d), dtype=torch.float32, device=q.device)
-    dv = torch.empty((T, hkv, d), dtype=torch.float32, device=q.device)
+    dk = torch.empty((T, hkv, d), dtype=torch.float32, device=q.device) if dk_out is None else dk_out
+    dv = torch.empty((T, hkv, d), dtype=torch.float32, device=q.device) if dv_out is None else dv_out
     lib = _native.lib()
     ws = torch.empty(lib.wlb_attn_bwd_workspace(tl, T, hq, hkv, d, tiles.n_docs),
                      dtype=torch.uint8, device=q.device)

@@ -135,14 +135,101 @@ def cp_doc_attention(q, k, v, shard: CPShard, group=None, scale=None):
     return CPDocAttention.apply(q, k, v, shard, group, scale)
 
 
+class NcclExchange:
+    """CP exchange through NCCL collectives (all-gather / reduce-scatter) plus
+    the row-permutation kernels."""
+
+    def __init__(self, group=None):
+        self.group = group
+
+    def gather(self, k, v, shard, b):
+        return gather_kv(k, v, shard, self.group)
+
+    def dkv_out(self, shard, b, cur):
+        return None, None
+
+    def scatter(self, dkf, dvf, shard, b):
+        return scatter_dkv(dkf, dvf, shard, self.group)
+
+
+class SymmExchange:
+    """CP exchange as ONE-SIDED NVLink traffic on symmetric memory.
+
+    Every rank owns two slots (micro-batches alternate) of a document-ordered
+    K/V buffer and of fp32 dK/dV partial buffers, mapped into every peer:
+
+      forward : barrier (slot free everywhere) -> wlb_cp_kv_push stores this
+                rank's rows into every rank's slot at their document positions
+                -> barrier.  The local slot then IS the gathered, un-permuted
+                K/V: no all-gather, no permutation pass.
+      backward: the attention backward writes its full-length partials
+                straight into the local dK/dV slot -> barrier ->
+                wlb_cp_dkv_pull sums every rank's partials for this rank's rows
+                -> barrier (slot reusable; the compute stream waits on it
+                before the backward of the micro-batch two steps later).
+    """
+
+    def __init__(self, group, t_max, hkv, d, device):
+        import torch.distributed._symmetric_memory as symm
+        self.group = group if group is not None else dist.group.WORLD
+        self.cp = dist.get_world_size(self.group)
+        self.t_max, self.hkv, self.d = t_max, hkv, d
+        self.n = t_max * hkv * d
+        self.kv = symm.empty(4 * self.n, dtype=torch.bfloat16, device=device)     # [slot][K|V]
+        self.kv_h = symm.rendezvous(self.kv, self.group)
+        self.dkv = symm.empty(4 * self.n, dtype=torch.float32, device=device)     # [slot][dK|dV]
+        self.dkv_h = symm.rendezvous(self.dkv, self.group)
+        self.kv_bases = torch.tensor(list(self.kv_h.buffer_ptrs), dtype=torch.int64, device=device)
+        self.dkv_bases = torch.tensor(list(self.dkv_h.buffer_ptrs), dtype=torch.int64, device=device)
+        self.free = [None, None]       # event: all ranks finished pulling slot s
+
+    def _view(self, buf, idx, T):
+        return buf[idx * self.n: idx * self.n + T * self.hkv * self.d].view(T, self.hkv, self.d)
+
+    def gather(self, k, v, shard, b):
+        s, T = b % 2, shard.gather_all.numel()
+        if T > self.t_max:
+            raise ValueError(f"micro-batch of {T} tokens exceeds the exchange capacity {self.t_max}")
+        self.kv_h.barrier(channel=0)
+        row = self.hkv * self.d * 2
+        _native.check(_native.lib().wlb_cp_kv_push(
+            k.data_ptr(), v.data_ptr(), shard.gather_local.data_ptr(), k.shape[0], row,
+            self.kv_bases.data_ptr(), 2 * s * self.n * 2, (2 * s + 1) * self.n * 2, self.cp,
+            _native.stream_ptr()), "wlb_cp_kv_push")
+        self.kv_h.barrier(channel=0)
+        return self._view(self.kv, 2 * s, T), self._view(self.kv, 2 * s + 1, T)
+
+    def dkv_out(self, shard, b, cur):
+        s, T = b % 2, shard.gather_all.numel()
+        if self.free[s] is not None:
+            cur.wait_event(self.free[s])
+        return self._view(self.dkv, 2 * s, T), self._view(self.dkv, 2 * s + 1, T)
+
+    def scatter(self, dkf, dvf, shard, b):
+        s = b % 2
+        tl = shard.gather_local.numel()
+        dk = torch.empty((tl, self.hkv, self.d), dtype=torch.float32, device=dkf.device)
+        dv = torch.empty_like(dk)
+        self.dkv_h.barrier(channel=1)
+        _native.check(_native.lib().wlb_cp_dkv_pull(
+            self.dkv_bases.data_ptr(), 2 * s * self.n * 4, (2 * s + 1) * self.n * 4,
+            shard.gather_local.data_ptr(), tl, self.hkv * self.d * 4, dk.data_ptr(), dv.data_ptr(),
+            self.cp, _native.stream_ptr()), "wlb_cp_dkv_pull")
+        self.dkv_h.barrier(channel=1)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.free[s] = ev
+        return dk, dv
+
+
 class CPStepPipeline:
     """CP attention over all micro-batches of a step with the exchange overlapped.
 
-    The K/V all-gather (+ document-order scatter) of micro-batch b+1 and the
-    dK/dV gather + reduce-scatter of micro-batch b-1 run on a dedicated
-    communication stream while micro-batch b's attention kernels run on the
-    compute stream; CUDA events order each exchange against its producer and
-    consumer.  Hooks:
+    The K/V exchange of micro-batch b+1 and the dK/dV exchange of micro-batch
+    b-1 run on a dedicated communication stream while micro-batch b's
+    attention kernels run on the compute stream; CUDA events order each
+    exchange against its producer and consumer.  `exchange` is NcclExchange
+    (default) or SymmExchange (one-sided NVLink stores / loads).  Hooks:
 
     * `ready[b]` (optional CUDA events): micro-batch b's inputs are valid once
       they fire (e.g. H2D copies); by default inputs are taken as resident.
@@ -152,17 +239,18 @@ class CPStepPipeline:
       b's outputs are enqueued; `event` fires when all four are complete.
     """
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, exchange=None):
         self.group = group
+        self.exchange = exchange if exchange is not None else NcclExchange(group)
         self.comm = torch.cuda.Stream()
 
-    def _gather(self, k, v, shard, cur, ready):
+    def _gather(self, k, v, shard, b, cur, ready):
         if ready is None:
             self.comm.wait_stream(cur)
         else:
             self.comm.wait_event(ready)
         with torch.cuda.stream(self.comm):
-            k_full, v_full = gather_kv(k, v, shard, self.group)
+            k_full, v_full = self.exchange.gather(k, v, shard, b)
             ev = torch.cuda.Event()
             ev.record(self.comm)
         return k_full, v_full, ev
@@ -176,21 +264,24 @@ class CPStepPipeline:
         n = len(shards)
         rdy = ready if ready is not None else [None] * n
         outs = [None] * n
-        pend = {0: self._gather(inputs[0][1], inputs[0][2], shards[0], cur, rdy[0])}
+        pend = {0: self._gather(inputs[0][1], inputs[0][2], shards[0], 0, cur, rdy[0])}
         tail = []
         for b in range(n):
             if b + 1 < n:
-                pend[b + 1] = self._gather(inputs[b + 1][1], inputs[b + 1][2], shards[b + 1], cur,
-                                           rdy[b + 1])
+                pend[b + 1] = self._gather(inputs[b + 1][1], inputs[b + 1][2], shards[b + 1], b + 1,
+                                           cur, rdy[b + 1])
             k_full, v_full, ev = pend.pop(b)
             cur.wait_event(ev)
             if rdy[b] is not None:
                 cur.wait_event(rdy[b])
             q, _, _, do = inputs[b]
+            dk_out, dv_out = self.exchange.dkv_out(shards[b], b, cur) if shards[b].cp > 1 else (None, None)
 
-            def kernels(q=q, do=do, k_full=k_full, v_full=v_full, sh=shards[b]):
+            def kernels(q=q, do=do, k_full=k_full, v_full=v_full, sh=shards[b], dk_out=dk_out,
+                        dv_out=dv_out):
                 o, lse = attn_forward(q, k_full, v_full, sh.tiles, scale)
-                dq, dkf, dvf = attn_backward(q, k_full, v_full, o, lse, do, sh.tiles, scale)
+                dq, dkf, dvf = attn_backward(q, k_full, v_full, o, lse, do, sh.tiles, scale,
+                                             dk_out, dv_out)
                 return o, dq, dkf, dvf
 
             o, dq, dkf, dvf = on_kernels(b, shards[b], kernels) if on_kernels else kernels()
@@ -201,7 +292,8 @@ class CPStepPipeline:
             done.record(cur)
             self.comm.wait_event(done)
             with torch.cuda.stream(self.comm):
-                dk, dv = scatter_dkv(dkf, dvf, shards[b], self.group)
+                dk, dv = self.exchange.scatter(dkf, dvf, shards[b], b) if shards[b].cp > 1 \
+                    else (dkf, dvf)
                 if shards[b].cp > 1:
                     for t in (dkf, dvf):
                         t.record_stream(self.comm)
@@ -215,7 +307,7 @@ class CPStepPipeline:
             else:
                 for t in (o, dq, dk, dv):      # freed now; keep them valid for pending work
                     t.record_stream(cur)
-                    if t.device.type == "cuda" and shards[b].cp > 1:
+                    if shards[b].cp > 1:
                         t.record_stream(self.comm)
         for ev in tail:
             cur.wait_event(ev)

@@ -1,0 +1,105 @@
+// Fused CP exchange over NVLink / NVSwitch peer memory (symmetric buffers).
+//
+// The reference has no collectives; the paper's CP exchange is an
+// all-gather of K/V in the forward and a reduce-scatter of dK/dV in the
+// backward.  With NCCL that is all-gather -> un-permute to
+// document order (an extra HBM pass) and gather-permute -> reduce-scatter.
+// Here both are ONE kernel each, on peer-mapped symmetric buffers:
+//
+//   kv_push   every local row i of K and V is stored straight into EVERY rank's
+//             document-ordered full K/V buffer at row gather_local[i]
+//             (NVLink stores; the un-permute is free: the destination index
+//             is the permutation).
+//   dkv_pull  each rank sums, for its own rows, the fp32 dK/dV partials of all
+//             ranks (NVLink loads), replacing the permute + reduce-scatter.
+//
+// One warp per row, 16-byte vectors; cross-rank ordering is done by the
+// caller's symmetric-memory barriers on the same stream.
+#include "common.cuh"
+
+namespace wlb {
+
+__global__ void kv_push_kernel(const int4* __restrict__ k, const int4* __restrict__ v,
+                               const int* __restrict__ gidx, long long n_rows, long long row_vecs,
+                               const unsigned long long* __restrict__ bases, long long k_off,
+                               long long v_off, int cp) {
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
+       r += warps) {
+    const long long g = gidx[r];
+    for (long long c = lane; c < row_vecs; c += 32) {
+      const int4 kv = k[r * row_vecs + c], vv = v[r * row_vecs + c];
+      for (int p = 0; p < cp; ++p) {
+        char* base = reinterpret_cast<char*>(bases[p]);
+        reinterpret_cast<int4*>(base + k_off)[g * row_vecs + c] = kv;
+        reinterpret_cast<int4*>(base + v_off)[g * row_vecs + c] = vv;
+      }
+    }
+  }
+}
+
+__global__ void dkv_pull_kernel(const unsigned long long* __restrict__ bases, long long dk_off,
+                                long long dv_off, const int* __restrict__ gidx, long long n_rows,
+                                long long row_vecs, float4* __restrict__ dk,
+                                float4* __restrict__ dv, int cp) {
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
+       r += warps) {
+    const long long g = gidx[r];
+    for (long long c = lane; c < row_vecs; c += 32) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+      for (int p = 0; p < cp; ++p) {
+        const char* base = reinterpret_cast<const char*>(bases[p]);
+        const float4 x = reinterpret_cast<const float4*>(base + dk_off)[g * row_vecs + c];
+        const float4 y = reinterpret_cast<const float4*>(base + dv_off)[g * row_vecs + c];
+        a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
+        b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
+      }
+      dk[r * row_vecs + c] = a;
+      dv[r * row_vecs + c] = b;
+    }
+  }
+}
+
+static int grid_for(long long n_rows) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  long long blocks = (n_rows + 7) / 8;
+  if (blocks > sms * 8LL) blocks = sms * 8LL;
+  return (int)(blocks > 0 ? blocks : 1);
+}
+
+}  // namespace wlb
+
+using namespace wlb;
+
+extern "C" int wlb_cp_kv_push(const void* k_local, const void* v_local, const int32_t* gather_local,
+                              int64_t n_rows, int64_t row_bytes, const uint64_t* peer_bases,
+                              int64_t k_off, int64_t v_off, int32_t cp, void* stream) {
+  WLB_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && k_off % 16 == 0 && v_off % 16 == 0,
+              "rows and offsets must be 16-byte aligned");
+  WLB_REQUIRE(cp >= 1, "cp must be >= 1");
+  if (n_rows <= 0) return WLB_OK;
+  kv_push_kernel<<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
+      (const int4*)k_local, (const int4*)v_local, gather_local, n_rows, row_bytes / 16,
+      (const unsigned long long*)peer_bases, k_off, v_off, cp);
+  WLB_LAUNCH_CHECK();
+  return WLB_OK;
+}
+
+extern "C" int wlb_cp_dkv_pull(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_off,
+                               const int32_t* gather_local, int64_t n_rows, int64_t row_bytes,
+                               float* dk, float* dv, int32_t cp, void* stream) {
+  WLB_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && dk_off % 16 == 0 && dv_off % 16 == 0,
+              "rows and offsets must be 16-byte aligned");
+  WLB_REQUIRE(cp >= 1, "cp must be >= 1");
+  if (n_rows <= 0) return WLB_OK;
+  dkv_pull_kernel<<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
+      (const unsigned long long*)peer_bases, dk_off, dv_off, gather_local, n_rows, row_bytes / 16,
+      (float4*)dk, (float4*)dv, cp);
+  WLB_LAUNCH_CHECK();
+  return WLB_OK;
+}

@@ -14,7 +14,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 import paper_2503_17924_b200 as wl  # noqa: E402
-from paper_2503_17924_b200.cp import cp_doc_attention, shard_for_rank  # noqa: E402
+from paper_2503_17924_b200.cp import (CPStepPipeline, NcclExchange, SymmExchange,  # noqa: E402
+                                      cp_doc_attention, shard_for_rank)
 from oracle import attention_oracle as ao  # noqa: E402
 from oracle import shard_oracle as so  # noqa: E402
 
@@ -25,6 +26,54 @@ def check(name, got, ref, atol=2e-2, rtol=1e-2):
     err = (got - ref).abs()
     ok = bool((err <= atol + rtol * ref.abs()).all())
     return ok, f"{name}: max abs err {err.max().item():.3e} (ref max {ref.abs().max().item():.2f})"
+
+
+def pipeline_cases(rank, world, dev):
+    """CPStepPipeline over 3 micro-batches (slot reuse in the symmetric
+    exchange) with both exchanges: each vs the oracle, and symm == NCCL."""
+    failures = []
+    hq, hkv, d = 4, 2, 128
+    mbs = [so.pad_lengths_for_cp(x, world) for x in
+           ([900, 3, 129, 1000, 1], [2048], [300, 300, 1000, 17, 512, 33])]
+    plan = wl.build_shard_plan(mbs, world, "adaptive")
+    shards = [shard_for_rank(plan, b, rank) for b in range(len(mbs))]
+    g = torch.Generator().manual_seed(11)
+    full, inputs = [], []
+    for b, lengths in enumerate(mbs):
+        T = sum(lengths)
+        t = [torch.randn(T, h, d, generator=g).bfloat16() for h in (hq, hkv, hkv, hq)]
+        full.append(t)
+        idx = shards[b].gather_local.long().cpu()
+        inputs.append(tuple(x[idx].to(dev) for x in t))
+    t_max = max(sum(x) for x in mbs)
+    res = {}
+    for name, ex in (("nccl", NcclExchange()),
+                     ("symm", SymmExchange(dist.group.WORLD, t_max, hkv, d, dev))):
+        pipe = CPStepPipeline(exchange=ex)
+        for _ in range(2):                      # second pass reuses both slots again
+            outs = pipe.run(shards, inputs)
+        torch.cuda.synchronize()
+        res[name] = [[t.float().cpu() for t in o] for o in outs]
+    for b, lengths in enumerate(mbs):
+        q, k, v, do = full[b]
+        idx = shards[b].gather_local.long().cpu()
+        segs = [(p, 0, x) for p, x in enumerate(lengths)]
+        ro, _, rdq, rdk, rdv = ao.segment_attention_fwd_bwd(q, k, v, do, lengths, segs)
+        for name in res:
+            for tn, got, ref in zip(("o", "dq", "dk", "dv"), res[name][b],
+                                    (ro[idx], rdq[idx], rdk[idx], rdv[idx])):
+                ok, msg = check(tn, got, ref)
+                tag = f"[rank {rank} pipeline {name} mb{b}] {msg}"
+                print(tag, flush=True)
+                if not ok:
+                    failures.append(tag)
+        for tn, a, c in zip(("o", "dq", "dk", "dv"), res["nccl"][b], res["symm"][b]):
+            # same kernels, same reduction order over ranks is not guaranteed
+            # (NCCL ring vs peer sum): fp32 partial sums agree to rounding
+            err = (a - c).abs().max().item()
+            if err > 1e-3 * max(1.0, a.abs().max().item()):
+                failures.append(f"[rank {rank} mb{b}] symm vs nccl {tn}: {err:.3e}")
+    return failures
 
 
 def main():
@@ -64,6 +113,7 @@ def main():
             print(tag, flush=True)
             if not ok:
                 failures.append(tag)
+    failures += pipeline_cases(rank, world, dev)
     dist.barrier()
     dist.destroy_process_group()
     if failures:
