@@ -36,7 +36,8 @@ sys.path.insert(0, ROOT)
 
 import paper_2503_17924_b200 as wl  # noqa: E402
 from paper_2503_17924_b200.attention import attn_backward, attn_forward  # noqa: E402
-from paper_2503_17924_b200.cp import CPStepPipeline, build_cp_shards  # noqa: E402
+from paper_2503_17924_b200.cp import (CPStepPipeline, NcclExchange, SymmExchange,  # noqa: E402
+                                      build_cp_shards)
 
 N_SEQ = 8
 METRIC = "doc-masked attn TFLOP/s/GPU & CP rank imbalance (max/mean) at CP=1/2/4/8"
@@ -209,6 +210,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", default="symm", choices=["nccl", "symm"],
+                    help="CP K/V + dK/dV exchange: NCCL collectives or one-sided NVLink "
+                         "stores/loads on symmetric memory")
     ap.add_argument("--clock-ms", type=int, default=500,
                     help="nvidia-smi sampling period during the timed region (0: off)")
     args = ap.parse_args()
@@ -241,11 +245,14 @@ def main():
     ev = lambda: torch.cuda.Event(enable_timing=True)
     launches = [0]
 
-    pipe = CPStepPipeline(group)
+    symm = args.exchange == "symm" and cp > 1
+    exchange = SymmExchange(dist.group.WORLD, T, hkv, d, dev) if symm else NcclExchange(group)
+    pipe = CPStepPipeline(group, exchange=exchange)
+    ex_launches = (2 if symm else 4) if cp > 1 else 0      # push+pull | 2 scatters + 2 gathers
 
     def step(record=None):
         shards = build_cp_shards(lengths, cp, rank, "adaptive")
-        launches[0] += 1 + N_SEQ + N_SEQ * (5 + (4 if cp > 1 else 0))   # plan, tiles, attn, permutes
+        launches[0] += 1 + N_SEQ + N_SEQ * (5 + ex_launches)   # plan, tiles, attn, exchange
 
         def timed(b, sh, kernels):
             if record is None:
@@ -386,7 +393,8 @@ def main():
         "config": {"workload": wk["name"], "seq_len": T, "sequences_per_step": N_SEQ,
                    "heads": [hq, hkv], "head_dim": d, "cp": cp, "policy": "adaptive",
                    "strategies": strategies, "l2": "inputs > L2 (256 MiB per tensor)",
-                   "parallelism": f"cp{cp}"},
+                   "parallelism": f"cp{cp}",
+                   "exchange": args.exchange if cp > 1 else "none"},
         "tflops_per_gpu": round(value / world, 2),
         "frac_of_peak": round(value / world / peak_sus, 4),
         "frac_of_burst_peak": round(value / world / peak, 4),
