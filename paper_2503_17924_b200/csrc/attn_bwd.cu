@@ -28,6 +28,21 @@
 namespace wlb {
 using namespace sm100;
 
+#ifdef WLB_TRACE
+// development aid: per-iteration clock64 stamps of the first two CTAs
+__device__ long long g_bwd_trace[2][8][128];
+#define TRACE(ev, i)                                                            \
+  do {                                                                          \
+    if (blockIdx.x < 2 && (i) < 128 && (threadIdx.x & 31) == 0 &&               \
+        (threadIdx.x >> 5) == ((ev) < 3 ? 1 : (ev) < 6 ? 4 : 12))               \
+      g_bwd_trace[blockIdx.x][ev][i] = clock64();                               \
+  } while (0)
+#else
+#define TRACE(ev, i) \
+  do {               \
+  } while (0)
+#endif
+
 template <int D, int NCW = 2>
 struct BwdCfg {
   static_assert(NCW == 2, "two compute warpgroups (one 32-query half each)");
@@ -59,11 +74,12 @@ struct BwdCfg {
   static constexpr int THREADS = 128 + 128 * NCW + 128;   // + dQ drain warpgroup
 };
 
-struct BwdBars {  // 172 bytes; OFF_BAR reserves 256
+struct BwdBars {  // 180 bytes; OFF_BAR reserves 256
   uint64_t kv_full;
   uint64_t q_full[3], q_empty[3];
   uint64_t s_full[2], p_full[2], mma2_done[2], s_free[2];
   uint64_t vec_full[3], vec_empty[3];
+  uint64_t acc_done;
   uint32_t tmem_base;
 };
 
@@ -113,6 +129,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       mbar_init(&bars->mma2_done[i], 1);
       mbar_init(&bars->s_free[i], 128);
     }
+    mbar_init(&bars->acc_done, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(&bars->tmem_base, C::TMEM_COLS);
@@ -156,6 +173,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         if (i < n_iter) {
           const int b = i & 1, st = i % C::QS;
           mbar_wait(&bars->q_full[st], (i / C::QS) & 1);
+          TRACE(0, i);
           tc_fence_after();
           const uint32_t qs = q_b + st * C::Q_BYTES, dos = do_b + st * C::Q_BYTES;
           // S^T[b] was last read by the compute warps of tile i-2 (before p_full,
@@ -168,7 +186,8 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             mma_ss_w(tmem + C::COL_S + b * 64, sdesc_sw128(k_b + ko, 16, 1024),
                      sdesc_sw128(qs + qo, 16, 1024), C::IDESC_ST, kk > 0);
           }
-          if (i >= 2) mbar_wait(&bars->s_free[b], ((i - 2) >> 1) & 1);
+          if (i >= 2) mbar_wait_fast(&bars->s_free[b], ((i - 2) >> 1) & 1);
+          TRACE(1, i);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
@@ -181,25 +200,33 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         }
         if (i >= 1) {
           const int j = i - 1, b = j & 1, st = j % C::QS;
-          mbar_wait(&bars->p_full[b], (j >> 1) & 1);
+          mbar_wait_fast(&bars->p_full[b], (j >> 1) & 1);
+          TRACE(2, j);
           tc_fence_after();
           const uint32_t qs = q_b + st * C::Q_BYTES, dos = do_b + st * C::Q_BYTES;
           const uint32_t dss = ds_b + b * C::T_BYTES;
-#pragma unroll
-          for (int kk = 0; kk < C::BM / 16; ++kk) {   // contract over queries (A from TMEM)
-            const uint32_t acc = (j > 0) || (kk > 0);
-            mma_ts_w(tmem + C::COL_DV, tmem + C::COL_S + b * 64 + kk * 8,
-                     sdesc_sw128(dos + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
-            mma_ts_w(tmem + C::COL_DK, tmem + C::COL_DP + b * 64 + kk * 8,
-                     sdesc_sw128(qs + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
-          }
+          // dQ^T first: it lands in the dP^T[b] columns (free once the compute
+          // warps loaded dP^T), so the drain of tile j overlaps dV/dK(j) and
+          // S(j+2) instead of stalling dP(j+2).
 #pragma unroll
           for (int kk = 0; kk < C::BN / 16; ++kk) {   // contract over keys
             mma_ss_w(tmem + C::COL_DP + b * 64, sdesc_sw128(k_b + kk * 2048, C::KV_SLAB, 1024),
                    sdesc_sw128(dss + kk * 2048, C::KV_SLAB, 1024), C::IDESC_DQT, kk > 0);
           }
           mma_commit_w(&bars->mma2_done[b]);
+          // P^T / dS^T (packed bf16) sit in the S^T[b] columns: queries
+          // [32c, 32c+32) at column 32c (P) and 32c+16 (dS), 8 columns per K16
+#pragma unroll
+          for (int kk = 0; kk < C::BM / 16; ++kk) {   // contract over queries (A from TMEM)
+            const uint32_t acc = (j > 0) || (kk > 0);
+            const uint32_t ca = C::COL_S + b * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
+            mma_ts_w(tmem + C::COL_DV, tmem + ca,
+                     sdesc_sw128(dos + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
+            mma_ts_w(tmem + C::COL_DK, tmem + ca + 16,
+                     sdesc_sw128(qs + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
+          }
           mma_commit_w(&bars->q_empty[st]);
+          if (j == n_iter - 1) mma_commit_w(&bars->acc_done);
         }
       }
     }
@@ -236,6 +263,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       const int h = g * group + j / qt_per_head;
       const int row0 = kt.z + (j % qt_per_head) * C::BM;
       mbar_wait(&bars->mma2_done[b], (j >> 1) & 1);
+      TRACE(6, j);
       tc_fence_after();
       uint32_t u[64];
       tmem_ld32(lane_base + C::COL_DP + b * 64, *reinterpret_cast<uint32_t(*)[32]>(u));
@@ -243,6 +271,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&bars->s_free[b]);
+      TRACE(7, j);
       if (D == 128 || lane < 16) {
         float* ptr = dq_acc + ((size_t)row0 * Hq + h) * D + d;
         const int nvalid = min(C::BM, kt.w - row0);
@@ -268,6 +297,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       const int b = i & 1, vb = i % C::QS;
       mbar_wait(&bars->vec_full[vb], (i / C::QS) & 1);
       mbar_wait(&bars->s_full[b], (i >> 1) & 1);
+      TRACE(3, i);
       tc_fence_after();
       uint32_t us[32], ud[32];
       tmem_ld32(lane_base + C::COL_S + b * 64 + ch * 32, us);
@@ -280,6 +310,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       // (rows are position-sorted, so the first and last columns bound them).
       const bool full = kt.y == C::BN && vp4[0].x >= C::BN - 1 && vp4[7].w >= C::BN - 1;
       tmem_ld_wait();
+      TRACE(4, i);
       uint32_t pk[16], dk2[16];
 #pragma unroll
       for (int e4 = 0; e4 < 8; ++e4) {
@@ -310,13 +341,13 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       }
       tc_fence_before();
       mbar_arrive(&bars->vec_empty[vb]);
-      // P^T (packed bf16) over this half's S^T columns and dS^T over its dP^T
-      // columns: A operands of the TS dV / dK MMAs.  S^T / dP^T of tile i are in
-      // registers already; the previous readers (dV/dK/dQ of tile i-2) finished
-      // before MMA1(i) (s_full implies it).  dS^T also goes to SMEM as the B
-      // operand of dQ^T = K^T dS^T.
-      tmem_st16(lane_base + C::COL_S + b * 64 + ch * 16, pk);
-      tmem_st16(lane_base + C::COL_DP + b * 64 + ch * 16, dk2);
+      // P^T and dS^T (packed bf16) over THIS warp's own 32 S^T columns (no
+      // other warp reads them): A operands of the TS dV / dK MMAs.  The
+      // previous readers (dV/dK of tile i-2) finished before MMA1(i)
+      // (s_full implies it).  dP^T[b] is free once loaded: dQ^T(i) goes
+      // there.  dS^T also goes to SMEM as the B operand of dQ^T = K^T dS^T.
+      tmem_st16(lane_base + C::COL_S + b * 64 + ch * 32, pk);
+      tmem_st16(lane_base + C::COL_S + b * 64 + ch * 32 + 16, dk2);
       uint8_t* drow = sDS + b * C::T_BYTES + t * 128;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -326,13 +357,11 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       fence_proxy_async_smem();
       tmem_st_wait();
       tc_fence_before();
+      TRACE(5, i);
       mbar_arrive(&bars->p_full[b]);
     }
-    {   // the last MMA group wrote the final dV / dK
-      const int j = n_iter - 1;
-      mbar_wait(&bars->mma2_done[j & 1], (j >> 1) & 1);
-      tc_fence_after();
-    }
+    mbar_wait(&bars->acc_done, n_iter > 0 ? 0 : 1);   // the last MMA group wrote dV / dK
+    tc_fence_after();
     // ------------------------------------------------------------ epilogue --
     // TMEM loads are warp-collective: issue converged, predicate the stores.
     float* dvr = dv + ((size_t)(kt.x + t) * Hkv + g) * D + ch * (D / 2);
@@ -551,6 +580,13 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
 }
 
 }  // namespace wlb
+
+#ifdef WLB_TRACE
+extern "C" int wlb_debug_bwd_trace(void* host) {
+  WLB_CUDA_TRY(cudaMemcpyFromSymbol(host, wlb::g_bwd_trace, sizeof(wlb::g_bwd_trace)));
+  return WLB_OK;
+}
+#endif
 
 extern "C" size_t wlb_attn_bwd_workspace(int32_t Tl, int32_t T, int32_t Hq, int32_t Hkv, int32_t D,
                                          int32_t n_docs) {

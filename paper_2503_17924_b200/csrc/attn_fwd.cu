@@ -28,12 +28,32 @@
 #include "sm100.cuh"
 #include "tmap.cuh"
 
+#ifndef WLB_FWD_TURNS
+#define WLB_FWD_TURNS 0   // 1: strict X/Y alternation of the softmax warpgroups
+                          //    (measured 7% slower: a lone softmax warp is
+                          //    issue/MUFU-latency bound, not contended)
+#endif
 #ifndef WLB_FWD_POLY
-#define WLB_FWD_POLY 8   // 0: MUFU only; k: one column pair in k uses the polynomial
+#define WLB_FWD_POLY 3   // column pairs (of every 8) whose exp2 runs on the FMA pipe
 #endif
 
 namespace wlb {
 using namespace sm100;
+
+#ifdef WLB_TRACE
+// development aid: per-KV-step clock64 stamps of the first CTA
+__device__ long long g_fwd_trace[12][256];
+#define FTRACE(ev, j)                                                           \
+  do {                                                                          \
+    if (blockIdx.x == 0 && (j) < 256 && (threadIdx.x & 31) == 0 &&              \
+        (threadIdx.x >> 5) == ((ev) < 2 || (ev) == 8 ? 1 : (ev) < 5 || (ev) > 8 ? 4 : 8))   \
+      g_fwd_trace[ev][j] = clock64();                                           \
+  } while (0)
+#else
+#define FTRACE(ev, j) \
+  do {                \
+  } while (0)
+#endif
 
 template <int D>
 struct FwdCfg {
@@ -164,10 +184,12 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       const int sp = (j - 1) % C::STAGES;
       mbar_wait(&bars->v_full[sp], ((j - 1) / C::STAGES) & 1);
       if (j < n_kv[0]) mbar_wait(&bars->k_full[j % C::STAGES], (j / C::STAGES) & 1);
+      FTRACE(8, j - 1);
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         if (j - 1 < n_kv[t]) {
-          mbar_wait(&bars->p_full[t], (j - 1) & 1);
+          mbar_wait_fast(&bars->p_full[t], (j - 1) & 1);
+          FTRACE(t, j - 1);
           tc_fence_after();
           pv(t, j - 1);                          // reads P_t before QK overwrites S_t
           if (j < n_kv[t]) qk(t, j);
@@ -193,6 +215,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       float m_run = -INFINITY, l_run = 0.f;
       for (int j = 0; j < nkv; ++j) {
         mbar_wait(&bars->s_full[t], j & 1);
+        FTRACE(2 + 3 * t, j);
         tc_fence_after();
         // all 128 scores of this row in registers (one TMEM wait per tile:
         // a chunked two-pass variant re-reading S measured ~40% slower)
@@ -205,50 +228,66 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
           for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(u[i]);
         }
         tmem_ld_wait();
+        // Softmax turns: Y(j) runs after X(j), X(j+1) after Y(j), so each
+        // warpgroup's exp2 work has the SMSP pipes to itself while the tensor
+        // pipe works on the other tile (overlapping them stretched both).
+        if (WLB_FWD_TURNS) {
+          if (t == 1)
+            named_bar_sync(1, 256);
+          else if (j >= 1 && j - 1 < n_kv[1])
+            named_bar_sync(2, 256);
+        }
+        FTRACE(3 + 3 * t, j);
         const int lim = lim0 - j * C::BN;
         const bool full = __all_sync(0xffffffffu, lim >= C::BN);
-        float mt = -INFINITY;
+        // row max as 4 independent chains (a single 128-long dependent
+        // FMNMX chain sat on the softmax critical path)
+        float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
         if (full) {
 #pragma unroll
-          for (int c = 0; c < C::BN; ++c) mt = fmaxf(mt, sv[c]);
+          for (int c = 0; c < C::BN; ++c) mx[c & 3] = fmaxf(mx[c & 3], sv[c]);
         } else {
 #pragma unroll
           for (int c = 0; c < C::BN; ++c) {
             sv[c] = c < lim ? sv[c] : -INFINITY;
-            mt = fmaxf(mt, sv[c]);
+            mx[c & 3] = fmaxf(mx[c & 3], sv[c]);
           }
         }
+        const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+        if (t == 0) FTRACE(9, j);
         const float m_new = fmaxf(m_run, mt * scale_log2);
         const bool rescale = __any_sync(0xffffffffu, m_new > m_run + 8.f);
         const float m_use = rescale ? m_new : m_run;
         const float alpha = ex2(m_run - m_use);
         // P = exp2(S*scale - m), written back as packed bf16 over the first 64
         // columns of S (P chunk c lands in S columns [16c, 16c+16), already
-        // consumed).  Optionally one column pair in WLB_FWD_POLY takes the
-        // polynomial exp2 to offload the MUFU.
-        float lsum = 0.f;
+        // consumed).
+        // Packed pairs: x = S*scale - m by FFMA2, row sums by FADD2 (two
+        // independent accumulators), WLB_FWD_POLY of every 8 column pairs take
+        // the FMA-pipe polynomial exp2, the rest the MUFU.
+        float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m_use, -m_use);
 #pragma unroll
         for (int c = 0; c < C::BN / 32; ++c) {
           uint32_t p[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int col = c * 32 + 2 * i;
-            const float x0 = fmaf(sv[col], scale_log2, -m_use);
-            const float x1 = fmaf(sv[col + 1], scale_log2, -m_use);
-            float p0, p1;
-            if (WLB_FWD_POLY && (i % (WLB_FWD_POLY > 0 ? WLB_FWD_POLY : 1)) == WLB_FWD_POLY - 1) {
-              p0 = ex2_poly(x0);
-              p1 = ex2_poly(x1);
+            const float2 x = ffma2(make_float2(sv[col], sv[col + 1]), sc2, nm2);
+            float2 pp;
+            if ((i & 7) < WLB_FWD_POLY) {
+              pp = ex2_poly2(x);
             } else {
-              p0 = ex2(x0);
-              p1 = ex2(x1);
+              pp.x = ex2(x.x);
+              pp.y = ex2(x.y);
             }
-            lsum += p0 + p1;
-            p[i] = pack_bf16(p0, p1);
+            ls[i & 1] = fadd2(ls[i & 1], pp);
+            p[i] = pack_bf16(pp.x, pp.y);
           }
           tmem_st16(s_col + c * 16, p);
         }
-        l_run = l_run * alpha + lsum;
+        if (t == 0) FTRACE(10, j);
+        l_run = l_run * alpha + ((ls[0].x + ls[0].y) + (ls[1].x + ls[1].y));
         if (rescale && j > 0) {                // PV(j-1) complete (ordered before QK(j))
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
@@ -261,8 +300,16 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
           }
         }
         tmem_st_wait();
+        if (t == 0) FTRACE(11, j);
         tc_fence_before();
+        FTRACE(4 + 3 * t, j);
         mbar_arrive(&bars->p_full[t]);
+        if (WLB_FWD_TURNS) {
+          if (t == 0 && j < n_kv[1])
+            named_bar_arrive(1, 256);
+          else if (t == 1 && j + 1 < n_kv[0])
+            named_bar_arrive(2, 256);
+        }
         m_run = m_use;
       }
       // ---------------------------------------------------------- epilogue --
@@ -320,6 +367,13 @@ static int launch_fwd(const void* q, const void* k, const void* v, void* o, floa
 }
 
 }  // namespace wlb
+
+#ifdef WLB_TRACE
+extern "C" int wlb_debug_fwd_trace(void* host) {
+  WLB_CUDA_TRY(cudaMemcpyFromSymbol(host, wlb::g_fwd_trace, sizeof(wlb::g_fwd_trace)));
+  return WLB_OK;
+}
+#endif
 
 extern "C" int wlb_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
                             const int32_t* tiles, const int32_t* n_tiles, int32_t max_tiles,

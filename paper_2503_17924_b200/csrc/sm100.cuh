@@ -56,6 +56,43 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Fast-reacting wait for the single MMA-issuing warp: a suspended warp is
+// woken ~300 cycles after the phase flips (measured), which sits directly on
+// the softmax -> MMA critical path.  WLB_MMA_WAIT: 0 suspend-hinted try_wait,
+// 1 try_wait with the default (short) limit, 2 test_wait poll.
+#ifndef WLB_MMA_WAIT
+#define WLB_MMA_WAIT 1
+#endif
+__device__ __forceinline__ void mbar_wait_fast(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+#if WLB_MMA_WAIT == 0
+  while (!mbar_try_wait(a, parity)) {
+  }
+#elif WLB_MMA_WAIT == 1
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+#else
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+#endif
+}
+
 // expect_tx issued once per warp (warp-uniform call site)
 __device__ __forceinline__ void mbar_expect_tx_w(uint64_t* bar, uint32_t bytes) {
   asm volatile(
@@ -239,6 +276,46 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+// Hardware named barriers (id 0 is __syncthreads); count = threads in total.
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2): one issue slot for two lanes of math.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+// ex2_poly on a pair with packed math (same polynomial and rounding trick)
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 t = fadd2(x, make_float2(12582912.f, 12582912.f));   // 1.5 * 2^23
+  const float2 u = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = ffma2(u, make_float2(-1.f, -1.f), x);             // x - round(x)
+  float2 p = ffma2(make_float2(0.055008892f, 0.055008892f), f, make_float2(0.242211f, 0.242211f));
+  p = ffma2(p, f, make_float2(0.69328296f, 0.69328296f));
+  p = ffma2(p, f, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

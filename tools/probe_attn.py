@@ -17,10 +17,13 @@ ap.add_argument("--hkv", type=int, default=32)
 ap.add_argument("--d", type=int, default=128)
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--single", action="store_true")
+ap.add_argument("--doc", type=int, default=0, help="uniform documents of this length")
 a = ap.parse_args()
 lengths = [d.length for d in wl.generate_synthetic_stream(wl.SyntheticSpec(a.T, a.T), 0, a.batch + 1)[a.batch]]
 if a.single:
     lengths = [a.T]
+if a.doc:
+    lengths = [a.doc] * (a.T // a.doc)
 plan = wl.build_shard_plan([lengths], 1, "per_document")
 g, pos, ro = plan.rank_local(0, 0)
 tiles = build_tiles(ro, pos, lengths)
