@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _native
 from .errors import ConfigError
-from .workload import CostProfile, Document, MicroBatch, attention_workload
+from .workload import CostProfile, Document, MicroBatch, attention_workload, latency_of_lengths
 
 
 @dataclass
@@ -156,3 +156,12 @@ def imbalance_degree_attention(microbatches) -> float:
     if not works or total == 0:
         return 1.0
     return max(works) * len(works) / total
+
+
+def imbalance_degree_latency(microbatches, pp_size: int, profile: CostProfile) -> float:
+    """max latency * pp_size / total latency (`packing.py:437-449`)."""
+    lats = [latency_of_lengths(mb.lengths(), profile) for mb in microbatches]
+    total = sum(lats)
+    if not lats or total == 0:
+        return 1.0
+    return max(lats) * pp_size / total

@@ -194,6 +194,45 @@ def records(b):
     print("wrote records_plans.jsonl, records_shards.jsonl")
 
 
+def pipeline_model(b):
+    """Stage pricing and the 1F1B critical path (pipeline.py:60-86, packing.py:437-449)."""
+    from balsim.pipeline import StageLatency, pp_critical_path, stage_latency_for_assignment
+    from balsim.packing import imbalance_degree_latency
+    from balsim.sharding import shard
+    rng = np.random.default_rng(99)
+    prof = b.CostProfile()
+    cases = []
+    for i in range(40):
+        cp = int(rng.choice([1, 2, 4, 8]))
+        pp = int(rng.choice([1, 2, 4]))
+        k = int(rng.integers(1, 12))
+        lengths = [int(x) for x in rng.integers(1, 6000, size=k)]
+        pad = -sum(lengths) % (2 * cp)
+        if pad:
+            lengths.append(pad)
+        mb = b.MicroBatch([b.Document(j, x) for j, x in enumerate(lengths)])
+        par = b.ParallelismConfig(context_window=65536, cp=cp, pp=pp)
+        policy = ["per_sequence", "per_document", "adaptive"][i % 3]
+        st = stage_latency_for_assignment(shard(mb, cp, policy, prof), par, prof)
+        cases.append({"lengths": lengths, "cp": cp, "pp": pp, "policy": policy,
+                      "forward": st.forward.hex(), "backward": st.backward.hex()})
+    paths = []
+    for _ in range(30):
+        n = int(rng.integers(0, 10))
+        pp = int(rng.integers(1, 6))
+        stages = [StageLatency(float(f), float(f) * 2) for f in rng.uniform(0.01, 1.0, size=n)]
+        paths.append({"stages": [[s.forward.hex(), s.backward.hex()] for s in stages], "pp": pp,
+                      "out": pp_critical_path(stages, pp).hex()})
+    imb = []
+    for _ in range(20):
+        mbs = [b.MicroBatch([b.Document(j, int(x)) for j, x in
+                             enumerate(rng.integers(1, 9000, size=int(rng.integers(1, 8))))])
+               for _ in range(int(rng.integers(1, 9)))]
+        imb.append({"mbs": [m.lengths() for m in mbs],
+                    "out": imbalance_degree_latency(mbs, len(mbs), prof).hex()})
+    _dump("pipeline_model.json.gz", {"stages": cases, "paths": paths, "imbalance_latency": imb})
+
+
 def main():
     b = _import_reference()
     sharding_random(b)
@@ -201,6 +240,7 @@ def main():
     kernels(b)
     packer_config5(b)
     records(b)
+    pipeline_model(b)
 
 
 if __name__ == "__main__":
