@@ -390,6 +390,460 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
   if (warp == 2) tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
+// ---------------------------------------------------------------------------
+// v3 (D = 128): 128-query tiles, every MMA N = 128.
+//
+// The v2 kernel above is bound by shared-memory operand bandwidth (128 B/clk
+// per SM): its N = 64 SS MMAs re-read the 32 KB K / V / K^T operands once per
+// 64 queries.  Here a tile has 128 queries, so each of S^T, dP^T and dQ^T is
+// one M=128 N=128 MMA chain (full rate) and the A operands are re-read half as
+// often.  TMEM (512 columns) then holds exactly one S^T and one dP^T:
+//
+//   [0,128)   S^T (fp32)  -> P^T (bf16, cols 64c..64c+32) and dS^T (bf16,
+//             cols 64c+32..64c+64) for query half c, written by the warps that
+//             read those S^T columns
+//   [128,256) dP^T (fp32) -> dQ^T (fp32) once the compute warps have read dP^T
+//   [256,384) dV, [384,512) dK accumulators
+//
+// Per tile the tensor pipe runs S | dP | dV | dK | dQ^T with no double
+// buffering; the compute warps hide inside it instead:
+//   * P for tile i is computed while dP^T(i) runs and is handed over in two
+//     32-query chunks (p_full[c]), so dV(i) starts on chunk 0;
+//   * dS is computed while dV(i) runs, again in two chunks (ds_full[c]);
+//   * the dQ drain warps load dQ^T(i) while S(i+1) runs (s_free gates dP(i+1)).
+// ---------------------------------------------------------------------------
+#ifdef WLB_TRACE
+__device__ long long g_bwd3_trace[16][128];
+#define TRACE3(ev, i)                                                             \
+  do {                                                                            \
+    if (blockIdx.x == 0 && (i) < 128 && (threadIdx.x & 31) == 0)                  \
+      g_bwd3_trace[ev][i] = clock64();                                            \
+  } while (0)
+#else
+#define TRACE3(ev, i) \
+  do {                \
+  } while (0)
+#endif
+
+struct Bwd3Cfg {
+  static constexpr int D = 128, BM = 128, BN = 128;
+  static constexpr int KV_BYTES = BN * D * 2, Q_BYTES = BM * D * 2, T_BYTES = BN * BM * 2;
+  static constexpr int SLAB = 128 * 128;   // 128 rows x 128 B (64 bf16) swizzle slab
+  static constexpr int QS = 2;             // Q/dO + query-vector ring depth
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = OFF_K + KV_BYTES;
+  static constexpr int OFF_Q = OFF_V + KV_BYTES;
+  static constexpr int OFF_DO = OFF_Q + QS * Q_BYTES;
+  static constexpr int OFF_DS = OFF_DO + QS * Q_BYTES;              // dS^T, 2 query slabs
+  static constexpr int OFF_VEC = OFF_DS + T_BYTES;                  // QS x {-lse2, delta}[BM] f32
+  static constexpr int OFF_POS = OFF_VEC + QS * 2 * BM * 4;         // QS x rel. position[BM] i8
+  static constexpr int OFF_BAR = OFF_POS + QS * BM;
+  static constexpr int SMEM = OFF_BAR + 192;
+  static constexpr uint32_t TMEM_COLS = 512;
+  static constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 384;
+  static constexpr uint32_t IDESC_ST = idesc_bf16(BN, BM, 0, 0);    // S^T, dP^T
+  static constexpr uint32_t IDESC_ACC = idesc_bf16(BN, D, 0, 1);    // dV, dK
+  static constexpr uint32_t IDESC_DQ = idesc_bf16(BM, D, 1, 1);     // dQ
+  static constexpr int THREADS = 512;
+};
+static_assert(Bwd3Cfg::SMEM <= 232448, "bwd v3 exceeds the 227 KB SMEM window");
+
+struct Bwd3Bars {
+  uint64_t kv_full;
+  uint64_t q_full[2], q_empty[2], vec_full[2], vec_empty[2];
+  uint64_t s_full, dp_full, p_full[2], ds_full[2], dq_full, s_free, acc_done;
+  uint32_t tmem_base;
+};
+static_assert(sizeof(Bwd3Bars) <= 192, "barrier block");
+
+#ifndef WLB_BWD_V3
+#define WLB_BWD_V3 1     // 0: D = 128 uses the v2 (64-query) kernel
+#endif
+#ifndef WLB_BWD_POLY
+#define WLB_BWD_POLY 0   // column pairs (of every 8) whose exp2 runs on the FMA pipe
+#endif
+
+// P for one 32-query chunk of one key row: p = exp2(s * scale_log2 + nl[q]),
+// zero where the key is past the row's position (MASK) -> packed bf16 pairs.
+template <bool MASK>
+__device__ __forceinline__ void bwd3_p_chunk(const uint32_t (&us)[32], const float* nl,
+                                             const int8_t* rp, int t, bool key_ok,
+                                             float scale_log2, uint32_t (&pk)[16]) {
+  const float2 sc2 = make_float2(scale_log2, scale_log2);
+  const float4* n4 = reinterpret_cast<const float4*>(nl);
+  int8_t pos[32];
+  if (MASK) {
+    *reinterpret_cast<int4*>(pos) = reinterpret_cast<const int4*>(rp)[0];
+    *reinterpret_cast<int4*>(pos + 16) = reinterpret_cast<const int4*>(rp)[1];
+  }
+#pragma unroll
+  for (int e4 = 0; e4 < 8; ++e4) {
+    const float4 l4 = n4[e4];
+#pragma unroll
+    for (int u2 = 0; u2 < 2; ++u2) {
+      const int e = 4 * e4 + 2 * u2;
+      const float2 x = ffma2(make_float2(__uint_as_float(us[e]), __uint_as_float(us[e + 1])), sc2,
+                             u2 ? make_float2(l4.z, l4.w) : make_float2(l4.x, l4.y));
+      float2 pp;
+      if (((e >> 1) & 7) < WLB_BWD_POLY) {
+        pp = ex2_poly2(x);
+      } else {
+        pp.x = ex2(x.x);
+        pp.y = ex2(x.y);
+      }
+      if (MASK) {
+        pp.x = (key_ok && pos[e] >= t) ? pp.x : 0.f;
+        pp.y = (key_ok && pos[e + 1] >= t) ? pp.y : 0.f;
+      }
+      pk[e >> 1] = pack_bf16(pp.x, pp.y);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(512, 1)
+attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                 const float* __restrict__ lse, const float* __restrict__ delta,
+                 float* __restrict__ dq_acc, float* __restrict__ dk, float* __restrict__ dv,
+                 const int4* __restrict__ kv_tiles, const int* __restrict__ n_kv_tiles,
+                 const int* __restrict__ positions, int Tl, int Hq, int Hkv, int n_slots,
+                 float scale, float scale_log2) {
+  using C = Bwd3Cfg;
+  constexpr int D = C::D;
+  extern __shared__ uint8_t smem_raw[];
+  if (smem_u32(smem_raw) & 1023) __trap();
+  uint8_t* smem = smem_raw;
+  const int item = blockIdx.x % n_slots, g = blockIdx.x / n_slots;
+  if (item >= n_kv_tiles[0]) return;
+  const int4 kt = kv_tiles[2 * item];
+  const int k0 = kv_tiles[2 * item + 1].x;
+  const int group = Hq / Hkv;
+  const int qt_per_head = (kt.w - kt.z + C::BM - 1) / C::BM;
+  const int n_iter = qt_per_head * group;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  Bwd3Bars* bars = reinterpret_cast<Bwd3Bars*>(smem + C::OFF_BAR);
+  uint8_t* sK = smem + C::OFF_K;
+  uint8_t* sV = smem + C::OFF_V;
+  uint8_t* sQ = smem + C::OFF_Q;
+  uint8_t* sDO = smem + C::OFF_DO;
+  uint8_t* sDS = smem + C::OFF_DS;
+  float* sVec = reinterpret_cast<float*>(smem + C::OFF_VEC);
+  int8_t* sPos = reinterpret_cast<int8_t*>(smem + C::OFF_POS);
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars->kv_full, 1);
+    for (int i = 0; i < C::QS; ++i) {
+      mbar_init(&bars->q_full[i], 1);
+      mbar_init(&bars->q_empty[i], 1);
+      mbar_init(&bars->vec_full[i], 32);
+      mbar_init(&bars->vec_empty[i], 256);
+    }
+    mbar_init(&bars->s_full, 1);
+    mbar_init(&bars->dp_full, 1);
+    for (int c = 0; c < 2; ++c) {
+      mbar_init(&bars->p_full[c], 256);
+      mbar_init(&bars->ds_full[c], 256);
+    }
+    mbar_init(&bars->dq_full, 1);
+    mbar_init(&bars->s_free, 128);
+    mbar_init(&bars->acc_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(&bars->tmem_base, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp < 4) setmaxnreg_dec<80>();   // TMA / MMA / alloc / vector warps
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer --
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    tma_prefetch(&tmDO);
+    mbar_expect_tx_w(&bars->kv_full, 2 * C::KV_BYTES);
+    for (int s = 0; s < 2; ++s) {
+      tma_load_3d_w(sK + s * C::SLAB, &tmK, &bars->kv_full, s * 64, g, kt.x);
+      tma_load_3d_w(sV + s * C::SLAB, &tmV, &bars->kv_full, s * 64, g, kt.x);
+    }
+    for (int i = 0; i < n_iter; ++i) {
+      const int st = i % C::QS;
+      const int h = g * group + i / qt_per_head;
+      const int row = kt.z + (i % qt_per_head) * C::BM;
+      mbar_wait(&bars->q_empty[st], ((i / C::QS) & 1) ^ 1);
+      mbar_expect_tx_w(&bars->q_full[st], 2 * C::Q_BYTES);
+      for (int s = 0; s < 2; ++s) {
+        tma_load_3d_w(sQ + st * C::Q_BYTES + s * C::SLAB, &tmQ, &bars->q_full[st], s * 64, h, row);
+        tma_load_3d_w(sDO + st * C::Q_BYTES + s * C::SLAB, &tmDO, &bars->q_full[st], s * 64, h, row);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer --
+    // Tensor-pipe order (steady state):
+    //   ... dV(i-1) | S(i) | dQ(i-1) | dK(i-1) | dP(i) | dV(i) | S(i+1) | ...
+    // so P(i) is computed under dQ(i-1), dK(i-1) and dP(i), dS(i) under dV(i)
+    // and S(i+1), and the dQ(i-1) drain under dK(i-1).  S(i) may overwrite the
+    // S^T columns as soon as dV(i-1) has read P^T(i-1) (same in-order pipe):
+    // dS^T lives only in SMEM, and dK reads it from there (SS MMA).
+    const uint32_t k_b = smem_u32(sK), v_b = smem_u32(sV), q_b = smem_u32(sQ),
+                   do_b = smem_u32(sDO), ds_b = smem_u32(sDS);
+    mbar_wait(&bars->kv_full, 0);
+    for (int i = 0; i <= n_iter; ++i) {
+      if (i < n_iter) {
+        const int st = i % C::QS;
+        const uint32_t qs = q_b + st * C::Q_BYTES;
+        mbar_wait(&bars->q_full[st], (i / C::QS) & 1);
+        TRACE3(0, i);
+        tc_fence_after();
+        // S^T = K Q^T (contract over D; K-major both)
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t o = (kk >> 2) * C::SLAB + (kk & 3) * 32;
+          mma_ss_w(tmem + C::COL_S, sdesc_sw128(k_b + o, 16, 1024), sdesc_sw128(qs + o, 16, 1024),
+                   C::IDESC_ST, kk > 0);
+        }
+        mma_commit_w(&bars->s_full);
+      }
+      if (i >= 1) {
+        const int j = i - 1, st = j % C::QS;
+        const uint32_t qs = q_b + st * C::Q_BYTES;
+        mbar_wait_fast(&bars->ds_full[0], j & 1);
+        mbar_wait_fast(&bars->ds_full[1], j & 1);
+        TRACE3(5, j);
+        tc_fence_after();
+        // dQ = dS K (contract over keys; A = dS from the dS^T buffer and B = K,
+        // both MN-major): lanes = queries, so the drain emits 16-B reductions
+#pragma unroll
+        for (int kk = 0; kk < C::BN / 16; ++kk)
+          mma_ss_w(tmem + C::COL_DP, sdesc_sw128(ds_b + kk * 2048, C::SLAB, 1024),
+                   sdesc_sw128(k_b + kk * 2048, C::SLAB, 1024), C::IDESC_DQ, kk > 0);
+        mma_commit_w(&bars->dq_full);
+        // dK += dS^T Q (contract over queries; A = dS^T K-major from SMEM)
+#pragma unroll
+        for (int kk = 0; kk < C::BM / 16; ++kk)
+          mma_ss_w(tmem + C::COL_DK, sdesc_sw128(ds_b + (kk >> 2) * C::SLAB + (kk & 3) * 32, 16, 1024),
+                   sdesc_sw128(qs + kk * 2048, C::SLAB, 1024), C::IDESC_ACC, (j > 0) || (kk > 0));
+        mma_commit_w(&bars->q_empty[st]);
+        if (j == n_iter - 1) mma_commit_w(&bars->acc_done);
+      }
+      if (i < n_iter) {
+        const int st = i % C::QS;
+        const uint32_t dos = do_b + st * C::Q_BYTES;
+        const uint32_t ph = i & 1;
+        // dP^T = V dO^T into the columns dQ(i-1) occupied: wait for the drain
+        if (i >= 1) mbar_wait_fast(&bars->s_free, (i - 1) & 1);
+        TRACE3(1, i);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t o = (kk >> 2) * C::SLAB + (kk & 3) * 32;
+          mma_ss_w(tmem + C::COL_DP, sdesc_sw128(v_b + o, 16, 1024), sdesc_sw128(dos + o, 16, 1024),
+                   C::IDESC_ST, kk > 0);
+        }
+        mma_commit_w(&bars->dp_full);
+        // dV += P^T dO, contract over queries, A = P^T from TMEM; chunk c holds
+        // queries [32c, 32c+32) of both 64-query halves
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          mbar_wait_fast(&bars->p_full[c], ph);
+          TRACE3(2 + c, i);
+          tc_fence_after();
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+            for (int sub = 0; sub < 2; ++sub) {
+              const int kk = hf * 4 + c * 2 + sub;   // queries [16kk, 16kk+16)
+              mma_ts_w(tmem + C::COL_DV, tmem + C::COL_S + 64 * hf + 16 * c + 8 * sub,
+                       sdesc_sw128(dos + kk * 2048, C::SLAB, 1024), C::IDESC_ACC,
+                       (i > 0) || (c | hf | sub));
+            }
+        }
+      }
+    }
+  } else if (warp == 3) {
+    // ------------------------------------------------- per-query vectors --
+    for (int i = 0; i < n_iter; ++i) {
+      const int b = i % C::QS;
+      const int h = g * group + i / qt_per_head;
+      const int row0 = kt.z + (i % qt_per_head) * C::BM;
+      mbar_wait(&bars->vec_empty[b], ((i / C::QS) & 1) ^ 1);
+      float* vec = sVec + b * 2 * C::BM;
+      int8_t* rp = sPos + b * C::BM;
+#pragma unroll
+      for (int e = lane; e < C::BM; e += 32) {
+        const int row = row0 + e;
+        const bool ok = row < kt.w;
+        vec[e] = ok ? -lse[(size_t)h * Tl + row] * 1.4426950408889634f : 0.f;
+        vec[C::BM + e] = ok ? delta[(size_t)h * Tl + row] : 0.f;
+        rp[e] = (int8_t)(ok ? min(positions[row] - k0, 127) : -1);
+      }
+      mbar_arrive(&bars->vec_full[b]);
+    }
+  } else if (warp >= 12) {
+    // ------------------------------------------------------------ dQ drain --
+    const int lg = warp & 3;             // TMEM lane quarter = 32 query rows
+    const uint32_t lane_base = tmem + ((uint32_t)(lg * 32) << 16);
+    // dq_acc layout [Hq][D/4][Tl][4]: the warp's 32 query rows of one 4-float
+    // column block are 512 contiguous bytes -> one coalesced 16-B-per-lane RED.
+    // The whole 128-column dQ row is loaded at once (192 registers via
+    // setmaxnreg), so the dP^T/dQ columns are released right away; the 32
+    // reductions are then paced over the next tile (after dp_full, ds_full[0],
+    // ds_full[1] of tile j+1) instead of bursting into L2 at once: a burst
+    // backed up the SM's memory queues and stalled the compute warps' TMEM
+    // loads.  (dp_full / ds_full of tile j+2 need s_free(j+1) from this warp,
+    // so those waits cannot alias a later phase.)
+    setmaxnreg_inc<160>();
+    const size_t blk = (size_t)Tl * 4;
+    for (int j = 0; j < n_iter; ++j) {
+      const int h = g * group + j / qt_per_head;
+      const int row = kt.z + (j % qt_per_head) * C::BM + lg * 32 + lane;
+#ifdef WLB_EXP_NORED
+      const bool ok = false;   // timing experiment: no dQ reductions (wrong dQ)
+#else
+      const bool ok = row < kt.w;
+#endif
+      float* base = dq_acc + (size_t)h * (D / 4) * blk + (size_t)row * 4;
+      mbar_wait(&bars->dq_full, j & 1);
+      if (warp == 12) TRACE3(12, j);
+      tc_fence_after();
+      uint32_t u[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        tmem_ld32(lane_base + C::COL_DP + c * 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32 * c));
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&bars->s_free);
+      if (warp == 12) TRACE3(13, j);
+      const bool last = j + 1 == n_iter;
+      const uint32_t nph = (j + 1) & 1;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (!last) {
+          if (c == 1) mbar_wait(&bars->dp_full, nph);
+          if (c == 2) mbar_wait(&bars->ds_full[0], nph);
+          if (c == 3) mbar_wait(&bars->ds_full[1], nph);
+        }
+        if (ok) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            red_add_v4(base + (size_t)(c * 8 + e) * blk, __uint_as_float(u[32 * c + 4 * e]) * scale,
+                       __uint_as_float(u[32 * c + 4 * e + 1]) * scale,
+                       __uint_as_float(u[32 * c + 4 * e + 2]) * scale,
+                       __uint_as_float(u[32 * c + 4 * e + 3]) * scale);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------- compute --
+    setmaxnreg_inc<136>();
+    const int lg = warp & 3;                 // TMEM lane quarter
+    const int hf = (warp - 4) >> 2;          // query half [64hf, 64hf+64)
+    const int t = lg * 32 + lane;            // key row in the tile
+    const bool key_ok = t < kt.y;
+    const uint32_t lane_base = tmem + ((uint32_t)(lg * 32) << 16);
+    uint8_t* drow = sDS + hf * C::SLAB + t * 128;
+
+    for (int i = 0; i < n_iter; ++i) {
+      const int vb = i % C::QS;
+      const uint32_t ph = i & 1;
+      const float* nl = sVec + vb * 2 * C::BM + 64 * hf;
+      const float* dl = nl + C::BM;
+      const int8_t* rp = sPos + vb * C::BM + 64 * hf;
+      mbar_wait(&bars->vec_full[vb], (i / C::QS) & 1);
+      mbar_wait(&bars->s_full, ph);
+      if (warp == 4) TRACE3(6, i);
+      tc_fence_after();
+      uint32_t pk[2][16];   // P (bf16 pairs), kept for dS
+      // ---- P^T = exp2(S^T * scale * log2e - lse2), per 32-query chunk
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t us[32];
+        tmem_ld32(lane_base + C::COL_S + 64 * hf + 32 * c, us);
+        const bool full = kt.y == C::BN && rp[32 * c] >= C::BN - 1 && rp[32 * c + 31] >= C::BN - 1;
+        tmem_ld_wait();
+        if (warp == 4 && c == 0) TRACE3(14, i);
+        if (full)
+          bwd3_p_chunk<false>(us, nl + 32 * c, rp + 32 * c, t, key_ok, scale_log2, pk[c]);
+        else
+          bwd3_p_chunk<true>(us, nl + 32 * c, rp + 32 * c, t, key_ok, scale_log2, pk[c]);
+        if (warp == 4 && c == 0) TRACE3(15, i);
+        // over S^T columns this warp already loaded (chunk 0's 32 columns)
+        tmem_st16(lane_base + C::COL_S + 64 * hf + 16 * c, pk[c]);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&bars->p_full[c]);
+        if (warp == 4) TRACE3(7 + c, i);
+      }
+      // ---- dS^T = P^T (dP^T - Delta), per chunk, into SMEM (for dQ and dK)
+      // (the buffer's previous readers, dQ(i-1) and dK(i-1), were issued
+      //  before dP(i): dp_full(i) implies they completed)
+      mbar_wait(&bars->dp_full, ph);
+      if (warp == 4) TRACE3(9, i);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t ud[32];
+        tmem_ld32(lane_base + C::COL_DP + 64 * hf + 32 * c, ud);
+        const float4* d4p = reinterpret_cast<const float4*>(dl + 32 * c);
+        tmem_ld_wait();
+        uint32_t dk2[16];
+#pragma unroll
+        for (int e4 = 0; e4 < 8; ++e4) {
+          const float4 d4 = d4p[e4];
+#pragma unroll
+          for (int u2 = 0; u2 < 2; ++u2) {
+            const int e = 4 * e4 + 2 * u2;
+            const uint32_t pp = pk[c][e >> 1];
+            const float2 pf = make_float2(__uint_as_float(pp << 16), __uint_as_float(pp & 0xffff0000u));
+            const float2 dd = fadd2(make_float2(__uint_as_float(ud[e]), __uint_as_float(ud[e + 1])),
+                                    u2 ? make_float2(-d4.z, -d4.w) : make_float2(-d4.x, -d4.y));
+            const float2 ds = fmul2(pf, dd);
+            dk2[e >> 1] = pack_bf16(ds.x, ds.y);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int chunk = 4 * c + j;   // 16-B chunk (8 queries) within the 128-B row
+          *reinterpret_cast<uint4*>(drow + ((chunk ^ (t & 7)) << 4)) =
+              make_uint4(dk2[4 * j], dk2[4 * j + 1], dk2[4 * j + 2], dk2[4 * j + 3]);
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&bars->ds_full[c]);
+        if (warp == 4) TRACE3(10 + c, i);
+      }
+      mbar_arrive(&bars->vec_empty[vb]);
+    }
+    mbar_wait(&bars->acc_done, n_iter > 0 ? 0 : 1);   // the last MMA group wrote dV / dK
+    tc_fence_after();
+    // ------------------------------------------------------------ epilogue --
+    float* dvr = dv + ((size_t)(kt.x + t) * Hkv + g) * D + hf * 64;
+    float* dkr = dk + ((size_t)(kt.x + t) * Hkv + g) * D + hf * 64;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      uint32_t a[32], bb[32];
+      tmem_ld32(lane_base + C::COL_DV + hf * 64 + c * 32, a);
+      tmem_ld32(lane_base + C::COL_DK + hf * 64 + c * 32, bb);
+      tmem_ld_wait();
+      if (key_ok) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          reinterpret_cast<float4*>(dvr + c * 32)[e] =
+              make_float4(__uint_as_float(a[4 * e]), __uint_as_float(a[4 * e + 1]),
+                          __uint_as_float(a[4 * e + 2]), __uint_as_float(a[4 * e + 3]));
+          reinterpret_cast<float4*>(dkr + c * 32)[e] =
+              make_float4(__uint_as_float(bb[4 * e]) * scale, __uint_as_float(bb[4 * e + 1]) * scale,
+                          __uint_as_float(bb[4 * e + 2]) * scale, __uint_as_float(bb[4 * e + 3]) * scale);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
 // Delta[h][i] = sum_d dO[i,h,d] * O[i,h,d] (fp32).  One warp per (row, head).
 template <int D>
 __global__ void bwd_delta_kernel(const __nv_bfloat16* __restrict__ o,
@@ -408,6 +862,21 @@ __global__ void bwd_delta_kernel(const __nv_bfloat16* __restrict__ o,
 #pragma unroll
   for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
   if (lane == 0) delta[(size_t)h * Tl + row] = s;
+}
+
+// v3 dQ accumulator [Hq][D/4][Tl][4] fp32 -> dq [Tl][Hq][D] bf16
+__global__ void dq_convert3_kernel(const float4* __restrict__ acc, uint2* __restrict__ dq, int Tl,
+                                   int Hq, int D) {
+  const long long n = (long long)Tl * Hq * (D / 4);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int db = (int)(i % (D / 4));           // output-ordered: consecutive threads write
+    const long long rh = i / (D / 4);            // consecutive 8-B pieces of a row
+    const int h = (int)(rh % Hq), row = (int)(rh / Hq);
+    const float4 v = acc[((long long)h * (D / 4) + db) * Tl + row];
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    dq[i] = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+  }
 }
 
 __global__ void dq_convert_kernel(const float4* __restrict__ acc, __nv_bfloat162* __restrict__ dq,
@@ -555,6 +1024,26 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   WLB_LAUNCH_CHECK();
   CUtensorMap tq, tk, tv, tdo;
   int rc;
+#if WLB_BWD_V3
+  if (D == 128) {
+    using C3 = Bwd3Cfg;
+    if ((rc = make_thd_tmap(&tq, q, Tl, Hq, D, C3::BM))) return rc;
+    if ((rc = make_thd_tmap(&tdo, dout, Tl, Hq, D, C3::BM))) return rc;
+    if ((rc = make_thd_tmap(&tk, k, T, Hkv, D, C3::BN))) return rc;
+    if ((rc = make_thd_tmap(&tv, v, T, Hkv, D, C3::BN))) return rc;
+    static bool attr3 = false;
+    if (!attr3) {
+      WLB_CUDA_TRY(cudaFuncSetAttribute(attn_bwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        C3::SMEM));
+      attr3 = true;
+    }
+    attn_bwd3_kernel<<<(unsigned)max_items * Hkv, C3::THREADS, C3::SMEM, stream>>>(
+        tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
+        Hkv, max_items, scale, scale * 1.4426950408889634f);
+    WLB_LAUNCH_CHECK();
+  } else
+#endif
+  {
   if ((rc = make_thd_tmap(&tq, q, Tl, Hq, D, C::BM))) return rc;
   if ((rc = make_thd_tmap(&tdo, dout, Tl, Hq, D, C::BM))) return rc;
   if ((rc = make_thd_tmap(&tk, k, T, Hkv, D, C::BN))) return rc;
@@ -572,7 +1061,16 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
       tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq, Hkv,
       max_items, scale, scale * 1.4426950408889634f);
   WLB_LAUNCH_CHECK();
+  }
   const long long n4 = (long long)Tl * Hq * D / 4;
+#if WLB_BWD_V3
+  if (D == 128) {
+    dq_convert3_kernel<<<(unsigned)std::min<long long>((n4 + 255) / 256, 148 * 16), 256, 0, stream>>>(
+        (const float4*)w.dq_acc, (uint2*)dq, Tl, Hq, D);
+    WLB_LAUNCH_CHECK();
+    return WLB_OK;
+  }
+#endif
   dq_convert_kernel<<<(unsigned)std::min<long long>((n4 + 255) / 256, 148 * 16), 256, 0, stream>>>(
       (const float4*)w.dq_acc, (__nv_bfloat162*)dq, n4);
   WLB_LAUNCH_CHECK();
@@ -582,6 +1080,10 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
 }  // namespace wlb
 
 #ifdef WLB_TRACE
+extern "C" int wlb_debug_bwd3_trace(void* host) {
+  WLB_CUDA_TRY(cudaMemcpyFromSymbol(host, wlb::g_bwd3_trace, sizeof(wlb::g_bwd3_trace)));
+  return WLB_OK;
+}
 extern "C" int wlb_debug_bwd_trace(void* host) {
   WLB_CUDA_TRY(cudaMemcpyFromSymbol(host, wlb::g_bwd_trace, sizeof(wlb::g_bwd_trace)));
   return WLB_OK;

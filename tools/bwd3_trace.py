@@ -1,0 +1,55 @@
+"""Development aid: per-tile timeline of the v3 backward kernel's first CTA.
+
+    WLB_NVCC_EXTRA=-DWLB_TRACE WLB_LIB_OUT=var/libT.so python -m paper_2503_17924_b200.build
+    WLB_LIB_PATH=var/libT.so python tools/bwd3_trace.py [--doc 32768]
+"""
+import argparse
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2503_17924_b200 as wl  # noqa: E402
+from paper_2503_17924_b200 import _native  # noqa: E402
+from paper_2503_17924_b200.attention import attn_backward, attn_forward, build_tiles  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--doc", type=int, default=32768)
+ap.add_argument("--hq", type=int, default=32)
+ap.add_argument("--hkv", type=int, default=32)
+a = ap.parse_args()
+lengths = [a.doc]
+plan = wl.build_shard_plan([lengths], 1, "per_document")
+g, pos, ro = plan.rank_local(0, 0)
+tiles = build_tiles(ro, pos, lengths)
+dev = torch.device("cuda")
+T, d = a.doc, 128
+q = torch.randn(T, a.hq, d, device=dev, dtype=torch.bfloat16)
+k = torch.randn(T, a.hkv, d, device=dev, dtype=torch.bfloat16)
+v = torch.randn_like(k)
+do = torch.randn_like(q)
+o, lse = attn_forward(q, k, v, tiles)
+for _ in range(3):
+    attn_backward(q, k, v, o, lse, do, tiles)
+torch.cuda.synchronize()
+buf = np.zeros((16, 128), dtype=np.int64)
+lib = _native.lib()
+lib.wlb_debug_bwd3_trace.argtypes = [ctypes.c_void_p]
+assert lib.wlb_debug_bwd3_trace(buf.ctypes.data) == 0
+t = buf.astype(np.float64)
+names = ["m_qfull", "m_sfree", "m_p0", "m_p1", "m_ds0", "m_ds1", "c_sfull", "c_p0", "c_p1",
+         "c_dpfull", "c_ds0", "c_ds1", "d_dqfull", "d_sfree", "c_s0reg", "c_p0math"]
+n = len(names)
+print("iter " + " ".join(f"{x:>8s}" for x in names) + "  per-tile")
+for i in range(10, 20):
+    row = " ".join(f"{t[e, i] - t[0, i]:8.0f}" for e in range(n))
+    print(f"{i:4d} {row}  {t[0, i + 1] - t[0, i]:7.0f}")
+it = np.arange(10, 100)
+print(f"steady-state cycles per 128-query tile: {np.diff(t[0, 10:101]).mean():.0f}")
+print("mean offsets from m_qfull(i) (S issue), iters 10..99:")
+for e in range(1, n):
+    print(f"  {names[e]:9s} {np.mean(t[e, it] - t[0, it]):8.0f}")
+print(f"  next S    {np.mean(t[0, it + 1] - t[0, it]):8.0f}")
