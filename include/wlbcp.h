@@ -114,6 +114,11 @@ int wlb_attn_bwd(const void* q, const void* k, const void* v, const void* o,
                  const int32_t* rowset_off, const int32_t* doc_start, int32_t n_docs,
                  const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq,
                  int32_t Hkv, int32_t D, float scale, void* ws, void* stream);
+/* Backward kernel selection for D = 128: the 128-query-tile kernel (v3) runs
+ * when Tl >= v3_min_rows * n_docs, else the 64-query kernel (v2).  Negative
+ * restores the default (4096); returns the previous threshold.  Process-wide
+ * tuning knob (no reference analogue). */
+int32_t wlb_attn_bwd_select(int32_t v3_min_rows);
 
 /* Row permutations for the CP exchange (rows of row_bytes, 16-B aligned).
  * scatter: dst[index[i]] = src[i];  gather: dst[i] = src[index[i]]. */

@@ -101,6 +101,13 @@ def attn_backward(q, k, v, o, lse, do, tiles: AttnTiles, scale: float | None = N
     return dq, dk, dv
 
 
+def set_bwd_v3_min_rows(rows: int) -> int:
+    """Backward kernel choice for D = 128: the 128-query-tile kernel runs when a
+    rank's local rows >= rows * n_docs (default 4096; negative restores it).
+    Returns the previous threshold."""
+    return int(_native.lib().wlb_attn_bwd_select(int(rows)))
+
+
 class DocPrefixAttention(torch.autograd.Function):
     """Single-rank (CP=1 or pre-gathered KV) autograd wrapper."""
 

@@ -457,7 +457,20 @@ struct Bwd3Bars {
 static_assert(sizeof(Bwd3Bars) <= 192, "barrier block");
 
 #ifndef WLB_BWD_V3
-#define WLB_BWD_V3 1     // 0: D = 128 uses the v2 (64-query) kernel
+#define WLB_BWD_V3 1     // 0: D = 128 always uses the v2 (64-query) kernel
+#endif
+// v3 wins on long row-sets (+2-3% at 22K-32K documents) and loses on short
+// ones (-7% on 2-3K documents: its serial first/last tile and 128-row tiles
+// cost more per work item), so it is used when the rank's mean local rows per
+// document reach this many.
+#ifndef WLB_BWD_V3_MIN_ROWS
+#define WLB_BWD_V3_MIN_ROWS 4096
+#endif
+#ifndef WLB_RED_PACE
+#define WLB_RED_PACE 0   // 0: dQ reductions paced by pipeline barriers; N: N batches + nanosleep
+#endif
+#ifndef WLB_RED_SLEEP
+#define WLB_RED_SLEEP 150
 #endif
 #ifndef WLB_BWD_POLY
 #define WLB_BWD_POLY 0   // column pairs (of every 8) whose exp2 runs on the FMA pipe
@@ -718,6 +731,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       if (warp == 12) TRACE3(13, j);
       const bool last = j + 1 == n_iter;
       const uint32_t nph = (j + 1) & 1;
+#if WLB_RED_PACE == 0
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         if (!last) {
@@ -734,6 +748,23 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                        __uint_as_float(u[32 * c + 4 * e + 3]) * scale);
         }
       }
+#else
+      (void)last;
+      (void)nph;
+#pragma unroll
+      for (int c = 0; c < WLB_RED_PACE; ++c) {
+        if (c > 0) __nanosleep(WLB_RED_SLEEP);
+        if (ok) {
+#pragma unroll
+          for (int e = 0; e < 32 / WLB_RED_PACE; ++e) {
+            const int q = c * (32 / WLB_RED_PACE) + e;
+            red_add_v4(base + (size_t)q * blk, __uint_as_float(u[4 * q]) * scale,
+                       __uint_as_float(u[4 * q + 1]) * scale, __uint_as_float(u[4 * q + 2]) * scale,
+                       __uint_as_float(u[4 * q + 3]) * scale);
+          }
+        }
+      }
+#endif
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------- compute --
@@ -974,6 +1005,8 @@ bwd_kv_tiles_kernel(int nd, const int* __restrict__ rowset_off, const int* __res
   if (threadIdx.x == 0) n_out[0] = total;
 }
 
+static int g_bwd_v3_min_rows = WLB_BWD_V3_MIN_ROWS;
+
 struct BwdWorkspace {
   float* dq_acc;
   float* delta;
@@ -1025,7 +1058,8 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   CUtensorMap tq, tk, tv, tdo;
   int rc;
 #if WLB_BWD_V3
-  if (D == 128) {
+  const bool v3 = D == 128 && (long long)Tl >= (long long)g_bwd_v3_min_rows * (n_docs > 0 ? n_docs : 1);
+  if (v3) {
     using C3 = Bwd3Cfg;
     if ((rc = make_thd_tmap(&tq, q, Tl, Hq, D, C3::BM))) return rc;
     if ((rc = make_thd_tmap(&tdo, dout, Tl, Hq, D, C3::BM))) return rc;
@@ -1064,7 +1098,7 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   }
   const long long n4 = (long long)Tl * Hq * D / 4;
 #if WLB_BWD_V3
-  if (D == 128) {
+  if (v3) {
     dq_convert3_kernel<<<(unsigned)std::min<long long>((n4 + 255) / 256, 148 * 16), 256, 0, stream>>>(
         (const float4*)w.dq_acc, (uint2*)dq, Tl, Hq, D);
     WLB_LAUNCH_CHECK();
@@ -1089,6 +1123,12 @@ extern "C" int wlb_debug_bwd_trace(void* host) {
   return WLB_OK;
 }
 #endif
+
+extern "C" int32_t wlb_attn_bwd_select(int32_t v3_min_rows) {
+  const int32_t prev = wlb::g_bwd_v3_min_rows;
+  wlb::g_bwd_v3_min_rows = v3_min_rows < 0 ? WLB_BWD_V3_MIN_ROWS : v3_min_rows;
+  return prev;
+}
 
 extern "C" size_t wlb_attn_bwd_workspace(int32_t Tl, int32_t T, int32_t Hq, int32_t Hkv, int32_t D,
                                          int32_t n_docs) {

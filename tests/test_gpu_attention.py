@@ -12,7 +12,8 @@ import pytest
 import torch
 
 import paper_2503_17924_b200 as wl
-from paper_2503_17924_b200.attention import attn_backward, attn_forward, build_tiles
+from paper_2503_17924_b200.attention import (attn_backward, attn_forward, build_tiles,
+                                             set_bwd_v3_min_rows)
 from oracle import attention_oracle as ao
 from oracle import shard_oracle as so
 
@@ -102,3 +103,35 @@ def test_bwd_gqa():
 @pytest.mark.parametrize("policy", ["per_document", "per_sequence"])
 def test_bwd_cp_ranks(policy):
     _rank_case([1000, 3, 250, 777, 40], 4, policy, 4, 2, 64, seed=14, with_bwd=True)
+
+
+# D = 128 backward kernels: v3 (128-query tiles) is chosen for long row-sets;
+# force each one on the same cases.
+@pytest.fixture(params=["v2", "v3"])
+def bwd_variant(request):
+    prev = set_bwd_v3_min_rows(1 << 30 if request.param == "v2" else 0)
+    yield request.param
+    set_bwd_v3_min_rows(prev)
+
+
+@pytest.mark.parametrize("case", ["single", "multi", "gqa", "cp_doc", "cp_seq", "ragged"])
+def test_bwd_d128_variants(bwd_variant, case):
+    if case == "single":
+        _rank_case([384], 1, "per_document", 2, 2, 128, seed=21, with_bwd=True)
+    elif case == "multi":
+        _rank_case([300, 17, 1, 640, 129, 2], 1, "per_document", 2, 2, 128, seed=22, with_bwd=True)
+    elif case == "gqa":
+        _rank_case([400, 260, 77], 1, "per_document", 8, 2, 128, seed=23, with_bwd=True)
+    elif case == "cp_doc":
+        _rank_case([1000, 3, 250, 777, 40], 4, "per_document", 4, 2, 128, seed=24, with_bwd=True)
+    elif case == "cp_seq":
+        _rank_case([1000, 3, 250, 777, 40], 4, "per_sequence", 4, 2, 128, seed=25, with_bwd=True)
+    else:   # row-sets that end mid-tile and 1-token documents between them
+        _rank_case([129, 1, 255, 1, 1, 383, 130], 2, "per_document", 2, 1, 128, seed=26,
+                   with_bwd=True)
+
+
+def test_bwd_long_doc_default_selection():
+    """A long document takes the v3 path under the default threshold."""
+    assert set_bwd_v3_min_rows(-1) == set_bwd_v3_min_rows(-1)
+    _rank_case([6144], 1, "per_document", 2, 2, 128, seed=27, with_bwd=True)
