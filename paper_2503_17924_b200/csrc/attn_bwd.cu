@@ -1007,6 +1007,26 @@ bwd_kv_tiles_kernel(int nd, const int* __restrict__ rowset_off, const int* __res
 
 static int g_bwd_v3_min_rows = WLB_BWD_V3_MIN_ROWS;
 
+// Zero the dK/dV rows of document p that no KV tile covers: keys at in-document
+// positions >= 128 * ceil((last local position + 1) / 128) (all of the document
+// when this rank holds none of its rows).  Same tile rule as bwd_kv_tiles_kernel.
+__global__ void zero_uncovered_kernel(const int* __restrict__ rowset_off,
+                                      const int* __restrict__ positions,
+                                      const int* __restrict__ doc_start, float4* __restrict__ dk,
+                                      float4* __restrict__ dv, int row_f4) {
+  const int p = blockIdx.x;
+  const int r0 = rowset_off[p], r1 = rowset_off[p + 1];
+  const int len = doc_start[p + 1] - doc_start[p];
+  const int covered = r1 > r0 ? min(len, (positions[r1 - 1] + 128) / 128 * 128) : 0;
+  const long long a = (long long)(doc_start[p] + covered) * row_f4;
+  const long long n = (long long)(len - covered) * row_f4;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    dk[a + i] = z;
+    dv[a + i] = z;
+  }
+}
+
 struct BwdWorkspace {
   float* dq_acc;
   float* delta;
@@ -1043,8 +1063,14 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   BwdWorkspace w = carve(ws, Tl, T, Hq, D, n_docs);
   const int max_items = T / 128 + n_docs + 1;
   WLB_CUDA_TRY(cudaMemsetAsync(w.dq_acc, 0, (size_t)Tl * Hq * D * 4, stream));
-  WLB_CUDA_TRY(cudaMemsetAsync(dk, 0, (size_t)T * Hkv * D * 4, stream));
-  WLB_CUDA_TRY(cudaMemsetAsync(dv, 0, (size_t)T * Hkv * D * 4, stream));
+  // dK/dV rows of every KV tile are stored whole by the kernel; only the keys
+  // no KV tile covers (past a document's last local query position) are zeroed
+  // here, instead of clearing 2 x T x Hkv x D x 4 bytes up front.
+  if (n_docs > 0) {
+    zero_uncovered_kernel<<<(unsigned)n_docs, 256, 0, stream>>>(
+        rowset_off, positions, doc_start, (float4*)dk, (float4*)dv, Hkv * D / 4);
+    WLB_LAUNCH_CHECK();
+  }
   {
     const long long warps = (long long)Tl * Hq;
     bwd_delta_kernel<D><<<(unsigned)((warps + 7) / 8), 256, 0, stream>>>(

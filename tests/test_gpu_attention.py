@@ -52,7 +52,12 @@ def _rank_case(lengths, cp, policy, hq, hkv, d, seed=0, with_bwd=False):
         o, lse = attn_forward(ql.to(dev), kd, vd, tiles)
         if with_bwd:
             ro_, rl, rdq, rdk, rdv = ao.segment_attention_fwd_bwd(ql, k, v, do[idx], lengths, ranges[w])
-            dq, dk, dv = attn_backward(ql.to(dev), kd, vd, o, lse, do[idx].contiguous().to(dev), tiles)
+            # dK/dV outputs start as NaN: every row must be written (the kernel
+            # stores covered KV tiles whole and zero-fills the rest)
+            nan = lambda: torch.full((kd.shape[0], kd.shape[1], kd.shape[2]), float("nan"),
+                                     dtype=torch.float32, device=dev)
+            dq, dk, dv = attn_backward(ql.to(dev), kd, vd, o, lse, do[idx].contiguous().to(dev),
+                                       tiles, dk_out=nan(), dv_out=nan())
             _close(dq, rdq, "dq")
             _close(dk, rdk, "dk")
             _close(dv, rdv, "dv")
