@@ -1007,23 +1007,35 @@ bwd_kv_tiles_kernel(int nd, const int* __restrict__ rowset_off, const int* __res
 
 static int g_bwd_v3_min_rows = WLB_BWD_V3_MIN_ROWS;
 
-// Zero the dK/dV rows of document p that no KV tile covers: keys at in-document
-// positions >= 128 * ceil((last local position + 1) / 128) (all of the document
-// when this rank holds none of its rows).  Same tile rule as bwd_kv_tiles_kernel.
+// Zero the dK/dV rows no KV tile covers: in document p, keys at in-document
+// positions >= 128 * ceil((last local position + 1) / 128) (all of p when this
+// rank holds none of its rows); same tile rule as bwd_kv_tiles_kernel.  Block b
+// owns global rows [b*ZR, (b+1)*ZR) and walks the documents overlapping them.
+constexpr int kZeroRows = 64;
 __global__ void zero_uncovered_kernel(const int* __restrict__ rowset_off,
                                       const int* __restrict__ positions,
-                                      const int* __restrict__ doc_start, float4* __restrict__ dk,
-                                      float4* __restrict__ dv, int row_f4) {
-  const int p = blockIdx.x;
-  const int r0 = rowset_off[p], r1 = rowset_off[p + 1];
-  const int len = doc_start[p + 1] - doc_start[p];
-  const int covered = r1 > r0 ? min(len, (positions[r1 - 1] + 128) / 128 * 128) : 0;
-  const long long a = (long long)(doc_start[p] + covered) * row_f4;
-  const long long n = (long long)(len - covered) * row_f4;
+                                      const int* __restrict__ doc_start, int n_docs,
+                                      float4* __restrict__ dk, float4* __restrict__ dv,
+                                      int row_f4) {
+  const int a0 = blockIdx.x * kZeroRows, a1 = min(a0 + kZeroRows, doc_start[n_docs]);
+  int lo = 0, hi = n_docs;                   // last document with doc_start <= a0
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (doc_start[mid] <= a0) lo = mid;
+    else hi = mid;
+  }
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
-    dk[a + i] = z;
-    dv[a + i] = z;
+  for (int p = lo; p < n_docs && doc_start[p] < a1; ++p) {
+    const int r0 = rowset_off[p], r1 = rowset_off[p + 1];
+    const int len = doc_start[p + 1] - doc_start[p];
+    const int covered = r1 > r0 ? min(len, (positions[r1 - 1] + 128) / 128 * 128) : 0;
+    const int z0 = max(a0, doc_start[p] + covered), z1 = min(a1, doc_start[p + 1]);
+    if (z0 >= z1) continue;
+    const long long base = (long long)z0 * row_f4, n = (long long)(z1 - z0) * row_f4;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+      dk[base + i] = z;
+      dv[base + i] = z;
+    }
   }
 }
 
@@ -1067,8 +1079,8 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   // no KV tile covers (past a document's last local query position) are zeroed
   // here, instead of clearing 2 x T x Hkv x D x 4 bytes up front.
   if (n_docs > 0) {
-    zero_uncovered_kernel<<<(unsigned)n_docs, 256, 0, stream>>>(
-        rowset_off, positions, doc_start, (float4*)dk, (float4*)dv, Hkv * D / 4);
+    zero_uncovered_kernel<<<(unsigned)((T + kZeroRows - 1) / kZeroRows), 256, 0, stream>>>(
+        rowset_off, positions, doc_start, n_docs, (float4*)dk, (float4*)dv, Hkv * D / 4);
     WLB_LAUNCH_CHECK();
   }
   {
