@@ -28,6 +28,8 @@
 #include "sm100.cuh"
 #include "tmap.cuh"
 
+#include <algorithm>
+
 #ifndef WLB_FWD_TURNS
 #define WLB_FWD_TURNS 0   // 1: strict X/Y alternation of the softmax warpgroups
                           //    (measured 7% slower: a lone softmax warp is
@@ -75,7 +77,7 @@ struct FwdCfg {
 };
 
 struct FwdBars {
-  uint64_t q_full;
+  uint64_t q_full, q_empty;
   uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
   uint64_t s_full[2], p_full[2], pv_done[2];   // per query tile (X = 0, Y = 1)
   uint32_t tmem_base;
@@ -87,19 +89,23 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ out,
                 float* __restrict__ lse, const int4* __restrict__ items,
                 const int* __restrict__ n_items, const int* __restrict__ positions, int Tl,
-                int Hq, int Hkv, int n_slots, float scale_log2) {
+                int Hq, int Hkv, int n_slots, int hpc, float scale_log2) {
   using C = FwdCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  // head-major order (LPT within a head): resident CTAs share one head's K/V in L2
-  const int item = blockIdx.x % n_slots, h = blockIdx.x / n_slots;
+  // head-major order (LPT within a head): resident CTAs share one head's K/V in L2.
+  // A CTA runs heads [h0, h0 + nh) of its tile pair back to back (hpc > 1 for
+  // short row-sets): the next head's Q and K/V loads and its first QK overlap
+  // this head's last PV and epilogue instead of a CTA teardown + launch.
+  const int item = blockIdx.x % n_slots, h0 = (blockIdx.x / n_slots) * hpc;
   if (item >= n_items[0]) return;
+  const int nh = min(hpc, Hq - h0);
   const int4 tx = items[2 * item], ty = items[2 * item + 1];
   // tile 0 = X {row0, nrows, kv_end}, tile 1 = Y
   const int kv_begin = tx.z;
   const int n_kv[2] = {(tx.w - kv_begin + C::BN - 1) / C::BN,
                        ty.y ? (ty.z - kv_begin + C::BN - 1) / C::BN : 0};
-  const int kvh = h / (Hq / Hkv);
+  const int group = Hq / Hkv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   FwdBars* bars = reinterpret_cast<FwdBars*>(smem + C::OFF_BAR);
@@ -109,6 +115,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
 
   if (threadIdx.x == 0) {
     mbar_init(&bars->q_full, 1);
+    mbar_init(&bars->q_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->k_full[i], 1);
       mbar_init(&bars->k_empty[i], 1);
@@ -131,31 +138,37 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
-    mbar_expect_tx_w(&bars->q_full, (ty.y ? 2 : 1) * C::Q_BYTES);
-    for (int s = 0; s < C::SLABS; ++s) {
-      tma_load_3d_w(sQ + s * C::BM * 128, &tmQ, &bars->q_full, s * 64, h, tx.x);
-      if (ty.y) tma_load_3d_w(sQ + C::Q_BYTES + s * C::BM * 128, &tmQ, &bars->q_full, s * 64, h, ty.x);
-    }
-    for (int j = 0; j < n_kv[0]; ++j) {
-      const int st = j % C::STAGES;
-      const uint32_t ph = (j / C::STAGES) & 1;
-      const int row = kv_begin + j * C::BN;
-      mbar_wait(&bars->k_empty[st], ph ^ 1);
-      mbar_expect_tx_w(&bars->k_full[st], C::KV_BYTES);
-      for (int s = 0; s < C::SLABS; ++s)
-        tma_load_3d_w(sK + st * C::KV_BYTES + s * C::BN * 128, &tmK, &bars->k_full[st], s * 64,
-                      kvh, row);
-      mbar_wait(&bars->v_empty[st], ph ^ 1);
-      mbar_expect_tx_w(&bars->v_full[st], C::KV_BYTES);
-      for (int s = 0; s < C::SLABS; ++s)
-        tma_load_3d_w(sV + st * C::KV_BYTES + s * C::BN * 128, &tmV, &bars->v_full[st], s * 64,
-                      kvh, row);
+    for (int hh = 0; hh < nh; ++hh) {
+      const int h = h0 + hh, kvh = h / group;
+      if (hh > 0) mbar_wait(&bars->q_empty, (hh - 1) & 1);   // last QK of head hh-1 done
+      mbar_expect_tx_w(&bars->q_full, (ty.y ? 2 : 1) * C::Q_BYTES);
+      for (int s = 0; s < C::SLABS; ++s) {
+        tma_load_3d_w(sQ + s * C::BM * 128, &tmQ, &bars->q_full, s * 64, h, tx.x);
+        if (ty.y)
+          tma_load_3d_w(sQ + C::Q_BYTES + s * C::BM * 128, &tmQ, &bars->q_full, s * 64, h, ty.x);
+      }
+      for (int j = 0; j < n_kv[0]; ++j) {
+        const int jj = hh * n_kv[0] + j;          // K/V ring position across heads
+        const int st = jj % C::STAGES;
+        const uint32_t ph = (jj / C::STAGES) & 1;
+        const int row = kv_begin + j * C::BN;
+        mbar_wait(&bars->k_empty[st], ph ^ 1);
+        mbar_expect_tx_w(&bars->k_full[st], C::KV_BYTES);
+        for (int s = 0; s < C::SLABS; ++s)
+          tma_load_3d_w(sK + st * C::KV_BYTES + s * C::BN * 128, &tmK, &bars->k_full[st], s * 64,
+                        kvh, row);
+        mbar_wait(&bars->v_empty[st], ph ^ 1);
+        mbar_expect_tx_w(&bars->v_full[st], C::KV_BYTES);
+        for (int s = 0; s < C::SLABS; ++s)
+          tma_load_3d_w(sV + st * C::KV_BYTES + s * C::BN * 128, &tmV, &bars->v_full[st], s * 64,
+                        kvh, row);
+      }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer --
     const uint32_t q_base = smem_u32(sQ), k_base = smem_u32(sK), v_base = smem_u32(sV);
-    auto qk = [&](int t, int j) {            // S_t = Q_t K_j^T
-      const int st = j % C::STAGES;
+    auto qk = [&](int t, int jj) {           // S_t = Q_t K_jj^T
+      const int st = jj % C::STAGES;
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
         const uint32_t qo = t * C::Q_BYTES + (kk >> 2) * C::BM * 128 + (kk & 3) * 32;
@@ -165,8 +178,8 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       }
       mma_commit_w(&bars->s_full[t]);
     };
-    auto pv = [&](int t, int j) {            // O_t += P_t V_j, P_t packed bf16 in TMEM
-      const int st = j % C::STAGES;
+    auto pv = [&](int t, int j, int jj) {   // O_t += P_t V_jj, P_t packed bf16 in TMEM
+      const int st = jj % C::STAGES;
 #pragma unroll
       for (int kk = 0; kk < C::BN / 16; ++kk)
         mma_ts_w(tmem + C::COL_O + t * D, tmem + C::COL_S + t * 128 + kk * 8,
@@ -174,29 +187,36 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                  C::IDESC_PV, (j > 0) || (kk > 0));
       mma_commit_w(&bars->pv_done[t]);
     };
-    mbar_wait(&bars->q_full, 0);
-    mbar_wait(&bars->k_full[0], 0);
-    tc_fence_after();
-    qk(0, 0);
-    if (n_kv[1] > 0) qk(1, 0);
-    mma_commit_w(&bars->k_empty[0]);
-    for (int j = 1; j <= n_kv[0]; ++j) {
-      const int sp = (j - 1) % C::STAGES;
-      mbar_wait(&bars->v_full[sp], ((j - 1) / C::STAGES) & 1);
-      if (j < n_kv[0]) mbar_wait(&bars->k_full[j % C::STAGES], (j / C::STAGES) & 1);
-      FTRACE(8, j - 1);
+    for (int hh = 0; hh < nh; ++hh) {
+      const int kb = hh * n_kv[0];            // K/V ring base of this head
+      const int sb[2] = {hh * n_kv[0], hh * n_kv[1]};   // per-tile step base
+      mbar_wait(&bars->q_full, hh & 1);
+      mbar_wait(&bars->k_full[kb % C::STAGES], (kb / C::STAGES) & 1);
+      tc_fence_after();
+      qk(0, kb);
+      if (n_kv[1] > 0) qk(1, kb);
+      mma_commit_w(&bars->k_empty[kb % C::STAGES]);
+      if (n_kv[0] == 1) mma_commit_w(&bars->q_empty);
+      for (int j = 1; j <= n_kv[0]; ++j) {
+        const int jp = kb + j - 1, jn = kb + j;
+        const int sp = jp % C::STAGES;
+        mbar_wait(&bars->v_full[sp], (jp / C::STAGES) & 1);
+        if (j < n_kv[0]) mbar_wait(&bars->k_full[jn % C::STAGES], (jn / C::STAGES) & 1);
+        FTRACE(8, j - 1);
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        if (j - 1 < n_kv[t]) {
-          mbar_wait_fast(&bars->p_full[t], (j - 1) & 1);
-          FTRACE(t, j - 1);
-          tc_fence_after();
-          pv(t, j - 1);                          // reads P_t before QK overwrites S_t
-          if (j < n_kv[t]) qk(t, j);
+        for (int t = 0; t < 2; ++t) {
+          if (j - 1 < n_kv[t]) {
+            mbar_wait_fast(&bars->p_full[t], (sb[t] + j - 1) & 1);
+            FTRACE(t, j - 1);
+            tc_fence_after();
+            pv(t, j - 1, jp);                    // reads P_t before QK overwrites S_t
+            if (j < n_kv[t]) qk(t, jn);
+          }
         }
+        mma_commit_w(&bars->v_empty[sp]);
+        if (j < n_kv[0]) mma_commit_w(&bars->k_empty[jn % C::STAGES]);
+        if (j == n_kv[0] - 1) mma_commit_w(&bars->q_empty);   // last QK of this head issued
       }
-      mma_commit_w(&bars->v_empty[sp]);
-      if (j < n_kv[0]) mma_commit_w(&bars->k_empty[j % C::STAGES]);
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------- softmax --
@@ -212,9 +232,11 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       const uint32_t lane_base = tmem + ((uint32_t)(wq * 32) << 16);
       const uint32_t s_col = lane_base + C::COL_S + t * 128;
       const uint32_t o_col = lane_base + C::COL_O + t * D;
+      for (int hh = 0; hh < nh; ++hh) {
+      const int h = h0 + hh, sb = hh * nkv;
       float m_run = -INFINITY, l_run = 0.f;
       for (int j = 0; j < nkv; ++j) {
-        mbar_wait(&bars->s_full[t], j & 1);
+        mbar_wait(&bars->s_full[t], (sb + j) & 1);
         FTRACE(2 + 3 * t, j);
         tc_fence_after();
         // all 128 scores of this row in registers (one TMEM wait per tile:
@@ -313,7 +335,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         m_run = m_use;
       }
       // ---------------------------------------------------------- epilogue --
-      mbar_wait(&bars->pv_done[t], (nkv - 1) & 1);
+      mbar_wait(&bars->pv_done[t], (sb + nkv - 1) & 1);
       tc_fence_after();
       const float inv_l = 1.f / l_run;
       __nv_bfloat16* orow = out + ((size_t)row * Hq + h) * D;
@@ -334,12 +356,17 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         }
       }
       if (valid) lse[(size_t)h * Tl + row] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+      // (the next head's first PV overwrites O_t only after this warpgroup's
+      //  p_full of that head's first step, i.e. after these TMEM loads)
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc(tmem, C::TMEM_COLS);
 }
+
+static int g_fwd_hpc_short = 4;
 
 template <int D>
 static int launch_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
@@ -359,9 +386,14 @@ static int launch_fwd(const void* q, const void* k, const void* v, void* o, floa
     attr = true;
   }
   const float scale_log2 = scale * 1.4426950408889634f;
-  attn_fwd_kernel<D><<<(unsigned)max_tiles * Hq, C::THREADS, C::SMEM, stream>>>(
+  // Heads per CTA: max_tiles = Tl/256 + n_docs + 1 (attention.py), so its excess
+  // over Tl/256 counts the documents.  Short row-sets (< 2048 local rows per
+  // document on average) get 4 heads per CTA to amortise the per-CTA latency.
+  const long long docs = std::max<long long>(1, (long long)max_tiles - Tl / (2 * C::BM) - 1);
+  const int hpc = (Hq % 4 == 0 && (long long)Tl < 2048 * docs) ? g_fwd_hpc_short : 1;
+  attn_fwd_kernel<D><<<(unsigned)max_tiles * ((Hq + hpc - 1) / hpc), C::THREADS, C::SMEM, stream>>>(
       tq, tk, tv, (__nv_bfloat16*)o, lse, (const int4*)tiles, n_tiles, positions, Tl, Hq, Hkv,
-      max_tiles, scale_log2);
+      max_tiles, hpc, scale_log2);
   WLB_LAUNCH_CHECK();
   return WLB_OK;
 }
