@@ -74,8 +74,8 @@ struct BwdCfg {
   static constexpr int THREADS = 128 + 128 * NCW + 128;   // + dQ drain warpgroup
 };
 
-struct BwdBars {  // 180 bytes; OFF_BAR reserves 256
-  uint64_t kv_full;
+struct BwdBars {  // 188 bytes; OFF_BAR reserves 256
+  uint64_t kv_full, kv_empty;
   uint64_t q_full[3], q_empty[3];
   uint64_t s_full[2], p_full[2], mma2_done[2], s_free[2];
   uint64_t vec_full[3], vec_empty[3];
@@ -84,6 +84,9 @@ struct BwdBars {  // 180 bytes; OFF_BAR reserves 256
 };
 
 // kv_tiles[2i] = {kv_begin (global), kv_len, row_first, row_end}, kv_tiles[2i+1].x = k0
+// A CTA runs KV heads [g0, g0 + nh) of its KV tile back to back (hpc > 1 for
+// short row-sets); the query tiles of all its heads form one flat sequence
+// I = head * n_iter + i, so every ring and barrier phase runs on across heads.
 template <int D, int NCW>
 __global__ void __launch_bounds__(256 + 128 * NCW, 1)
 attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -91,21 +94,27 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const float* __restrict__ lse, const float* __restrict__ delta,
                 float* __restrict__ dq_acc, float* __restrict__ dk, float* __restrict__ dv,
                 const int4* __restrict__ kv_tiles, const int* __restrict__ n_kv_tiles,
-                const int* __restrict__ positions, int Tl, int Hq, int Hkv, int n_slots,
+                const int* __restrict__ positions, int Tl, int Hq, int Hkv, int n_slots, int hpc,
                 float scale, float scale_log2) {
   using C = BwdCfg<D, NCW>;
   extern __shared__ uint8_t smem_raw[];
   if (smem_u32(smem_raw) & 1023) __trap();   // SW128 tiles need 1024-B alignment
   uint8_t* smem = smem_raw;
   // head-major order (LPT within a head): resident CTAs share one head's Q/dO/dQ in L2
-  const int item = blockIdx.x % n_slots, g = blockIdx.x / n_slots;
+  const int item = blockIdx.x % n_slots, g0 = (blockIdx.x / n_slots) * hpc;
   if (item >= n_kv_tiles[0]) return;
+  const int nh = min(hpc, Hkv - g0);
   const int4 kt = kv_tiles[2 * item];
   const int k0 = kv_tiles[2 * item + 1].x;   // in-document position of key 0 of the tile
   const int group = Hq / Hkv;
   const int qt_per_head = (kt.w - kt.z + C::BM - 1) / C::BM;
-  const int n_iter = qt_per_head * group;
+  const int n_iter = qt_per_head * group;    // query tiles per KV head
+  const int n_all = n_iter * nh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // flat tile I -> (KV head, query head, first row)
+  auto tile_g = [&](int I) { return g0 + I / n_iter; };
+  auto tile_h = [&](int I) { return tile_g(I) * group + (I % n_iter) / qt_per_head; };
+  auto tile_row = [&](int I) { return kt.z + ((I % n_iter) % qt_per_head) * C::BM; };
 
   BwdBars* bars = reinterpret_cast<BwdBars*>(smem + C::OFF_BAR);
   uint8_t* sK = smem + C::OFF_K;
@@ -117,6 +126,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
 
   if (threadIdx.x == 0) {
     mbar_init(&bars->kv_full, 1);
+    mbar_init(&bars->kv_empty, 1);
     for (int i = 0; i < C::QS; ++i) {
       mbar_init(&bars->q_full[i], 1);
       mbar_init(&bars->q_empty[i], 1);
@@ -145,21 +155,24 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       tma_prefetch(&tmK);
       tma_prefetch(&tmV);
       tma_prefetch(&tmDO);
-      mbar_expect_tx_w(&bars->kv_full, 2 * C::KV_BYTES);
-      for (int s = 0; s < C::SLABS; ++s) {
-        tma_load_3d_w(sK + s * C::KV_SLAB, &tmK, &bars->kv_full, s * 64, g, kt.x);
-        tma_load_3d_w(sV + s * C::KV_SLAB, &tmV, &bars->kv_full, s * 64, g, kt.x);
-      }
-      for (int i = 0; i < n_iter; ++i) {
-        const int st = i % C::QS;
-        const int h = g * group + i / qt_per_head;
-        const int row = kt.z + (i % qt_per_head) * C::BM;
-        mbar_wait(&bars->q_empty[st], ((i / C::QS) & 1) ^ 1);
+      for (int I = 0; I < n_all; ++I) {
+        if (I % n_iter == 0) {                 // next KV head: K/V once the last reader is done
+          const int gl = I / n_iter;
+          if (gl > 0) mbar_wait(&bars->kv_empty, (gl - 1) & 1);
+          mbar_expect_tx_w(&bars->kv_full, 2 * C::KV_BYTES);
+          for (int s = 0; s < C::SLABS; ++s) {
+            tma_load_3d_w(sK + s * C::KV_SLAB, &tmK, &bars->kv_full, s * 64, g0 + gl, kt.x);
+            tma_load_3d_w(sV + s * C::KV_SLAB, &tmV, &bars->kv_full, s * 64, g0 + gl, kt.x);
+          }
+        }
+        const int st = I % C::QS;
+        const int h = tile_h(I), row = tile_row(I);
+        mbar_wait(&bars->q_empty[st], ((I / C::QS) & 1) ^ 1);
         mbar_expect_tx_w(&bars->q_full[st], 2 * C::Q_BYTES);
         for (int s = 0; s < C::SLABS; ++s) {
           tma_load_3d_w(sQ + st * C::Q_BYTES + s * C::Q_SLAB, &tmQ, &bars->q_full[st], s * 64, h, row);
           tma_load_3d_w(sDO + st * C::Q_BYTES + s * C::Q_SLAB, &tmDO, &bars->q_full[st], s * 64, h,
-                      row);
+                        row);
         }
       }
     }
@@ -168,75 +181,88 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     {   // whole warp; one elected lane issues
       const uint32_t k_b = smem_u32(sK), v_b = smem_u32(sV), q_b = smem_u32(sQ),
                      do_b = smem_u32(sDO), ds_b = smem_u32(sDS);
-      mbar_wait(&bars->kv_full, 0);
-      for (int i = 0; i <= n_iter; ++i) {
-        if (i < n_iter) {
-          const int b = i & 1, st = i % C::QS;
-          mbar_wait(&bars->q_full[st], (i / C::QS) & 1);
-          TRACE(0, i);
-          tc_fence_after();
-          const uint32_t qs = q_b + st * C::Q_BYTES, dos = do_b + st * C::Q_BYTES;
-          // S^T[b] was last read by the compute warps of tile i-2 (before p_full,
-          // already waited); dP^T[b] also held dQ^T of tile i-2, so only the dP
-          // half waits for the drain warps.
+      // S^T / dP^T of tile I (first MMA group)
+      auto first_half = [&](int I) {
+        const int b = I & 1, st = I % C::QS;
+        mbar_wait(&bars->q_full[st], (I / C::QS) & 1);
+        TRACE(0, I);
+        tc_fence_after();
+        const uint32_t qs = q_b + st * C::Q_BYTES, dos = do_b + st * C::Q_BYTES;
+        // S^T[b] was last read by the compute warps of tile I-2 (before p_full,
+        // already waited); dP^T[b] also held dQ^T of tile I-2, so only the dP
+        // half waits for the drain warps.
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {   // contract over D: K-major both
-            const uint32_t ko = (kk >> 2) * C::KV_SLAB + (kk & 3) * 32;
-            const uint32_t qo = (kk >> 2) * C::Q_SLAB + (kk & 3) * 32;
-            mma_ss_w(tmem + C::COL_S + b * 64, sdesc_sw128(k_b + ko, 16, 1024),
-                     sdesc_sw128(qs + qo, 16, 1024), C::IDESC_ST, kk > 0);
-          }
-          if (i >= 2) mbar_wait_fast(&bars->s_free[b], ((i - 2) >> 1) & 1);
-          TRACE(1, i);
-          tc_fence_after();
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t ko = (kk >> 2) * C::KV_SLAB + (kk & 3) * 32;
-            const uint32_t qo = (kk >> 2) * C::Q_SLAB + (kk & 3) * 32;
-            mma_ss_w(tmem + C::COL_DP + b * 64, sdesc_sw128(v_b + ko, 16, 1024),
-                     sdesc_sw128(dos + qo, 16, 1024), C::IDESC_ST, kk > 0);
-          }
-          mma_commit_w(&bars->s_full[b]);
+        for (int kk = 0; kk < D / 16; ++kk) {   // contract over D: K-major both
+          const uint32_t ko = (kk >> 2) * C::KV_SLAB + (kk & 3) * 32;
+          const uint32_t qo = (kk >> 2) * C::Q_SLAB + (kk & 3) * 32;
+          mma_ss_w(tmem + C::COL_S + b * 64, sdesc_sw128(k_b + ko, 16, 1024),
+                   sdesc_sw128(qs + qo, 16, 1024), C::IDESC_ST, kk > 0);
         }
-        if (i >= 1) {
-          const int j = i - 1, b = j & 1, st = j % C::QS;
-          mbar_wait_fast(&bars->p_full[b], (j >> 1) & 1);
-          TRACE(2, j);
-          tc_fence_after();
-          const uint32_t qs = q_b + st * C::Q_BYTES, dos = do_b + st * C::Q_BYTES;
-          const uint32_t dss = ds_b + b * C::T_BYTES;
-          // dQ^T first: it lands in the dP^T[b] columns (free once the compute
-          // warps loaded dP^T), so the drain of tile j overlaps dV/dK(j) and
-          // S(j+2) instead of stalling dP(j+2).
+        if (I >= 2) mbar_wait_fast(&bars->s_free[b], ((I - 2) >> 1) & 1);
+        TRACE(1, I);
+        tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < C::BN / 16; ++kk) {   // contract over keys
-            mma_ss_w(tmem + C::COL_DP + b * 64, sdesc_sw128(k_b + kk * 2048, C::KV_SLAB, 1024),
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t ko = (kk >> 2) * C::KV_SLAB + (kk & 3) * 32;
+          const uint32_t qo = (kk >> 2) * C::Q_SLAB + (kk & 3) * 32;
+          mma_ss_w(tmem + C::COL_DP + b * 64, sdesc_sw128(v_b + ko, 16, 1024),
+                   sdesc_sw128(dos + qo, 16, 1024), C::IDESC_ST, kk > 0);
+        }
+        mma_commit_w(&bars->s_full[b]);
+      };
+      // dQ^T, dV, dK of tile J (second MMA group)
+      auto second_half = [&](int J) {
+        const int b = J & 1, st = J % C::QS, j = J % n_iter;
+        mbar_wait_fast(&bars->p_full[b], (J >> 1) & 1);
+        TRACE(2, J);
+        tc_fence_after();
+        const uint32_t qs = q_b + st * C::Q_BYTES, dos = do_b + st * C::Q_BYTES;
+        const uint32_t dss = ds_b + b * C::T_BYTES;
+        // dQ^T first: it lands in the dP^T[b] columns (free once the compute
+        // warps loaded dP^T), so the drain of tile J overlaps dV/dK(J) and
+        // S(J+2) instead of stalling dP(J+2).
+#pragma unroll
+        for (int kk = 0; kk < C::BN / 16; ++kk) {   // contract over keys
+          mma_ss_w(tmem + C::COL_DP + b * 64, sdesc_sw128(k_b + kk * 2048, C::KV_SLAB, 1024),
                    sdesc_sw128(dss + kk * 2048, C::KV_SLAB, 1024), C::IDESC_DQT, kk > 0);
-          }
-          mma_commit_w(&bars->mma2_done[b]);
-          // P^T / dS^T (packed bf16) sit in the S^T[b] columns: queries
-          // [32c, 32c+32) at column 32c (P) and 32c+16 (dS), 8 columns per K16
+        }
+        mma_commit_w(&bars->mma2_done[b]);
+        // P^T / dS^T (packed bf16) sit in the S^T[b] columns: queries
+        // [32c, 32c+32) at column 32c (P) and 32c+16 (dS), 8 columns per K16
 #pragma unroll
-          for (int kk = 0; kk < C::BM / 16; ++kk) {   // contract over queries (A from TMEM)
-            const uint32_t acc = (j > 0) || (kk > 0);
-            const uint32_t ca = C::COL_S + b * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
-            mma_ts_w(tmem + C::COL_DV, tmem + ca,
-                     sdesc_sw128(dos + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
-            mma_ts_w(tmem + C::COL_DK, tmem + ca + 16,
-                     sdesc_sw128(qs + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
-          }
-          mma_commit_w(&bars->q_empty[st]);
-          if (j == n_iter - 1) mma_commit_w(&bars->acc_done);
+        for (int kk = 0; kk < C::BM / 16; ++kk) {   // contract over queries (A from TMEM)
+          const uint32_t acc = (j > 0) || (kk > 0);
+          const uint32_t ca = C::COL_S + b * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
+          mma_ts_w(tmem + C::COL_DV, tmem + ca,
+                   sdesc_sw128(dos + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
+          mma_ts_w(tmem + C::COL_DK, tmem + ca + 16,
+                   sdesc_sw128(qs + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
+        }
+        mma_commit_w(&bars->q_empty[st]);
+        if (j == n_iter - 1) {                  // last tile of this KV head
+          mma_commit_w(&bars->acc_done);
+          mma_commit_w(&bars->kv_empty);
+        }
+      };
+      // Pipelined one tile deep (S/dP of tile I before dQ/dV/dK of tile I-1),
+      // except across a KV-head boundary: tile I of the next head needs the new
+      // K/V, which may only land after the last reader of the old ones.
+      for (int I = 0; I <= n_all; ++I) {
+        const bool head_start = I < n_all && I % n_iter == 0;
+        if (I < n_all && !head_start) first_half(I);
+        if (I >= 1) second_half(I - 1);
+        if (head_start) {
+          mbar_wait(&bars->kv_full, (I / n_iter) & 1);
+          first_half(I);
         }
       }
     }
   } else if (warp == 3) {
     // ------------------------------------------------- per-query vectors --
-    for (int i = 0; i < n_iter; ++i) {
-      const int b = i % C::QS;
-      const int h = g * group + i / qt_per_head;
-      const int row0 = kt.z + (i % qt_per_head) * C::BM;
-      mbar_wait(&bars->vec_empty[b], ((i / C::QS) & 1) ^ 1);
+    for (int I = 0; I < n_all; ++I) {
+      const int b = I % C::QS;
+      const int h = tile_h(I), row0 = tile_row(I);
+      mbar_wait(&bars->vec_empty[b], ((I / C::QS) & 1) ^ 1);
       float* vec = sVec + b * 3 * C::BM;
 #pragma unroll
       for (int e = lane; e < C::BM; e += 32) {
@@ -258,12 +284,11 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     const uint32_t lane_base = tmem + ((uint32_t)(lg * 32) << 16);
     const int d = D == 128 ? lg * 32 + lane : lg * 16 + lane;
     const size_t stride = (size_t)Hq * D;
-    for (int j = 0; j < n_iter; ++j) {
-      const int b = j & 1;
-      const int h = g * group + j / qt_per_head;
-      const int row0 = kt.z + (j % qt_per_head) * C::BM;
-      mbar_wait(&bars->mma2_done[b], (j >> 1) & 1);
-      TRACE(6, j);
+    for (int J = 0; J < n_all; ++J) {
+      const int b = J & 1;
+      const int h = tile_h(J), row0 = tile_row(J);
+      mbar_wait(&bars->mma2_done[b], (J >> 1) & 1);
+      TRACE(6, J);
       tc_fence_after();
       uint32_t u[64];
       tmem_ld32(lane_base + C::COL_DP + b * 64, *reinterpret_cast<uint32_t(*)[32]>(u));
@@ -271,7 +296,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&bars->s_free[b]);
-      TRACE(7, j);
+      TRACE(7, J);
       if (D == 128 || lane < 16) {
         float* ptr = dq_acc + ((size_t)row0 * Hq + h) * D + d;
         const int nvalid = min(C::BM, kt.w - row0);
@@ -293,11 +318,11 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     const bool key_ok = t < kt.y;
     const uint32_t lane_base = tmem + ((uint32_t)(lg * 32) << 16);
 
-    for (int i = 0; i < n_iter; ++i) {
-      const int b = i & 1, vb = i % C::QS;
-      mbar_wait(&bars->vec_full[vb], (i / C::QS) & 1);
-      mbar_wait(&bars->s_full[b], (i >> 1) & 1);
-      TRACE(3, i);
+    for (int I = 0; I < n_all; ++I) {
+      const int b = I & 1, vb = I % C::QS;
+      mbar_wait(&bars->vec_full[vb], (I / C::QS) & 1);
+      mbar_wait(&bars->s_full[b], (I >> 1) & 1);
+      TRACE(3, I);
       tc_fence_after();
       uint32_t us[32], ud[32];
       tmem_ld32(lane_base + C::COL_S + b * 64 + ch * 32, us);
@@ -310,7 +335,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       // (rows are position-sorted, so the first and last columns bound them).
       const bool full = kt.y == C::BN && vp4[0].x >= C::BN - 1 && vp4[7].w >= C::BN - 1;
       tmem_ld_wait();
-      TRACE(4, i);
+      TRACE(4, I);
       uint32_t pk[16], dk2[16];
 #pragma unroll
       for (int e4 = 0; e4 < 8; ++e4) {
@@ -343,8 +368,8 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       mbar_arrive(&bars->vec_empty[vb]);
       // P^T and dS^T (packed bf16) over THIS warp's own 32 S^T columns (no
       // other warp reads them): A operands of the TS dV / dK MMAs.  The
-      // previous readers (dV/dK of tile i-2) finished before MMA1(i)
-      // (s_full implies it).  dP^T[b] is free once loaded: dQ^T(i) goes
+      // previous readers (dV/dK of tile I-2) finished before MMA1(I)
+      // (s_full implies it).  dP^T[b] is free once loaded: dQ^T(I) goes
       // there.  dS^T also goes to SMEM as the B operand of dQ^T = K^T dS^T.
       tmem_st16(lane_base + C::COL_S + b * 64 + ch * 32, pk);
       tmem_st16(lane_base + C::COL_S + b * 64 + ch * 32 + 16, dk2);
@@ -357,31 +382,38 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       fence_proxy_async_smem();
       tmem_st_wait();
       tc_fence_before();
-      TRACE(5, i);
+      TRACE(5, I);
       mbar_arrive(&bars->p_full[b]);
-    }
-    mbar_wait(&bars->acc_done, n_iter > 0 ? 0 : 1);   // the last MMA group wrote dV / dK
-    tc_fence_after();
-    // ------------------------------------------------------------ epilogue --
-    // TMEM loads are warp-collective: issue converged, predicate the stores.
-    float* dvr = dv + ((size_t)(kt.x + t) * Hkv + g) * D + ch * (D / 2);
-    float* dkr = dk + ((size_t)(kt.x + t) * Hkv + g) * D + ch * (D / 2);
+      if (I % n_iter == n_iter - 1) {
+        // ---------------------------------------------------------- epilogue --
+        // the last MMA group of this KV head wrote dV / dK; the next head's
+        // first dV/dK MMA (accumulate = 0) waits for this warp's next p_full,
+        // i.e. for these TMEM loads
+        const int g = tile_g(I);
+        mbar_wait(&bars->acc_done, (I / n_iter) & 1);
+        tc_fence_after();
+        // TMEM loads are warp-collective: issue converged, predicate the stores.
+        float* dvr = dv + ((size_t)(kt.x + t) * Hkv + g) * D + ch * (D / 2);
+        float* dkr = dk + ((size_t)(kt.x + t) * Hkv + g) * D + ch * (D / 2);
 #pragma unroll
-    for (int c = 0; c < D / 64; ++c) {
-      uint32_t a[32], bb[32];
-      tmem_ld32(lane_base + C::COL_DV + ch * (D / 2) + c * 32, a);
-      tmem_ld32(lane_base + C::COL_DK + ch * (D / 2) + c * 32, bb);
-      tmem_ld_wait();
-      if (key_ok) {
+        for (int c = 0; c < D / 64; ++c) {
+          uint32_t a[32], bb[32];
+          tmem_ld32(lane_base + C::COL_DV + ch * (D / 2) + c * 32, a);
+          tmem_ld32(lane_base + C::COL_DK + ch * (D / 2) + c * 32, bb);
+          tmem_ld_wait();
+          if (key_ok) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          reinterpret_cast<float4*>(dvr + c * 32)[e] =
-              make_float4(__uint_as_float(a[4 * e]), __uint_as_float(a[4 * e + 1]),
-                          __uint_as_float(a[4 * e + 2]), __uint_as_float(a[4 * e + 3]));
-          reinterpret_cast<float4*>(dkr + c * 32)[e] =
-              make_float4(__uint_as_float(bb[4 * e]) * scale, __uint_as_float(bb[4 * e + 1]) * scale,
-                          __uint_as_float(bb[4 * e + 2]) * scale, __uint_as_float(bb[4 * e + 3]) * scale);
+            for (int e = 0; e < 8; ++e) {
+              reinterpret_cast<float4*>(dvr + c * 32)[e] =
+                  make_float4(__uint_as_float(a[4 * e]), __uint_as_float(a[4 * e + 1]),
+                              __uint_as_float(a[4 * e + 2]), __uint_as_float(a[4 * e + 3]));
+              reinterpret_cast<float4*>(dkr + c * 32)[e] =
+                  make_float4(__uint_as_float(bb[4 * e]) * scale, __uint_as_float(bb[4 * e + 1]) * scale,
+                              __uint_as_float(bb[4 * e + 2]) * scale, __uint_as_float(bb[4 * e + 3]) * scale);
+            }
+          }
         }
+        tc_fence_before();
       }
     }
   }
@@ -1006,6 +1038,7 @@ bwd_kv_tiles_kernel(int nd, const int* __restrict__ rowset_off, const int* __res
 }
 
 static int g_bwd_v3_min_rows = WLB_BWD_V3_MIN_ROWS;
+static int g_bwd_hpc_short = 4;
 
 // Zero the dK/dV rows no KV tile covers: in document p, keys at in-document
 // positions >= 128 * ceil((last local position + 1) / 128) (all of p when this
@@ -1129,9 +1162,14 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
                                       C::SMEM));
     attr = true;
   }
-  attn_bwd_kernel<D, 2><<<(unsigned)max_items * Hkv, C::THREADS, C::SMEM, stream>>>(
+  // several KV heads per CTA for short row-sets (< 2048 local rows per
+  // document on average): the next head's loads overlap this head's tail
+  const int hpc = (Hkv % 4 == 0 && (long long)Tl < 2048LL * (n_docs > 0 ? n_docs : 1))
+                      ? g_bwd_hpc_short : 1;
+  attn_bwd_kernel<D, 2><<<(unsigned)max_items * ((Hkv + hpc - 1) / hpc), C::THREADS, C::SMEM,
+                          stream>>>(
       tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq, Hkv,
-      max_items, scale, scale * 1.4426950408889634f);
+      max_items, hpc, scale, scale * 1.4426950408889634f);
   WLB_LAUNCH_CHECK();
   }
   const long long n4 = (long long)Tl * Hq * D / 4;

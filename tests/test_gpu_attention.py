@@ -140,3 +140,21 @@ def test_bwd_long_doc_default_selection():
     """A long document takes the v3 path under the default threshold."""
     assert set_bwd_v3_min_rows(-1) == set_bwd_v3_min_rows(-1)
     _rank_case([6144], 1, "per_document", 2, 2, 128, seed=27, with_bwd=True)
+
+
+# Short row-sets with KV heads divisible by 4 run several heads per CTA (the
+# forward and the v2 backward loop over heads with phases carried across them).
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("case", ["mha", "gqa", "cp2"])
+def test_multi_head_per_cta(d, case):
+    prev = set_bwd_v3_min_rows(1 << 30)
+    try:
+        if case == "mha":
+            _rank_case([300, 17, 1, 640, 129, 2], 1, "per_document", 4, 4, d, seed=31, with_bwd=True)
+        elif case == "gqa":
+            _rank_case([200, 260, 77, 1, 90], 1, "per_document", 16, 4, d, seed=32, with_bwd=True)
+        else:
+            _rank_case([500, 3, 250, 777, 40, 129], 2, "per_sequence", 8, 8, d, seed=33,
+                       with_bwd=True)
+    finally:
+        set_bwd_v3_min_rows(prev)
