@@ -119,6 +119,11 @@ int wlb_attn_bwd(const void* q, const void* k, const void* v, const void* o,
  * restores the default (4096); returns the previous threshold.  Process-wide
  * tuning knob (no reference analogue). */
 int32_t wlb_attn_bwd_select(int32_t v3_min_rows);
+/* v3 as 2-CTA clusters (KV tiles 2q, 2q+1 of a document share query tiles and
+ * exchange dQ halves over distributed shared memory, halving the dQ
+ * reductions).  Experimental, measured slower: 1 on, 0 off (default),
+ * negative = default; returns the previous setting. */
+int32_t wlb_attn_bwd_pairs(int32_t on);
 
 /* Row permutations for the CP exchange (rows of row_bytes, 16-B aligned).
  * scatter: dst[index[i]] = src[i];  gather: dst[i] = src[index[i]]. */

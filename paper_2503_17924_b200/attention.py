@@ -108,6 +108,12 @@ def set_bwd_v3_min_rows(rows: int) -> int:
     return int(_native.lib().wlb_attn_bwd_select(int(rows)))
 
 
+def set_bwd_pairs(on: int) -> int:
+    """v3 backward as 2-CTA clusters sharing dQ (1 on, 0 off, negative =
+    default).  Returns the previous setting."""
+    return int(_native.lib().wlb_attn_bwd_pairs(int(on)))
+
+
 class DocPrefixAttention(torch.autograd.Function):
     """Single-rank (CP=1 or pre-gathered KV) autograd wrapper."""
 

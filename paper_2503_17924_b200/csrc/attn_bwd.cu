@@ -445,11 +445,11 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
 //   * the dQ drain warps load dQ^T(i) while S(i+1) runs (s_free gates dP(i+1)).
 // ---------------------------------------------------------------------------
 #ifdef WLB_TRACE
-__device__ long long g_bwd3_trace[16][128];
+__device__ long long g_bwd3_trace[2][16][128];   // CTAs 0 and 1 (a cluster pair)
 #define TRACE3(ev, i)                                                             \
   do {                                                                            \
-    if (blockIdx.x == 0 && (i) < 128 && (threadIdx.x & 31) == 0)                  \
-      g_bwd3_trace[ev][i] = clock64();                                            \
+    if (blockIdx.x < 2 && (i) < 128 && (threadIdx.x & 31) == 0)                   \
+      g_bwd3_trace[blockIdx.x][ev][i] = clock64();                                \
   } while (0)
 #else
 #define TRACE3(ev, i) \
@@ -470,7 +470,7 @@ struct Bwd3Cfg {
   static constexpr int OFF_VEC = OFF_DS + T_BYTES;                  // QS x {-lse2, delta}[BM] f32
   static constexpr int OFF_POS = OFF_VEC + QS * 2 * BM * 4;         // QS x rel. position[BM] i8
   static constexpr int OFF_BAR = OFF_POS + QS * BM;
-  static constexpr int SMEM = OFF_BAR + 192;
+  static constexpr int SMEM = OFF_BAR + 256;
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 384;
   static constexpr uint32_t IDESC_ST = idesc_bf16(BN, BM, 0, 0);    // S^T, dP^T
@@ -484,9 +484,10 @@ struct Bwd3Bars {
   uint64_t kv_full;
   uint64_t q_full[2], q_empty[2], vec_full[2], vec_empty[2];
   uint64_t s_full, dp_full, p_full[2], ds_full[2], dq_full, s_free, acc_done;
+  uint64_t do_full, do_empty, rx_full[4], peer_free;   // PAIR: single dO buffer, dQ exchange
   uint32_t tmem_base;
 };
-static_assert(sizeof(Bwd3Bars) <= 192, "barrier block");
+static_assert(sizeof(Bwd3Bars) <= 256, "barrier block");
 
 #ifndef WLB_BWD_V3
 #define WLB_BWD_V3 1     // 0: D = 128 always uses the v2 (64-query) kernel
@@ -545,6 +546,7 @@ __device__ __forceinline__ void bwd3_p_chunk(const uint32_t (&us)[32], const flo
   }
 }
 
+template <bool PAIR>
 __global__ void __launch_bounds__(512, 1)
 attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -558,10 +560,27 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
   extern __shared__ uint8_t smem_raw[];
   if (smem_u32(smem_raw) & 1023) __trap();
   uint8_t* smem = smem_raw;
-  const int item = blockIdx.x % n_slots, g = blockIdx.x / n_slots;
+  // PAIR: a 2-CTA cluster runs KV tiles 2q and 2q+1 of one document over the
+  // same query tiles (kv_tiles holds pair items: {kv_begin, kv_len, row_first,
+  // row_end} of tile 2q, then {k0, kv_begin', kv_len', k0'} with kv_begin' < 0
+  // for a lone last tile); each CTA reduces half of the pair's summed dQ.
+  const int cta = PAIR ? (int)cluster_ctarank() : 0;
+  const int slot = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int item = slot % n_slots, g = slot / n_slots;
   if (item >= n_kv_tiles[0]) return;
-  const int4 kt = kv_tiles[2 * item];
-  const int k0 = kv_tiles[2 * item + 1].x;
+  int4 kt = kv_tiles[2 * item];
+  int k0 = kv_tiles[2 * item + 1].x;
+  bool paired = false;
+  if (PAIR) {
+    const int4 t2 = kv_tiles[2 * item + 1];
+    paired = t2.y >= 0;
+    if (!paired && cta == 1) return;         // lone tile: CTA 1 idles, CTA 0 runs solo
+    if (cta == 1) {
+      kt.x = t2.y;
+      kt.y = t2.z;
+      k0 = t2.w;
+    }
+  }
   const int group = Hq / Hkv;
   const int qt_per_head = (kt.w - kt.z + C::BM - 1) / C::BM;
   const int n_iter = qt_per_head * group;
@@ -593,6 +612,10 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     mbar_init(&bars->dq_full, 1);
     mbar_init(&bars->s_free, 128);
     mbar_init(&bars->acc_done, 1);
+    mbar_init(&bars->do_full, 1);
+    mbar_init(&bars->do_empty, 1);
+    for (int c = 0; c < 4; ++c) mbar_init(&bars->rx_full[c], 128);
+    mbar_init(&bars->peer_free, 128);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(&bars->tmem_base, C::TMEM_COLS);
@@ -600,6 +623,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+  if (PAIR && paired) cluster_sync();       // peer barriers initialised before remote use
 
   if (warp < 4) setmaxnreg_dec<80>();   // TMA / MMA / alloc / vector warps
   if (warp == 0) {
@@ -618,10 +642,23 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       const int h = g * group + i / qt_per_head;
       const int row = kt.z + (i % qt_per_head) * C::BM;
       mbar_wait(&bars->q_empty[st], ((i / C::QS) & 1) ^ 1);
-      mbar_expect_tx_w(&bars->q_full[st], 2 * C::Q_BYTES);
-      for (int s = 0; s < 2; ++s) {
-        tma_load_3d_w(sQ + st * C::Q_BYTES + s * C::SLAB, &tmQ, &bars->q_full[st], s * 64, h, row);
-        tma_load_3d_w(sDO + st * C::Q_BYTES + s * C::SLAB, &tmDO, &bars->q_full[st], s * 64, h, row);
+      if (PAIR) {
+        // dO single-buffered (its second stage is the dQ exchange buffer): it
+        // is read by dP(i) and dV(i) only, and dO(i+1) has S(i+1), dQ(i) and
+        // dK(i) to land in
+        mbar_expect_tx_w(&bars->q_full[st], C::Q_BYTES);
+        for (int s = 0; s < 2; ++s)
+          tma_load_3d_w(sQ + st * C::Q_BYTES + s * C::SLAB, &tmQ, &bars->q_full[st], s * 64, h, row);
+        mbar_wait(&bars->do_empty, (i & 1) ^ 1);
+        mbar_expect_tx_w(&bars->do_full, C::Q_BYTES);
+        for (int s = 0; s < 2; ++s)
+          tma_load_3d_w(sDO + s * C::SLAB, &tmDO, &bars->do_full, s * 64, h, row);
+      } else {
+        mbar_expect_tx_w(&bars->q_full[st], 2 * C::Q_BYTES);
+        for (int s = 0; s < 2; ++s) {
+          tma_load_3d_w(sQ + st * C::Q_BYTES + s * C::SLAB, &tmQ, &bars->q_full[st], s * 64, h, row);
+          tma_load_3d_w(sDO + st * C::Q_BYTES + s * C::SLAB, &tmDO, &bars->q_full[st], s * 64, h, row);
+        }
       }
     }
   } else if (warp == 1) {
@@ -658,25 +695,27 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         mbar_wait_fast(&bars->ds_full[1], j & 1);
         TRACE3(5, j);
         tc_fence_after();
+        const uint32_t dsb = ds_b;
         // dQ = dS K (contract over keys; A = dS from the dS^T buffer and B = K,
         // both MN-major): lanes = queries, so the drain emits 16-B reductions
 #pragma unroll
         for (int kk = 0; kk < C::BN / 16; ++kk)
-          mma_ss_w(tmem + C::COL_DP, sdesc_sw128(ds_b + kk * 2048, C::SLAB, 1024),
+          mma_ss_w(tmem + C::COL_DP, sdesc_sw128(dsb + kk * 2048, C::SLAB, 1024),
                    sdesc_sw128(k_b + kk * 2048, C::SLAB, 1024), C::IDESC_DQ, kk > 0);
         mma_commit_w(&bars->dq_full);
         // dK += dS^T Q (contract over queries; A = dS^T K-major from SMEM)
 #pragma unroll
         for (int kk = 0; kk < C::BM / 16; ++kk)
-          mma_ss_w(tmem + C::COL_DK, sdesc_sw128(ds_b + (kk >> 2) * C::SLAB + (kk & 3) * 32, 16, 1024),
+          mma_ss_w(tmem + C::COL_DK, sdesc_sw128(dsb + (kk >> 2) * C::SLAB + (kk & 3) * 32, 16, 1024),
                    sdesc_sw128(qs + kk * 2048, C::SLAB, 1024), C::IDESC_ACC, (j > 0) || (kk > 0));
         mma_commit_w(&bars->q_empty[st]);
         if (j == n_iter - 1) mma_commit_w(&bars->acc_done);
       }
       if (i < n_iter) {
         const int st = i % C::QS;
-        const uint32_t dos = do_b + st * C::Q_BYTES;
+        const uint32_t dos = PAIR ? do_b : do_b + st * C::Q_BYTES;
         const uint32_t ph = i & 1;
+        if (PAIR) mbar_wait(&bars->do_full, ph);
         // dP^T = V dO^T into the columns dQ(i-1) occupied: wait for the drain
         if (i >= 1) mbar_wait_fast(&bars->s_free, (i - 1) & 1);
         TRACE3(1, i);
@@ -705,6 +744,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                        (i > 0) || (c | hf | sub));
             }
         }
+        if (PAIR) mma_commit_w(&bars->do_empty);   // single dO buffer: dV(i) was its last reader
       }
     }
   } else if (warp == 3) {
@@ -763,6 +803,68 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       if (warp == 12) TRACE3(13, j);
       const bool last = j + 1 == n_iter;
       const uint32_t nph = (j + 1) & 1;
+      if (PAIR && paired) {
+        // Exchange halves with the peer CTA: keep head-dims [64*cta, 64*cta+64),
+        // send the other 64 (st.async into the peer's exchange buffer, row q,
+        // 16-B chunks XOR-swizzled by q so a quarter-warp's loads hit distinct
+        // banks), add the peer's, reduce half as many bytes into dq_acc.
+        const int q = lg * 32 + lane, peer = cta ^ 1;
+        // kept half -> u[0, 64), sent half -> u[64, 128) (register selects, no
+        // dynamic indexing)
+#pragma unroll
+        for (int e = 0; e < 64; ++e) {
+          const uint32_t lo = u[e], hi = u[64 + e];
+          u[e] = cta ? hi : lo;
+          u[64 + e] = cta ? lo : hi;
+        }
+        // The exchange runs in 4 quarters of 16 head-dims, paced like the
+        // reductions (a 32 KB st.async burst jammed the SM's memory queue and
+        // stalled the compute warps' loads).  Quarter c of row q sits at
+        // rx + c*8K + q*64, its 16-B chunks XOR-swizzled by (q>>1)&3.
+        uint8_t* rx = sDO + C::Q_BYTES;     // the unused second dO stage
+        const uint32_t rx_row = smem_u32(rx) + q * 64;
+        const uint32_t prow = mapa_shared(rx_row, peer);
+        const int sw = (q >> 1) & 3;
+        // (CTA-scope waits: a cluster-scope acquire invalidates the SM's L1 on
+        //  every completion; the peer's loads of its buffer are complete before
+        //  its release-arrive, and st.async data is visible through the
+        //  rx_full transaction counts)
+        mbar_wait_fast(&bars->peer_free, (j & 1) ^ 1);     // peer consumed tile j-1
+        if (warp == 12) TRACE3(4, j);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (!last) {
+            if (c == 1) mbar_wait(&bars->dp_full, nph);
+            if (c == 2) mbar_wait(&bars->ds_full[0], nph);
+            if (c == 3) mbar_wait(&bars->ds_full[1], nph);
+          }
+          mbar_expect_tx(&bars->rx_full[c], 64);
+          const uint32_t pbar = mapa_shared(smem_u32(&bars->rx_full[c]), peer);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            st_async_v4(prow + c * 8192 + ((e ^ sw) << 4), pbar, u[64 + 16 * c + 4 * e],
+                        u[64 + 16 * c + 4 * e + 1], u[64 + 16 * c + 4 * e + 2],
+                        u[64 + 16 * c + 4 * e + 3]);
+          // (no suspend hint: a remote completion wakes a suspended waiter late)
+          mbar_wait_fast(&bars->rx_full[c], j & 1);
+          if (warp == 12 && c == 0) TRACE3(14, j);
+          if (warp == 12 && c == 3) TRACE3(15, j);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint4 r = *reinterpret_cast<const uint4*>(rx + c * 8192 + q * 64 + ((e ^ sw) << 4));
+            const int dd = 16 * c + 4 * e;          // kept head-dims 64*cta + dd
+            if (ok)
+              red_add_v4(base + (size_t)(16 * cta + dd / 4) * blk,
+                         (__uint_as_float(u[dd]) + __uint_as_float(r.x)) * scale,
+                         (__uint_as_float(u[dd + 1]) + __uint_as_float(r.y)) * scale,
+                         (__uint_as_float(u[dd + 2]) + __uint_as_float(r.z)) * scale,
+                         (__uint_as_float(u[dd + 3]) + __uint_as_float(r.w)) * scale);
+          }
+        }
+        fence_proxy_async_smem();           // loads done before the peer's next st.async
+        mbar_arrive_remote(mapa_shared(smem_u32(&bars->peer_free), peer));
+        continue;
+      }
 #if WLB_RED_PACE == 0
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -806,11 +908,10 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     const int t = lg * 32 + lane;            // key row in the tile
     const bool key_ok = t < kt.y;
     const uint32_t lane_base = tmem + ((uint32_t)(lg * 32) << 16);
-    uint8_t* drow = sDS + hf * C::SLAB + t * 128;
-
     for (int i = 0; i < n_iter; ++i) {
       const int vb = i % C::QS;
       const uint32_t ph = i & 1;
+      uint8_t* drow = sDS + hf * C::SLAB + t * 128;
       const float* nl = sVec + vb * 2 * C::BM + 64 * hf;
       const float* dl = nl + C::BM;
       const int8_t* rp = sPos + vb * C::BM + 64 * hf;
@@ -826,12 +927,12 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         tmem_ld32(lane_base + C::COL_S + 64 * hf + 32 * c, us);
         const bool full = kt.y == C::BN && rp[32 * c] >= C::BN - 1 && rp[32 * c + 31] >= C::BN - 1;
         tmem_ld_wait();
-        if (warp == 4 && c == 0) TRACE3(14, i);
+
         if (full)
           bwd3_p_chunk<false>(us, nl + 32 * c, rp + 32 * c, t, key_ok, scale_log2, pk[c]);
         else
           bwd3_p_chunk<true>(us, nl + 32 * c, rp + 32 * c, t, key_ok, scale_log2, pk[c]);
-        if (warp == 4 && c == 0) TRACE3(15, i);
+
         // over S^T columns this warp already loaded (chunk 0's 32 columns)
         tmem_st16(lane_base + C::COL_S + 64 * hf + 16 * c, pk[c]);
         tmem_st_wait();
@@ -905,6 +1006,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc(tmem, C::TMEM_COLS);
+  if (PAIR && paired) cluster_sync();       // no CTA leaves while its peer may write it
 }
 
 // Delta[h][i] = sum_d dO[i,h,d] * O[i,h,d] (fp32).  D/8 lanes per (row, head),
@@ -983,7 +1085,7 @@ constexpr int kKvBins = 2048;
 __global__ void __launch_bounds__(kKvThreads)
 bwd_kv_tiles_kernel(int nd, const int* __restrict__ rowset_off, const int* __restrict__ positions,
                     const int* __restrict__ doc_start, int max_items, int4* __restrict__ out,
-                    int* __restrict__ n_out, int4* __restrict__ scratch) {
+                    int* __restrict__ n_out, int4* __restrict__ scratch, int pairs) {
   __shared__ long long warp_tot[kKvThreads / 32 + 1];
   __shared__ int hist[kKvBins];
   __shared__ int maxkey_s;
@@ -998,6 +1100,7 @@ bwd_kv_tiles_kernel(int nd, const int* __restrict__ rowset_off, const int* __res
     if (p < nd) {
       const int r0 = rowset_off[p], r1 = rowset_off[p + 1];
       if (r1 > r0) nt = (positions[r1 - 1] + 128) / 128;
+      if (pairs) nt = (nt + 1) / 2;            // items = tile pairs (2q, 2q+1)
     }
     long long tot;
     const long long off = carry + block_exclusive_scan(nt, warp_tot, &tot);
@@ -1016,7 +1119,7 @@ bwd_kv_tiles_kernel(int nd, const int* __restrict__ rowset_off, const int* __res
       if (doc_base[mid] <= it) lo = mid;
       else hi = mid;
     }
-    const int p = lo, t = it - doc_base[p], k0 = t * 128;
+    const int p = lo, t = (it - doc_base[p]) * (pairs ? 2 : 1), k0 = t * 128;
     const int r0 = rowset_off[p], r1 = rowset_off[p + 1];
     int a = r0, b = r1;                       // first row with position >= k0
     while (a < b) {
@@ -1024,9 +1127,17 @@ bwd_kv_tiles_kernel(int nd, const int* __restrict__ rowset_off, const int* __res
       if (positions[mid] >= k0) b = mid;
       else a = mid + 1;
     }
-    const int len = doc_start[p + 1] - doc_start[p] - k0;
+    const int dl = doc_start[p + 1] - doc_start[p];
+    const int len = dl - k0;
     scratch[2 * it] = make_int4(doc_start[p] + k0, len < 128 ? len : 128, a, r1);
-    scratch[2 * it + 1] = make_int4(k0, p, 0, 0);
+    if (pairs) {                              // second tile of the pair, if it exists
+      const int k1 = k0 + 128;
+      const bool has = r1 > r0 && k1 <= positions[r1 - 1];
+      scratch[2 * it + 1] = make_int4(k0, has ? doc_start[p] + k1 : -1,
+                                      has ? min(128, dl - k1) : 0, k1);
+    } else {
+      scratch[2 * it + 1] = make_int4(k0, p, 0, 0);
+    }
   }
   __syncthreads();
   const int total = n_items;
@@ -1062,6 +1173,16 @@ bwd_kv_tiles_kernel(int nd, const int* __restrict__ rowset_off, const int* __res
 
 static int g_bwd_v3_min_rows = WLB_BWD_V3_MIN_ROWS;
 static int g_bwd_hpc_short = 4;
+// v3 as 2-CTA clusters exchanging dQ halves over DSMEM (experimental, off):
+// it halves the dQ reduction bytes but adds the same number of DSMEM bytes to
+// the SM's outbound memory path, which is what bounds the reductions (plain
+// stores instead of reductions measured the same as reductions), and the
+// pair's exchange couples the two CTAs' pipelines: 650-725 vs 960-980 TFLOP/s
+// on a 32K document (profiles/r01_bwd3_pairs_trace.txt).
+#ifndef WLB_BWD_PAIRS
+#define WLB_BWD_PAIRS 0
+#endif
+static int g_bwd_pairs = WLB_BWD_PAIRS;
 
 // Zero the dK/dV rows no KV tile covers: in document p, keys at in-document
 // positions >= 128 * ceil((last local position + 1) / 128) (all of p when this
@@ -1146,14 +1267,19 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
         (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, w.delta, Tl, Hq);
     WLB_LAUNCH_CHECK();
   }
+#if WLB_BWD_V3
+  const bool v3 = D == 128 && (long long)Tl >= (long long)g_bwd_v3_min_rows * (n_docs > 0 ? n_docs : 1);
+  const bool pairs = v3 && g_bwd_pairs;
+#else
+  const bool pairs = false;
+#endif
   bwd_kv_tiles_kernel<<<1, kKvThreads, 0, stream>>>(n_docs, rowset_off, positions, doc_start,
                                                      max_items, w.kv_tiles, w.n_kv,
-                                                     w.kv_tiles + 2 * max_items);
+                                                     w.kv_tiles + 2 * max_items, pairs ? 1 : 0);
   WLB_LAUNCH_CHECK();
   CUtensorMap tq, tk, tv, tdo;
   int rc;
 #if WLB_BWD_V3
-  const bool v3 = D == 128 && (long long)Tl >= (long long)g_bwd_v3_min_rows * (n_docs > 0 ? n_docs : 1);
   if (v3) {
     using C3 = Bwd3Cfg;
     if ((rc = make_thd_tmap(&tq, q, Tl, Hq, D, C3::BM))) return rc;
@@ -1162,13 +1288,36 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
     if ((rc = make_thd_tmap(&tv, v, T, Hkv, D, C3::BN))) return rc;
     static bool attr3 = false;
     if (!attr3) {
-      WLB_CUDA_TRY(cudaFuncSetAttribute(attn_bwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        C3::SMEM));
+      WLB_CUDA_TRY(cudaFuncSetAttribute(attn_bwd3_kernel<false>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C3::SMEM));
+      WLB_CUDA_TRY(cudaFuncSetAttribute(attn_bwd3_kernel<true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C3::SMEM));
       attr3 = true;
     }
-    attn_bwd3_kernel<<<(unsigned)max_items * Hkv, C3::THREADS, C3::SMEM, stream>>>(
-        tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
-        Hkv, max_items, scale, scale * 1.4426950408889634f);
+    const float sl2 = scale * 1.4426950408889634f;
+    if (pairs) {
+      // 2-CTA clusters: one pair of KV tiles per cluster
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(2 * max_items * Hkv));
+      cfg.blockDim = dim3(C3::THREADS);
+      cfg.dynamicSmemBytes = C3::SMEM;
+      cfg.stream = stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      WLB_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn_bwd3_kernel<true>, tq, tk, tv, tdo, lse,
+                                      (const float*)w.delta, w.dq_acc, dk, dv,
+                                      (const int4*)w.kv_tiles, (const int*)w.n_kv, positions, Tl,
+                                      Hq, Hkv, max_items, scale, sl2));
+    } else {
+      attn_bwd3_kernel<false><<<(unsigned)max_items * Hkv, C3::THREADS, C3::SMEM, stream>>>(
+          tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
+          Hkv, max_items, scale, sl2);
+    }
     WLB_LAUNCH_CHECK();
   } else
 #endif
@@ -1223,6 +1372,12 @@ extern "C" int wlb_debug_bwd_trace(void* host) {
   return WLB_OK;
 }
 #endif
+
+extern "C" int32_t wlb_attn_bwd_pairs(int32_t on) {
+  const int32_t prev = wlb::g_bwd_pairs;
+  wlb::g_bwd_pairs = on < 0 ? WLB_BWD_PAIRS : (on != 0);
+  return prev;
+}
 
 extern "C" int32_t wlb_attn_bwd_select(int32_t v3_min_rows) {
   const int32_t prev = wlb::g_bwd_v3_min_rows;

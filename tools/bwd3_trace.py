@@ -35,13 +35,14 @@ o, lse = attn_forward(q, k, v, tiles)
 for _ in range(3):
     attn_backward(q, k, v, o, lse, do, tiles)
 torch.cuda.synchronize()
-buf = np.zeros((16, 128), dtype=np.int64)
+buf = np.zeros((2, 16, 128), dtype=np.int64)
 lib = _native.lib()
 lib.wlb_debug_bwd3_trace.argtypes = [ctypes.c_void_p]
 assert lib.wlb_debug_bwd3_trace(buf.ctypes.data) == 0
-t = buf.astype(np.float64)
-names = ["m_qfull", "m_sfree", "m_p0", "m_p1", "m_ds0", "m_ds1", "c_sfull", "c_p0", "c_p1",
-         "c_dpfull", "c_ds0", "c_ds1", "d_dqfull", "d_sfree", "c_s0reg", "c_p0math"]
+t2 = buf.astype(np.float64)
+t = t2[0]
+names = ["m_qfull", "m_sfree", "m_p0", "m_p1", "d_pfree", "m_ds1", "c_sfull", "c_p0", "c_p1",
+         "c_dpfull", "c_ds0", "c_ds1", "d_dqfull", "d_sfree", "d_rx0", "d_rx3"]
 n = len(names)
 print("iter " + " ".join(f"{x:>8s}" for x in names) + "  per-tile")
 for i in range(10, 20):
@@ -53,3 +54,10 @@ print("mean offsets from m_qfull(i) (S issue), iters 10..99:")
 for e in range(1, n):
     print(f"  {names[e]:9s} {np.mean(t[e, it] - t[0, it]):8.0f}")
 print(f"  next S    {np.mean(t[0, it + 1] - t[0, it]):8.0f}")
+
+if t2[1].any():
+    t1 = t2[1]
+    print("CTA 1 (same zero: CTA 0's m_qfull(i)):")
+    for e in range(1, n):
+        print(f"  {names[e]:9s} {np.mean(t1[e, it] - t[0, it]):8.0f}")
+    print(f"  m_qfull   {np.mean(t1[0, it] - t[0, it]):8.0f}")

@@ -19,9 +19,11 @@ ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--single", action="store_true")
 ap.add_argument("--doc", type=int, default=0, help="uniform documents of this length")
 ap.add_argument("--v3-min-rows", type=int, default=-1, help="backward kernel selection threshold")
+ap.add_argument("--pairs", type=int, default=-1, help="v3 backward as 2-CTA clusters (1/0)")
 a = ap.parse_args()
-from paper_2503_17924_b200.attention import set_bwd_v3_min_rows  # noqa: E402
+from paper_2503_17924_b200.attention import set_bwd_pairs, set_bwd_v3_min_rows  # noqa: E402
 set_bwd_v3_min_rows(a.v3_min_rows)
+set_bwd_pairs(a.pairs)
 lengths = [d.length for d in wl.generate_synthetic_stream(wl.SyntheticSpec(a.T, a.T), 0, a.batch + 1)[a.batch]]
 if a.single:
     lengths = [a.T]
