@@ -1,0 +1,3 @@
+for rep in 1 2 3; do for v in "$@"; do
+echo "$v $(WLB_LIB_PATH=var/lib$v.so python tools/probe_attn.py --single --iters 8 | sed 's/| bwd.*//') | $(WLB_LIB_PATH=var/lib$v.so python tools/probe_attn.py --batch 1 --iters 8 | sed 's/.*fwd/fwd/; s/| bwd.*//')"
+done; done
