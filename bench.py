@@ -54,10 +54,14 @@ def _peaks():
     return 1590.0, 1400.0, "fallback"
 
 
-def _workload(n):
+def _workload(n, shape="llama7b"):
+    """BASELINE configs: 2 (7B 32x128, 32K, CP=1) at N=1, 3 (7B, 128K, CP=N) at
+    N>1; --shape llama70b-gqa gives config 4 (64 query / 8 KV heads x 128)."""
+    hq, hkv = (64, 8) if shape == "llama70b-gqa" else (32, 32)
+    tag = "llama70b-gqa" if shape == "llama70b-gqa" else "llama7b"
     if n == 1:
-        return dict(name="llama7b-attn-32k-cp1", window=32768, hq=32, hkv=32, d=128, cp=1)
-    return dict(name=f"llama7b-attn-128k-cp{n}", window=131072, hq=32, hkv=32, d=128, cp=n)
+        return dict(name=f"{tag}-attn-32k-cp1", window=32768, hq=hq, hkv=hkv, d=128, cp=1)
+    return dict(name=f"{tag}-attn-128k-cp{n}", window=131072, hq=hq, hkv=hkv, d=128, cp=n)
 
 
 def _lengths(window):
@@ -170,7 +174,7 @@ def run_reference(args, world, rank):
     host cores, rank 0 only."""
     if rank != 0:
         return
-    wk = _workload(world)
+    wk = _workload(world, args.shape)
     lengths = _lengths(wk["window"])
     vals = []
     secs_tot = flops_tot = 0.0
@@ -213,6 +217,9 @@ def main():
     ap.add_argument("--exchange", default="symm", choices=["nccl", "symm"],
                     help="CP K/V + dK/dV exchange: NCCL collectives or one-sided NVLink "
                          "stores/loads on symmetric memory")
+    ap.add_argument("--shape", default="llama7b", choices=["llama7b", "llama70b-gqa"],
+                    help="attention shape: Llama-7B 32x128 (configs 2/3) or Llama-70B GQA "
+                         "64q/8kv x128 (config 4)")
     ap.add_argument("--clock-ms", type=int, default=500,
                     help="nvidia-smi sampling period during the timed region (0: off)")
     args = ap.parse_args()
@@ -228,7 +235,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     group = None
-    wk = _workload(world)
+    wk = _workload(world, args.shape)
     cp, hq, hkv, d = wk["cp"], wk["hq"], wk["hkv"], wk["d"]
     lengths = _lengths(wk["window"])
     T = wk["window"]
