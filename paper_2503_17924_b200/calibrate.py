@@ -37,13 +37,21 @@ Q_GRID = (1, 16, 64, 128, 256, 512, 1024, 2048, 4096, 8192)
 KV_GRID = (2048, 8192, 32768)
 
 
-def _time_range(q_len, kv_len, hq, hkv, d, iters, warmup, dev):
-    """Seconds for fwd+bwd of one range: rows at positions [kv-q, kv) of one doc."""
-    pos = torch.arange(kv_len - q_len, kv_len, dtype=torch.int32, device=dev)
-    rowset = torch.tensor([0, q_len], dtype=torch.int32, device=dev)
-    tiles = build_tiles(rowset, pos, [kv_len])
-    q = torch.randn(q_len, hq, d, device=dev, dtype=torch.bfloat16)
-    k = torch.randn(kv_len, hkv, d, device=dev, dtype=torch.bfloat16)
+def _time_range(q_len, kv_len, hq, hkv, d, iters, warmup, dev, copies=None):
+    """Seconds per range for fwd+bwd of `copies` identical ranges in one launch:
+    rows at positions [kv-q, kv) of `copies` documents of kv tokens.
+
+    A rank's ranges all run in one launch, spread over the SMs, so the
+    marginal cost of a range in a full-GPU batch (not the latency of a lone
+    range, which is launch- and occupancy-bound for small q) is what the
+    additive reference model (`sharding.py:151-160`) should be fitted to."""
+    if copies is None:
+        copies = max(1, min(64, (1 << 17) // kv_len))
+    pos = torch.arange(kv_len - q_len, kv_len, dtype=torch.int32, device=dev).repeat(copies)
+    rowset = torch.arange(0, (copies + 1) * q_len, q_len, dtype=torch.int32, device=dev)
+    tiles = build_tiles(rowset, pos, [kv_len] * copies)
+    q = torch.randn(q_len * copies, hq, d, device=dev, dtype=torch.bfloat16)
+    k = torch.randn(kv_len * copies, hkv, d, device=dev, dtype=torch.bfloat16)
     v = torch.randn_like(k)
     do = torch.randn_like(q)
     for _ in range(warmup):
@@ -58,7 +66,7 @@ def _time_range(q_len, kv_len, hq, hkv, d, iters, warmup, dev):
         b.record()
         b.synchronize()
         times.append(a.elapsed_time(b) / 1e3)
-    return statistics.median(times)
+    return statistics.median(times) / copies
 
 
 def measure(hq=32, hkv=32, d=128, q_grid=Q_GRID, kv_grid=KV_GRID, iters=5, warmup=2):

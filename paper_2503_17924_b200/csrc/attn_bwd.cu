@@ -1337,7 +1337,9 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   }
   // several KV heads per CTA for short row-sets (< 2048 local rows per
   // document on average): the next head's loads overlap this head's tail
-  const int hpc = (Hkv % 4 == 0 && (long long)Tl < 2048LL * (n_docs > 0 ? n_docs : 1))
+  // (only with >= 6 waves of CTAs left: Tl/128 bounds the KV tiles from below)
+  const int hpc = (Hkv % 4 == 0 && (long long)Tl < 2048LL * (n_docs > 0 ? n_docs : 1) &&
+                   (long long)(Tl / 128) * Hkv >= 6LL * 148 * g_bwd_hpc_short)
                       ? g_bwd_hpc_short : 1;
   attn_bwd_kernel<D, 2><<<(unsigned)max_items * ((Hkv + hpc - 1) / hpc), C::THREADS, C::SMEM,
                           stream>>>(

@@ -389,8 +389,12 @@ static int launch_fwd(const void* q, const void* k, const void* v, void* o, floa
   // Heads per CTA: max_tiles = Tl/256 + n_docs + 1 (attention.py), so its excess
   // over Tl/256 counts the documents.  Short row-sets (< 2048 local rows per
   // document on average) get 4 heads per CTA to amortise the per-CTA latency.
+  // Only when that still leaves >= 6 waves of CTAs (a small rank's few tiles
+  // need the parallelism more: config-5 ranks of ~4K rows lost 10% with it).
   const long long docs = std::max<long long>(1, (long long)max_tiles - Tl / (2 * C::BM) - 1);
-  const int hpc = (Hq % 4 == 0 && (long long)Tl < 2048 * docs) ? g_fwd_hpc_short : 1;
+  const int hpc = (Hq % 4 == 0 && (long long)Tl < 2048 * docs &&
+                   (long long)max_tiles * Hq >= 6LL * 148 * g_fwd_hpc_short)
+                      ? g_fwd_hpc_short : 1;
   attn_fwd_kernel<D><<<(unsigned)max_tiles * ((Hq + hpc - 1) / hpc), C::THREADS, C::SMEM, stream>>>(
       tq, tk, tv, (__nv_bfloat16*)o, lse, (const int4*)tiles, n_tiles, positions, Tl, Hq, Hkv,
       max_tiles, hpc, scale_log2);
