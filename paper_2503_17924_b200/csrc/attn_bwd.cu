@@ -23,6 +23,12 @@
 #include "sm100.cuh"
 #include "tmap.cuh"
 
+#ifndef WLB_HPC_ROWS
+#define WLB_HPC_ROWS 4096   // several heads per CTA below this many local rows per document
+                           // (2048-row documents: fwd +5%, bwd +3% vs a 2048 threshold;
+                           //  8192 cost a 6-document 32K sequence 7% in the forward)
+#endif
+
 #include <algorithm>
 
 namespace wlb {
@@ -1338,7 +1344,7 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   // several KV heads per CTA for short row-sets (< 2048 local rows per
   // document on average): the next head's loads overlap this head's tail
   // (only with >= 6 waves of CTAs left: Tl/128 bounds the KV tiles from below)
-  const int hpc = (Hkv % 4 == 0 && (long long)Tl < 2048LL * (n_docs > 0 ? n_docs : 1) &&
+  const int hpc = (Hkv % 4 == 0 && (long long)Tl < (long long)WLB_HPC_ROWS * (n_docs > 0 ? n_docs : 1) &&
                    (long long)(Tl / 128) * Hkv >= 6LL * 148 * g_bwd_hpc_short)
                       ? g_bwd_hpc_short : 1;
   attn_bwd_kernel<D, 2><<<(unsigned)max_items * ((Hkv + hpc - 1) / hpc), C::THREADS, C::SMEM,

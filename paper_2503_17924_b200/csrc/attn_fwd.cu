@@ -28,6 +28,12 @@
 #include "sm100.cuh"
 #include "tmap.cuh"
 
+#ifndef WLB_HPC_ROWS
+#define WLB_HPC_ROWS 4096   // several heads per CTA below this many local rows per document
+                           // (2048-row documents: fwd +5%, bwd +3% vs a 2048 threshold;
+                           //  8192 cost a 6-document 32K sequence 7% in the forward)
+#endif
+
 #include <algorithm>
 
 #ifndef WLB_FWD_TURNS
@@ -392,7 +398,7 @@ static int launch_fwd(const void* q, const void* k, const void* v, void* o, floa
   // Only when that still leaves >= 6 waves of CTAs (a small rank's few tiles
   // need the parallelism more: config-5 ranks of ~4K rows lost 10% with it).
   const long long docs = std::max<long long>(1, (long long)max_tiles - Tl / (2 * C::BM) - 1);
-  const int hpc = (Hq % 4 == 0 && (long long)Tl < 2048 * docs &&
+  const int hpc = (Hq % 4 == 0 && (long long)Tl < (long long)WLB_HPC_ROWS * docs &&
                    (long long)max_tiles * Hq >= 6LL * 148 * g_fwd_hpc_short)
                       ? g_fwd_hpc_short : 1;
   attn_fwd_kernel<D><<<(unsigned)max_tiles * ((Hq + hpc - 1) / hpc), C::THREADS, C::SMEM, stream>>>(
