@@ -63,12 +63,22 @@ __global__ void dkv_pull_kernel(const unsigned long long* __restrict__ bases, lo
   }
 }
 
+// Push/pull blocks (256 threads) per 8 SMs.  The exchange runs on its own
+// stream beside the attention kernels, which hold one CTA per SM: a grid of
+// 8 blocks per SM took SMs from the attention for the whole exchange (N=4
+// bench 3688-3695 TFLOP/s); 2 per SM moves the same bytes under the compute
+// with less interference (3746-3750); 1 per 4 SMs left the exchange exposed
+// (3385).
+#ifndef WLB_XCHG_BLOCKS_PER_SM
+#define WLB_XCHG_BLOCKS_PER_SM 16
+#endif
 static int grid_for(long long n_rows) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   long long blocks = (n_rows + 7) / 8;
-  if (blocks > sms * 8LL) blocks = sms * 8LL;
+  const long long cap = (long long)sms * WLB_XCHG_BLOCKS_PER_SM / 8;
+  if (blocks > cap) blocks = cap;
   return (int)(blocks > 0 ? blocks : 1);
 }
 
