@@ -17,6 +17,8 @@ all-gather output order, so one index serves both permutations.
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass
 
 import torch
@@ -242,7 +244,13 @@ class CPStepPipeline:
     def __init__(self, group=None, exchange=None):
         self.group = group
         self.exchange = exchange if exchange is not None else NcclExchange(group)
-        self.comm = torch.cuda.Stream()
+        # The exchange stream outranks the compute stream (CUDA: lower value =
+        # higher priority; default streams are 0): its blocks are dispatched
+        # as soon as an SM frees up, so an exchange is done before the
+        # micro-batch that needs it (N=4 bench 3781-3789 vs 3746-3752 at equal
+        # priority; raising the compute stream instead gained nothing).
+        # WLB_COMM_PRIORITY overrides it for experiments.
+        self.comm = torch.cuda.Stream(priority=int(os.environ.get("WLB_COMM_PRIORITY", "-1")))
 
     def _gather(self, k, v, shard, b, cur, ready):
         if ready is None:

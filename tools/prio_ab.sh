@@ -1,0 +1,3 @@
+run() { env $1 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29655 bench.py --gpus 4 --no-e2e 2>/dev/null | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('$1', d['value'], d['imbalance'], [round(x/d['steps'],1) for x in d['rank_kernel_ms']], d['ms_per_step'])"; }
+for rep in 1 2; do run X=0; run WLB_COMPUTE_PRIORITY=-1; run WLB_COMM_PRIORITY=-1; done
