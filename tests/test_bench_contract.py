@@ -1,0 +1,46 @@
+"""bench.py contract pieces that run without a GPU: the workload table behind
+`metric`/`config` (BASELINE.json configs 2-4) and the reference arm's rank
+rule (rank 0 alone prints; the other ranks exit without work)."""
+
+import importlib.util
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _bench():
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.path.insert(0, ROOT)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def test_workloads_match_baseline_configs():
+    b = _bench()
+    w1 = b._workload(1)
+    assert (w1["window"], w1["hq"], w1["hkv"], w1["d"], w1["cp"]) == (32768, 32, 32, 128, 1)
+    for n in (2, 4, 8):
+        w = b._workload(n)
+        assert (w["window"], w["hq"], w["hkv"], w["d"], w["cp"]) == (131072, 32, 32, 128, n)
+        assert w["window"] % (2 * n) == 0          # sharding needs T divisible by 2*cp
+        g = b._workload(n, "llama70b-gqa")
+        assert (g["hq"], g["hkv"], g["d"]) == (64, 8, 128) and g["name"].startswith("llama70b-gqa")
+
+
+def test_synthetic_lengths_fill_each_sequence():
+    b = _bench()
+    for window in (32768, 131072):
+        ls = b._lengths(window)
+        assert len(ls) == b.N_SEQ
+        assert all(sum(x) == window and min(x) >= 1 for x in ls)
+
+
+def test_reference_arm_non_zero_ranks_do_nothing(capsys):
+    b = _bench()
+
+    class A:
+        steps, warmup = 1, 0
+    b.run_reference(A(), world=4, rank=2)
+    assert capsys.readouterr().out == ""
