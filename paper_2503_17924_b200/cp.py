@@ -141,6 +141,8 @@ class NcclExchange:
     """CP exchange through NCCL collectives (all-gather / reduce-scatter) plus
     the row-permutation kernels."""
 
+    depth = 1            # collectives on one communicator stay on one stream
+
     def __init__(self, group=None):
         self.group = group
 
@@ -157,8 +159,13 @@ class NcclExchange:
 class SymmExchange:
     """CP exchange as ONE-SIDED NVLink traffic on symmetric memory.
 
-    Every rank owns two slots (micro-batches alternate) of a document-ordered
-    K/V buffer and of fp32 dK/dV partial buffers, mapped into every peer:
+    Every rank owns `slots` slots (micro-batch b uses slot b % slots) of a
+    document-ordered K/V buffer and of fp32 dK/dV partial buffers, mapped
+    into every peer.  With more than 2 slots the pipeline pushes K/V
+    slots-1 micro-batches ahead on a stream of its own (3 slots measured
+    slower at N=4: 3748-3758 vs 3785-3791 TFLOP/s; the early pushes added
+    more interference with the attention kernels than the exposure they
+    hid):
 
       forward : barrier (slot free everywhere) -> wlb_cp_kv_push stores this
                 rank's rows into every rank's slot at their document positions
@@ -168,28 +175,31 @@ class SymmExchange:
                 straight into the local dK/dV slot -> barrier ->
                 wlb_cp_dkv_pull sums every rank's partials for this rank's rows
                 -> barrier (slot reusable; the compute stream waits on it
-                before the backward of the micro-batch two steps later).
+                before the backward of the micro-batch `slots` steps later).
     """
 
-    def __init__(self, group, t_max, hkv, d, device):
+    def __init__(self, group, t_max, hkv, d, device, slots=2):
         import torch.distributed._symmetric_memory as symm
         self.group = group if group is not None else dist.group.WORLD
         self.cp = dist.get_world_size(self.group)
         self.t_max, self.hkv, self.d = t_max, hkv, d
         self.n = t_max * hkv * d
-        self.kv = symm.empty(4 * self.n, dtype=torch.bfloat16, device=device)     # [slot][K|V]
+        self.slots = int(os.environ.get("WLB_XCHG_SLOTS", slots))   # experiment override
+        slots = self.slots
+        self.depth = slots - 1          # K/V pushed this many micro-batches ahead
+        self.kv = symm.empty(2 * slots * self.n, dtype=torch.bfloat16, device=device)  # [slot][K|V]
         self.kv_h = symm.rendezvous(self.kv, self.group)
-        self.dkv = symm.empty(4 * self.n, dtype=torch.float32, device=device)     # [slot][dK|dV]
+        self.dkv = symm.empty(2 * slots * self.n, dtype=torch.float32, device=device)  # [slot][dK|dV]
         self.dkv_h = symm.rendezvous(self.dkv, self.group)
         self.kv_bases = torch.tensor(list(self.kv_h.buffer_ptrs), dtype=torch.int64, device=device)
         self.dkv_bases = torch.tensor(list(self.dkv_h.buffer_ptrs), dtype=torch.int64, device=device)
-        self.free = [None, None]       # event: all ranks finished pulling slot s
+        self.free = [None] * slots     # event: all ranks finished pulling slot s
 
     def _view(self, buf, idx, T):
         return buf[idx * self.n: idx * self.n + T * self.hkv * self.d].view(T, self.hkv, self.d)
 
     def gather(self, k, v, shard, b):
-        s, T = b % 2, shard.gather_all.numel()
+        s, T = b % self.slots, shard.gather_all.numel()
         if T > self.t_max:
             raise ValueError(f"micro-batch of {T} tokens exceeds the exchange capacity {self.t_max}")
         self.kv_h.barrier(channel=0)
@@ -202,13 +212,13 @@ class SymmExchange:
         return self._view(self.kv, 2 * s, T), self._view(self.kv, 2 * s + 1, T)
 
     def dkv_out(self, shard, b, cur):
-        s, T = b % 2, shard.gather_all.numel()
+        s, T = b % self.slots, shard.gather_all.numel()
         if self.free[s] is not None:
             cur.wait_event(self.free[s])
         return self._view(self.dkv, 2 * s, T), self._view(self.dkv, 2 * s + 1, T)
 
     def scatter(self, dkf, dvf, shard, b):
-        s = b % 2
+        s = b % self.slots
         tl = shard.gather_local.numel()
         dk = torch.empty((tl, self.hkv, self.d), dtype=torch.float32, device=dkf.device)
         dv = torch.empty_like(dk)
@@ -244,23 +254,29 @@ class CPStepPipeline:
     def __init__(self, group=None, exchange=None):
         self.group = group
         self.exchange = exchange if exchange is not None else NcclExchange(group)
+        self.depth = getattr(self.exchange, "depth", 1)
         # The exchange stream outranks the compute stream (CUDA: lower value =
         # higher priority; default streams are 0): its blocks are dispatched
         # as soon as an SM frees up, so an exchange is done before the
         # micro-batch that needs it (N=4 bench 3781-3789 vs 3746-3752 at equal
         # priority; raising the compute stream instead gained nothing).
         # WLB_COMM_PRIORITY overrides it for experiments.
-        self.comm = torch.cuda.Stream(priority=int(os.environ.get("WLB_COMM_PRIORITY", "-1")))
+        prio = int(os.environ.get("WLB_COMM_PRIORITY", "-1"))
+        self.comm = torch.cuda.Stream(priority=prio)          # dK/dV (and NCCL K/V)
+        # one-sided K/V pushes run ahead on their own stream (depth > 1)
+        self.push = torch.cuda.Stream(priority=prio) if self.depth > 1 else self.comm
 
     def _gather(self, k, v, shard, b, cur, ready):
-        if ready is None:
-            self.comm.wait_stream(cur)
-        else:
-            self.comm.wait_event(ready)
-        with torch.cuda.stream(self.comm):
+        # the slot being overwritten was last read by compute already enqueued
+        # on `cur` (b - slots <= the last enqueued micro-batch), so wait for it
+        # as well as for the inputs
+        self.push.wait_stream(cur)
+        if ready is not None:
+            self.push.wait_event(ready)
+        with torch.cuda.stream(self.push):
             k_full, v_full = self.exchange.gather(k, v, shard, b)
             ev = torch.cuda.Event()
-            ev.record(self.comm)
+            ev.record(self.push)
         return k_full, v_full, ev
 
     def run(self, shards, inputs, scale=None, ready=None, on_kernels=None, on_outputs=None,
@@ -272,12 +288,14 @@ class CPStepPipeline:
         n = len(shards)
         rdy = ready if ready is not None else [None] * n
         outs = [None] * n
-        pend = {0: self._gather(inputs[0][1], inputs[0][2], shards[0], 0, cur, rdy[0])}
+        pend = {}
+        for b in range(min(self.depth, n)):
+            pend[b] = self._gather(inputs[b][1], inputs[b][2], shards[b], b, cur, rdy[b])
         tail = []
         for b in range(n):
-            if b + 1 < n:
-                pend[b + 1] = self._gather(inputs[b + 1][1], inputs[b + 1][2], shards[b + 1], b + 1,
-                                           cur, rdy[b + 1])
+            nb = b + self.depth
+            if nb < n:
+                pend[nb] = self._gather(inputs[nb][1], inputs[nb][2], shards[nb], nb, cur, rdy[nb])
             k_full, v_full, ev = pend.pop(b)
             cur.wait_event(ev)
             if rdy[b] is not None:
@@ -296,6 +314,8 @@ class CPStepPipeline:
             if shards[b].cp > 1:
                 for t in (k_full, v_full):
                     t.record_stream(cur)
+                    if self.push is not self.comm:
+                        t.record_stream(self.push)
             done = torch.cuda.Event()
             done.record(cur)
             self.comm.wait_event(done)
