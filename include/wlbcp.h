@@ -125,6 +125,15 @@ int32_t wlb_attn_bwd_select(int32_t v3_min_rows);
  * negative = default; returns the previous setting. */
 int32_t wlb_attn_bwd_pairs(int32_t on);
 
+/* Split a fused QKV projection y[Tl][Hq+2*Hkv][D] (bf16) into THD q / k / v
+ * and apply rotate-half rotary embeddings at the IN-DOCUMENT positions the
+ * shard builder emits (positions[Tl], TokenRange coordinates,
+ * workload.py:33-45), theta_i = base^(-2i/D).  The step before the path
+ * (SURVEY.md 8f row 3); no reference analogue (the reference does not model
+ * the projection). */
+int wlb_qkv_rope(const void* y, void* q, void* k, void* v, const int32_t* positions,
+                 int32_t Tl, int32_t Hq, int32_t Hkv, int32_t D, float base, void* stream);
+
 /* Row permutations for the CP exchange (rows of row_bytes, 16-B aligned).
  * scatter: dst[index[i]] = src[i];  gather: dst[i] = src[index[i]]. */
 int wlb_rows_scatter(const void* src, void* dst, const int32_t* index, int64_t n_rows,

@@ -101,6 +101,24 @@ def attn_backward(q, k, v, o, lse, do, tiles: AttnTiles, scale: float | None = N
     return dq, dk, dv
 
 
+def qkv_rope(y, positions, hq: int, hkv: int, d: int, base: float = 10000.0):
+    """Split a fused QKV projection y [Tl, (hq + 2*hkv)*d] bf16 into THD q, k, v
+    with rotary embeddings at the builder's in-document positions [Tl]."""
+    if y.dtype != torch.bfloat16 or not y.is_cuda or not y.is_contiguous():
+        raise ValueError("y must be a contiguous CUDA bf16 tensor")
+    tl = y.shape[0]
+    if y.numel() != tl * (hq + 2 * hkv) * d or positions.numel() != tl:
+        raise ValueError("y / positions do not match Tl x (hq + 2*hkv) x d")
+    q = torch.empty((tl, hq, d), dtype=torch.bfloat16, device=y.device)
+    k = torch.empty((tl, hkv, d), dtype=torch.bfloat16, device=y.device)
+    v = torch.empty_like(k)
+    p = _native.ptr
+    _native.check(_native.lib().wlb_qkv_rope(p(y), p(q), p(k), p(v), p(positions), tl, hq, hkv,
+                                             d, float(base), _native.stream_ptr()),
+                  "wlb_qkv_rope")
+    return q, k, v
+
+
 def set_bwd_v3_min_rows(rows: int) -> int:
     """Backward kernel choice for D = 128: the 128-query-tile kernel runs when a
     rank's local rows >= rows * n_docs (default 4096; negative restores it).

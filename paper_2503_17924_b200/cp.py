@@ -25,7 +25,7 @@ import torch
 import torch.distributed as dist
 
 from . import _native
-from .attention import AttnTiles, attn_backward, attn_forward, build_tiles
+from .attention import AttnTiles, attn_backward, attn_forward, build_tiles, qkv_rope
 from .sharding import ShardPlan, build_shard_plan
 from .workload import CostProfile
 
@@ -50,6 +50,18 @@ class CPShard:
     @property
     def strategy(self):
         return self.plan.strategy(self.index)
+
+
+def project_qkv(x_local, w_qkv, shard: CPShard, hq: int, hkv: int, d: int,
+                base: float = 10000.0):
+    """The step before the path: this rank's local hidden states x [T/cp, hidden]
+    (rank-local order, `shard.gather_local`) times the fused QKV weight
+    [hidden, (hq + 2*hkv)*d] (a plain cuBLAS GEMM), then one pass that splits
+    the result into THD q, k, v and applies rotary embeddings at each row's
+    in-document position (`shard.tiles.positions`), ready for
+    `cp_doc_attention` / `CPStepPipeline`."""
+    y = torch.matmul(x_local, w_qkv)
+    return qkv_rope(y, shard.tiles.positions, hq, hkv, d, base)
 
 
 def shard_for_rank(plan: ShardPlan, index: int, rank: int) -> CPShard:

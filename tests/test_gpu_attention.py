@@ -160,3 +160,43 @@ def test_multi_head_per_cta(d, case):
                        with_bwd=True)
     finally:
         set_bwd_v3_min_rows(prev)
+
+
+def _rope_ref(x, pos, base):
+    """fp32 rotate-half RoPE (fp64 angles) of x [Tl, H, D] at positions [Tl]."""
+    d = x.shape[-1]
+    inv = base ** (-torch.arange(0, d // 2, dtype=torch.float64) * 2 / d)
+    ang = pos.double()[:, None] * inv[None, :]
+    c, s = torch.cos(ang).float()[:, None, :], torch.sin(ang).float()[:, None, :]
+    a, b = x[..., : d // 2], x[..., d // 2:]
+    return torch.cat((a * c - b * s, b * c + a * s), dim=-1)
+
+
+@pytest.mark.parametrize("cp,policy", [(1, "per_document"), (2, "per_document"), (4, "per_sequence")])
+def test_project_qkv_rope_in_document_positions(cp, policy):
+    """QKV projection + RoPE at in-document positions vs a torch fp32 reference:
+    every document restarts at rotary position 0 on every rank."""
+    from paper_2503_17924_b200.cp import project_qkv, shard_for_rank
+    lengths = so.pad_lengths_for_cp([700, 1, 257, 3000, 64], cp)
+    hq, hkv, d, hidden = 4, 2, 128, 256
+    plan = wl.build_shard_plan([lengths], cp, policy)
+    g = torch.Generator().manual_seed(41)
+    w = (torch.randn(hidden, (hq + 2 * hkv) * d, generator=g) / hidden ** 0.5).to(torch.bfloat16)
+    x_all = torch.randn(sum(lengths), hidden, generator=g).to(torch.bfloat16)
+    dev = torch.device("cuda")
+    for r in range(cp):
+        sh = shard_for_rank(plan, 0, r)
+        idx = sh.gather_local.long().cpu()
+        xl = x_all[idx]
+        q, k, v = project_qkv(xl.to(dev), w.to(dev), sh, hq, hkv, d, base=500000.0)
+        y = (xl.float() @ w.float()).view(-1, hq + 2 * hkv, d)
+        # in-document positions of the rank's rows, recomputed on the host
+        starts = [0]
+        for L in lengths:
+            starts.append(starts[-1] + L)
+        gl = idx.tolist()
+        pos = torch.tensor([t - max(s0 for s0 in starts[:-1] if s0 <= t) for t in gl])
+        assert torch.equal(pos, sh.tiles.positions.cpu().long())
+        _close(q, _rope_ref(y[:, :hq], pos, 500000.0), "q")
+        _close(k, _rope_ref(y[:, hq:hq + hkv], pos, 500000.0), "k")
+        _close(v, y[:, hq + hkv:], "v")
