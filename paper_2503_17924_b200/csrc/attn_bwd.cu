@@ -505,6 +505,15 @@ static_assert(sizeof(Bwd3Bars) <= 256, "barrier block");
 #ifndef WLB_BWD_V3_MIN_ROWS
 #define WLB_BWD_V3_MIN_ROWS 4096
 #endif
+#ifndef WLB_RED_B0          // dQ reduction batches (v4 REDs per thread, of 32)
+#define WLB_RED_B0 8
+#endif
+#ifndef WLB_RED_B1
+#define WLB_RED_B1 8
+#endif
+#ifndef WLB_RED_B2
+#define WLB_RED_B2 8
+#endif
 #ifndef WLB_RED_PACE
 #define WLB_RED_PACE 0   // 0: dQ reductions paced by pipeline barriers; N: N batches + nanosleep
 #endif
@@ -872,21 +881,20 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         continue;
       }
 #if WLB_RED_PACE == 0
+      // 32 16-B reductions per thread: the first WLB_RED_B0 right away, then
+      // batches after dp_full, ds_full[0] and ds_full[1] of the next tile
+      constexpr int T1 = WLB_RED_B0, T2 = T1 + WLB_RED_B1, T3 = T2 + WLB_RED_B2;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int e = 0; e < 32; ++e) {
         if (!last) {
-          if (c == 1) mbar_wait(&bars->dp_full, nph);
-          if (c == 2) mbar_wait(&bars->ds_full[0], nph);
-          if (c == 3) mbar_wait(&bars->ds_full[1], nph);
+          if (e == T1 && T1 < 32) mbar_wait(&bars->dp_full, nph);
+          if (e == T2 && T2 < 32) mbar_wait(&bars->ds_full[0], nph);
+          if (e == T3 && T3 < 32) mbar_wait(&bars->ds_full[1], nph);
         }
-        if (ok) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            red_add_v4(base + (size_t)(c * 8 + e) * blk, __uint_as_float(u[32 * c + 4 * e]) * scale,
-                       __uint_as_float(u[32 * c + 4 * e + 1]) * scale,
-                       __uint_as_float(u[32 * c + 4 * e + 2]) * scale,
-                       __uint_as_float(u[32 * c + 4 * e + 3]) * scale);
-        }
+        if (ok)
+          red_add_v4(base + (size_t)e * blk, __uint_as_float(u[4 * e]) * scale,
+                     __uint_as_float(u[4 * e + 1]) * scale, __uint_as_float(u[4 * e + 2]) * scale,
+                     __uint_as_float(u[4 * e + 3]) * scale);
       }
 #else
       (void)last;
