@@ -433,22 +433,26 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
 //
 // The v2 kernel above is bound by shared-memory operand bandwidth (128 B/clk
 // per SM): its N = 64 SS MMAs re-read the 32 KB K / V / K^T operands once per
-// 64 queries.  Here a tile has 128 queries, so each of S^T, dP^T and dQ^T is
+// 64 queries.  Here a tile has 128 queries, so each of S^T, dP^T and dQ is
 // one M=128 N=128 MMA chain (full rate) and the A operands are re-read half as
 // often.  TMEM (512 columns) then holds exactly one S^T and one dP^T:
 //
-//   [0,128)   S^T (fp32)  -> P^T (bf16, cols 64c..64c+32) and dS^T (bf16,
-//             cols 64c+32..64c+64) for query half c, written by the warps that
-//             read those S^T columns
-//   [128,256) dP^T (fp32) -> dQ^T (fp32) once the compute warps have read dP^T
+//   [0,128)   S^T (fp32) -> P^T (bf16, columns 64c..64c+32 for query half c,
+//             written by the warps that read those S^T columns)
+//   [128,256) dP^T (fp32) -> dQ (fp32, lanes = queries) once the compute
+//             warps have read dP^T
 //   [256,384) dV, [384,512) dK accumulators
+//   dS^T lives in SMEM only (B of dQ = dS K, A of dK += dS^T Q).
 //
-// Per tile the tensor pipe runs S | dP | dV | dK | dQ^T with no double
-// buffering; the compute warps hide inside it instead:
-//   * P for tile i is computed while dP^T(i) runs and is handed over in two
-//     32-query chunks (p_full[c]), so dV(i) starts on chunk 0;
-//   * dS is computed while dV(i) runs, again in two chunks (ds_full[c]);
-//   * the dQ drain warps load dQ^T(i) while S(i+1) runs (s_free gates dP(i+1)).
+// Tensor-pipe order (see the MMA issuer): ... dV(i-1) | S(i) | dQ(i-1) |
+// dK(i-1) | dP(i) | dV(i) | S(i+1) ...  With no double buffering the compute
+// warps hide inside it instead:
+//   * P(i) is computed under dQ(i-1), dK(i-1) and dP(i), and handed over in
+//     two 32-query chunks (p_full[c]) so dV(i) starts on chunk 0;
+//   * dS(i) is computed under dV(i) and S(i+1), again in two chunks;
+//   * the dQ drain warps load dQ(i-1) under dK(i-1) (s_free gates dP(i)) and
+//     pace its 16-B reductions over the next tile.
+// PAIR = true is the experimental 2-CTA-cluster variant (off by default).
 // ---------------------------------------------------------------------------
 #ifdef WLB_TRACE
 __device__ long long g_bwd3_trace[2][16][128];   // CTAs 0 and 1 (a cluster pair)
