@@ -12,13 +12,18 @@
 //           P^T -> TMEM over S^T, dS^T -> TMEM over dP^T AND SMEM, bf16)
 //   dV  += P^T dO,  dK += dS^T Q     TS MMAs (A read from TMEM), TMEM accumulators
 //   dQ^T = K^T dS^T                  TMEM, aliases dP^T of the same buffer;
-//          drained by the compute warps with warp-coalesced fp32 reductions
-//          (lane = head-dim index, so each red covers 128 contiguous bytes).
+//          drained by a dedicated warpgroup with warp-coalesced fp32
+//          reductions (lane = head-dim index, so each red covers 128
+//          contiguous bytes).
 //
 // The MMA warp issues S/dP for tile i+1 before the dV/dK/dQ group of tile i,
 // so the tensor pipe runs while the compute warps work on the previous tile.
 // dK/dV are written once per work item as fp32 partials over the full
-// document-ordered sequence (the CP reduce-scatter sums them over ranks).
+// document-ordered sequence (the CP reduce-scatter sums them over ranks);
+// keys no work item covers are zero-filled separately.  For short row-sets a
+// CTA walks several KV heads of its tile in one flat tile sequence.  This is
+// the "v2" kernel (any D); the 128-query "v3" kernel below takes over for
+// long row-sets at D = 128 (wlb_attn_bwd_select).
 #include "common.cuh"
 #include "sm100.cuh"
 #include "tmap.cuh"
