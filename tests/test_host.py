@@ -132,3 +132,22 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"(import\s+oracle|from\s+oracle|liboracle|oracle/)", src), f
+
+
+def test_abi_argument_validation_without_gpu():
+    """Entry points validate sizes before touching the device and report
+    WLB_EINVAL (-> ValueError in the wrappers), as the reference's callers
+    raise ValueError for bad arguments (sharding.py:77-83)."""
+    from paper_2503_17924_b200 import _native
+    lib = _native.lib()
+    # head dim not a multiple of 4, non-positive base
+    assert lib.wlb_qkv_rope(None, None, None, None, None, 8, 4, 2, 6, 1e4, None) == _native.WLB_EINVAL
+    assert lib.wlb_qkv_rope(None, None, None, None, None, 8, 4, 2, 128, 1.0, None) == _native.WLB_EINVAL
+    assert b"rope" in lib.wlb_last_error()
+    # Tl == 0 is a no-op
+    assert lib.wlb_qkv_rope(None, None, None, None, None, 0, 4, 2, 128, 1e4, None) == _native.WLB_OK
+    # attention: unsupported head dim / GQA ratio
+    assert lib.wlb_attn_fwd(None, None, None, None, None, None, None, 1, None, 8, 8, 4, 4, 96,
+                            0.1, None) == _native.WLB_EINVAL
+    assert lib.wlb_attn_bwd(None, None, None, None, None, None, None, None, None, None, None, 1,
+                            None, 8, 8, 6, 4, 128, 0.1, None, None) == _native.WLB_EINVAL
