@@ -13,6 +13,11 @@ __global__ void k(float* out, long long* clk, int iters) {
     for (int i = 0; i < 8; ++i) {
       if (MODE == 0) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
       else if (MODE == 1) asm volatile("fma.rn.f32 %0, %0, %0, %0;" : "+f"(a[i]));
+      else if (MODE == 3) {
+        unsigned h = __float_as_uint(a[i]);
+        asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(h));
+        a[i] = __uint_as_float(h);
+      }
       else {
         float2 v = make_float2(a[i], a[(i + 1) & 7]);
         asm volatile("{.reg .b64 r; mov.b64 r, {%0, %1}; fma.rn.f32x2 r, r, r, r; mov.b64 {%0, %1}, r;}" : "+f"(v.x), "+f"(v.y));
@@ -29,19 +34,20 @@ __global__ void k(float* out, long long* clk, int iters) {
 }
 int main() {
   float* out; long long* clk; cudaMalloc(&out, 148 * 1024 * 4); cudaMalloc(&clk, 148 * 8);
-  const char* names[3] = {"MUFU.EX2", "FFMA", "FFMA2"};
-  for (int mode = 0; mode < 3; ++mode)
+  const char* names[4] = {"MUFU.EX2", "FFMA", "FFMA2", "EX2.F16x2"};
+  for (int mode = 0; mode < 4; ++mode)
     for (int th = 128; th <= 512; th *= 2) {
       int iters = 4096;
       for (int rep = 0; rep < 2; ++rep) {
         if (mode == 0) k<0><<<148, th>>>(out, clk, iters);
         else if (mode == 1) k<1><<<148, th>>>(out, clk, iters);
-        else k<2><<<148, th>>>(out, clk, iters);
+        else if (mode == 2) k<2><<<148, th>>>(out, clk, iters);
+        else k<3><<<148, th>>>(out, clk, iters);
       }
       cudaDeviceSynchronize();
       long long h[148]; cudaMemcpy(h, clk, sizeof(h), cudaMemcpyDeviceToHost);
       double c = 0; for (int i = 0; i < 148; ++i) c += h[i]; c /= 148;
-      double ops = (double)th * iters * 8 * (mode == 2 ? 2 : 1);
+      double ops = (double)th * iters * 8 * (mode >= 2 ? 2 : 1);
       printf("%-9s threads/SM %4d: %.2f results/clk/SM\n", names[mode], th, ops / c);
     }
   return 0;
