@@ -114,6 +114,15 @@ int wlb_attn_bwd(const void* q, const void* k, const void* v, const void* o,
                  const int32_t* rowset_off, const int32_t* doc_start, int32_t n_docs,
                  const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq,
                  int32_t Hkv, int32_t D, float scale, void* ws, void* stream);
+/* wlb_attn_bwd with flags: WLB_BWD_DKV_BF16 writes the dK/dV partials as
+ * bf16 [T][Hkv][D] (the symmetric CP exchange then moves half the bytes and
+ * sums them in fp32, wlb_cp_dkv_pull_ex); 0 is wlb_attn_bwd. */
+#define WLB_BWD_DKV_BF16 1
+int wlb_attn_bwd_ex(const void* q, const void* k, const void* v, const void* o,
+                    const void* do_, const float* lse, void* dq, void* dk, void* dv,
+                    const int32_t* rowset_off, const int32_t* doc_start, int32_t n_docs,
+                    const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq,
+                    int32_t Hkv, int32_t D, float scale, void* ws, int32_t flags, void* stream);
 /* Backward kernel selection for D = 128: the 128-query-tile kernel (v3) runs
  * when Tl >= v3_min_rows * n_docs, else the 64-query kernel (v2).  Negative
  * restores the default (4096); returns the previous threshold.  Process-wide
@@ -155,6 +164,11 @@ int wlb_cp_kv_push(const void* k_local, const void* v_local, const int32_t* gath
 int wlb_cp_dkv_pull(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_off,
                     const int32_t* gather_local, int64_t n_rows, int64_t row_bytes,
                     float* dk, float* dv, int32_t cp, void* stream);
+/* As wlb_cp_dkv_pull; with WLB_BWD_DKV_BF16 the peers' partials are bf16
+ * (row_bytes = the bf16 row) and are summed in fp32 into fp32 dk / dv. */
+int wlb_cp_dkv_pull_ex(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_off,
+                       const int32_t* gather_local, int64_t n_rows, int64_t row_bytes,
+                       float* dk, float* dv, int32_t cp, int32_t flags, void* stream);
 
 #ifdef __cplusplus
 }

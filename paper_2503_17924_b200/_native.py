@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("WLB_LIB_PATH",
                           os.path.join(os.path.dirname(os.path.abspath(__file__)), "libwlbcp.so"))
 
 WLB_OK, WLB_EINVAL, WLB_ENODEV, WLB_ECUDA = 0, 22, 19, 1000
+WLB_BWD_DKV_BF16 = 1
 
 _p, _i32, _i64, _f64, _f32, _sz = C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_float, C.c_size_t
 
@@ -35,6 +36,8 @@ SIGNATURES = {
     "wlb_attn_fwd": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, _i32, _p, _i32, _i32, _i32, _i32,
                                _i32, _f32, _p]),
     "wlb_attn_bwd_workspace": (_sz, [_i32, _i32, _i32, _i32, _i32, _i32]),
+    "wlb_attn_bwd_ex": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i32, _p, _i32,
+                                  _i32, _i32, _i32, _i32, _f32, _p, _i32, _p]),
     "wlb_attn_bwd_select": (_i32, [_i32]),
     "wlb_attn_bwd_pairs": (_i32, [_i32]),
     "wlb_qkv_rope": (C.c_int, [_p, _p, _p, _p, _p, _i32, _i32, _i32, _i32, _f32, _p]),
@@ -44,6 +47,7 @@ SIGNATURES = {
     "wlb_rows_gather": (C.c_int, [_p, _p, _p, _i64, _i64, _p]),
     "wlb_cp_kv_push": (C.c_int, [_p, _p, _p, _i64, _i64, _p, _i64, _i64, _i32, _p]),
     "wlb_cp_dkv_pull": (C.c_int, [_p, _i64, _i64, _p, _i64, _i64, _p, _p, _i32, _p]),
+    "wlb_cp_dkv_pull_ex": (C.c_int, [_p, _i64, _i64, _p, _i64, _i64, _p, _p, _i32, _i32, _p]),
 }
 
 _lib = None

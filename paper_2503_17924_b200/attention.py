@@ -81,7 +81,8 @@ def attn_forward(q, k, v, tiles: AttnTiles, scale: float | None = None):
 def attn_backward(q, k, v, o, lse, do, tiles: AttnTiles, scale: float | None = None,
                   dk_out=None, dv_out=None):
     """dQ [Tl,Hq,D] bf16 and fp32 dK/dV partials over the full sequence
-    (written into dk_out / dv_out when given, e.g. symmetric exchange buffers)."""
+    (written into dk_out / dv_out when given, e.g. symmetric exchange buffers;
+    bf16 dk_out / dv_out take bf16 partials)."""
     _check_inputs(q, k, v)
     tl, hq, d = q.shape
     T, hkv = k.shape[0], k.shape[1]
@@ -90,14 +91,17 @@ def attn_backward(q, k, v, o, lse, do, tiles: AttnTiles, scale: float | None = N
     dq = torch.empty_like(q)
     dk = torch.empty((T, hkv, d), dtype=torch.float32, device=q.device) if dk_out is None else dk_out
     dv = torch.empty((T, hkv, d), dtype=torch.float32, device=q.device) if dv_out is None else dv_out
+    if dk.dtype != dv.dtype or dk.dtype not in (torch.float32, torch.bfloat16):
+        raise ValueError("dk_out / dv_out must both be fp32 or both bf16")
+    flags = _native.WLB_BWD_DKV_BF16 if dk.dtype == torch.bfloat16 else 0
     lib = _native.lib()
     ws = torch.empty(lib.wlb_attn_bwd_workspace(tl, T, hq, hkv, d, tiles.n_docs),
                      dtype=torch.uint8, device=q.device)
     p = _native.ptr
-    _native.check(lib.wlb_attn_bwd(
+    _native.check(lib.wlb_attn_bwd_ex(
         p(q), p(k), p(v), p(o), p(do), p(lse), p(dq), p(dk), p(dv), p(tiles.rowset_off),
         p(tiles.doc_start), tiles.n_docs, p(tiles.positions), tl, T, hq, hkv, d, scale, p(ws),
-        _native.stream_ptr()), "wlb_attn_bwd")
+        flags, _native.stream_ptr()), "wlb_attn_bwd_ex")
     return dq, dk, dv
 
 

@@ -172,8 +172,9 @@ class SymmExchange:
     """CP exchange as ONE-SIDED NVLink traffic on symmetric memory.
 
     Every rank owns `slots` slots (micro-batch b uses slot b % slots) of a
-    document-ordered K/V buffer and of fp32 dK/dV partial buffers, mapped
-    into every peer.  With more than 2 slots the pipeline pushes K/V
+    document-ordered K/V buffer and of bf16 dK/dV partial buffers (summed in
+    fp32 by the pull; WLB_XCHG_DKV=fp32 keeps fp32 partials), mapped into
+    every peer.  With more than 2 slots the pipeline pushes K/V
     slots-1 micro-batches ahead on a stream of its own (3 slots measured
     slower at N=4: 3748-3758 vs 3785-3791 TFLOP/s; the early pushes added
     more interference with the attention kernels than the exposure they
@@ -201,7 +202,11 @@ class SymmExchange:
         self.depth = slots - 1          # K/V pushed this many micro-batches ahead
         self.kv = symm.empty(2 * slots * self.n, dtype=torch.bfloat16, device=device)  # [slot][K|V]
         self.kv_h = symm.rendezvous(self.kv, self.group)
-        self.dkv = symm.empty(2 * slots * self.n, dtype=torch.float32, device=device)  # [slot][dK|dV]
+        # dK/dV partials in bf16 (WLB_XCHG_DKV=fp32 for fp32): the backward
+        # writes half the bytes and the pull moves half, summing in fp32
+        self.dkv_bf16 = os.environ.get("WLB_XCHG_DKV", "bf16") != "fp32"
+        dkv_dtype = torch.bfloat16 if self.dkv_bf16 else torch.float32
+        self.dkv = symm.empty(2 * slots * self.n, dtype=dkv_dtype, device=device)  # [slot][dK|dV]
         self.dkv_h = symm.rendezvous(self.dkv, self.group)
         self.kv_bases = torch.tensor(list(self.kv_h.buffer_ptrs), dtype=torch.int64, device=device)
         self.dkv_bases = torch.tensor(list(self.dkv_h.buffer_ptrs), dtype=torch.int64, device=device)
@@ -235,10 +240,12 @@ class SymmExchange:
         dk = torch.empty((tl, self.hkv, self.d), dtype=torch.float32, device=dkf.device)
         dv = torch.empty_like(dk)
         self.dkv_h.barrier(channel=1)
-        _native.check(_native.lib().wlb_cp_dkv_pull(
-            self.dkv_bases.data_ptr(), 2 * s * self.n * 4, (2 * s + 1) * self.n * 4,
-            shard.gather_local.data_ptr(), tl, self.hkv * self.d * 4, dk.data_ptr(), dv.data_ptr(),
-            self.cp, _native.stream_ptr()), "wlb_cp_dkv_pull")
+        es = 2 if self.dkv_bf16 else 4
+        _native.check(_native.lib().wlb_cp_dkv_pull_ex(
+            self.dkv_bases.data_ptr(), 2 * s * self.n * es, (2 * s + 1) * self.n * es,
+            shard.gather_local.data_ptr(), tl, self.hkv * self.d * es, dk.data_ptr(), dv.data_ptr(),
+            self.cp, _native.WLB_BWD_DKV_BF16 if self.dkv_bf16 else 0, _native.stream_ptr()),
+            "wlb_cp_dkv_pull_ex")
         self.dkv_h.barrier(channel=1)
         ev = torch.cuda.Event()
         ev.record()

@@ -94,6 +94,38 @@ struct BwdBars {  // 188 bytes; OFF_BAR reserves 256
   uint32_t tmem_base;
 };
 
+// 32 consecutive dV and dK values (dK scaled) of one key row at element offset
+// `off`: fp32, or bf16 when the partials go through the bf16 CP exchange.
+__device__ __forceinline__ void store_dkv32(void* dv, void* dk, size_t off, const uint32_t (&a)[32],
+                                            const uint32_t (&bb)[32], float scale, bool bf16) {
+  if (bf16) {
+    uint4* v4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dv) + off);
+    uint4* k4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dk) + off);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      v4[e] = make_uint4(pack_bf16(__uint_as_float(a[8 * e]), __uint_as_float(a[8 * e + 1])),
+                         pack_bf16(__uint_as_float(a[8 * e + 2]), __uint_as_float(a[8 * e + 3])),
+                         pack_bf16(__uint_as_float(a[8 * e + 4]), __uint_as_float(a[8 * e + 5])),
+                         pack_bf16(__uint_as_float(a[8 * e + 6]), __uint_as_float(a[8 * e + 7])));
+      k4[e] = make_uint4(
+          pack_bf16(__uint_as_float(bb[8 * e]) * scale, __uint_as_float(bb[8 * e + 1]) * scale),
+          pack_bf16(__uint_as_float(bb[8 * e + 2]) * scale, __uint_as_float(bb[8 * e + 3]) * scale),
+          pack_bf16(__uint_as_float(bb[8 * e + 4]) * scale, __uint_as_float(bb[8 * e + 5]) * scale),
+          pack_bf16(__uint_as_float(bb[8 * e + 6]) * scale, __uint_as_float(bb[8 * e + 7]) * scale));
+    }
+  } else {
+    float4* v4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(dv) + off);
+    float4* k4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(dk) + off);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      v4[e] = make_float4(__uint_as_float(a[4 * e]), __uint_as_float(a[4 * e + 1]),
+                          __uint_as_float(a[4 * e + 2]), __uint_as_float(a[4 * e + 3]));
+      k4[e] = make_float4(__uint_as_float(bb[4 * e]) * scale, __uint_as_float(bb[4 * e + 1]) * scale,
+                          __uint_as_float(bb[4 * e + 2]) * scale, __uint_as_float(bb[4 * e + 3]) * scale);
+    }
+  }
+}
+
 // kv_tiles[2i] = {kv_begin (global), kv_len, row_first, row_end}, kv_tiles[2i+1].x = k0
 // A CTA runs KV heads [g0, g0 + nh) of its KV tile back to back (hpc > 1 for
 // short row-sets); the query tiles of all its heads form one flat sequence
@@ -103,10 +135,10 @@ __global__ void __launch_bounds__(256 + 128 * NCW, 1)
 attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                 const float* __restrict__ lse, const float* __restrict__ delta,
-                float* __restrict__ dq_acc, float* __restrict__ dk, float* __restrict__ dv,
+                float* __restrict__ dq_acc, void* __restrict__ dk, void* __restrict__ dv,
                 const int4* __restrict__ kv_tiles, const int* __restrict__ n_kv_tiles,
                 const int* __restrict__ positions, int Tl, int Hq, int Hkv, int n_slots, int hpc,
-                float scale, float scale_log2) {
+                float scale, float scale_log2, int dkv_bf16) {
   using C = BwdCfg<D, NCW>;
   extern __shared__ uint8_t smem_raw[];
   if (smem_u32(smem_raw) & 1023) __trap();   // SW128 tiles need 1024-B alignment
@@ -404,25 +436,14 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         mbar_wait(&bars->acc_done, (I / n_iter) & 1);
         tc_fence_after();
         // TMEM loads are warp-collective: issue converged, predicate the stores.
-        float* dvr = dv + ((size_t)(kt.x + t) * Hkv + g) * D + ch * (D / 2);
-        float* dkr = dk + ((size_t)(kt.x + t) * Hkv + g) * D + ch * (D / 2);
+        const size_t off = ((size_t)(kt.x + t) * Hkv + g) * D + ch * (D / 2);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
           uint32_t a[32], bb[32];
           tmem_ld32(lane_base + C::COL_DV + ch * (D / 2) + c * 32, a);
           tmem_ld32(lane_base + C::COL_DK + ch * (D / 2) + c * 32, bb);
           tmem_ld_wait();
-          if (key_ok) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              reinterpret_cast<float4*>(dvr + c * 32)[e] =
-                  make_float4(__uint_as_float(a[4 * e]), __uint_as_float(a[4 * e + 1]),
-                              __uint_as_float(a[4 * e + 2]), __uint_as_float(a[4 * e + 3]));
-              reinterpret_cast<float4*>(dkr + c * 32)[e] =
-                  make_float4(__uint_as_float(bb[4 * e]) * scale, __uint_as_float(bb[4 * e + 1]) * scale,
-                              __uint_as_float(bb[4 * e + 2]) * scale, __uint_as_float(bb[4 * e + 3]) * scale);
-            }
-          }
+          if (key_ok) store_dkv32(dv, dk, off + c * 32, a, bb, scale, dkv_bf16 != 0);
         }
         tc_fence_before();
       }
@@ -575,10 +596,10 @@ __global__ void __launch_bounds__(512, 1)
 attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                  const float* __restrict__ lse, const float* __restrict__ delta,
-                 float* __restrict__ dq_acc, float* __restrict__ dk, float* __restrict__ dv,
+                 float* __restrict__ dq_acc, void* __restrict__ dk, void* __restrict__ dv,
                  const int4* __restrict__ kv_tiles, const int* __restrict__ n_kv_tiles,
                  const int* __restrict__ positions, int Tl, int Hq, int Hkv, int n_slots,
-                 float scale, float scale_log2) {
+                 float scale, float scale_log2, int dkv_bf16) {
   using C = Bwd3Cfg;
   constexpr int D = C::D;
   extern __shared__ uint8_t smem_raw[];
@@ -1005,25 +1026,14 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     mbar_wait(&bars->acc_done, n_iter > 0 ? 0 : 1);   // the last MMA group wrote dV / dK
     tc_fence_after();
     // ------------------------------------------------------------ epilogue --
-    float* dvr = dv + ((size_t)(kt.x + t) * Hkv + g) * D + hf * 64;
-    float* dkr = dk + ((size_t)(kt.x + t) * Hkv + g) * D + hf * 64;
+    const size_t off = ((size_t)(kt.x + t) * Hkv + g) * D + hf * 64;
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       uint32_t a[32], bb[32];
       tmem_ld32(lane_base + C::COL_DV + hf * 64 + c * 32, a);
       tmem_ld32(lane_base + C::COL_DK + hf * 64 + c * 32, bb);
       tmem_ld_wait();
-      if (key_ok) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          reinterpret_cast<float4*>(dvr + c * 32)[e] =
-              make_float4(__uint_as_float(a[4 * e]), __uint_as_float(a[4 * e + 1]),
-                          __uint_as_float(a[4 * e + 2]), __uint_as_float(a[4 * e + 3]));
-          reinterpret_cast<float4*>(dkr + c * 32)[e] =
-              make_float4(__uint_as_float(bb[4 * e]) * scale, __uint_as_float(bb[4 * e + 1]) * scale,
-                          __uint_as_float(bb[4 * e + 2]) * scale, __uint_as_float(bb[4 * e + 3]) * scale);
-        }
-      }
+      if (key_ok) store_dkv32(dv, dk, off + c * 32, a, bb, scale, dkv_bf16 != 0);
     }
   }
   tc_fence_before();
@@ -1215,8 +1225,8 @@ constexpr int kZeroRows = 64;
 __global__ void zero_uncovered_kernel(const int* __restrict__ rowset_off,
                                       const int* __restrict__ positions,
                                       const int* __restrict__ doc_start, int n_docs,
-                                      float4* __restrict__ dk, float4* __restrict__ dv,
-                                      int row_f4) {
+                                      uint4* __restrict__ dk, uint4* __restrict__ dv,
+                                      int row_f4) {   // row length in 16-B units
   const int a0 = blockIdx.x * kZeroRows, a1 = min(a0 + kZeroRows, doc_start[n_docs]);
   int lo = 0, hi = n_docs;                   // last document with doc_start <= a0
   while (hi - lo > 1) {
@@ -1224,7 +1234,7 @@ __global__ void zero_uncovered_kernel(const int* __restrict__ rowset_off,
     if (doc_start[mid] <= a0) lo = mid;
     else hi = mid;
   }
-  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  const uint4 z = make_uint4(0, 0, 0, 0);
   for (int p = lo; p < n_docs && doc_start[p] < a1; ++p) {
     const int r0 = rowset_off[p], r1 = rowset_off[p + 1];
     const int len = doc_start[p + 1] - doc_start[p];
@@ -1267,10 +1277,10 @@ static BwdWorkspace carve(void* base, int Tl, int T, int Hq, int D, int n_docs) 
 
 template <int D>
 static int launch_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,
-                      const float* lse, void* dq, float* dk, float* dv, const int32_t* rowset_off,
+                      const float* lse, void* dq, void* dk, void* dv, const int32_t* rowset_off,
                       const int32_t* doc_start, int32_t n_docs, const int32_t* positions,
                       int32_t Tl, int32_t T, int32_t Hq, int32_t Hkv, float scale, void* ws,
-                      cudaStream_t stream) {
+                      int dkv_bf16, cudaStream_t stream) {
   using C = BwdCfg<D>;
   BwdWorkspace w = carve(ws, Tl, T, Hq, D, n_docs);
   const int max_items = T / 128 + n_docs + 1;
@@ -1280,7 +1290,8 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   // here, instead of clearing 2 x T x Hkv x D x 4 bytes up front.
   if (n_docs > 0) {
     zero_uncovered_kernel<<<(unsigned)((T + kZeroRows - 1) / kZeroRows), 256, 0, stream>>>(
-        rowset_off, positions, doc_start, n_docs, (float4*)dk, (float4*)dv, Hkv * D / 4);
+        rowset_off, positions, doc_start, n_docs, (uint4*)dk, (uint4*)dv,
+        Hkv * D * (dkv_bf16 ? 2 : 4) / 16);
     WLB_LAUNCH_CHECK();
   }
   {
@@ -1335,11 +1346,11 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
       WLB_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn_bwd3_kernel<true>, tq, tk, tv, tdo, lse,
                                       (const float*)w.delta, w.dq_acc, dk, dv,
                                       (const int4*)w.kv_tiles, (const int*)w.n_kv, positions, Tl,
-                                      Hq, Hkv, max_items, scale, sl2));
+                                      Hq, Hkv, max_items, scale, sl2, dkv_bf16));
     } else {
       attn_bwd3_kernel<false><<<(unsigned)max_items * Hkv, C3::THREADS, C3::SMEM, stream>>>(
           tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
-          Hkv, max_items, scale, sl2);
+          Hkv, max_items, scale, sl2, dkv_bf16);
     }
     WLB_LAUNCH_CHECK();
   } else
@@ -1367,7 +1378,7 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   attn_bwd_kernel<D, 2><<<(unsigned)max_items * ((Hkv + hpc - 1) / hpc), C::THREADS, C::SMEM,
                           stream>>>(
       tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq, Hkv,
-      max_items, hpc, scale, scale * 1.4426950408889634f);
+      max_items, hpc, scale, scale * 1.4426950408889634f, dkv_bf16);
   WLB_LAUNCH_CHECK();
   }
   const long long n4 = (long long)Tl * Hq * D / 4;
@@ -1416,17 +1427,29 @@ extern "C" size_t wlb_attn_bwd_workspace(int32_t Tl, int32_t T, int32_t Hq, int3
   return wlb::carve(nullptr, Tl, T, Hq, D, n_docs).bytes;
 }
 
+extern "C" int wlb_attn_bwd_ex(const void* q, const void* k, const void* v, const void* o,
+                               const void* do_, const float* lse, void* dq, void* dk, void* dv,
+                               const int32_t* rowset_off, const int32_t* doc_start, int32_t n_docs,
+                               const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq,
+                               int32_t Hkv, int32_t D, float scale, void* ws, int32_t flags,
+                               void* stream) {
+  WLB_REQUIRE(D == 64 || D == 128, "head dim %d unsupported (64 or 128)", D);
+  WLB_REQUIRE(Hq > 0 && Hkv > 0 && Hq % Hkv == 0, "Hq must be a multiple of Hkv");
+  WLB_REQUIRE(Tl >= 0 && T > 0 && n_docs >= 0 && ws != nullptr, "bad sizes");
+  WLB_REQUIRE((flags & ~WLB_BWD_DKV_BF16) == 0, "unknown backward flags 0x%x", flags);
+  const int bf = (flags & WLB_BWD_DKV_BF16) != 0;
+  if (D == 64)
+    return wlb::launch_bwd<64>(q, k, v, o, do_, lse, dq, dk, dv, rowset_off, doc_start, n_docs,
+                               positions, Tl, T, Hq, Hkv, scale, ws, bf, (cudaStream_t)stream);
+  return wlb::launch_bwd<128>(q, k, v, o, do_, lse, dq, dk, dv, rowset_off, doc_start, n_docs,
+                              positions, Tl, T, Hq, Hkv, scale, ws, bf, (cudaStream_t)stream);
+}
+
 extern "C" int wlb_attn_bwd(const void* q, const void* k, const void* v, const void* o,
                             const void* do_, const float* lse, void* dq, float* dk, float* dv,
                             const int32_t* rowset_off, const int32_t* doc_start, int32_t n_docs,
                             const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq,
                             int32_t Hkv, int32_t D, float scale, void* ws, void* stream) {
-  WLB_REQUIRE(D == 64 || D == 128, "head dim %d unsupported (64 or 128)", D);
-  WLB_REQUIRE(Hq > 0 && Hkv > 0 && Hq % Hkv == 0, "Hq must be a multiple of Hkv");
-  WLB_REQUIRE(Tl >= 0 && T > 0 && n_docs >= 0 && ws != nullptr, "bad sizes");
-  if (D == 64)
-    return wlb::launch_bwd<64>(q, k, v, o, do_, lse, dq, dk, dv, rowset_off, doc_start, n_docs,
-                               positions, Tl, T, Hq, Hkv, scale, ws, (cudaStream_t)stream);
-  return wlb::launch_bwd<128>(q, k, v, o, do_, lse, dq, dk, dv, rowset_off, doc_start, n_docs,
-                              positions, Tl, T, Hq, Hkv, scale, ws, (cudaStream_t)stream);
+  return wlb_attn_bwd_ex(q, k, v, o, do_, lse, dq, dk, dv, rowset_off, doc_start, n_docs,
+                         positions, Tl, T, Hq, Hkv, D, scale, ws, 0, stream);
 }

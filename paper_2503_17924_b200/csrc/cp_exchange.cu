@@ -15,6 +15,8 @@
 //
 // One warp per row, 16-byte vectors; cross-rank ordering is done by the
 // caller's symmetric-memory barriers on the same stream.
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 
 namespace wlb {
@@ -63,6 +65,41 @@ __global__ void dkv_pull_kernel(const unsigned long long* __restrict__ bases, lo
   }
 }
 
+// bf16 partials: each lane reads 8 bf16 (16 B) of every peer, sums in fp32
+// and writes 8 fp32 (two float4) of the local row.  row_vecs counts 16-B
+// units of the bf16 row.
+__global__ void dkv_pull_bf16_kernel(const unsigned long long* __restrict__ bases, long long dk_off,
+                                     long long dv_off, const int* __restrict__ gidx,
+                                     long long n_rows, long long row_vecs, float4* __restrict__ dk,
+                                     float4* __restrict__ dv, int cp) {
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
+       r += warps) {
+    const long long g = gidx[r];
+    for (long long c = lane; c < row_vecs; c += 32) {
+      float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, b[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int p = 0; p < cp; ++p) {
+        const char* base = reinterpret_cast<const char*>(bases[p]);
+        const uint4 x = reinterpret_cast<const uint4*>(base + dk_off)[g * row_vecs + c];
+        const uint4 y = reinterpret_cast<const uint4*>(base + dv_off)[g * row_vecs + c];
+        const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&x);
+        const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 xf = __bfloat1622float2(x2[e]), yf = __bfloat1622float2(y2[e]);
+          a[2 * e] += xf.x; a[2 * e + 1] += xf.y;
+          b[2 * e] += yf.x; b[2 * e + 1] += yf.y;
+        }
+      }
+      dk[(r * row_vecs + c) * 2] = make_float4(a[0], a[1], a[2], a[3]);
+      dk[(r * row_vecs + c) * 2 + 1] = make_float4(a[4], a[5], a[6], a[7]);
+      dv[(r * row_vecs + c) * 2] = make_float4(b[0], b[1], b[2], b[3]);
+      dv[(r * row_vecs + c) * 2 + 1] = make_float4(b[4], b[5], b[6], b[7]);
+    }
+  }
+}
+
 // Push/pull blocks (256 threads) per 8 SMs.  The exchange runs on its own
 // stream beside the attention kernels, which hold one CTA per SM: a grid of
 // 8 blocks per SM took SMs from the attention for the whole exchange (N=4
@@ -96,6 +133,25 @@ extern "C" int wlb_cp_kv_push(const void* k_local, const void* v_local, const in
   kv_push_kernel<<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
       (const int4*)k_local, (const int4*)v_local, gather_local, n_rows, row_bytes / 16,
       (const unsigned long long*)peer_bases, k_off, v_off, cp);
+  WLB_LAUNCH_CHECK();
+  return WLB_OK;
+}
+
+extern "C" int wlb_cp_dkv_pull_ex(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_off,
+                                  const int32_t* gather_local, int64_t n_rows, int64_t row_bytes,
+                                  float* dk, float* dv, int32_t cp, int32_t flags, void* stream) {
+  WLB_REQUIRE((flags & ~WLB_BWD_DKV_BF16) == 0, "unknown pull flags 0x%x", flags);
+  if (!(flags & WLB_BWD_DKV_BF16))
+    return wlb_cp_dkv_pull(peer_bases, dk_off, dv_off, gather_local, n_rows, row_bytes, dk, dv,
+                           cp, stream);
+  WLB_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && dk_off % 16 == 0 && dv_off % 16 == 0,
+              "rows and offsets must be 16-byte aligned");
+  WLB_REQUIRE(cp >= 1, "cp must be >= 1");
+  if (n_rows <= 0) return WLB_OK;
+  // row_bytes is the bf16 partial row; the local fp32 output rows are twice as long
+  dkv_pull_bf16_kernel<<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
+      (const unsigned long long*)peer_bases, dk_off, dv_off, gather_local, n_rows, row_bytes / 16,
+      (float4*)dk, (float4*)dv, cp);
   WLB_LAUNCH_CHECK();
   return WLB_OK;
 }

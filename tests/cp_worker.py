@@ -68,10 +68,13 @@ def pipeline_cases(rank, world, dev):
                 if not ok:
                     failures.append(tag)
         for tn, a, c in zip(("o", "dq", "dk", "dv"), res["nccl"][b], res["symm"][b]):
-            # same kernels, same reduction order over ranks is not guaranteed
-            # (NCCL ring vs peer sum): fp32 partial sums agree to rounding
+            # same kernels; o and dq are rank-local (dq only differs by the order
+            # of its fp32 atomic reductions), dK/dV partials are summed in fp32 by
+            # NCCL and, from bf16 partials, in fp32 by the symmetric pull: they
+            # agree to bf16 rounding of the partials
             err = (a - c).abs().max().item()
-            if err > 1e-3 * max(1.0, a.abs().max().item()):
+            tol = (1e-3 if tn in ("o", "dq") else 8e-3) * max(1.0, a.abs().max().item())
+            if err > tol:
                 failures.append(f"[rank {rank} mb{b}] symm vs nccl {tn}: {err:.3e}")
     return failures
 

@@ -35,7 +35,7 @@ def _inputs(T, tl, hq, hkv, d, seed):
     return mk(T, hq, d), mk(T, hkv, d), mk(T, hkv, d), mk(T, hq, d)
 
 
-def _rank_case(lengths, cp, policy, hq, hkv, d, seed=0, with_bwd=False):
+def _rank_case(lengths, cp, policy, hq, hkv, d, seed=0, with_bwd=False, dkv_dtype=torch.float32):
     lengths = so.pad_lengths_for_cp(lengths, cp)
     T = sum(lengths)
     q, k, v, do = _inputs(T, T // cp, hq, hkv, d, seed)
@@ -55,7 +55,7 @@ def _rank_case(lengths, cp, policy, hq, hkv, d, seed=0, with_bwd=False):
             # dK/dV outputs start as NaN: every row must be written (the kernel
             # stores covered KV tiles whole and zero-fills the rest)
             nan = lambda: torch.full((kd.shape[0], kd.shape[1], kd.shape[2]), float("nan"),
-                                     dtype=torch.float32, device=dev)
+                                     dtype=dkv_dtype, device=dev)
             dq, dk, dv = attn_backward(ql.to(dev), kd, vd, o, lse, do[idx].contiguous().to(dev),
                                        tiles, dk_out=nan(), dv_out=nan())
             _close(dq, rdq, "dq")
@@ -200,3 +200,12 @@ def test_project_qkv_rope_in_document_positions(cp, policy):
         _close(q, _rope_ref(y[:, :hq], pos, 500000.0), "q")
         _close(k, _rope_ref(y[:, hq:hq + hkv], pos, 500000.0), "k")
         _close(v, y[:, hq + hkv:], "v")
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_bwd_bf16_partials(d):
+    """bf16 dK/dV partials (the symmetric CP exchange's format): every row
+    written, within the bf16 bar of the fp32 oracle."""
+    _rank_case([1000, 3, 250, 777, 40], 4, "per_document", 4, 2, d, seed=51, with_bwd=True,
+               dkv_dtype=torch.bfloat16)
+    _rank_case([6144], 1, "per_document", 2, 2, d, seed=52, with_bwd=True, dkv_dtype=torch.bfloat16)
