@@ -28,3 +28,46 @@ def test_pipeline_matches_direct_cp1():
         assert torch.equal(o, o2)                              # deterministic forward
         assert (dq.float() - dq2.float()).abs().max() < 1e-2   # dQ uses fp32 atomics
         assert torch.allclose(dk, dk2, atol=1e-4) and torch.allclose(dv, dv2, atol=1e-4)
+
+
+def test_pipeline_host_buffers_hooks():
+    """The e2e path: inputs arrive by H2D copies on another stream (`ready`
+    events), outputs leave through `on_outputs` (D2H on a third stream) with
+    keep_outputs=False; results equal the direct kernels."""
+    lengths = [[300, 17, 1, 640, 129, 2, 959], [2048], [1000, 1048]]
+    dev = torch.device("cuda")
+    g = torch.Generator().manual_seed(5)
+    host = []
+    for ls in lengths:
+        T = sum(ls)
+        mk = lambda h: torch.randn((T, h, 128), generator=g).to(torch.bfloat16).pin_memory()
+        host.append((mk(4), mk(2), mk(2), mk(4)))
+    dev_in = [tuple(torch.empty_like(t, device=dev) for t in hs) for hs in host]
+    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    ready = []
+    with torch.cuda.stream(h2d):
+        for dst, src in zip(dev_in, host):
+            for a, b in zip(dst, src):
+                a.copy_(b, non_blocking=True)
+            e = torch.cuda.Event()
+            e.record(h2d)
+            ready.append(e)
+    got = [None] * len(lengths)
+
+    def on_outputs(b, outs, fin):
+        d2h.wait_event(fin)
+        with torch.cuda.stream(d2h):
+            got[b] = tuple(t.to("cpu", non_blocking=True) for t in outs)
+            for t in outs:
+                t.record_stream(d2h)
+
+    shards = build_cp_shards(lengths, 1, 0, "adaptive")
+    CPStepPipeline().run(shards, dev_in, ready=ready, on_outputs=on_outputs, keep_outputs=False)
+    torch.cuda.synchronize()
+    for b, ((q, k, v, do), sh) in enumerate(zip(dev_in, shards)):
+        o2, lse = attn_forward(q, k, v, sh.tiles)
+        dq2, dk2, dv2 = attn_backward(q, k, v, o2, lse, do, sh.tiles)
+        o, dq, dk, dv = got[b]
+        assert torch.equal(o, o2.cpu())
+        assert (dq.float() - dq2.float().cpu()).abs().max() < 1e-2
+        assert torch.allclose(dk, dk2.cpu(), atol=1e-4) and torch.allclose(dv, dv2.cpu(), atol=1e-4)
