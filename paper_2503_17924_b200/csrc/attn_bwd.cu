@@ -1205,7 +1205,10 @@ bwd_kv_tiles_kernel(int nd, const int* __restrict__ rowset_off, const int* __res
 }
 
 static int g_bwd_v3_min_rows = WLB_BWD_V3_MIN_ROWS;
-static int g_bwd_hpc_short = 4;
+#ifndef WLB_HPC
+#define WLB_HPC 4   // KV heads per CTA for short row-sets (2 the same, 8 up to 4% slower)
+#endif
+static int g_bwd_hpc_short = WLB_HPC;
 // v3 as 2-CTA clusters exchanging dQ halves over DSMEM (experimental, off):
 // it halves the dQ reduction bytes but adds the same number of DSMEM bytes to
 // the SM's outbound memory path, which is what bounds the reductions (plain
@@ -1372,7 +1375,7 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   // several KV heads per CTA for short row-sets (< 2048 local rows per
   // document on average): the next head's loads overlap this head's tail
   // (only with >= 6 waves of CTAs left: Tl/128 bounds the KV tiles from below)
-  const int hpc = (Hkv % 4 == 0 && (long long)Tl < (long long)WLB_HPC_ROWS * (n_docs > 0 ? n_docs : 1) &&
+  const int hpc = (Hkv % g_bwd_hpc_short == 0 && (long long)Tl < (long long)WLB_HPC_ROWS * (n_docs > 0 ? n_docs : 1) &&
                    (long long)(Tl / 128) * Hkv >= 6LL * 148 * g_bwd_hpc_short)
                       ? g_bwd_hpc_short : 1;
   attn_bwd_kernel<D, 2><<<(unsigned)max_items * ((Hkv + hpc - 1) / hpc), C::THREADS, C::SMEM,

@@ -372,7 +372,10 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
   if (warp == 2) tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
-static int g_fwd_hpc_short = 4;
+#ifndef WLB_HPC
+#define WLB_HPC 4   // heads per CTA for short row-sets (2 measured the same, 8 up to 17% slower)
+#endif
+static int g_fwd_hpc_short = WLB_HPC;
 
 template <int D>
 static int launch_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
@@ -398,7 +401,7 @@ static int launch_fwd(const void* q, const void* k, const void* v, void* o, floa
   // Only when that still leaves >= 6 waves of CTAs (a small rank's few tiles
   // need the parallelism more: config-5 ranks of ~4K rows lost 10% with it).
   const long long docs = std::max<long long>(1, (long long)max_tiles - Tl / (2 * C::BM) - 1);
-  const int hpc = (Hq % 4 == 0 && (long long)Tl < (long long)WLB_HPC_ROWS * docs &&
+  const int hpc = (Hq % g_fwd_hpc_short == 0 && (long long)Tl < (long long)WLB_HPC_ROWS * docs &&
                    (long long)max_tiles * Hq >= 6LL * 148 * g_fwd_hpc_short)
                       ? g_fwd_hpc_short : 1;
   attn_fwd_kernel<D><<<(unsigned)max_tiles * ((Hq + hpc - 1) / hpc), C::THREADS, C::SMEM, stream>>>(
