@@ -1,3 +1,4 @@
+# forward A/B of library builds (dev aid): fwd_ab.sh A B ...
 for rep in 1 2 3; do for v in "$@"; do
 echo "$v $(WLB_LIB_PATH=var/lib$v.so python tools/probe_attn.py --single --iters 8 | sed 's/| bwd.*//') | $(WLB_LIB_PATH=var/lib$v.so python tools/probe_attn.py --batch 1 --iters 8 | sed 's/.*fwd/fwd/; s/| bwd.*//')"
 done; done
