@@ -41,6 +41,9 @@
                           //    (measured 7% slower: a lone softmax warp is
                           //    issue/MUFU-latency bound, not contended)
 #endif
+#ifndef WLB_FWD_MMA8
+#define WLB_FWD_MMA8 1   // 8-MMA chains under one elect.sync (fewer issue slots on the MMA warp's SMSP)
+#endif
 #ifndef WLB_FWD_POLY
 #define WLB_FWD_POLY 3   // column pairs (of every 8) whose exp2 runs on the FMA pipe
 #endif
@@ -173,6 +176,39 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer --
     const uint32_t q_base = smem_u32(sQ), k_base = smem_u32(sK), v_base = smem_u32(sV);
+#if WLB_FWD_MMA8
+    // one elect.sync per 8-MMA chain, descriptors as base + constant offsets
+    uint32_t koff[8];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) koff[kk] = ((kk >> 2) * C::BN * 128 + (kk & 3) * 32) >> 4;
+    auto qk = [&](int t, int jj) {           // S_t = Q_t K_jj^T
+      const int st = jj % C::STAGES;
+      static_assert(D == 128 || D == 64, "head dim");
+      if (D == 128) {
+        uint32_t qoff[8];
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) qoff[kk] = ((kk >> 2) * C::BM * 128 + (kk & 3) * 32) >> 4;
+        mma_ss8_w(tmem + C::COL_S + t * 128, sdesc_sw128(q_base + t * C::Q_BYTES, 16, 1024),
+                  sdesc_sw128(k_base + st * C::KV_BYTES, 16, 1024), qoff, koff, C::IDESC_QK, 0);
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t qo = t * C::Q_BYTES + (kk >> 2) * C::BM * 128 + (kk & 3) * 32;
+          const uint32_t ko = st * C::KV_BYTES + (kk >> 2) * C::BN * 128 + (kk & 3) * 32;
+          mma_ss_w(tmem + C::COL_S + t * 128, sdesc_sw128(q_base + qo, 16, 1024),
+                   sdesc_sw128(k_base + ko, 16, 1024), C::IDESC_QK, kk > 0);
+        }
+      }
+      mma_commit_w(&bars->s_full[t]);
+    };
+    auto pv = [&](int t, int j, int jj) {   // O_t += P_t V_jj, P_t packed bf16 in TMEM
+      const int st = jj % C::STAGES;
+      mma_ts8_w(tmem + C::COL_O + t * D, tmem + C::COL_S + t * 128, 8,
+                sdesc_sw128(v_base + st * C::KV_BYTES, C::BN * 128, 1024), 2048 >> 4, C::IDESC_PV,
+                j > 0);
+      mma_commit_w(&bars->pv_done[t]);
+    };
+#else
     auto qk = [&](int t, int jj) {           // S_t = Q_t K_jj^T
       const int st = jj % C::STAGES;
 #pragma unroll
@@ -193,6 +229,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                  C::IDESC_PV, (j > 0) || (kk > 0));
       mma_commit_w(&bars->pv_done[t]);
     };
+#endif
     for (int hh = 0; hh < nh; ++hh) {
       const int kb = hh * n_kv[0];            // K/V ring base of this head
       const int sb[2] = {hh * n_kv[0], hh * n_kv[1]};   // per-tile step base

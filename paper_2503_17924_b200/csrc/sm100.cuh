@@ -63,6 +63,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #ifndef WLB_MMA_WAIT
 #define WLB_MMA_WAIT 1
 #endif
+#ifndef WLB_MMA_HINT
+#define WLB_MMA_HINT 32
+#endif
 __device__ __forceinline__ void mbar_wait_fast(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
 #if WLB_MMA_WAIT == 0
@@ -79,6 +82,32 @@ __device__ __forceinline__ void mbar_wait_fast(uint64_t* bar, uint32_t parity) {
         : "r"(a), "r"(parity)
         : "memory");
   } while (!ok);
+#elif WLB_MMA_WAIT == 3
+  // short explicit suspend hint: fewer probes stealing the SMSP's issue slots
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity), "n"(WLB_MMA_HINT)
+        : "memory");
+  } while (!ok);
+#elif WLB_MMA_WAIT == 4
+  // poll with a nanosleep back-off
+  uint32_t ok;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) break;
+    __nanosleep(WLB_MMA_HINT);
+  }
 #else
   uint32_t ok;
   do {
@@ -178,6 +207,63 @@ __device__ __forceinline__ void mma_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint6
       "setp.ne.b32 p, %4, 0;\n\t" WLB_ELECT
       "@P tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// Eight K16 steps of one MMA chain under ONE elect.sync: D (+)= A_k B_k for
+// k = 0..7, descriptor k = base + k * step (in 16-B units, low address field;
+// addresses stay below 256 KB so the field never carries).  `acc0` is the
+// accumulate flag of the first step; the rest accumulate.
+__device__ __forceinline__ void mma_ss8_w(uint32_t d_tmem, uint64_t a0, uint64_t b0,
+                                          const uint32_t (&ao)[8], const uint32_t (&bo)[8],
+                                          uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p, P;\n\t.reg .b64 a, b;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t" WLB_ELECT
+      "add.s64 a, %1, %5;\n\tadd.s64 b, %2, %13;\n\t"
+      "@P tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, p;\n\t"
+      "add.s64 a, %1, %6;\n\tadd.s64 b, %2, %14;\n\t"
+      "@P tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, %1, %7;\n\tadd.s64 b, %2, %15;\n\t"
+      "@P tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, %1, %8;\n\tadd.s64 b, %2, %16;\n\t"
+      "@P tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, %1, %9;\n\tadd.s64 b, %2, %17;\n\t"
+      "@P tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, %1, %10;\n\tadd.s64 b, %2, %18;\n\t"
+      "@P tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, %1, %11;\n\tadd.s64 b, %2, %19;\n\t"
+      "@P tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, %1, %12;\n\tadd.s64 b, %2, %20;\n\t"
+      "@P tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n\t}" ::"r"(d_tmem),
+      "l"(a0), "l"(b0), "r"(idesc), "r"(acc0), "l"((uint64_t)ao[0]), "l"((uint64_t)ao[1]),
+      "l"((uint64_t)ao[2]), "l"((uint64_t)ao[3]), "l"((uint64_t)ao[4]), "l"((uint64_t)ao[5]),
+      "l"((uint64_t)ao[6]), "l"((uint64_t)ao[7]), "l"((uint64_t)bo[0]), "l"((uint64_t)bo[1]),
+      "l"((uint64_t)bo[2]), "l"((uint64_t)bo[3]), "l"((uint64_t)bo[4]), "l"((uint64_t)bo[5]),
+      "l"((uint64_t)bo[6]), "l"((uint64_t)bo[7]));
+}
+// same with A from TMEM: A column a_tmem + k * a_col_step
+__device__ __forceinline__ void mma_ts8_w(uint32_t d_tmem, uint32_t a_tmem, uint32_t a_col_step,
+                                          uint64_t b0, uint32_t b_step16, uint32_t idesc,
+                                          uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p, P;\n\t.reg .b64 b;\n\t.reg .b32 a;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t" WLB_ELECT
+      "mov.b32 a, %1;\n\tmov.b64 b, %3;\n\t"
+      "@P tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, p;\n\t"
+      "add.s32 a, a, %2;\n\tadd.s64 b, b, %6;\n\t"
+      "@P tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, 1;\n\t"
+      "add.s32 a, a, %2;\n\tadd.s64 b, b, %6;\n\t"
+      "@P tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, 1;\n\t"
+      "add.s32 a, a, %2;\n\tadd.s64 b, b, %6;\n\t"
+      "@P tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, 1;\n\t"
+      "add.s32 a, a, %2;\n\tadd.s64 b, b, %6;\n\t"
+      "@P tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, 1;\n\t"
+      "add.s32 a, a, %2;\n\tadd.s64 b, b, %6;\n\t"
+      "@P tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, 1;\n\t"
+      "add.s32 a, a, %2;\n\tadd.s64 b, b, %6;\n\t"
+      "@P tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, 1;\n\t"
+      "add.s32 a, a, %2;\n\tadd.s64 b, b, %6;\n\t"
+      "@P tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, 1;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "r"(a_col_step), "l"(b0), "r"(idesc), "r"(acc0), "l"((uint64_t)b_step16));
 }
 __device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
   asm volatile(
