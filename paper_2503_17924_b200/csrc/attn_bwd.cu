@@ -716,6 +716,14 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     // dS^T lives only in SMEM, and dK reads it from there (SS MMA).
     const uint32_t k_b = smem_u32(sK), v_b = smem_u32(sV), q_b = smem_u32(sQ),
                    do_b = smem_u32(sDO), ds_b = smem_u32(sDS);
+    // descriptor offsets (16-B units) of the 8 K16 steps: K-major operands step
+    // 32 B within a 128-B swizzle row and a slab every 4; MN-major ones 16 rows
+    uint32_t kmaj_off[8], mn_off[8];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      kmaj_off[kk] = ((kk >> 2) * C::SLAB + (kk & 3) * 32) >> 4;
+      mn_off[kk] = (kk * 2048) >> 4;
+    }
     mbar_wait(&bars->kv_full, 0);
     for (int i = 0; i <= n_iter; ++i) {
       if (i < n_iter) {
@@ -724,13 +732,10 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         mbar_wait(&bars->q_full[st], (i / C::QS) & 1);
         TRACE3(0, i);
         tc_fence_after();
-        // S^T = K Q^T (contract over D; K-major both)
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t o = (kk >> 2) * C::SLAB + (kk & 3) * 32;
-          mma_ss_w(tmem + C::COL_S, sdesc_sw128(k_b + o, 16, 1024), sdesc_sw128(qs + o, 16, 1024),
-                   C::IDESC_ST, kk > 0);
-        }
+        // S^T = K Q^T (contract over D; K-major both); 8-MMA chains under one
+        // elect.sync keep the MMA warp's issue slots off its SMSP's compute warps
+        mma_ss8_w(tmem + C::COL_S, sdesc_sw128(k_b, 16, 1024), sdesc_sw128(qs, 16, 1024), kmaj_off,
+                  kmaj_off, C::IDESC_ST, 0);
         mma_commit_w(&bars->s_full);
       }
       if (i >= 1) {
@@ -743,16 +748,12 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         const uint32_t dsb = ds_b;
         // dQ = dS K (contract over keys; A = dS from the dS^T buffer and B = K,
         // both MN-major): lanes = queries, so the drain emits 16-B reductions
-#pragma unroll
-        for (int kk = 0; kk < C::BN / 16; ++kk)
-          mma_ss_w(tmem + C::COL_DP, sdesc_sw128(dsb + kk * 2048, C::SLAB, 1024),
-                   sdesc_sw128(k_b + kk * 2048, C::SLAB, 1024), C::IDESC_DQ, kk > 0);
+        mma_ss8_w(tmem + C::COL_DP, sdesc_sw128(dsb, C::SLAB, 1024), sdesc_sw128(k_b, C::SLAB, 1024),
+                  mn_off, mn_off, C::IDESC_DQ, 0);
         mma_commit_w(&bars->dq_full);
         // dK += dS^T Q (contract over queries; A = dS^T K-major from SMEM)
-#pragma unroll
-        for (int kk = 0; kk < C::BM / 16; ++kk)
-          mma_ss_w(tmem + C::COL_DK, sdesc_sw128(dsb + (kk >> 2) * C::SLAB + (kk & 3) * 32, 16, 1024),
-                   sdesc_sw128(qs + kk * 2048, C::SLAB, 1024), C::IDESC_ACC, (j > 0) || (kk > 0));
+        mma_ss8_w(tmem + C::COL_DK, sdesc_sw128(dsb, 16, 1024), sdesc_sw128(qs, C::SLAB, 1024),
+                  kmaj_off, mn_off, C::IDESC_ACC, j > 0);
         mma_commit_w(&bars->q_empty[st]);
         if (j == n_iter - 1) mma_commit_w(&bars->acc_done);
       }
@@ -765,12 +766,8 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         if (i >= 1) mbar_wait_fast(&bars->s_free, (i - 1) & 1);
         TRACE3(1, i);
         tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t o = (kk >> 2) * C::SLAB + (kk & 3) * 32;
-          mma_ss_w(tmem + C::COL_DP, sdesc_sw128(v_b + o, 16, 1024), sdesc_sw128(dos + o, 16, 1024),
-                   C::IDESC_ST, kk > 0);
-        }
+        mma_ss8_w(tmem + C::COL_DP, sdesc_sw128(v_b, 16, 1024), sdesc_sw128(dos, 16, 1024), kmaj_off,
+                  kmaj_off, C::IDESC_ST, 0);
         mma_commit_w(&bars->dp_full);
         // dV += P^T dO, contract over queries, A = P^T from TMEM; chunk c holds
         // queries [32c, 32c+32) of both 64-query halves
