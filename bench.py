@@ -91,12 +91,18 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+        self.first = []  # pre-timed-region sample, not reported
+        if self.proc is not None:
+            # block until nvidia-smi is live, so its samples cover the timed region
+            line = self.proc.stdout.readline()
+            if line.strip():
+                self.first.append(line)
         return self
 
     def __exit__(self, *exc):
         self.lines = []
         if self.proc is not None:
-            time.sleep(0.25)
+            time.sleep(0.05)
             self.proc.terminate()
             out, _ = self.proc.communicate(timeout=10)
             self.lines = [l for l in out.splitlines() if l.strip()]
@@ -220,7 +226,7 @@ def main():
     ap.add_argument("--shape", default="llama7b", choices=["llama7b", "llama70b-gqa"],
                     help="attention shape: Llama-7B 32x128 (configs 2/3) or Llama-70B GQA "
                          "64q/8kv x128 (config 4)")
-    ap.add_argument("--clock-ms", type=int, default=500,
+    ap.add_argument("--clock-ms", type=int, default=100,
                     help="nvidia-smi sampling period during the timed region (0: off)")
     args = ap.parse_args()
 
