@@ -44,3 +44,21 @@ def test_reference_arm_non_zero_ranks_do_nothing(capsys):
         steps, warmup = 1, 0
     b.run_reference(A(), world=4, rank=2)
     assert capsys.readouterr().out == ""
+
+
+def test_clock_summary_flags_throttle_reasons():
+    """`clocks` keeps the busy-clock median and every throttle reason seen
+    (the contract rejects hw_slowdown / thermal runs; sw_power_cap is noted)."""
+    b = _bench()
+    c = b.ClockSampler(0, 0)
+    with c:
+        pass
+    assert c.summary()["samples"] == 0
+    c.lines = ["1800, 1965, Not Active, Not Active, Not Active, Active",
+               "1700, 1965, Not Active, Active, Not Active, Not Active",
+               "300, 1965, Not Active, Not Active, Not Active, Not Active",
+               "garbage"]
+    s = c.summary()
+    assert s["samples"] == 3 and s["sm_max_mhz"] == 1965.0
+    assert s["sm_mhz"] == 1750.0                    # idle 300 MHz sample excluded
+    assert s["reasons"] == ["hw_thermal_slowdown", "sw_power_cap"]
