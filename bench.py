@@ -23,6 +23,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import select
 import statistics
 import subprocess
 import sys
@@ -94,7 +95,8 @@ class ClockSampler:
         self.first = []  # pre-timed-region sample, not reported
         if self.proc is not None:
             # block until nvidia-smi is live, so its samples cover the timed region
-            line = self.proc.stdout.readline()
+            ready, _, _ = select.select([self.proc.stdout], [], [], 10.0)
+            line = self.proc.stdout.readline() if ready else ""
             if line.strip():
                 self.first.append(line)
         return self
