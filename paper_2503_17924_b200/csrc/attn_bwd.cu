@@ -531,7 +531,9 @@ static_assert(sizeof(Bwd3Bars) <= 256, "barrier block");
 // v3 wins on long row-sets (+2-3% at 22K-32K documents) and loses on short
 // ones (-7% on 2-3K documents: its serial first/last tile and 128-row tiles
 // cost more per work item), so it is used when the rank's mean local rows per
-// document reach this many.
+// document reach this many.  Re-checked on the final code with the N=1 bench
+// (profiles/r01c_ab_bwd_v3_min_rows.txt): 4096 935-939, 2048 921-931, 8192
+// 929-933 TFLOP/s.
 #ifndef WLB_BWD_V3_MIN_ROWS
 #define WLB_BWD_V3_MIN_ROWS 4096
 #endif
