@@ -31,7 +31,9 @@
 #ifndef WLB_HPC_ROWS
 #define WLB_HPC_ROWS 4096   // several heads per CTA below this many local rows per document
                            // (2048-row documents: fwd +5%, bwd +3% vs a 2048 threshold;
-                           //  8192 cost a 6-document 32K sequence 7% in the forward)
+                           //  8192 cost a 6-document 32K sequence 7% in the forward;
+                           //  N=4 128K bench: 2048/4096/8192 within noise,
+                           //  profiles/r01c_ab_hpc_rows_n4.txt)
 #endif
 
 #include <algorithm>
