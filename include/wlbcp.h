@@ -169,6 +169,19 @@ int wlb_cp_dkv_pull(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_off,
 int wlb_cp_dkv_pull_ex(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_off,
                        const int32_t* gather_local, int64_t n_rows, int64_t row_bytes,
                        float* dk, float* dv, int32_t cp, int32_t flags, void* stream);
+/* As wlb_cp_dkv_pull_ex, reading a peer's partial row only where that peer's
+ * backward covered it: rank p covers document d's keys below
+ * min(len_d, roundup128(last local position of p in d + 1)), the rest are the
+ * zeros the backward writes, so the sums are identical.  rowset_all:
+ * [cp][rowset_stride] row-set offsets of every rank (the shard plan's
+ * rowset_off for this micro-batch); positions_all: [cp][n_rows] in-document
+ * positions of every rank's local rows; doc_start: [n_docs+1]. */
+int wlb_cp_dkv_pull_cov(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_off,
+                        const int32_t* gather_local, int64_t n_rows, int64_t row_bytes,
+                        float* dk, float* dv, int32_t cp, int32_t flags,
+                        const int32_t* rowset_all, int32_t rowset_stride,
+                        const int32_t* positions_all, const int32_t* doc_start, int32_t n_docs,
+                        void* stream);
 
 #ifdef __cplusplus
 }

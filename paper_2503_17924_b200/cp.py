@@ -211,6 +211,8 @@ class SymmExchange:
         self.kv_bases = torch.tensor(list(self.kv_h.buffer_ptrs), dtype=torch.int64, device=device)
         self.dkv_bases = torch.tensor(list(self.dkv_h.buffer_ptrs), dtype=torch.int64, device=device)
         self.free = [None] * slots     # event: all ranks finished pulling slot s
+        # skip peers' uncovered (all-zero) partial rows in the pull; WLB_XCHG_PULL=all reads every row
+        self.pull_covered = os.environ.get("WLB_XCHG_PULL", "covered") != "all"
 
     def _view(self, buf, idx, T):
         return buf[idx * self.n: idx * self.n + T * self.hkv * self.d].view(T, self.hkv, self.d)
@@ -241,11 +243,24 @@ class SymmExchange:
         dv = torch.empty_like(dk)
         self.dkv_h.barrier(channel=1)
         es = 2 if self.dkv_bf16 else 4
-        _native.check(_native.lib().wlb_cp_dkv_pull_ex(
-            self.dkv_bases.data_ptr(), 2 * s * self.n * es, (2 * s + 1) * self.n * es,
-            shard.gather_local.data_ptr(), tl, self.hkv * self.d * es, dk.data_ptr(), dv.data_ptr(),
-            self.cp, _native.WLB_BWD_DKV_BF16 if self.dkv_bf16 else 0, _native.stream_ptr()),
-            "wlb_cp_dkv_pull_ex")
+        flags = _native.WLB_BWD_DKV_BF16 if self.dkv_bf16 else 0
+        if self.pull_covered and shard.tiles.n_docs > 0:
+            # read a peer's partial row only where that peer's backward wrote it
+            plan, b_ = shard.plan, shard.index
+            rows = plan.rowset_off[b_]
+            assert rows.is_contiguous()
+            pos = plan.positions[plan.tok_off[b_]:]
+            _native.check(_native.lib().wlb_cp_dkv_pull_cov(
+                self.dkv_bases.data_ptr(), 2 * s * self.n * es, (2 * s + 1) * self.n * es,
+                shard.gather_local.data_ptr(), tl, self.hkv * self.d * es, dk.data_ptr(),
+                dv.data_ptr(), self.cp, flags, rows.data_ptr(), rows.shape[-1], pos.data_ptr(),
+                shard.tiles.doc_start.data_ptr(), shard.tiles.n_docs, _native.stream_ptr()),
+                "wlb_cp_dkv_pull_cov")
+        else:
+            _native.check(_native.lib().wlb_cp_dkv_pull_ex(
+                self.dkv_bases.data_ptr(), 2 * s * self.n * es, (2 * s + 1) * self.n * es,
+                shard.gather_local.data_ptr(), tl, self.hkv * self.d * es, dk.data_ptr(),
+                dv.data_ptr(), self.cp, flags, _native.stream_ptr()), "wlb_cp_dkv_pull_ex")
         self.dkv_h.barrier(channel=1)
         ev = torch.cuda.Event()
         ev.record()

@@ -100,6 +100,79 @@ __global__ void dkv_pull_bf16_kernel(const unsigned long long* __restrict__ base
   }
 }
 
+// Coverage-aware pull: a peer's partial row is read only where that peer's
+// backward wrote it.  Rank p's KV tiles cover the keys of document d up to
+// its last local query position there, rounded up to the 128-key tile
+// (capped at the document length); every key past that is an exact zero
+// (zero_uncovered_kernel).  Skipping those rows gives the same fp32 sums and
+// cuts the NVLink reads, most under per-sequence shards where a short
+// document lives in one rank's chunk.  rowset_all: [cp][rs] per-rank row-set
+// offsets per document; pos_all: [cp][tl] per-rank in-document positions.
+template <bool BF16>
+__global__ void dkv_pull_cov_kernel(const unsigned long long* __restrict__ bases, long long dk_off,
+                                    long long dv_off, const int* __restrict__ gidx,
+                                    long long n_rows, long long row_vecs, float4* __restrict__ dk,
+                                    float4* __restrict__ dv, int cp,
+                                    const int* __restrict__ rowset_all, int rs,
+                                    const int* __restrict__ pos_all, long long tl,
+                                    const int* __restrict__ doc_start, int n_docs) {
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
+       r += warps) {
+    const int g = gidx[r];
+    int lo = 0, hi = n_docs;                   // last document with doc_start <= g
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (doc_start[mid] <= g) lo = mid;
+      else hi = mid;
+    }
+    bool covers = false;
+    if (lane < cp) {
+      const int r0 = rowset_all[lane * rs + lo], r1 = rowset_all[lane * rs + lo + 1];
+      if (r1 > r0) {
+        const int len = doc_start[lo + 1] - doc_start[lo];
+        const int cov = min(len, (pos_all[lane * tl + r1 - 1] + 128) / 128 * 128);
+        covers = g - doc_start[lo] < cov;
+      }
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, covers);
+    for (long long c = lane; c < row_vecs; c += 32) {
+      float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, b[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int p = 0; p < cp; ++p) {
+        if (!((mask >> p) & 1u)) continue;
+        const char* base = reinterpret_cast<const char*>(bases[p]);
+        if (BF16) {
+          const uint4 x = reinterpret_cast<const uint4*>(base + dk_off)[g * row_vecs + c];
+          const uint4 y = reinterpret_cast<const uint4*>(base + dv_off)[g * row_vecs + c];
+          const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&x);
+          const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 xf = __bfloat1622float2(x2[e]), yf = __bfloat1622float2(y2[e]);
+            a[2 * e] += xf.x; a[2 * e + 1] += xf.y;
+            b[2 * e] += yf.x; b[2 * e + 1] += yf.y;
+          }
+        } else {
+          const float4 x = reinterpret_cast<const float4*>(base + dk_off)[g * row_vecs + c];
+          const float4 y = reinterpret_cast<const float4*>(base + dv_off)[g * row_vecs + c];
+          a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
+          b[0] += y.x; b[1] += y.y; b[2] += y.z; b[3] += y.w;
+        }
+      }
+      if (BF16) {
+        dk[(r * row_vecs + c) * 2] = make_float4(a[0], a[1], a[2], a[3]);
+        dk[(r * row_vecs + c) * 2 + 1] = make_float4(a[4], a[5], a[6], a[7]);
+        dv[(r * row_vecs + c) * 2] = make_float4(b[0], b[1], b[2], b[3]);
+        dv[(r * row_vecs + c) * 2 + 1] = make_float4(b[4], b[5], b[6], b[7]);
+      } else {
+        dk[r * row_vecs + c] = make_float4(a[0], a[1], a[2], a[3]);
+        dv[r * row_vecs + c] = make_float4(b[0], b[1], b[2], b[3]);
+      }
+    }
+  }
+}
+
 // Push/pull blocks (256 threads) per 8 SMs.  The exchange runs on its own
 // stream beside the attention kernels, which hold one CTA per SM: a grid of
 // 8 blocks per SM took SMs from the attention for the whole exchange (N=4
@@ -166,6 +239,34 @@ extern "C" int wlb_cp_dkv_pull(const uint64_t* peer_bases, int64_t dk_off, int64
   dkv_pull_kernel<<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
       (const unsigned long long*)peer_bases, dk_off, dv_off, gather_local, n_rows, row_bytes / 16,
       (float4*)dk, (float4*)dv, cp);
+  WLB_LAUNCH_CHECK();
+  return WLB_OK;
+}
+
+extern "C" int wlb_cp_dkv_pull_cov(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_off,
+                                   const int32_t* gather_local, int64_t n_rows, int64_t row_bytes,
+                                   float* dk, float* dv, int32_t cp, int32_t flags,
+                                   const int32_t* rowset_all, int32_t rowset_stride,
+                                   const int32_t* positions_all, const int32_t* doc_start,
+                                   int32_t n_docs, void* stream) {
+  WLB_REQUIRE((flags & ~WLB_BWD_DKV_BF16) == 0, "unknown pull flags 0x%x", flags);
+  WLB_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && dk_off % 16 == 0 && dv_off % 16 == 0,
+              "rows and offsets must be 16-byte aligned");
+  WLB_REQUIRE(cp >= 1 && cp <= 32, "cp must be in [1, 32]");
+  WLB_REQUIRE(n_docs >= 1 && rowset_stride >= n_docs + 1, "bad row-set table (n_docs %d, stride %d)",
+              n_docs, rowset_stride);
+  if (n_rows <= 0) return WLB_OK;
+  const long long tl = n_rows;   // every rank holds T / cp rows
+  if (flags & WLB_BWD_DKV_BF16)
+    dkv_pull_cov_kernel<true><<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
+        (const unsigned long long*)peer_bases, dk_off, dv_off, gather_local, n_rows,
+        row_bytes / 16, (float4*)dk, (float4*)dv, cp, rowset_all, rowset_stride, positions_all,
+        tl, doc_start, n_docs);
+  else
+    dkv_pull_cov_kernel<false><<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
+        (const unsigned long long*)peer_bases, dk_off, dv_off, gather_local, n_rows,
+        row_bytes / 16, (float4*)dk, (float4*)dv, cp, rowset_all, rowset_stride, positions_all,
+        tl, doc_start, n_docs);
   WLB_LAUNCH_CHECK();
   return WLB_OK;
 }

@@ -29,13 +29,22 @@ def check(name, got, ref, atol=2e-2, rtol=1e-2):
 
 
 def pipeline_cases(rank, world, dev):
+    failures = []
+    for policy in ("adaptive", "per_sequence"):
+        failures += _pipeline_cases(rank, world, dev, policy)
+    return failures
+
+
+def _pipeline_cases(rank, world, dev, policy):
     """CPStepPipeline over 3 micro-batches (slot reuse in the symmetric
-    exchange) with both exchanges: each vs the oracle, and symm == NCCL."""
+    exchange) with both exchanges: each vs the oracle, and symm == NCCL.  The
+    symmetric pull that skips peers' uncovered rows (default) must equal the
+    pull that reads every row bit for bit."""
     failures = []
     hq, hkv, d = 4, 2, 128
     mbs = [so.pad_lengths_for_cp(x, world) for x in
            ([900, 3, 129, 1000, 1], [2048], [300, 300, 1000, 17, 512, 33])]
-    plan = wl.build_shard_plan(mbs, world, "adaptive")
+    plan = wl.build_shard_plan(mbs, world, policy)
     shards = [shard_for_rank(plan, b, rank) for b in range(len(mbs))]
     g = torch.Generator().manual_seed(11)
     full, inputs = [], []
@@ -47,8 +56,11 @@ def pipeline_cases(rank, world, dev):
         inputs.append(tuple(x[idx].to(dev) for x in t))
     t_max = max(sum(x) for x in mbs)
     res = {}
+    symm_all = SymmExchange(dist.group.WORLD, t_max, hkv, d, dev)
+    symm_all.pull_covered = False
     for name, ex in (("nccl", NcclExchange()),
-                     ("symm", SymmExchange(dist.group.WORLD, t_max, hkv, d, dev))):
+                     ("symm", SymmExchange(dist.group.WORLD, t_max, hkv, d, dev)),
+                     ("symm-all", symm_all)):
         pipe = CPStepPipeline(exchange=ex)
         for _ in range(2):                      # second pass reuses both slots again
             outs = pipe.run(shards, inputs)
@@ -63,7 +75,7 @@ def pipeline_cases(rank, world, dev):
             for tn, got, ref in zip(("o", "dq", "dk", "dv"), res[name][b],
                                     (ro[idx], rdq[idx], rdk[idx], rdv[idx])):
                 ok, msg = check(tn, got, ref)
-                tag = f"[rank {rank} pipeline {name} mb{b}] {msg}"
+                tag = f"[rank {rank} pipeline {policy} {name} mb{b}] {msg}"
                 print(tag, flush=True)
                 if not ok:
                     failures.append(tag)
@@ -75,7 +87,11 @@ def pipeline_cases(rank, world, dev):
             err = (a - c).abs().max().item()
             tol = (1e-3 if tn in ("o", "dq") else 8e-3) * max(1.0, a.abs().max().item())
             if err > tol:
-                failures.append(f"[rank {rank} mb{b}] symm vs nccl {tn}: {err:.3e}")
+                failures.append(f"[rank {rank} {policy} mb{b}] symm vs nccl {tn}: {err:.3e}")
+        for tn, a, c in zip(("dk", "dv"), res["symm"][b][2:], res["symm-all"][b][2:]):
+            if not torch.equal(a, c):
+                failures.append(f"[rank {rank} {policy} mb{b}] covered pull != full pull {tn}: "
+                                f"{(a - c).abs().max().item():.3e}")
     return failures
 
 
