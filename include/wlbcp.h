@@ -176,6 +176,15 @@ int wlb_cp_dkv_pull_ex(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_of
  * [cp][rowset_stride] row-set offsets of every rank (the shard plan's
  * rowset_off for this micro-batch); positions_all: [cp][n_rows] in-document
  * positions of every rank's local rows; doc_start: [n_docs+1]. */
+/* As wlb_cp_kv_push, storing local row i only into the ranks that read it
+ * (same coverage rule and tables as wlb_cp_dkv_pull_cov).  Rows a rank does
+ * not cover keep earlier contents, which must be finite (start the buffers
+ * zeroed): its tiles read them only under the mask. */
+int wlb_cp_kv_push_cov(const void* k_local, const void* v_local, const int32_t* gather_local,
+                       int64_t n_rows, int64_t row_bytes, const uint64_t* peer_bases,
+                       int64_t k_off, int64_t v_off, int32_t cp, const int32_t* rowset_all,
+                       int32_t rowset_stride, const int32_t* positions_all,
+                       const int32_t* doc_start, int32_t n_docs, void* stream);
 int wlb_cp_dkv_pull_cov(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_off,
                         const int32_t* gather_local, int64_t n_rows, int64_t row_bytes,
                         float* dk, float* dv, int32_t cp, int32_t flags,

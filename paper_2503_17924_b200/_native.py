@@ -48,6 +48,8 @@ SIGNATURES = {
     "wlb_cp_kv_push": (C.c_int, [_p, _p, _p, _i64, _i64, _p, _i64, _i64, _i32, _p]),
     "wlb_cp_dkv_pull": (C.c_int, [_p, _i64, _i64, _p, _i64, _i64, _p, _p, _i32, _p]),
     "wlb_cp_dkv_pull_ex": (C.c_int, [_p, _i64, _i64, _p, _i64, _i64, _p, _p, _i32, _i32, _p]),
+    "wlb_cp_kv_push_cov": (C.c_int, [_p, _p, _p, _i64, _i64, _p, _i64, _i64, _i32,
+                                     _p, _i32, _p, _p, _i32, _p]),
     "wlb_cp_dkv_pull_cov": (C.c_int, [_p, _i64, _i64, _p, _i64, _i64, _p, _p, _i32, _i32,
                                       _p, _i32, _p, _p, _i32, _p]),
 }

@@ -201,6 +201,7 @@ class SymmExchange:
         slots = self.slots
         self.depth = slots - 1          # K/V pushed this many micro-batches ahead
         self.kv = symm.empty(2 * slots * self.n, dtype=torch.bfloat16, device=device)  # [slot][K|V]
+        self.kv.zero_()   # rows a rank does not cover are read only under the mask: keep them finite
         self.kv_h = symm.rendezvous(self.kv, self.group)
         # dK/dV partials in bf16 (WLB_XCHG_DKV=fp32 for fp32): the backward
         # writes half the bytes and the pull moves half, summing in fp32
@@ -213,6 +214,17 @@ class SymmExchange:
         self.free = [None] * slots     # event: all ranks finished pulling slot s
         # skip peers' uncovered (all-zero) partial rows in the pull; WLB_XCHG_PULL=all reads every row
         self.pull_covered = os.environ.get("WLB_XCHG_PULL", "covered") != "all"
+        # push K/V rows only to the ranks that read them; WLB_XCHG_PUSH=all stores to every rank
+        self.push_covered = os.environ.get("WLB_XCHG_PUSH", "covered") != "all"
+
+    @staticmethod
+    def _tables(shard):
+        """Every rank's row-set offsets [cp][max_docs+1] and in-document
+        positions [cp][T/cp] of this micro-batch (device views of the plan)."""
+        plan, b = shard.plan, shard.index
+        rows = plan.rowset_off[b]
+        assert rows.is_contiguous()
+        return rows, plan.positions[plan.tok_off[b]:]
 
     def _view(self, buf, idx, T):
         return buf[idx * self.n: idx * self.n + T * self.hkv * self.d].view(T, self.hkv, self.d)
@@ -223,10 +235,19 @@ class SymmExchange:
             raise ValueError(f"micro-batch of {T} tokens exceeds the exchange capacity {self.t_max}")
         self.kv_h.barrier(channel=0)
         row = self.hkv * self.d * 2
-        _native.check(_native.lib().wlb_cp_kv_push(
-            k.data_ptr(), v.data_ptr(), shard.gather_local.data_ptr(), k.shape[0], row,
-            self.kv_bases.data_ptr(), 2 * s * self.n * 2, (2 * s + 1) * self.n * 2, self.cp,
-            _native.stream_ptr()), "wlb_cp_kv_push")
+        if self.push_covered and shard.tiles.n_docs > 0:
+            # store each row only into the ranks whose attention reads it
+            rows, pos = self._tables(shard)
+            _native.check(_native.lib().wlb_cp_kv_push_cov(
+                k.data_ptr(), v.data_ptr(), shard.gather_local.data_ptr(), k.shape[0], row,
+                self.kv_bases.data_ptr(), 2 * s * self.n * 2, (2 * s + 1) * self.n * 2, self.cp,
+                rows.data_ptr(), rows.shape[-1], pos.data_ptr(), shard.tiles.doc_start.data_ptr(),
+                shard.tiles.n_docs, _native.stream_ptr()), "wlb_cp_kv_push_cov")
+        else:
+            _native.check(_native.lib().wlb_cp_kv_push(
+                k.data_ptr(), v.data_ptr(), shard.gather_local.data_ptr(), k.shape[0], row,
+                self.kv_bases.data_ptr(), 2 * s * self.n * 2, (2 * s + 1) * self.n * 2, self.cp,
+                _native.stream_ptr()), "wlb_cp_kv_push")
         self.kv_h.barrier(channel=0)
         return self._view(self.kv, 2 * s, T), self._view(self.kv, 2 * s + 1, T)
 
@@ -246,10 +267,7 @@ class SymmExchange:
         flags = _native.WLB_BWD_DKV_BF16 if self.dkv_bf16 else 0
         if self.pull_covered and shard.tiles.n_docs > 0:
             # read a peer's partial row only where that peer's backward wrote it
-            plan, b_ = shard.plan, shard.index
-            rows = plan.rowset_off[b_]
-            assert rows.is_contiguous()
-            pos = plan.positions[plan.tok_off[b_]:]
+            rows, pos = self._tables(shard)
             _native.check(_native.lib().wlb_cp_dkv_pull_cov(
                 self.dkv_bases.data_ptr(), 2 * s * self.n * es, (2 * s + 1) * self.n * es,
                 shard.gather_local.data_ptr(), tl, self.hkv * self.d * es, dk.data_ptr(),

@@ -100,6 +100,63 @@ __global__ void dkv_pull_bf16_kernel(const unsigned long long* __restrict__ base
   }
 }
 
+// Coverage test shared by the covered push / pull: does rank `lane` (< cp)
+// read (forward K/V) or write (backward dK/dV partials) global row g?  Rank p
+// touches document d's keys below min(len_d, roundup128(last local position
+// of p in d + 1)): the forward's and the backward's KV tiles are 128 keys
+// from the document start.  Returns the warp's mask of such ranks.
+__device__ __forceinline__ unsigned covering_ranks(int g, int lane, int cp,
+                                                   const int* __restrict__ rowset_all, int rs,
+                                                   const int* __restrict__ pos_all, long long tl,
+                                                   const int* __restrict__ doc_start, int n_docs) {
+  int lo = 0, hi = n_docs;                     // last document with doc_start <= g
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (doc_start[mid] <= g) lo = mid;
+    else hi = mid;
+  }
+  bool covers = false;
+  if (lane < cp) {
+    const int r0 = rowset_all[lane * rs + lo], r1 = rowset_all[lane * rs + lo + 1];
+    if (r1 > r0) {
+      const int len = doc_start[lo + 1] - doc_start[lo];
+      const int cov = min(len, (pos_all[lane * tl + r1 - 1] + 128) / 128 * 128);
+      covers = g - doc_start[lo] < cov;
+    }
+  }
+  return __ballot_sync(0xffffffffu, covers);
+}
+
+// Covered push: local row i goes only to the ranks whose attention reads it.
+// Rows a rank does not cover stay as they were (earlier micro-batches' K/V,
+// or the zeros the buffers start with): its tiles read them only under the
+// causal / document mask, where P = 0 against a finite value.
+__global__ void kv_push_cov_kernel(const int4* __restrict__ k, const int4* __restrict__ v,
+                                   const int* __restrict__ gidx, long long n_rows,
+                                   long long row_vecs, const unsigned long long* __restrict__ bases,
+                                   long long k_off, long long v_off, int cp,
+                                   const int* __restrict__ rowset_all, int rs,
+                                   const int* __restrict__ pos_all,
+                                   const int* __restrict__ doc_start, int n_docs) {
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
+       r += warps) {
+    const long long g = gidx[r];
+    const unsigned mask =
+        covering_ranks((int)g, lane, cp, rowset_all, rs, pos_all, n_rows, doc_start, n_docs);
+    for (long long c = lane; c < row_vecs; c += 32) {
+      const int4 kv = k[r * row_vecs + c], vv = v[r * row_vecs + c];
+      for (int p = 0; p < cp; ++p) {
+        if (!((mask >> p) & 1u)) continue;
+        char* base = reinterpret_cast<char*>(bases[p]);
+        reinterpret_cast<int4*>(base + k_off)[g * row_vecs + c] = kv;
+        reinterpret_cast<int4*>(base + v_off)[g * row_vecs + c] = vv;
+      }
+    }
+  }
+}
+
 // Coverage-aware pull: a peer's partial row is read only where that peer's
 // backward wrote it.  Rank p's KV tiles cover the keys of document d up to
 // its last local query position there, rounded up to the 128-key tile
@@ -121,22 +178,8 @@ __global__ void dkv_pull_cov_kernel(const unsigned long long* __restrict__ bases
   for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
        r += warps) {
     const int g = gidx[r];
-    int lo = 0, hi = n_docs;                   // last document with doc_start <= g
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (doc_start[mid] <= g) lo = mid;
-      else hi = mid;
-    }
-    bool covers = false;
-    if (lane < cp) {
-      const int r0 = rowset_all[lane * rs + lo], r1 = rowset_all[lane * rs + lo + 1];
-      if (r1 > r0) {
-        const int len = doc_start[lo + 1] - doc_start[lo];
-        const int cov = min(len, (pos_all[lane * tl + r1 - 1] + 128) / 128 * 128);
-        covers = g - doc_start[lo] < cov;
-      }
-    }
-    const unsigned mask = __ballot_sync(0xffffffffu, covers);
+    const unsigned mask =
+        covering_ranks(g, lane, cp, rowset_all, rs, pos_all, tl, doc_start, n_docs);
     for (long long c = lane; c < row_vecs; c += 32) {
       float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, b[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       for (int p = 0; p < cp; ++p) {
@@ -267,6 +310,26 @@ extern "C" int wlb_cp_dkv_pull_cov(const uint64_t* peer_bases, int64_t dk_off, i
         (const unsigned long long*)peer_bases, dk_off, dv_off, gather_local, n_rows,
         row_bytes / 16, (float4*)dk, (float4*)dv, cp, rowset_all, rowset_stride, positions_all,
         tl, doc_start, n_docs);
+  WLB_LAUNCH_CHECK();
+  return WLB_OK;
+}
+
+extern "C" int wlb_cp_kv_push_cov(const void* k_local, const void* v_local,
+                                  const int32_t* gather_local, int64_t n_rows, int64_t row_bytes,
+                                  const uint64_t* peer_bases, int64_t k_off, int64_t v_off,
+                                  int32_t cp, const int32_t* rowset_all, int32_t rowset_stride,
+                                  const int32_t* positions_all, const int32_t* doc_start,
+                                  int32_t n_docs, void* stream) {
+  WLB_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && k_off % 16 == 0 && v_off % 16 == 0,
+              "rows and offsets must be 16-byte aligned");
+  WLB_REQUIRE(cp >= 1 && cp <= 32, "cp must be in [1, 32]");
+  WLB_REQUIRE(n_docs >= 1 && rowset_stride >= n_docs + 1, "bad row-set table (n_docs %d, stride %d)",
+              n_docs, rowset_stride);
+  if (n_rows <= 0) return WLB_OK;
+  kv_push_cov_kernel<<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
+      (const int4*)k_local, (const int4*)v_local, gather_local, n_rows, row_bytes / 16,
+      (const unsigned long long*)peer_bases, k_off, v_off, cp, rowset_all, rowset_stride,
+      positions_all, doc_start, n_docs);
   WLB_LAUNCH_CHECK();
   return WLB_OK;
 }

@@ -38,8 +38,8 @@ def pipeline_cases(rank, world, dev):
 def _pipeline_cases(rank, world, dev, policy):
     """CPStepPipeline over 3 micro-batches (slot reuse in the symmetric
     exchange) with both exchanges: each vs the oracle, and symm == NCCL.  The
-    symmetric pull that skips peers' uncovered rows (default) must equal the
-    pull that reads every row bit for bit."""
+    symmetric push / pull that skip ranks' uncovered rows (default) must equal
+    the ones that move every row bit for bit (o, dK, dV; dQ sums by atomics)."""
     failures = []
     hq, hkv, d = 4, 2, 128
     mbs = [so.pad_lengths_for_cp(x, world) for x in
@@ -57,7 +57,7 @@ def _pipeline_cases(rank, world, dev, policy):
     t_max = max(sum(x) for x in mbs)
     res = {}
     symm_all = SymmExchange(dist.group.WORLD, t_max, hkv, d, dev)
-    symm_all.pull_covered = False
+    symm_all.pull_covered = symm_all.push_covered = False
     for name, ex in (("nccl", NcclExchange()),
                      ("symm", SymmExchange(dist.group.WORLD, t_max, hkv, d, dev)),
                      ("symm-all", symm_all)):
@@ -88,9 +88,11 @@ def _pipeline_cases(rank, world, dev, policy):
             tol = (1e-3 if tn in ("o", "dq") else 8e-3) * max(1.0, a.abs().max().item())
             if err > tol:
                 failures.append(f"[rank {rank} {policy} mb{b}] symm vs nccl {tn}: {err:.3e}")
-        for tn, a, c in zip(("dk", "dv"), res["symm"][b][2:], res["symm-all"][b][2:]):
+        for tn, a, c in (("o", res["symm"][b][0], res["symm-all"][b][0]),
+                         ("dk", res["symm"][b][2], res["symm-all"][b][2]),
+                         ("dv", res["symm"][b][3], res["symm-all"][b][3])):
             if not torch.equal(a, c):
-                failures.append(f"[rank {rank} {policy} mb{b}] covered pull != full pull {tn}: "
+                failures.append(f"[rank {rank} {policy} mb{b}] covered push/pull != full {tn}: "
                                 f"{(a - c).abs().max().item():.3e}")
     return failures
 
