@@ -1,6 +1,10 @@
 """Benchmark: document-masked CP attention fwd+bwd on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload auto|128k] [--shape llama7b|llama70b-gqa]
+
+With --gpus N > 1 and no torchrun environment, the script re-launches itself
+under `torch.distributed.run --nproc-per-node N` (one process per GPU).
 
 One step = the hot path over one synthetic global batch: the 8 long-tail
 sequences `generate_synthetic_stream(SyntheticSpec(T, T), seed=0, n_batches=8)`
@@ -9,9 +13,11 @@ the GPU (one batched `wlb_shard_plan` launch), then run through CP
 document-masked attention forward and backward (tcgen05 kernels, NCCL
 all-gather / reduce-scatter for N > 1).
 
-Workloads (BASELINE.json configs): N = 1 -> config 2, Llama-7B attention
-(32 q / 32 kv heads, d = 128), seq 32K, CP = 1.  N > 1 -> config 3 shape at
-seq 128K, CP = N (one process per GPU, torchrun).
+Workloads (BASELINE.json configs), `--workload auto` (default): N = 1 ->
+config 2, Llama-7B attention (32 q / 32 kv heads, d = 128), seq 32K, CP = 1;
+N > 1 -> config 3 shape at seq 128K, CP = N (one process per GPU).
+`--workload 128k` runs the same 8 x 128K sequences at CP = N for every N,
+including N = 1, so N = 1/2/4/8 is a strong-scaling curve of fixed work.
 
 FLOPs are algorithmic and unmasked: 14 * D * Hq * pairs, pairs = sum over
 documents of L(L+1)/2 (`attention_workload`, workload.py:196-198).
@@ -55,14 +61,50 @@ def _peaks():
     return 1590.0, 1400.0, "fallback"
 
 
-def _workload(n, shape="llama7b"):
+def _workload(n, shape="llama7b", workload="auto"):
     """BASELINE configs: 2 (7B 32x128, 32K, CP=1) at N=1, 3 (7B, 128K, CP=N) at
-    N>1; --shape llama70b-gqa gives config 4 (64 query / 8 KV heads x 128)."""
+    N>1; --shape llama70b-gqa gives config 4 (64 query / 8 KV heads x 128);
+    --workload 128k keeps the 128K sequences at every N (CP = N, N = 1 too)."""
     hq, hkv = (64, 8) if shape == "llama70b-gqa" else (32, 32)
     tag = "llama70b-gqa" if shape == "llama70b-gqa" else "llama7b"
-    if n == 1:
+    if n == 1 and workload == "auto":
         return dict(name=f"{tag}-attn-32k-cp1", window=32768, hq=hq, hkv=hkv, d=128, cp=1)
     return dict(name=f"{tag}-attn-128k-cp{n}", window=131072, hq=hq, hkv=hkv, d=128, cp=n)
+
+
+def _cpu_model():
+    """`lscpu` model name of the host (BASELINE.md 4 asks for it with the core count)."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return None
+
+
+def _host_steps(lengths_list, cp):
+    """Reference host-side steps on this host's CPU:
+    pad_for_cp + per-sequence / per-document sharding + model latencies +
+    adaptive selection of every micro-batch, through the oracle port of
+    sharding.py:86-188 (the reference's Python cannot travel to the GPU box).
+    Returns ms per micro-batch (median of 3 passes).
+    TEST/BASELINE ONLY: the checker is never the thing measured for `value`."""
+    from oracle import shard_oracle as so
+    import paper_2503_17924_b200 as pkg
+    prof = pkg.CostProfile()
+    cq = [q for q, _ in prof.tflops_curve]
+    cv = [v for _, v in prof.tflops_curve]
+    passes = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        for ls in lengths_list:
+            ls = so.pad_lengths_for_cp(ls, cp)
+            strat = so.adaptive(ls, cp, prof.tile_size, cq, cv, prof.op_scale)
+            so.shard(ls, cp, strat)              # the reference rebuilds the winner
+        passes.append((time.perf_counter() - t0) * 1e3 / len(lengths_list))
+    return statistics.median(passes)
 
 
 def _lengths(window):
@@ -182,7 +224,7 @@ def run_reference(args, world, rank):
     host cores, rank 0 only."""
     if rank != 0:
         return
-    wk = _workload(world, args.shape)
+    wk = _workload(world, args.shape, args.workload)
     lengths = _lengths(wk["window"])
     vals = []
     secs_tot = flops_tot = 0.0
@@ -203,11 +245,12 @@ def run_reference(args, world, rank):
                    "heads": [wk["hq"], wk["hkv"]], "head_dim": wk["d"], "cp": wk["cp"],
                    "policy": "per_document (CPU sample)", "parallelism": f"cp{wk['cp']}"},
         "cpu_baseline": {"value": round(value, 4), "unit": "TFLOP/s", "cores": os.cpu_count(),
-                         "kind": "port",
+                         "cpu_model": _cpu_model(), "kind": "port",
                          "sample": "per step: head 0 of one synthetic sequence (cycling the 8), "
                                    "documents in order up to 1.5e9 causal pairs (last one "
                                    "prefix-cut), per_document shard + torch-CPU fp32 "
-                                   "doc-prefix attention fwd+bwd (oracle/attention_oracle.py)"},
+                                   "doc-prefix attention fwd+bwd (oracle/attention_oracle.py)",
+                         "host_shard_select_ms_per_mb": round(_host_steps(lengths, wk["cp"]), 3)},
         "e2e": {"value": round(value, 4), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -228,11 +271,25 @@ def main():
     ap.add_argument("--shape", default="llama7b", choices=["llama7b", "llama70b-gqa"],
                     help="attention shape: Llama-7B 32x128 (configs 2/3) or Llama-70B GQA "
                          "64q/8kv x128 (config 4)")
+    ap.add_argument("--workload", default="auto", choices=["auto", "128k"],
+                    help="auto: 32K CP=1 at N=1 (config 2), 128K CP=N at N>1 (config 3); "
+                         "128k: 128K CP=N at every N (fixed total work: strong scaling)")
     ap.add_argument("--clock-ms", type=int, default=100,
                     help="nvidia-smi sampling period during the timed region (0: off)")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (the driver launches
+        # torchrun itself; a bare `python bench.py --gpus N` lands here)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={29500 + os.getpid() % 1000}", os.path.abspath(__file__),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one process per GPU")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
@@ -243,7 +300,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     group = None
-    wk = _workload(world, args.shape)
+    wk = _workload(world, args.shape, args.workload)
     cp, hq, hkv, d = wk["cp"], wk["hq"], wk["hkv"], wk["d"]
     lengths = _lengths(wk["window"])
     T = wk["window"]
@@ -368,7 +425,7 @@ def main():
         e2e_step()
         barrier()
         a, b_ = ev(), ev()
-        n_e2e = max(1, min(args.steps, 3))
+        n_e2e = args.steps
         a.record()
         for _ in range(n_e2e):
             e2e_step()
@@ -405,8 +462,13 @@ def main():
         "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "value_basis": "whole job: step FLOPs (all ranks) / max-over-ranks step time; "
+                       "per GPU in tflops_per_gpu",
         "config": {"workload": wk["name"], "seq_len": T, "sequences_per_step": N_SEQ,
                    "heads": [hq, hkv], "head_dim": d, "cp": cp, "policy": "adaptive",
+                   "workload_rule": "N=1: config 2 (32K, CP=1); N>1: config 3 (128K, CP=N); "
+                                    "--workload 128k: 128K at CP=N for every N"
+                                    if args.workload == "auto" else "128K at CP=N for every N",
                    "strategies": strategies, "l2": "inputs > L2 (256 MiB per tensor)",
                    "parallelism": f"cp{cp}",
                    "exchange": args.exchange if cp > 1 else "none"},
@@ -432,9 +494,12 @@ def main():
         tflops, done, secs = _cpu_sample(lengths, 1, d, budget_s=15.0)
         line["cpu_baseline"] = {
             "value": round(tflops, 4), "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
+            "cpu_model": _cpu_model(),
             "sample": f"head 0 of synthetic sequences {done}, each bounded to 1.5e9 causal "
                       f"pairs ({secs:.1f} s): per_document shard + torch-CPU fp32 "
-                      "doc-prefix attention fwd+bwd (oracle)"}
+                      "doc-prefix attention fwd+bwd (oracle)",
+            "host_shard_select_ms_per_mb": round(_host_steps(lengths, cp), 3),
+            "gpu_shard_select": "one wlb_shard_plan launch per step (all micro-batches)"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -176,10 +176,12 @@ int wlb_cp_dkv_pull_ex(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_of
  * [cp][rowset_stride] row-set offsets of every rank (the shard plan's
  * rowset_off for this micro-batch); positions_all: [cp][n_rows] in-document
  * positions of every rank's local rows; doc_start: [n_docs+1]. */
-/* As wlb_cp_kv_push, storing local row i only into the ranks that read it
- * (same coverage rule and tables as wlb_cp_dkv_pull_cov).  Rows a rank does
- * not cover keep earlier contents, which must be finite (start the buffers
- * zeroed): its tiles read them only under the mask. */
+/* As wlb_cp_kv_push, storing local row i only into the ranks that load it:
+ * the coverage rule of wlb_cp_dkv_pull_cov, plus the rows a rank's last
+ * 128-key tile of an earlier document reads past that document's end (up to
+ * 127 rows, under the mask).  Every row any rank's tiles load is therefore
+ * rewritten by this micro-batch; rows no tile loads keep earlier contents.
+ * cp <= 32 (the coverage mask is a warp ballot). */
 int wlb_cp_kv_push_cov(const void* k_local, const void* v_local, const int32_t* gather_local,
                        int64_t n_rows, int64_t row_bytes, const uint64_t* peer_bases,
                        int64_t k_off, int64_t v_off, int32_t cp, const int32_t* rowset_all,

@@ -23,7 +23,7 @@ Contents
                       reference vectors (the reference has none).
 * `_ref/`           -- (git-ignored build output) the reference's own Cython
                       kernels compiled from `/root/reference` by
-                      `oracle/build_ref.sh`, used to pin `kernels_oracle.c`.
+                      `oracle/build.sh`, used to pin `kernels_oracle.c`.
 
 Pinning: `tests/golden/*.json.gz` hold vectors produced by importing the
 reference package itself (`tests/golden/make_golden.py`); `tests/test_oracle.py`

@@ -194,28 +194,45 @@ class SymmExchange:
     def __init__(self, group, t_max, hkv, d, device, slots=2):
         import torch.distributed._symmetric_memory as symm
         self.group = group if group is not None else dist.group.WORLD
-        self.cp = dist.get_world_size(self.group)
-        self.t_max, self.hkv, self.d = t_max, hkv, d
-        self.n = t_max * hkv * d
-        self.slots = int(os.environ.get("WLB_XCHG_SLOTS", slots))   # experiment override
-        slots = self.slots
-        self.depth = slots - 1          # K/V pushed this many micro-batches ahead
-        self.kv = symm.empty(2 * slots * self.n, dtype=torch.bfloat16, device=device)  # [slot][K|V]
-        self.kv.zero_()   # rows a rank does not cover are read only under the mask: keep them finite
-        self.kv_h = symm.rendezvous(self.kv, self.group)
+        cp = dist.get_world_size(self.group)
+        slots = int(os.environ.get("WLB_XCHG_SLOTS", slots))   # experiment override
+        n = t_max * hkv * d
+        kv = symm.empty(2 * slots * n, dtype=torch.bfloat16, device=device)  # [slot][K|V]
+        kv.zero_()
+        kv_h = symm.rendezvous(kv, self.group)
+        dkv = symm.empty(2 * slots * n, dtype=self._dkv_dtype(), device=device)  # [slot][dK|dV]
+        dkv_h = symm.rendezvous(dkv, self.group)
+        self._setup(cp, t_max, hkv, d, device, slots, kv, dkv, list(kv_h.buffer_ptrs),
+                    list(dkv_h.buffer_ptrs))
+        self._kv_barrier = lambda: kv_h.barrier(channel=0)
+        self._dkv_barrier = lambda: dkv_h.barrier(channel=1)
+
+    @staticmethod
+    def _dkv_dtype():
         # dK/dV partials in bf16 (WLB_XCHG_DKV=fp32 for fp32): the backward
         # writes half the bytes and the pull moves half, summing in fp32
-        self.dkv_bf16 = os.environ.get("WLB_XCHG_DKV", "bf16") != "fp32"
-        dkv_dtype = torch.bfloat16 if self.dkv_bf16 else torch.float32
-        self.dkv = symm.empty(2 * slots * self.n, dtype=dkv_dtype, device=device)  # [slot][dK|dV]
-        self.dkv_h = symm.rendezvous(self.dkv, self.group)
-        self.kv_bases = torch.tensor(list(self.kv_h.buffer_ptrs), dtype=torch.int64, device=device)
-        self.dkv_bases = torch.tensor(list(self.dkv_h.buffer_ptrs), dtype=torch.int64, device=device)
+        return torch.float32 if os.environ.get("WLB_XCHG_DKV", "bf16") == "fp32" else torch.bfloat16
+
+    def _setup(self, cp, t_max, hkv, d, device, slots, kv, dkv, kv_ptrs, dkv_ptrs):
+        self.cp = cp
+        self.t_max, self.hkv, self.d = t_max, hkv, d
+        self.n = t_max * hkv * d
+        self.slots = slots
+        self.depth = slots - 1          # K/V pushed this many micro-batches ahead
+        self.kv, self.dkv = kv, dkv
+        self.dkv_bf16 = dkv.dtype == torch.bfloat16
+        self.kv_bases = torch.tensor(kv_ptrs, dtype=torch.int64, device=device)
+        self.dkv_bases = torch.tensor(dkv_ptrs, dtype=torch.int64, device=device)
         self.free = [None] * slots     # event: all ranks finished pulling slot s
+        # The covered kernels take a warp-ballot rank mask (cp <= 32); larger
+        # groups use the full push / pull, which work for any cp.
+        covered_ok = self.cp <= 32
         # skip peers' uncovered (all-zero) partial rows in the pull; WLB_XCHG_PULL=all reads every row
-        self.pull_covered = os.environ.get("WLB_XCHG_PULL", "covered") != "all"
-        # push K/V rows only to the ranks that read them; WLB_XCHG_PUSH=all stores to every rank
-        self.push_covered = os.environ.get("WLB_XCHG_PUSH", "covered") != "all"
+        self.pull_covered = covered_ok and os.environ.get("WLB_XCHG_PULL", "covered") != "all"
+        # push K/V rows only to the ranks that load them (including a last
+        # tile's reads past its document's end, so no stale row is ever read);
+        # WLB_XCHG_PUSH=all stores to every rank
+        self.push_covered = covered_ok and os.environ.get("WLB_XCHG_PUSH", "covered") != "all"
 
     @staticmethod
     def _tables(shard):
@@ -233,7 +250,7 @@ class SymmExchange:
         s, T = b % self.slots, shard.gather_all.numel()
         if T > self.t_max:
             raise ValueError(f"micro-batch of {T} tokens exceeds the exchange capacity {self.t_max}")
-        self.kv_h.barrier(channel=0)
+        self._kv_barrier()
         row = self.hkv * self.d * 2
         if self.push_covered and shard.tiles.n_docs > 0:
             # store each row only into the ranks whose attention reads it
@@ -248,7 +265,7 @@ class SymmExchange:
                 k.data_ptr(), v.data_ptr(), shard.gather_local.data_ptr(), k.shape[0], row,
                 self.kv_bases.data_ptr(), 2 * s * self.n * 2, (2 * s + 1) * self.n * 2, self.cp,
                 _native.stream_ptr()), "wlb_cp_kv_push")
-        self.kv_h.barrier(channel=0)
+        self._kv_barrier()
         return self._view(self.kv, 2 * s, T), self._view(self.kv, 2 * s + 1, T)
 
     def dkv_out(self, shard, b, cur):
@@ -262,7 +279,7 @@ class SymmExchange:
         tl = shard.gather_local.numel()
         dk = torch.empty((tl, self.hkv, self.d), dtype=torch.float32, device=dkf.device)
         dv = torch.empty_like(dk)
-        self.dkv_h.barrier(channel=1)
+        self._dkv_barrier()
         es = 2 if self.dkv_bf16 else 4
         flags = _native.WLB_BWD_DKV_BF16 if self.dkv_bf16 else 0
         if self.pull_covered and shard.tiles.n_docs > 0:
@@ -279,11 +296,43 @@ class SymmExchange:
                 self.dkv_bases.data_ptr(), 2 * s * self.n * es, (2 * s + 1) * self.n * es,
                 shard.gather_local.data_ptr(), tl, self.hkv * self.d * es, dk.data_ptr(),
                 dv.data_ptr(), self.cp, flags, _native.stream_ptr()), "wlb_cp_dkv_pull_ex")
-        self.dkv_h.barrier(channel=1)
+        self._dkv_barrier()
         ev = torch.cuda.Event()
         ev.record()
         self.free[s] = ev
         return dk, dv
+
+
+class LocalPeersExchange(SymmExchange):
+    """One-GPU emulation of a CP group's symmetric exchange: every rank's slot
+    buffers are ordinary allocations on ONE device and `kv_bases` /
+    `dkv_bases` hold all of them, so the same push / pull kernels and the same
+    `gather` / `dkv_out` / `scatter` code run for cp = 2..8 without peers.
+    Cross-rank ordering is the caller's: run every rank's `gather` before any
+    rank's attention, and every rank's backward before any rank's `scatter`
+    (stream order on one device; the barriers are no-ops).  Used by the
+    exchange parity tests and tools/cp_emulate.py."""
+
+    @classmethod
+    def create(cls, cp, t_max, hkv, d, device, slots=2, fill=0.0):
+        """cp exchange objects, rank r's at index r.  `fill` initialises the
+        K/V slots (e.g. NaN, to prove every row a tile loads is rewritten)."""
+        n = t_max * hkv * d
+        kvs = [torch.full((2 * slots * n,), fill, dtype=torch.bfloat16, device=device)
+               for _ in range(cp)]
+        dkvs = [torch.full((2 * slots * n,), float("nan"), dtype=cls._dkv_dtype(), device=device)
+                for _ in range(cp)]
+        kv_ptrs = [t.data_ptr() for t in kvs]
+        dkv_ptrs = [t.data_ptr() for t in dkvs]
+        out = []
+        for r in range(cp):
+            ex = cls.__new__(cls)
+            ex.group = None
+            ex._setup(cp, t_max, hkv, d, device, slots, kvs[r], dkvs[r], kv_ptrs, dkv_ptrs)
+            ex._kv_barrier = ex._dkv_barrier = lambda: None
+            ex.rank = r
+            out.append(ex)
+        return out
 
 
 class CPStepPipeline:

@@ -1322,14 +1322,8 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
     if ((rc = make_thd_tmap(&tdo, dout, Tl, Hq, D, C3::BM))) return rc;
     if ((rc = make_thd_tmap(&tk, k, T, Hkv, D, C3::BN))) return rc;
     if ((rc = make_thd_tmap(&tv, v, T, Hkv, D, C3::BN))) return rc;
-    static bool attr3 = false;
-    if (!attr3) {
-      WLB_CUDA_TRY(cudaFuncSetAttribute(attn_bwd3_kernel<false>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C3::SMEM));
-      WLB_CUDA_TRY(cudaFuncSetAttribute(attn_bwd3_kernel<true>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C3::SMEM));
-      attr3 = true;
-    }
+    WLB_SMEM_ATTR(attn_bwd3_kernel<false>, C3::SMEM);
+    WLB_SMEM_ATTR(attn_bwd3_kernel<true>, C3::SMEM);
     const float sl2 = scale * 1.4426950408889634f;
     if (pairs) {
       // 2-CTA clusters: one pair of KV tiles per cluster
@@ -1365,12 +1359,7 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   // (A 128-query, single-buffered variant with all-N=128 MMAs measured 1.5x
   //  slower: the S/dP -> compute -> dV/dK/dQ serialisation costs more than the
   //  SMEM bandwidth it saves.)
-  static bool attr = false;
-  if (!attr) {
-    WLB_CUDA_TRY(cudaFuncSetAttribute(attn_bwd_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      C::SMEM));
-    attr = true;
-  }
+  WLB_SMEM_ATTR((attn_bwd_kernel<D, 2>), C::SMEM);
   // several KV heads per CTA for short row-sets (< 2048 local rows per
   // document on average): the next head's loads overlap this head's tail
   // (only with >= 6 waves of CTAs left: Tl/128 bounds the KV tiles from below)

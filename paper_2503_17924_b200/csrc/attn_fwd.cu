@@ -427,12 +427,7 @@ static int launch_fwd(const void* q, const void* k, const void* v, void* o, floa
   if ((rc = make_thd_tmap(&tq, q, Tl, Hq, D, C::BM))) return rc;
   if ((rc = make_thd_tmap(&tk, k, T, Hkv, D, C::BN))) return rc;
   if ((rc = make_thd_tmap(&tv, v, T, Hkv, D, C::BN))) return rc;
-  static bool attr = false;
-  if (!attr) {
-    WLB_CUDA_TRY(cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      C::SMEM));
-    attr = true;
-  }
+  WLB_SMEM_ATTR(attn_fwd_kernel<D>, C::SMEM);
   const float scale_log2 = scale * 1.4426950408889634f;
   // Heads per CTA: max_tiles = Tl/256 + n_docs + 1 (attention.py), so its excess
   // over Tl/256 counts the documents.  Short row-sets (< 2048 local rows per

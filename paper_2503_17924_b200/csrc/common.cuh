@@ -32,6 +32,21 @@ void set_error(const char* fmt, ...);
     }                                                                             \
   } while (0)
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute is per-device state, so the "done" flag is a bit per device
+// of the calling thread's current device (up to 64 devices).
+#define WLB_SMEM_ATTR(kernel, bytes)                                                   \
+  do {                                                                                 \
+    static unsigned long long _done = 0;                                               \
+    int _dev = 0;                                                                      \
+    WLB_CUDA_TRY(cudaGetDevice(&_dev));                                                \
+    if (!((_done >> (_dev & 63)) & 1ull)) {                                            \
+      WLB_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                        (bytes)));                                     \
+      _done |= 1ull << (_dev & 63);                                                    \
+    }                                                                                  \
+  } while (0)
+
 // Block-wide exclusive scan of one int64 per thread.  `warp_tot` must hold
 // blockDim.x/32 + 1 entries of shared memory.  Returns the exclusive prefix and
 // writes the block total to *total (all threads).

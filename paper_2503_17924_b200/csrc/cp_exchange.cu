@@ -104,7 +104,15 @@ __global__ void dkv_pull_bf16_kernel(const unsigned long long* __restrict__ base
 // read (forward K/V) or write (backward dK/dV partials) global row g?  Rank p
 // touches document d's keys below min(len_d, roundup128(last local position
 // of p in d + 1)): the forward's and the backward's KV tiles are 128 keys
-// from the document start.  Returns the warp's mask of such ranks.
+// from the document start.  With SPILL (the push), a rank's last tile of an
+// EARLIER document also reads rows past that document's end (up to 127 rows
+// into the following documents, under the mask): those rows are pushed too,
+// so every row a tile loads belongs to the current micro-batch.  A stale row
+// left by an earlier micro-batch would otherwise reach O and dQ as 0 * Inf =
+// NaN through the masked P.V / dS products.  (The backward writes dK/dV only
+// for keys inside the document, so the pull takes SPILL = false.)  Returns
+// the warp's mask of such ranks.
+template <bool SPILL>
 __device__ __forceinline__ unsigned covering_ranks(int g, int lane, int cp,
                                                    const int* __restrict__ rowset_all, int rs,
                                                    const int* __restrict__ pos_all, long long tl,
@@ -117,20 +125,29 @@ __device__ __forceinline__ unsigned covering_ranks(int g, int lane, int cp,
   }
   bool covers = false;
   if (lane < cp) {
-    const int r0 = rowset_all[lane * rs + lo], r1 = rowset_all[lane * rs + lo + 1];
-    if (r1 > r0) {
-      const int len = doc_start[lo + 1] - doc_start[lo];
-      const int cov = min(len, (pos_all[lane * tl + r1 - 1] + 128) / 128 * 128);
-      covers = g - doc_start[lo] < cov;
+    for (int d = lo; d >= 0; --d) {
+      // a tile of document d reaches at most roundup128(len_d) <= len_d + 127
+      // rows past its start: documents ending 127+ rows before g cannot
+      if (d < lo && doc_start[d + 1] + 127 <= g) break;
+      const int r0 = rowset_all[lane * rs + d], r1 = rowset_all[lane * rs + d + 1];
+      if (r1 > r0) {
+        const int len = doc_start[d + 1] - doc_start[d];
+        const int tiles = (pos_all[lane * tl + r1 - 1] + 128) / 128 * 128;
+        const int cov = SPILL ? tiles : min(len, tiles);
+        if (g - doc_start[d] < cov) {
+          covers = true;
+          break;
+        }
+      }
+      if (!SPILL) break;
     }
   }
   return __ballot_sync(0xffffffffu, covers);
 }
 
-// Covered push: local row i goes only to the ranks whose attention reads it.
-// Rows a rank does not cover stay as they were (earlier micro-batches' K/V,
-// or the zeros the buffers start with): its tiles read them only under the
-// causal / document mask, where P = 0 against a finite value.
+// Covered push: local row i goes only to the ranks whose attention reads it,
+// including the rows a rank's last tile of a document reads past that
+// document's end (SPILL).  Rows a rank never loads stay as they were.
 __global__ void kv_push_cov_kernel(const int4* __restrict__ k, const int4* __restrict__ v,
                                    const int* __restrict__ gidx, long long n_rows,
                                    long long row_vecs, const unsigned long long* __restrict__ bases,
@@ -144,7 +161,7 @@ __global__ void kv_push_cov_kernel(const int4* __restrict__ k, const int4* __res
        r += warps) {
     const long long g = gidx[r];
     const unsigned mask =
-        covering_ranks((int)g, lane, cp, rowset_all, rs, pos_all, n_rows, doc_start, n_docs);
+        covering_ranks<true>((int)g, lane, cp, rowset_all, rs, pos_all, n_rows, doc_start, n_docs);
     for (long long c = lane; c < row_vecs; c += 32) {
       const int4 kv = k[r * row_vecs + c], vv = v[r * row_vecs + c];
       for (int p = 0; p < cp; ++p) {
@@ -179,7 +196,7 @@ __global__ void dkv_pull_cov_kernel(const unsigned long long* __restrict__ bases
        r += warps) {
     const int g = gidx[r];
     const unsigned mask =
-        covering_ranks(g, lane, cp, rowset_all, rs, pos_all, tl, doc_start, n_docs);
+        covering_ranks<false>(g, lane, cp, rowset_all, rs, pos_all, tl, doc_start, n_docs);
     for (long long c = lane; c < row_vecs; c += 32) {
       float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, b[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       for (int p = 0; p < cp; ++p) {
@@ -225,6 +242,10 @@ __global__ void dkv_pull_cov_kernel(const unsigned long long* __restrict__ bases
 #ifndef WLB_XCHG_BLOCKS_PER_SM
 #define WLB_XCHG_BLOCKS_PER_SM 16
 #endif
+static bool aligned16(const void* a, const void* b) {
+  return (((uintptr_t)a | (uintptr_t)b) & 15) == 0;
+}
+
 static int grid_for(long long n_rows) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -244,6 +265,7 @@ extern "C" int wlb_cp_kv_push(const void* k_local, const void* v_local, const in
                               int64_t k_off, int64_t v_off, int32_t cp, void* stream) {
   WLB_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && k_off % 16 == 0 && v_off % 16 == 0,
               "rows and offsets must be 16-byte aligned");
+  WLB_REQUIRE(aligned16(k_local, v_local), "k_local / v_local must be 16-byte aligned");
   WLB_REQUIRE(cp >= 1, "cp must be >= 1");
   if (n_rows <= 0) return WLB_OK;
   kv_push_kernel<<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
@@ -262,6 +284,7 @@ extern "C" int wlb_cp_dkv_pull_ex(const uint64_t* peer_bases, int64_t dk_off, in
                            cp, stream);
   WLB_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && dk_off % 16 == 0 && dv_off % 16 == 0,
               "rows and offsets must be 16-byte aligned");
+  WLB_REQUIRE(aligned16(dk, dv), "dk / dv must be 16-byte aligned");
   WLB_REQUIRE(cp >= 1, "cp must be >= 1");
   if (n_rows <= 0) return WLB_OK;
   // row_bytes is the bf16 partial row; the local fp32 output rows are twice as long
@@ -277,6 +300,7 @@ extern "C" int wlb_cp_dkv_pull(const uint64_t* peer_bases, int64_t dk_off, int64
                                float* dk, float* dv, int32_t cp, void* stream) {
   WLB_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && dk_off % 16 == 0 && dv_off % 16 == 0,
               "rows and offsets must be 16-byte aligned");
+  WLB_REQUIRE(aligned16(dk, dv), "dk / dv must be 16-byte aligned");
   WLB_REQUIRE(cp >= 1, "cp must be >= 1");
   if (n_rows <= 0) return WLB_OK;
   dkv_pull_kernel<<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
@@ -295,6 +319,7 @@ extern "C" int wlb_cp_dkv_pull_cov(const uint64_t* peer_bases, int64_t dk_off, i
   WLB_REQUIRE((flags & ~WLB_BWD_DKV_BF16) == 0, "unknown pull flags 0x%x", flags);
   WLB_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && dk_off % 16 == 0 && dv_off % 16 == 0,
               "rows and offsets must be 16-byte aligned");
+  WLB_REQUIRE(aligned16(dk, dv), "dk / dv must be 16-byte aligned");
   WLB_REQUIRE(cp >= 1 && cp <= 32, "cp must be in [1, 32]");
   WLB_REQUIRE(n_docs >= 1 && rowset_stride >= n_docs + 1, "bad row-set table (n_docs %d, stride %d)",
               n_docs, rowset_stride);
@@ -322,6 +347,7 @@ extern "C" int wlb_cp_kv_push_cov(const void* k_local, const void* v_local,
                                   int32_t n_docs, void* stream) {
   WLB_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && k_off % 16 == 0 && v_off % 16 == 0,
               "rows and offsets must be 16-byte aligned");
+  WLB_REQUIRE(aligned16(k_local, v_local), "k_local / v_local must be 16-byte aligned");
   WLB_REQUIRE(cp >= 1 && cp <= 32, "cp must be in [1, 32]");
   WLB_REQUIRE(n_docs >= 1 && rowset_stride >= n_docs + 1, "bad row-set table (n_docs %d, stride %d)",
               n_docs, rowset_stride);

@@ -84,6 +84,7 @@ __device__ __forceinline__ double range_latency(long long q, long long kv, long 
 }
 
 constexpr int kPlanThreads = 512;
+constexpr int kSmemDocs = 12000;   // documents whose starts + cursors fit shared memory (188 KB)
 
 __global__ void __launch_bounds__(kPlanThreads)
 shard_plan_kernel(const int* __restrict__ mb_doc_off, const long long* __restrict__ doc_len,
@@ -93,15 +94,19 @@ shard_plan_kernel(const int* __restrict__ mb_doc_off, const long long* __restric
                   int* __restrict__ choice, double* __restrict__ rank_latency,
                   long long* __restrict__ rank_pairs, int* __restrict__ seg_count,
                   int* __restrict__ segs, int* __restrict__ rowset_off,
-                  int* __restrict__ gather_index, int* __restrict__ positions) {
+                  int* __restrict__ gather_index, int* __restrict__ positions,
+                  long long* __restrict__ gscratch) {
   extern __shared__ long long smem_ll[];
-  long long* dstart = smem_ll;                  // [max_docs+1] document starts
-  long long* cursor = dstart + max_docs + 1;    // [max_docs]   remainder cursor
   __shared__ long long warp_tot[kPlanThreads / 32 + 1];
   __shared__ long long total_s;
   __shared__ int chosen_s;
 
   const int b = blockIdx.x;
+  // document starts [max_docs+1] and remainder cursor [max_docs]: shared
+  // memory, or this micro-batch's slice of a global scratch when they do not
+  // fit (more than kSmemDocs documents)
+  long long* dstart = gscratch ? gscratch + (size_t)b * (2 * (size_t)max_docs + 1) : smem_ll;
+  long long* cursor = dstart + max_docs + 1;
   const int d0 = mb_doc_off[b];
   const int nd = mb_doc_off[b + 1] - d0;
   const long long* L = doc_len + d0;
@@ -351,18 +356,27 @@ extern "C" int wlb_shard_plan(int32_t n_mb, const int32_t* mb_doc_off, const int
   WLB_REQUIRE(cp >= 1, "cp must be >= 1");
   WLB_REQUIRE(policy >= 0 && policy <= 2, "unknown policy %d", policy);
   WLB_REQUIRE(n_curve >= 1 && tile >= 1, "bad cost profile");
-  WLB_REQUIRE(max_docs >= 1 && max_docs <= 12000, "max_docs out of range");
-  WLB_REQUIRE(max_segs >= 4 * max_docs + 2, "max_segs must be >= 4*max_docs+2");
+  WLB_REQUIRE(max_docs >= 1, "max_docs out of range");
+  WLB_REQUIRE(max_segs >= 4 * (int64_t)max_docs + 2, "max_segs must be >= 4*max_docs+2");
   if (n_mb <= 0) return WLB_OK;
-  size_t smem = sizeof(long long) * (2 * (size_t)max_docs + 1);
-  if (smem > 48 * 1024)
+  const size_t per_mb = sizeof(long long) * (2 * (size_t)max_docs + 1);
+  long long* gscratch = nullptr;
+  size_t smem = per_mb;
+  if (max_docs > kSmemDocs) {
+    // stream-ordered global scratch (freed after the launch, on the same stream)
+    WLB_CUDA_TRY(cudaMallocAsync((void**)&gscratch, per_mb * (size_t)n_mb, (cudaStream_t)stream));
+    smem = 0;
+  } else if (smem > 48 * 1024) {
     WLB_CUDA_TRY(cudaFuncSetAttribute(shard_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
+  }
   shard_plan_kernel<<<n_mb, kPlanThreads, smem, (cudaStream_t)stream>>>(
       mb_doc_off, (const long long*)doc_len, (const long long*)mb_tok_off, cp, policy, tile,
       (const long long*)curve_q, curve_v, n_curve, op_scale, max_segs, max_docs, choice,
-      rank_latency, (long long*)rank_pairs, seg_count, segs, rowset_off, gather_index, positions);
+      rank_latency, (long long*)rank_pairs, seg_count, segs, rowset_off, gather_index, positions,
+      gscratch);
   WLB_LAUNCH_CHECK();
+  if (gscratch) WLB_CUDA_TRY(cudaFreeAsync(gscratch, (cudaStream_t)stream));
   return WLB_OK;
 }
 

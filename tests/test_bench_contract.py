@@ -62,3 +62,28 @@ def test_clock_summary_flags_throttle_reasons():
     assert s["samples"] == 3 and s["sm_max_mhz"] == 1965.0
     assert s["sm_mhz"] == 1750.0                    # idle 300 MHz sample excluded
     assert s["reasons"] == ["hw_thermal_slowdown", "sw_power_cap"]
+
+
+def test_fixed_128k_workload_for_strong_scaling():
+    """--workload 128k keeps the same 8 x 128K sequences at every N (CP = N,
+    N = 1 included), so N = 1/2/4/8 measure fixed total work."""
+    b = _bench()
+    for n in (1, 2, 4, 8):
+        w = b._workload(n, workload="128k")
+        assert (w["window"], w["cp"]) == (131072, n)
+
+
+def test_gpus_must_match_world_size(monkeypatch):
+    """Under torchrun, --gpus N must equal WORLD_SIZE (no silent N=1 run)."""
+    b = _bench()
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4"])
+    import pytest
+    with pytest.raises(SystemExit, match="WORLD_SIZE=2"):
+        b.main()
+
+
+def test_host_steps_times_the_reference_selector():
+    b = _bench()
+    ms = b._host_steps(b._lengths(8192)[:2], 2)
+    assert ms > 0

@@ -72,7 +72,7 @@ def test_cp_nccl_fwd_bwd_matches_oracle():
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
-    world = 4 if n >= 4 else 2
+    world = min(n, 8)              # every visible GPU of the box, up to CP = 8
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", "--master-port=29631",
            os.path.join(ROOT, "tests", "cp_worker.py")]

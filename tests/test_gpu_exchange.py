@@ -1,0 +1,117 @@
+"""CP exchange parity on ONE GPU at cp = 2, 4, 8.
+
+`LocalPeersExchange` puts every rank's symmetric slot buffers on one device
+and hands the kernels all of their addresses as `peer_bases`, so the product
+push / pull (`wlb_cp_kv_push(_cov)`, `wlb_cp_dkv_pull(_ex/_cov)`) and the
+`SymmExchange.gather / dkv_out / scatter` code run for a whole CP group in
+one process: every rank pushes, every rank runs its attention forward and
+backward (partials into its dK/dV slot), every rank pulls.  The results are
+checked against the unsharded fp32 oracle (AllGather K/V, ReduceScatter
+dK/dV: `/root/reference/PAPER.md:102`), with the north-star bar
+|err| <= 2e-2 + 1e-2 |ref|.
+
+Every K/V slot is filled with NaN before each push: any row a rank's tiles
+load that the push did not rewrite (a stale row left by an earlier
+micro-batch) would turn O / dQ into NaN through the masked P.V and dS
+products.  The covered (default) and the full push / pull must give the same
+O, dK and dV bit for bit.
+"""
+
+import pytest
+import torch
+
+import paper_2503_17924_b200 as wl
+from paper_2503_17924_b200.attention import attn_backward, attn_forward
+from paper_2503_17924_b200.cp import LocalPeersExchange, shard_for_rank
+from oracle import attention_oracle as ao
+from oracle import shard_oracle as so
+
+pytestmark = pytest.mark.gpu
+
+ATOL, RTOL = 2e-2, 1e-2
+MBS = ([900, 3, 129, 1000, 1], [2048], [300, 300, 1000, 17, 512, 33], [5000, 7, 64, 1, 2000])
+
+
+def _close(got, ref, tag):
+    got = got.float()
+    err = (got - ref).abs()
+    excess = (err - (ATOL + RTOL * ref.abs())).max().item()
+    assert torch.isfinite(got).all(), f"{tag}: non-finite values"
+    assert excess <= 0, f"{tag}: max abs err {err.max().item():.3e}, excess {excess:.3e}"
+
+
+def _run_group(cp, policy, hq, hkv, d, covered=True, passes=2, seed=0):
+    dev = torch.device("cuda")
+    mbs = [so.pad_lengths_for_cp(x, cp) for x in MBS]
+    plan = wl.build_shard_plan(mbs, cp, policy)
+    shards = [[shard_for_rank(plan, b, r) for r in range(cp)] for b in range(len(mbs))]
+    t_max = max(sum(x) for x in mbs)
+    ex = LocalPeersExchange.create(cp, t_max, hkv, d, dev, fill=float("nan"))
+    for e in ex:
+        e.push_covered = e.pull_covered = covered
+    g = torch.Generator(device=dev).manual_seed(seed)
+    cur = torch.cuda.current_stream()
+    results = []
+    for p in range(passes):
+        for b, lengths in enumerate(mbs):
+            T = sum(lengths)
+            mk = lambda h: torch.randn((T, h, d), generator=g, device=dev).to(torch.bfloat16)
+            q, k, v, do = mk(hq), mk(hkv), mk(hkv), mk(hq)
+            s = b % ex[0].slots
+            for e in ex:       # a stale, non-finite slot (e.g. from a skipped step)
+                e.kv[2 * s * e.n:(2 * s + 2) * e.n].fill_(float("nan"))
+            idx = [shards[b][r].gather_local.long() for r in range(cp)]
+            full = [ex[r].gather(k[idx[r]].contiguous(), v[idx[r]].contiguous(), shards[b][r], b)
+                    for r in range(cp)]
+            parts = []
+            for r in range(cp):
+                sh = shards[b][r]
+                ql, dol = q[idx[r]].contiguous(), do[idx[r]].contiguous()
+                o, lse = attn_forward(ql, full[r][0], full[r][1], sh.tiles)
+                dk_out, dv_out = ex[r].dkv_out(sh, b, cur)
+                dq, dkf, dvf = attn_backward(ql, full[r][0], full[r][1], o, lse, dol, sh.tiles,
+                                             dk_out=dk_out, dv_out=dv_out)
+                parts.append((o, dq, dkf, dvf))
+            outs = []
+            for r in range(cp):
+                dk, dv = ex[r].scatter(parts[r][2], parts[r][3], shards[b][r], b)
+                outs.append((parts[r][0], parts[r][1], dk, dv))
+            torch.cuda.synchronize()
+            segs = [(i, 0, x) for i, x in enumerate(lengths)]
+            ro, _, rdq, rdk, rdv = ao.segment_attention_fwd_bwd_blocked(
+                q.float(), k.float(), v.float(), do.float(), lengths, segs)
+            for r in range(cp):
+                tag = f"[cp={cp} {policy} {shards[b][r].strategy.value} mb{b} pass{p} rank {r}"
+                for name, got, ref in zip(("o", "dq", "dk", "dv"), outs[r],
+                                          (ro[idx[r]], rdq[idx[r]], rdk[idx[r]], rdv[idx[r]])):
+                    _close(got, ref, f"{tag} {name}]")
+            results.append([[t.float().clone() for t in o] for o in outs])
+    return results
+
+
+@pytest.mark.parametrize("policy", ["adaptive", "per_sequence", "per_document"])
+@pytest.mark.parametrize("cp", [2, 4, 8])
+def test_local_peers_exchange_matches_oracle(cp, policy):
+    _run_group(cp, policy, 4, 2, 128)
+
+
+@pytest.mark.parametrize("cp", [4, 8])
+def test_covered_push_pull_equal_full(cp):
+    """Covered push / pull == full push / pull bit for bit (O, dK, dV; dQ is
+    rank-local and summed by fp32 atomics, so it is compared to the oracle only)."""
+    a = _run_group(cp, "adaptive", 4, 2, 64, covered=True, passes=1, seed=9)
+    b = _run_group(cp, "adaptive", 4, 2, 64, covered=False, passes=1, seed=9)
+    for mb_a, mb_b in zip(a, b):
+        for ra, rb in zip(mb_a, mb_b):
+            for i in (0, 2, 3):
+                assert torch.equal(ra[i], rb[i])
+
+
+def test_fp32_partials(monkeypatch):
+    """WLB_XCHG_DKV=fp32: fp32 dK/dV partials through the same exchange."""
+    monkeypatch.setenv("WLB_XCHG_DKV", "fp32")
+    _run_group(8, "adaptive", 8, 2, 128, passes=1, seed=3)
+
+
+def test_gqa_8to1_cp8():
+    _run_group(8, "per_document", 16, 2, 128, passes=1, seed=4)

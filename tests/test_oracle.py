@@ -134,3 +134,54 @@ def test_attention_oracle_shard_invariance():
             gidx, _ = so.local_layout(lengths, a[w])
             out, _ = ao.segment_attention(q[gidx], k, v, lengths, a[w])
             assert torch.allclose(out, full[gidx], atol=1e-5)
+
+
+def _sdpa_doc_causal(q, k, v, do, lengths):
+    """Independent reference: torch's own is_causal SDPA per document (GQA by
+    repeat_interleave), fwd + autograd bwd, fp32."""
+    import torch.nn.functional as F
+    q = q.clone().requires_grad_(True)
+    k = k.clone().requires_grad_(True)
+    v = v.clone().requires_grad_(True)
+    hq, hkv = q.shape[1], k.shape[1]
+    outs, s0 = [], 0
+    for L in lengths:
+        qs = q[s0:s0 + L].transpose(0, 1)
+        ks = k[s0:s0 + L].repeat_interleave(hq // hkv, dim=1).transpose(0, 1)
+        vs = v[s0:s0 + L].repeat_interleave(hq // hkv, dim=1).transpose(0, 1)
+        outs.append(F.scaled_dot_product_attention(qs, ks, vs, is_causal=True).transpose(0, 1))
+        s0 += L
+    out = torch.cat(outs, 0)
+    out.backward(do)
+    return out.detach(), q.grad, k.grad, v.grad
+
+
+def test_attention_oracle_matches_independent_sdpa():
+    """Both oracle forms (autograd and the query-blocked explicit backward used
+    at config scale) against torch's is_causal SDPA per document, every CP rank
+    under both strategies: the concatenated per-rank outputs and the rank-summed
+    dK/dV partials equal the unsharded per-document result."""
+    g = torch.Generator().manual_seed(3)
+    hq, hkv, d = 8, 2, 32
+    for cp in (1, 2, 4):
+        lengths = so.pad_lengths_for_cp([130, 1, 67, 300, 9, 2], cp)
+        T = sum(lengths)
+        q, do = torch.randn(T, hq, d, generator=g), torch.randn(T, hq, d, generator=g)
+        k, v = torch.randn(T, hkv, d, generator=g), torch.randn(T, hkv, d, generator=g)
+        ro, rdq, rdk, rdv = _sdpa_doc_causal(q, k, v, do, lengths)
+        for strat in (so.SEQ, so.DOC):
+            a = so.shard(lengths, cp, strat)
+            dk_sum, dv_sum = torch.zeros_like(k), torch.zeros_like(v)
+            for w in range(cp):
+                idx = torch.tensor(so.local_layout(lengths, a[w])[0], dtype=torch.long)
+                auto = ao.segment_attention_fwd_bwd(q[idx], k, v, do[idx], lengths, a[w])
+                blk = ao.segment_attention_fwd_bwd_blocked(q[idx], k, v, do[idx], lengths, a[w],
+                                                           block=48)
+                for x, y in zip(auto, blk):
+                    assert torch.allclose(x, y, atol=2e-5, rtol=1e-5)
+                for x, y in zip((blk[0], blk[2]), (ro[idx], rdq[idx])):
+                    assert torch.allclose(x, y, atol=2e-5, rtol=1e-5)
+                dk_sum += blk[3]
+                dv_sum += blk[4]
+            assert torch.allclose(dk_sum, rdk, atol=2e-5, rtol=1e-5)
+            assert torch.allclose(dv_sum, rdv, atol=2e-5, rtol=1e-5)
