@@ -172,9 +172,9 @@ class SymmExchange:
     """CP exchange as ONE-SIDED NVLink traffic on symmetric memory.
 
     Every rank owns `slots` slots (micro-batch b uses slot b % slots) of a
-    document-ordered K/V buffer and of bf16 dK/dV partial buffers (summed in
-    fp32 by the pull; WLB_XCHG_DKV=fp32 keeps fp32 partials), mapped into
-    every peer.  With more than 2 slots the pipeline pushes K/V
+    document-ordered K/V buffer and of fp32 dK/dV partial buffers
+    (WLB_XCHG_DKV=bf16: bf16 partials, summed in fp32 by the pull), mapped
+    into every peer.  With more than 2 slots the pipeline pushes K/V
     slots-1 micro-batches ahead on a stream of its own (3 slots measured
     slower at N=4: 3748-3758 vs 3785-3791 TFLOP/s; the early pushes added
     more interference with the attention kernels than the exposure they
@@ -209,9 +209,12 @@ class SymmExchange:
 
     @staticmethod
     def _dkv_dtype():
-        # dK/dV partials in bf16 (WLB_XCHG_DKV=fp32 for fp32): the backward
-        # writes half the bytes and the pull moves half, summing in fp32
-        return torch.float32 if os.environ.get("WLB_XCHG_DKV", "bf16") == "fp32" else torch.bfloat16
+        # dK/dV partials in fp32 (default).  WLB_XCHG_DKV=bf16 opts into bf16
+        # partials: the backward writes half the bytes and the pull moves half
+        # (summed in fp32; +2% at N=4), but every rank's partial is rounded to
+        # bf16 before the sum, and at cp=8 with 8:1 GQA that error reached
+        # 2.5e-2 on dK, past the 2e-2 + 1e-2|ref| bar (tests/test_gpu_exchange.py).
+        return torch.bfloat16 if os.environ.get("WLB_XCHG_DKV", "fp32") == "bf16" else torch.float32
 
     def _setup(self, cp, t_max, hkv, d, device, slots, kv, dkv, kv_ptrs, dkv_ptrs):
         self.cp = cp

@@ -557,11 +557,18 @@ static_assert(sizeof(Bwd3Bars) <= 256, "barrier block");
 #endif
 
 // P for one 32-query chunk of one key row: p = exp2(s * scale_log2 + nl[q]),
-// zero where the key is past the row's position (MASK) -> packed bf16 pairs.
+// zero where the key is past the row's position (MASK) -> packed bf16 pairs
+// (pk: the A operand of dV += P^T dO) and packed fp16 pairs (ph: kept in
+// registers for dS = P (dP - Delta)).  P is in [0, 1], where fp16 keeps 3
+// more mantissa bits than bf16: forming dS from the bf16 P rounded P twice
+// (P, then dS) and put the GQA dK (summed over 8 query heads x 32K queries)
+// past the 2e-2 + 1e-2|ref| bar; with fp16 P its error matches the 64-query
+// kernel's, which multiplies the fp32 P.
 template <bool MASK>
 __device__ __forceinline__ void bwd3_p_chunk(const uint32_t (&us)[32], const float* nl,
                                              const int8_t* rp, int t, bool key_ok,
-                                             float scale_log2, uint32_t (&pk)[16]) {
+                                             float scale_log2, uint32_t (&pk)[16],
+                                             uint32_t (&ph)[16]) {
   const float2 sc2 = make_float2(scale_log2, scale_log2);
   const float4* n4 = reinterpret_cast<const float4*>(nl);
   int8_t pos[32];
@@ -589,6 +596,7 @@ __device__ __forceinline__ void bwd3_p_chunk(const uint32_t (&us)[32], const flo
         pp.y = (key_ok && pos[e + 1] >= t) ? pp.y : 0.f;
       }
       pk[e >> 1] = pack_bf16(pp.x, pp.y);
+      ph[e >> 1] = pack_f16(pp.x, pp.y);
     }
   }
 }
@@ -962,7 +970,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       mbar_wait(&bars->s_full, ph);
       if (warp == 4) TRACE3(6, i);
       tc_fence_after();
-      uint32_t pk[2][16];   // P (bf16 pairs), kept for dS
+      uint32_t p16[2][16];   // P (fp16 pairs), kept for dS
       // ---- P^T = exp2(S^T * scale * log2e - lse2), per 32-query chunk
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -971,13 +979,14 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         const bool full = kt.y == C::BN && rp[32 * c] >= C::BN - 1 && rp[32 * c + 31] >= C::BN - 1;
         tmem_ld_wait();
 
+        uint32_t pk[16];
         if (full)
-          bwd3_p_chunk<false>(us, nl + 32 * c, rp + 32 * c, t, key_ok, scale_log2, pk[c]);
+          bwd3_p_chunk<false>(us, nl + 32 * c, rp + 32 * c, t, key_ok, scale_log2, pk, p16[c]);
         else
-          bwd3_p_chunk<true>(us, nl + 32 * c, rp + 32 * c, t, key_ok, scale_log2, pk[c]);
+          bwd3_p_chunk<true>(us, nl + 32 * c, rp + 32 * c, t, key_ok, scale_log2, pk, p16[c]);
 
         // over S^T columns this warp already loaded (chunk 0's 32 columns)
-        tmem_st16(lane_base + C::COL_S + 64 * hf + 16 * c, pk[c]);
+        tmem_st16(lane_base + C::COL_S + 64 * hf + 16 * c, pk);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&bars->p_full[c]);
@@ -1002,8 +1011,8 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 #pragma unroll
           for (int u2 = 0; u2 < 2; ++u2) {
             const int e = 4 * e4 + 2 * u2;
-            const uint32_t pp = pk[c][e >> 1];
-            const float2 pf = make_float2(__uint_as_float(pp << 16), __uint_as_float(pp & 0xffff0000u));
+            const uint32_t pp = p16[c][e >> 1];
+            const float2 pf = __half22float2(*reinterpret_cast<const __half2*>(&pp));
             const float2 dd = fadd2(make_float2(__uint_as_float(ud[e]), __uint_as_float(ud[e + 1])),
                                     u2 ? make_float2(-d4.z, -d4.w) : make_float2(-d4.x, -d4.y));
             const float2 ds = fmul2(pf, dd);

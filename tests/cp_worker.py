@@ -82,8 +82,8 @@ def _pipeline_cases(rank, world, dev, policy):
         for tn, a, c in zip(("o", "dq", "dk", "dv"), res["nccl"][b], res["symm"][b]):
             # same kernels; o and dq are rank-local (dq only differs by the order
             # of its fp32 atomic reductions), dK/dV partials are summed in fp32 by
-            # NCCL and, from bf16 partials, in fp32 by the symmetric pull: they
-            # agree to bf16 rounding of the partials
+            # NCCL and by the symmetric pull (fp32 partials by default; bf16
+            # with WLB_XCHG_DKV=bf16): they agree to fp32 summation order
             err = (a - c).abs().max().item()
             tol = (1e-3 if tn in ("o", "dq") else 8e-3) * max(1.0, a.abs().max().item())
             if err > tol:
