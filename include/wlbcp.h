@@ -28,6 +28,8 @@ extern "C" {
 #define WLB_STRATEGY_PER_SEQUENCE 0
 #define WLB_STRATEGY_PER_DOCUMENT 1
 #define WLB_POLICY_ADAPTIVE 2
+#define WLB_POLICY_MEASURED 3   /* adaptive, priced by the B200 tile model */
+#define WLB_TILE_MODEL_LEN 11
 
 int32_t wlb_abi_version(void);
 const char* wlb_last_error(void);
@@ -70,6 +72,30 @@ int wlb_shard_plan(int32_t n_mb, const int32_t* mb_doc_off, const int64_t* doc_l
                    int32_t* choice, double* rank_latency, int64_t* rank_pairs,
                    int32_t* seg_count, int32_t* segs, int32_t* rowset_off,
                    int32_t* gather_index, int32_t* positions, void* stream);
+
+/* wlb_shard_plan with the MEASURED-latency selector (north-star item 4;
+ * PAPER.md:425-429 selects with profiled kernel latency; the reference's
+ * CostProfile form, sharding.py:151-188, prices dense q x kv rectangles).
+ * Both strategies are priced from the work lists the attention kernels will
+ * run: forward 128-row query tiles (pairs) x 128-key KV steps, backward
+ * 128-key KV tiles x 64- or 128-query steps, per (strategy, rank).
+ * policy: WLB_STRATEGY_PER_SEQUENCE / _PER_DOCUMENT (features and latencies
+ *   still computed) or WLB_POLICY_MEASURED (per-sequence if its slowest rank
+ *   is predicted no slower, else per-document).
+ * model (device) [WLB_TILE_MODEL_LEN] fp64: {SMs, Hq, Hkv, fwd_item_s,
+ *   fwd_step_s, bwd_item_s, bwd_step64_s, bwd_step128_s, v3_min_rows,
+ *   const_s, d_is_128}, calibrated on B200 (paper_2503_17924_b200/calibrate.py).
+ * rank_latency receives the predicted seconds [n_mb][2][cp]; features (may
+ *   be NULL) [n_mb][2][cp][8] int64: fwd items, fwd steps, max fwd item
+ *   steps, bwd items, bwd 64-q steps, bwd 128-q steps, max bwd item steps
+ *   (64, 128).  Other arguments as wlb_shard_plan; cp <= 64. */
+int wlb_shard_plan_measured(int32_t n_mb, const int32_t* mb_doc_off, const int64_t* doc_len,
+                            const int64_t* mb_tok_off, int32_t cp, int32_t policy,
+                            const double* model, int32_t max_segs, int32_t max_docs,
+                            int32_t* choice, double* rank_latency, int64_t* rank_pairs,
+                            int32_t* seg_count, int32_t* segs, int32_t* rowset_off,
+                            int32_t* gather_index, int32_t* positions, int64_t* features,
+                            void* stream);
 
 /* Tile-padded model latency of arbitrary (q, kv) ranges, summed in order
  * (replaces _kernels.kernel_latency_sum, _compiled.pyx:30-47).  All device;

@@ -31,6 +31,8 @@ SIGNATURES = {
     "wlb_heuristic_fill": (C.c_int, [_p, _i64, _i32, _i64, _f64, _f64, _p]),
     "wlb_shard_plan": (C.c_int, [_i32, _p, _p, _p, _i32, _i32, _i64, _p, _p, _i32, _f64, _i32,
                                  _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "wlb_shard_plan_measured": (C.c_int, [_i32, _p, _p, _p, _i32, _i32, _p, _i32, _i32, _p, _p,
+                                          _p, _p, _p, _p, _p, _p, _p, _p]),
     "wlb_kernel_latency_sum": (C.c_int, [_p, _p, _i64, _i64, _p, _p, _i32, _f64, _p, _p]),
     "wlb_attn_tiles": (C.c_int, [_i32, _p, _p, _p, _i32, _i32, _p, _p, _p]),
     "wlb_attn_fwd": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, _i32, _p, _i32, _i32, _i32, _i32,

@@ -102,6 +102,127 @@ def calibrate(hq=32, hkv=32, d=128, **kw) -> tuple[CostProfile, dict]:
     return fit_profile(table), table
 
 
+# ------------------------------------------------------------------------------
+# Tile model (tilemodel.py): the production measured-latency selector.
+# ------------------------------------------------------------------------------
+
+def _time_ms(fn, reps):
+    fn()
+    best = float("inf")
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        best = min(best, a.elapsed_time(b))
+    return best
+
+
+def measure_tile_workloads(workloads, hq, hkv, d, reps=2, model=None):
+    """Per (workload, strategy, rank): the planner's work-list features and the
+    MEASURED forward and backward kernel times on this GPU.
+
+    `workloads`: list of (tag, cp, [lengths per micro-batch]).  Each rank's
+    kernels run with the full document-ordered K/V resident (exact per-rank
+    kernel time; the exchange is not timed)."""
+    from .sharding import build_shard_plan
+    from .tilemodel import FEATURES, TileModel
+    _native.require_device()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    model = TileModel(hq=hq, hkv=hkv, d=d) if model is None else model
+    rows = []
+    for tag, cp, mbs in workloads:
+        t_max = max(sum(x) for x in mbs)
+        q_full = torch.randn(t_max, hq, d, device=dev, dtype=torch.bfloat16)
+        k = torch.randn(t_max, hkv, d, device=dev, dtype=torch.bfloat16)
+        v = torch.randn_like(k)
+        for strat in ("per_sequence", "per_document"):
+            plan = build_shard_plan(mbs, cp, strat, model=model)
+            feats = plan.features.cpu()
+            s_idx = 0 if strat == "per_sequence" else 1
+            for b, lengths in enumerate(mbs):
+                T = sum(lengths)
+                for r in range(cp):
+                    g, pos, ro = plan.rank_local(b, r)
+                    q = q_full[g.long()]
+                    tiles = build_tiles(ro, pos, lengths)
+                    kk, vv = k[:T], v[:T]
+                    box = {}
+
+                    def fwd():
+                        box["o"], box["lse"] = attn_forward(q, kk, vv, tiles)
+
+                    t_f = _time_ms(fwd, reps)
+                    t_b = _time_ms(lambda: attn_backward(q, kk, vv, box["o"], box["lse"], q, tiles),
+                                   reps)
+                    rows.append({"tag": tag, "cp": cp, "mb": b, "strategy": strat, "rank": r,
+                                 "tl": T // cp, "n_docs": len(lengths),
+                                 "features": dict(zip(FEATURES, feats[b, s_idx, r].tolist())),
+                                 "fwd_ms": t_f, "bwd_ms": t_b})
+        del q_full, k, v
+    return rows
+
+
+def fit_tile_model(rows, hq, hkv, d, sms=148, v3_min_rows=4096):
+    """Least-squares fit of the tile model's per-unit costs to measured rows
+    (forward and backward separately; non-negative), returning a TileModel."""
+    import numpy as np
+    from scipy.optimize import nnls
+    from .tilemodel import TileModel
+    af, yf, ab, yb = [], [], [], []
+    for r in rows:
+        f = r["features"]
+        af.append([f["fwd_items"] * hq / sms, f["fwd_steps"] * hq / sms, 1.0])
+        yf.append(r["fwd_ms"] * 1e-3)
+        v3 = d == 128 and r["tl"] >= v3_min_rows * max(1, r["n_docs"])
+        ab.append([f["bwd_items"] * hkv / sms, 0.0 if v3 else f["bwd_q64"] * hq / sms,
+                   f["bwd_q128"] * hq / sms if v3 else 0.0, 1.0])
+        yb.append(r["bwd_ms"] * 1e-3)
+    # relative least squares: every workload weighs the same whatever its size
+    wf = 1.0 / np.asarray(yf)
+    wb = 1.0 / np.asarray(yb)
+    xf, _ = nnls(np.asarray(af) * wf[:, None], np.asarray(yf) * wf)
+    xb, _ = nnls(np.asarray(ab) * wb[:, None], np.asarray(yb) * wb)
+    return TileModel(hq=hq, hkv=hkv, d=d, sms=sms, fwd_item_s=float(xf[0]),
+                     fwd_step_s=float(xf[1]), bwd_item_s=float(xb[0]),
+                     bwd_step64_s=float(xb[1]), bwd_step128_s=float(xb[2]),
+                     v3_min_rows=v3_min_rows, const_s=float(xf[2] + xb[3]),
+                     source=f"least squares over {len(rows)} measured rank workloads on "
+                            f"{torch.cuda.get_device_name()}")
+
+
+def selection_report(rows, model, profile_choices=None):
+    """Per (workload, micro-batch): measured group time of each strategy (max
+    over ranks of fwd + bwd), the measured-faster strategy, the tile model's
+    choice and (optionally) another selector's choices keyed like the rows.
+    Identical shardings (e.g. a single document) are ties: any choice is right."""
+    groups = {}
+    for r in rows:
+        key = (r["tag"], r["cp"], r["mb"])
+        g = groups.setdefault(key, {"per_sequence": [], "per_document": []})
+        g[r["strategy"]].append(r)
+    out = []
+    for key, g in sorted(groups.items()):
+        meas = {s: max(x["fwd_ms"] + x["bwd_ms"] for x in g[s]) for s in g}
+        pred = {s: max(model.predict(x["features"], x["tl"], x["n_docs"]) for x in g[s])
+                for s in g}
+        same = [x["features"] for x in g["per_sequence"]] == [x["features"] for x in g["per_document"]]
+        best = min(meas, key=meas.get)
+        pick = "per_sequence" if pred["per_sequence"] <= pred["per_document"] else "per_document"
+        rec = {"tag": key[0], "cp": key[1], "mb": key[2], "measured_ms": meas,
+               "predicted_ms": {s: v * 1e3 for s, v in pred.items()}, "measured_best": best,
+               "model_choice": pick, "tie": same,
+               "model_correct": same or pick == best,
+               "loss_if_wrong": 0.0 if same or pick == best else meas[pick] / meas[best] - 1}
+        if profile_choices is not None:
+            c = profile_choices.get(key)
+            rec["profile_choice"] = c
+            rec["profile_correct"] = same or c == best
+        out.append(rec)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--hq", type=int, default=32)

@@ -75,10 +75,11 @@ def shard_for_rank(plan: ShardPlan, index: int, rank: int) -> CPShard:
 
 
 def build_cp_shards(microbatches, cp: int, rank: int, policy: str = "adaptive",
-                    profile: CostProfile | None = None) -> list[CPShard]:
+                    profile: CostProfile | None = None, model=None) -> list[CPShard]:
     """Shard + select every micro-batch of a step in one GPU launch, then cut
-    this rank's attention tiles."""
-    plan = build_shard_plan(microbatches, cp, policy, profile)
+    this rank's attention tiles.  policy "measured" selects with the B200 tile
+    model `model` (`tilemodel.TileModel`)."""
+    plan = build_shard_plan(microbatches, cp, policy, profile, model=model)
     return [shard_for_rank(plan, b, rank) for b in range(plan.n_mb)]
 
 

@@ -83,6 +83,122 @@ __device__ __forceinline__ double range_latency(long long q, long long kv, long 
   return __ddiv_rn(__dmul_rn(op_scale, (double)(padded * kv)), cv[j]);
 }
 
+// ---------------------------------------------------------------------------
+// Measured-latency selector (north-star item 4; PAPER.md:425-429 selects with
+// profiled kernel latency).  The reference-form CostProfile charges each
+// canonical range as a dense q x kv rectangle (workload.py:239-255) and cannot
+// see what the B200 kernels actually run.  This model prices the work lists
+// themselves, per (strategy, rank), from the canonical ranges:
+//   forward : back-aligned 128-row query tiles of each (rank, document)
+//             row-set, paired from the end (wlb_attn_tiles); a tile costs one
+//             step per 128-key KV tile below its last row's position
+//   backward: 128-key KV tiles of each row-set up to its last position
+//             (bwd_kv_tiles_kernel); a KV tile costs one step per 64-query
+//             (v2) or 128-query (v3) tile of the rows that can see it
+// Integer features per (strategy, rank), kFeat of them:
+enum { kF_ITEMS = 0, kF_STEPS, kF_MAX, kB_ITEMS, kB_Q64, kB_Q128, kB_MAX64, kB_MAX128, kFeat };
+// and model[WLB_TILE_MODEL_LEN] (seconds): predicted rank time =
+//   max((fi*F_ITEMS + fs*F_STEPS) * Hq / SMs, fi + fs*F_MAX)
+// + max((bi*B_ITEMS*Hkv + bs*B_Q*Hq) / SMs, bi + bs*B_MAX*(Hq/Hkv)) + c0,
+// B_Q / B_MAX / bs of the backward kernel the library will pick (v3 when the
+// rank's rows per document reach v3_min_rows and D = 128).
+constexpr int kMaxModelCp = 64;
+
+__device__ __forceinline__ int rowset_pos(const Seg* r, int n, int i) {
+  for (int k = 0; k < n; ++k) {
+    const int len = r[k].e - r[k].s;
+    if (i < len) return r[k].s + i;
+    i -= len;
+  }
+  return r[n - 1].e - 1;
+}
+
+__device__ void tile_model_select(int b, int nd, const long long* L, const long long* dstart,
+                                  const long long* cursor, long long C, int cp, int policy,
+                                  const double* model, long long* features, double* rank_latency,
+                                  int* choice, int* chosen_s) {
+  __shared__ unsigned long long feat[2][kMaxModelCp][kFeat];
+  for (int i = threadIdx.x; i < 2 * cp * kFeat; i += blockDim.x)
+    (&feat[0][0][0])[i] = 0;
+  __syncthreads();
+  for (long long it = threadIdx.x; it < 2LL * cp * nd; it += blockDim.x) {
+    const int strat = (int)(it / ((long long)cp * nd));
+    const int w = (int)((it / nd) % cp), p = (int)(it % nd);
+    Seg r[4];
+    const int n = strat ? per_doc_ranges(L[p], cursor[p], cp, w, r)
+                        : per_seq_ranges(dstart[p], dstart[p + 1], C, cp, w, r);
+    if (n == 0) continue;
+    int R = 0;
+    for (int k = 0; k < n; ++k) R += r[k].e - r[k].s;
+    // forward: tiles from the end, paired (X = later, Y = earlier)
+    const int nt = (R + 127) / 128;
+    unsigned long long steps = 0, fmax = 0;
+    for (int t = 0; t < nt; t += 2) {
+      const unsigned long long kx = (rowset_pos(r, n, R - 1 - 128 * t) + 128) / 128;
+      const unsigned long long ky = t + 1 < nt ? (rowset_pos(r, n, R - 1 - 128 * (t + 1)) + 128) / 128 : 0;
+      steps += kx + ky;
+      fmax = max(fmax, kx + ky);
+    }
+    // backward: KV tiles below the last position, rows with position >= k0
+    const int nkv = (r[n - 1].e - 1 + 128) / 128;
+    unsigned long long q64 = 0, q128 = 0, m64 = 0, m128 = 0;
+    for (int t = 0; t < nkv; ++t) {
+      const int k0 = 128 * t;
+      int cnt = 0;
+      for (int k = 0; k < n; ++k) cnt += max(0, r[k].e - max(r[k].s, k0));
+      const unsigned long long a = (cnt + 63) / 64, c = (cnt + 127) / 128;
+      q64 += a;
+      q128 += c;
+      m64 = max(m64, a);
+      m128 = max(m128, c);
+    }
+    unsigned long long* f = feat[strat][w];
+    atomicAdd(&f[kF_ITEMS], (unsigned long long)((nt + 1) / 2));
+    atomicAdd(&f[kF_STEPS], steps);
+    atomicMax(&f[kF_MAX], fmax);
+    atomicAdd(&f[kB_ITEMS], (unsigned long long)nkv);
+    atomicAdd(&f[kB_Q64], q64);
+    atomicAdd(&f[kB_Q128], q128);
+    atomicMax(&f[kB_MAX64], m64);
+    atomicMax(&f[kB_MAX128], m128);
+  }
+  __syncthreads();
+  if (features)
+    for (int i = threadIdx.x; i < 2 * cp * kFeat; i += blockDim.x)
+      features[(long long)b * 2 * cp * kFeat + i] = (long long)(&feat[0][0][0])[(i / (cp * kFeat)) * kMaxModelCp * kFeat + i % (cp * kFeat)];
+  if (threadIdx.x < 2 * cp) {
+    const int strat = threadIdx.x / cp, w = threadIdx.x % cp;
+    const unsigned long long* f = feat[strat][w];
+    const double sms = model[0], hq = model[1], hkv = model[2];
+    const double fi = model[3], fs = model[4], bi = model[5], bs64 = model[6], bs128 = model[7];
+    const double v3_rows = model[8], c0 = model[9], d128 = model[10];
+    const long long T = dstart[nd];
+    const bool v3 = d128 != 0.0 && (double)(T / cp) >= v3_rows * (double)(nd > 0 ? nd : 1);
+    const double bq = (double)(v3 ? f[kB_Q128] : f[kB_Q64]);
+    const double bm = (double)(v3 ? f[kB_MAX128] : f[kB_MAX64]);
+    const double bs = v3 ? bs128 : bs64;
+    const double tf = fmax((fi * (double)f[kF_ITEMS] + fs * (double)f[kF_STEPS]) * hq / sms,
+                           fi + fs * (double)f[kF_MAX]);
+    const double tb = fmax((bi * (double)f[kB_ITEMS] * hkv + bs * bq * hq) / sms,
+                           bi + bs * bm * (hq / hkv));
+    rank_latency[((long long)b * 2 + strat) * cp + w] = tf + tb + c0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int c = policy;
+    if (policy == WLB_POLICY_MEASURED) {
+      double g[2];
+      for (int s = 0; s < 2; ++s) {
+        g[s] = 0.0;
+        for (int w = 0; w < cp; ++w) g[s] = fmax(g[s], rank_latency[((long long)b * 2 + s) * cp + w]);
+      }
+      c = g[0] <= g[1] ? WLB_STRATEGY_PER_SEQUENCE : WLB_STRATEGY_PER_DOCUMENT;
+    }
+    *chosen_s = c;
+    choice[b] = c;
+  }
+}
+
 constexpr int kPlanThreads = 512;
 constexpr int kSmemDocs = 12000;   // documents whose starts + cursors fit shared memory (188 KB)
 
@@ -95,7 +211,8 @@ shard_plan_kernel(const int* __restrict__ mb_doc_off, const long long* __restric
                   long long* __restrict__ rank_pairs, int* __restrict__ seg_count,
                   int* __restrict__ segs, int* __restrict__ rowset_off,
                   int* __restrict__ gather_index, int* __restrict__ positions,
-                  long long* __restrict__ gscratch) {
+                  long long* __restrict__ gscratch, const double* __restrict__ model,
+                  long long* __restrict__ features) {
   extern __shared__ long long smem_ll[];
   __shared__ long long warp_tot[kPlanThreads / 32 + 1];
   __shared__ long long total_s;
@@ -168,6 +285,12 @@ shard_plan_kernel(const int* __restrict__ mb_doc_off, const long long* __restric
   __syncthreads();
   __threadfence_block();
 
+  if (model) {
+    // -- 3'. measured policy: price both strategies from the work lists the
+    //        attention kernels will run, with B200-calibrated per-tile costs
+    tile_model_select(b, nd, L, dstart, cursor, C, cp, policy, model, features, rank_latency,
+                      choice, &chosen_s);
+  } else {
   // -- 3. per-worker model latency (sequential, canonical order: bit-exact) ----
   if (threadIdx.x < 2 * cp) {
     const int strat = threadIdx.x / cp, w = threadIdx.x % cp;
@@ -193,6 +316,7 @@ shard_plan_kernel(const int* __restrict__ mb_doc_off, const long long* __restric
     }
     chosen_s = c;
     choice[b] = c;
+  }
   }
   __syncthreads();
   const int strat = chosen_s;
@@ -346,6 +470,39 @@ attn_tiles_kernel(int nd, const int* __restrict__ rowset_off, const int* __restr
 
 using namespace wlb;
 
+static int launch_plan(int32_t n_mb, const int32_t* mb_doc_off, const int64_t* doc_len,
+                       const int64_t* mb_tok_off, int32_t cp, int32_t policy, int64_t tile,
+                       const int64_t* curve_q, const double* curve_v, int32_t n_curve,
+                       double op_scale, int32_t max_segs, int32_t max_docs, int32_t* choice,
+                       double* rank_latency, int64_t* rank_pairs, int32_t* seg_count,
+                       int32_t* segs, int32_t* rowset_off, int32_t* gather_index,
+                       int32_t* positions, const double* model, int64_t* features,
+                       cudaStream_t stream) {
+  WLB_REQUIRE(max_docs >= 1, "max_docs out of range");
+  WLB_REQUIRE(max_segs >= 4 * (int64_t)max_docs + 2, "max_segs must be >= 4*max_docs+2");
+  if (n_mb <= 0) return WLB_OK;
+  const size_t per_mb = sizeof(long long) * (2 * (size_t)max_docs + 1);
+  long long* gscratch = nullptr;
+  size_t smem = per_mb;
+  // the measured policy's per-(strategy, rank) features take 8 KB of static smem
+  const int smem_docs = model ? kSmemDocs - 512 : kSmemDocs;
+  if (max_docs > smem_docs) {
+    // stream-ordered global scratch (freed after the launch, on the same stream)
+    WLB_CUDA_TRY(cudaMallocAsync((void**)&gscratch, per_mb * (size_t)n_mb, stream));
+    smem = 0;
+  } else if (smem > 48 * 1024) {
+    WLB_SMEM_ATTR(shard_plan_kernel, (int)smem);
+  }
+  shard_plan_kernel<<<n_mb, kPlanThreads, smem, stream>>>(
+      mb_doc_off, (const long long*)doc_len, (const long long*)mb_tok_off, cp, policy, tile,
+      (const long long*)curve_q, curve_v, n_curve, op_scale, max_segs, max_docs, choice,
+      rank_latency, (long long*)rank_pairs, seg_count, segs, rowset_off, gather_index, positions,
+      gscratch, model, (long long*)features);
+  WLB_LAUNCH_CHECK();
+  if (gscratch) WLB_CUDA_TRY(cudaFreeAsync(gscratch, stream));
+  return WLB_OK;
+}
+
 extern "C" int wlb_shard_plan(int32_t n_mb, const int32_t* mb_doc_off, const int64_t* doc_len,
                               const int64_t* mb_tok_off, int32_t cp, int32_t policy, int64_t tile,
                               const int64_t* curve_q, const double* curve_v, int32_t n_curve,
@@ -356,28 +513,29 @@ extern "C" int wlb_shard_plan(int32_t n_mb, const int32_t* mb_doc_off, const int
   WLB_REQUIRE(cp >= 1, "cp must be >= 1");
   WLB_REQUIRE(policy >= 0 && policy <= 2, "unknown policy %d", policy);
   WLB_REQUIRE(n_curve >= 1 && tile >= 1, "bad cost profile");
-  WLB_REQUIRE(max_docs >= 1, "max_docs out of range");
-  WLB_REQUIRE(max_segs >= 4 * (int64_t)max_docs + 2, "max_segs must be >= 4*max_docs+2");
-  if (n_mb <= 0) return WLB_OK;
-  const size_t per_mb = sizeof(long long) * (2 * (size_t)max_docs + 1);
-  long long* gscratch = nullptr;
-  size_t smem = per_mb;
-  if (max_docs > kSmemDocs) {
-    // stream-ordered global scratch (freed after the launch, on the same stream)
-    WLB_CUDA_TRY(cudaMallocAsync((void**)&gscratch, per_mb * (size_t)n_mb, (cudaStream_t)stream));
-    smem = 0;
-  } else if (smem > 48 * 1024) {
-    WLB_CUDA_TRY(cudaFuncSetAttribute(shard_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-  }
-  shard_plan_kernel<<<n_mb, kPlanThreads, smem, (cudaStream_t)stream>>>(
-      mb_doc_off, (const long long*)doc_len, (const long long*)mb_tok_off, cp, policy, tile,
-      (const long long*)curve_q, curve_v, n_curve, op_scale, max_segs, max_docs, choice,
-      rank_latency, (long long*)rank_pairs, seg_count, segs, rowset_off, gather_index, positions,
-      gscratch);
-  WLB_LAUNCH_CHECK();
-  if (gscratch) WLB_CUDA_TRY(cudaFreeAsync(gscratch, (cudaStream_t)stream));
-  return WLB_OK;
+  return launch_plan(n_mb, mb_doc_off, doc_len, mb_tok_off, cp, policy, tile, curve_q, curve_v,
+                     n_curve, op_scale, max_segs, max_docs, choice, rank_latency, rank_pairs,
+                     seg_count, segs, rowset_off, gather_index, positions, nullptr, nullptr,
+                     (cudaStream_t)stream);
+}
+
+extern "C" int wlb_shard_plan_measured(int32_t n_mb, const int32_t* mb_doc_off,
+                                       const int64_t* doc_len, const int64_t* mb_tok_off,
+                                       int32_t cp, int32_t policy, const double* model,
+                                       int32_t max_segs, int32_t max_docs, int32_t* choice,
+                                       double* rank_latency, int64_t* rank_pairs,
+                                       int32_t* seg_count, int32_t* segs, int32_t* rowset_off,
+                                       int32_t* gather_index, int32_t* positions,
+                                       int64_t* features, void* stream) {
+  WLB_REQUIRE(cp >= 1 && cp <= kMaxModelCp, "cp must be in [1, %d] for the measured policy",
+              kMaxModelCp);
+  WLB_REQUIRE(policy == WLB_STRATEGY_PER_SEQUENCE || policy == WLB_STRATEGY_PER_DOCUMENT ||
+                  policy == WLB_POLICY_MEASURED,
+              "unknown policy %d", policy);
+  WLB_REQUIRE(model != nullptr, "model is required");
+  return launch_plan(n_mb, mb_doc_off, doc_len, mb_tok_off, cp, policy, 1, nullptr, nullptr, 0,
+                     1.0, max_segs, max_docs, choice, rank_latency, rank_pairs, seg_count, segs,
+                     rowset_off, gather_index, positions, model, features, (cudaStream_t)stream);
 }
 
 extern "C" int wlb_kernel_latency_sum(const int64_t* q_lens, const int64_t* kv_lens, int64_t n,

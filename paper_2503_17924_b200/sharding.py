@@ -22,6 +22,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _native
+from .tilemodel import FEATURES, TileModel
 from .workload import CostProfile, MicroBatch, TokenRange
 
 _DEFAULT_PROFILE = CostProfile()
@@ -38,7 +39,7 @@ class ShardStrategy(str, enum.Enum):
 
 
 _STRATS = (ShardStrategy.PER_SEQUENCE, ShardStrategy.PER_DOCUMENT)
-_POLICY_CODE = {"per_sequence": 0, "per_document": 1, "adaptive": 2}
+_POLICY_CODE = {"per_sequence": 0, "per_document": 1, "adaptive": 2, "measured": 3}
 
 
 @dataclass
@@ -80,6 +81,10 @@ class ShardPlan:
     rowset_off: torch.Tensor          # [n_mb, cp, max_docs+1] int32
     gather_index: torch.Tensor | None  # [sum T] int32
     positions: torch.Tensor | None     # [sum T] int32
+    # measured-latency model path only: the model and the per-(strategy,
+    # rank) work-list features it priced, [n_mb, 2, cp, 8] int64 (FEATURES)
+    model: TileModel | None = None
+    features: torch.Tensor | None = None
     _host: dict = field(default_factory=dict)
 
     @property
@@ -121,11 +126,17 @@ class ShardPlan:
 
 def build_shard_plan(microbatches, cp: int, policy: str = "adaptive",
                      profile: CostProfile | None = None, with_tokens: bool = True,
-                     device=None) -> ShardPlan:
+                     device=None, model: TileModel | None = None) -> ShardPlan:
     """Shard (and select) many micro-batches in one GPU launch.
 
     `microbatches`: MicroBatch objects or plain length lists.  Raises
     ValueError exactly where the reference would (`sharding.py:77-83,200`).
+
+    policy "adaptive" selects with the reference CostProfile (bit-exact with
+    balsim); "measured" selects with the B200 tile model (`tilemodel.py`,
+    `model` or the shipped calibration for the default 32 x 128 shape) and
+    also fills `features`.  Passing `model` with "per_sequence" /
+    "per_document" prices both strategies with it without selecting.
     """
     if policy not in _POLICY_CODE:
         raise ValueError(f"unknown sharding policy {policy!r}")
@@ -167,6 +178,20 @@ def build_shard_plan(microbatches, cp: int, policy: str = "adaptive",
     gidx = torch.empty(tok_off[-1], **i32) if with_tokens else None
     pos = torch.empty(tok_off[-1], **i32) if with_tokens else None
     p = _native.ptr
+    if policy == "measured" or model is not None:
+        if policy == "adaptive":
+            raise ValueError("a tile model prices the 'measured' policy, not 'adaptive'")
+        model = TileModel.for_shape(32, 32, 128) if model is None else model
+        d_model = up(model.array(), torch.float64, dev)
+        feats = torch.empty((n_mb, 2, cp, len(FEATURES)), dtype=torch.int64, device=dev)
+        _native.check(_native.lib().wlb_shard_plan_measured(
+            n_mb, p(d_doc_off), p(d_len), p(d_tok), cp, _POLICY_CODE[policy], p(d_model),
+            max_segs, max_docs, p(choice), p(lat), p(pairs), p(seg_count), p(segs), p(rowset),
+            p(gidx), p(pos), p(feats), _native.stream_ptr()), "wlb_shard_plan_measured")
+        return ShardPlan(cp=cp, lengths=lengths, doc_ids=ids, tok_off=tok_off[:-1],
+                         choice=choice, rank_latency=lat, rank_pairs=pairs, seg_count=seg_count,
+                         segs=segs, rowset_off=rowset, gather_index=gidx, positions=pos,
+                         model=model, features=feats)
     _native.check(_native.lib().wlb_shard_plan(
         n_mb, p(d_doc_off), p(d_len), p(d_tok), cp, _POLICY_CODE[policy], profile.tile_size,
         p(d_cq), p(d_cv), len(cq), profile.op_scale, max_segs, max_docs, p(choice), p(lat),
