@@ -134,3 +134,75 @@ def test_attention_tiles_cover_rows_once():
             ext.append((kvx - kvb + 127) // 128)
         assert bool((seen == 1).all())
         assert ext == sorted(ext, reverse=True)   # longest first
+
+
+def _work_list_features(plan, b, rank):
+    """The 8 tile-model features of one rank, recomputed from the work lists
+    the kernels run: wlb_attn_tiles items (forward) and the backward's KV-tile
+    rule (128-key tiles below a row-set's last position; rows with position
+    >= k0), from the rank's positions / row-set offsets."""
+    from paper_2503_17924_b200.attention import build_tiles
+    lengths = plan.lengths[b]
+    g, pos, ro = plan.rank_local(b, rank)
+    t = build_tiles(ro, pos, lengths)
+    n = int(t.n_tiles.item())
+    items = t.tiles[:2 * n].cpu().view(n, 8).tolist()
+    f_steps = f_max = 0
+    for rx, nx, kvb, kvx, ry, ny, kvy, _ in items:
+        s = (kvx - kvb + 127) // 128 + ((kvy - kvb + 127) // 128 if ny else 0)
+        f_steps += s
+        f_max = max(f_max, s)
+    pos, ro = pos.cpu().tolist(), ro.cpu().tolist()
+    b_items = q64 = q128 = m64 = m128 = 0
+    for p in range(len(lengths)):
+        rows = pos[ro[p]:ro[p + 1]]
+        if not rows:
+            continue
+        for tk in range((rows[-1] + 128) // 128):
+            cnt = sum(1 for x in rows if x >= 128 * tk)
+            b_items += 1
+            q64 += (cnt + 63) // 64
+            q128 += (cnt + 127) // 128
+            m64, m128 = max(m64, (cnt + 63) // 64), max(m128, (cnt + 127) // 128)
+    return [n, f_steps, f_max, b_items, q64, q128, m64, m128]
+
+
+@pytest.mark.parametrize("cp", [1, 2, 4, 8])
+def test_tile_model_features_match_kernel_work_lists(cp):
+    """The measured-latency selector prices exactly the work the attention
+    kernels run: its per-(strategy, rank) features equal counts taken from
+    the kernels' own tile lists, for both strategies."""
+    mbs = [so.pad_lengths_for_cp(x, cp) for x in
+           ([700, 3, 129, 2000, 1, 257], [4096], [300] * 9 + [17, 5000], [1] * 40 + [64])]
+    model = wl.TileModel()
+    for s, strat in enumerate(("per_sequence", "per_document")):
+        plan = wl.build_shard_plan(mbs, cp, strat, model=model)
+        feats = plan.features.cpu()
+        for b in range(len(mbs)):
+            for r in range(cp):
+                assert feats[b, s, r].tolist() == _work_list_features(plan, b, r), (strat, b, r)
+
+
+def test_measured_policy_selects_by_predicted_latency():
+    """policy="measured": per-sequence iff its slowest rank's predicted time is
+    <= per-document's (ties -> per-sequence, the reference's rule); the
+    prediction equals TileModel.predict on the returned features."""
+    cp = 4
+    mbs = [so.pad_lengths_for_cp(x, cp) for x in
+           ([30000, 100, 2000], [512] * 32, [8192], [100] * 40 + [20000])]
+    model = wl.TileModel()
+    plan = wl.build_shard_plan(mbs, cp, "measured", model=model)
+    lat, feats = plan.rank_latency.cpu(), plan.features.cpu()
+    for b, ls in enumerate(mbs):
+        tl = sum(ls) // cp
+        for s in range(2):
+            for r in range(cp):
+                pred = model.predict(feats[b, s, r].tolist(), tl, len(ls))
+                assert abs(lat[b, s, r].item() - pred) <= 1e-12 * max(1.0, pred)
+        g = lat[b].max(dim=1).values
+        exp = "per_sequence" if g[0] <= g[1] else "per_document"
+        assert plan.strategy(b).value == exp
+    # the chosen strategy's token layout is the one built
+    a = plan.assignment(0)
+    ref = so.shard(mbs[0], cp, so.SEQ if a.strategy == wl.ShardStrategy.PER_SEQUENCE else so.DOC)
+    assert to_workers(a) == [[list(x) for x in w] for w in ref]
