@@ -118,7 +118,7 @@ __device__ void tile_model_select(int b, int nd, const long long* L, const long 
                                   const double* model, long long* features, double* rank_latency,
                                   int* choice, int* chosen_s) {
   __shared__ unsigned long long feat[2][kMaxModelCp][kFeat];
-  for (int i = threadIdx.x; i < 2 * cp * kFeat; i += blockDim.x)
+  for (int i = threadIdx.x; i < 2 * kMaxModelCp * kFeat; i += blockDim.x)
     (&feat[0][0][0])[i] = 0;
   __syncthreads();
   for (long long it = threadIdx.x; it < 2LL * cp * nd; it += blockDim.x) {
