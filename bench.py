@@ -322,8 +322,14 @@ def main():
     pipe = CPStepPipeline(group, exchange=exchange)
     ex_launches = (2 if symm else 4) if cp > 1 else 0      # push+pull | 2 scatters + 2 gathers
 
+    # CP > 1: per-sequence vs per-document chosen by the measured-latency tile
+    # model calibrated on B200 (tilemodel.py); CP = 1 has one sharding, which
+    # the reference selector (bit-exact with balsim) picks
+    policy = "measured" if cp > 1 else "adaptive"
+    model = wl.TileModel.for_shape(hq, hkv, d) if cp > 1 else None
+
     def step(record=None):
-        shards = build_cp_shards(lengths, cp, rank, "adaptive")
+        shards = build_cp_shards(lengths, cp, rank, policy, model=model)
         launches[0] += 1 + N_SEQ + N_SEQ * (5 + ex_launches)   # plan, tiles, attn, exchange
 
         def timed(b, sh, kernels):
@@ -400,7 +406,7 @@ def main():
         cur = torch.cuda.current_stream()
 
         def e2e_step():
-            shards = build_cp_shards(lengths, cp, rank, "adaptive")
+            shards = build_cp_shards(lengths, cp, rank, policy, model=model)
             h2d_s.wait_stream(cur)             # previous step is done reading the inputs
             ready = []
             with torch.cuda.stream(h2d_s):
@@ -465,7 +471,7 @@ def main():
         "value_basis": "whole job: step FLOPs (all ranks) / max-over-ranks step time; "
                        "per GPU in tflops_per_gpu",
         "config": {"workload": wk["name"], "seq_len": T, "sequences_per_step": N_SEQ,
-                   "heads": [hq, hkv], "head_dim": d, "cp": cp, "policy": "adaptive",
+                   "heads": [hq, hkv], "head_dim": d, "cp": cp, "policy": policy,
                    "workload_rule": "N=1: config 2 (32K, CP=1); N>1: config 3 (128K, CP=N); "
                                     "--workload 128k: 128K at CP=N for every N"
                                     if args.workload == "auto" else "128K at CP=N for every N",

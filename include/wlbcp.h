@@ -142,8 +142,14 @@ int wlb_attn_bwd(const void* q, const void* k, const void* v, const void* o,
                  int32_t Hkv, int32_t D, float scale, void* ws, void* stream);
 /* wlb_attn_bwd with flags: WLB_BWD_DKV_BF16 writes the dK/dV partials as
  * bf16 [T][Hkv][D] (the symmetric CP exchange then moves half the bytes and
- * sums them in fp32, wlb_cp_dkv_pull_ex); 0 is wlb_attn_bwd. */
+ * sums them in fp32, wlb_cp_dkv_pull_ex); WLB_BWD_COVERED_ONLY skips the
+ * zero fill of uncovered rows; 0 is wlb_attn_bwd. */
 #define WLB_BWD_DKV_BF16 1
+/* WLB_BWD_COVERED_ONLY: write only the dK/dV partial rows this rank's KV
+ * tiles cover (keys below roundup128(last local position + 1) of each
+ * document); the rest are left untouched instead of zero-filled.  For
+ * consumers that read covered rows only (wlb_cp_dkv_pull_cov). */
+#define WLB_BWD_COVERED_ONLY 2
 int wlb_attn_bwd_ex(const void* q, const void* k, const void* v, const void* o,
                     const void* do_, const float* lse, void* dq, void* dk, void* dv,
                     const int32_t* rowset_off, const int32_t* doc_start, int32_t n_docs,

@@ -79,10 +79,12 @@ def attn_forward(q, k, v, tiles: AttnTiles, scale: float | None = None):
 
 
 def attn_backward(q, k, v, o, lse, do, tiles: AttnTiles, scale: float | None = None,
-                  dk_out=None, dv_out=None):
+                  dk_out=None, dv_out=None, covered_only: bool = False):
     """dQ [Tl,Hq,D] bf16 and fp32 dK/dV partials over the full sequence
     (written into dk_out / dv_out when given, e.g. symmetric exchange buffers;
-    bf16 dk_out / dv_out take bf16 partials)."""
+    bf16 dk_out / dv_out take bf16 partials).  covered_only: rows no KV tile
+    of this rank covers are left unwritten instead of zeroed (for the covered
+    CP pull, which never reads them)."""
     _check_inputs(q, k, v)
     tl, hq, d = q.shape
     T, hkv = k.shape[0], k.shape[1]
@@ -94,6 +96,8 @@ def attn_backward(q, k, v, o, lse, do, tiles: AttnTiles, scale: float | None = N
     if dk.dtype != dv.dtype or dk.dtype not in (torch.float32, torch.bfloat16):
         raise ValueError("dk_out / dv_out must both be fp32 or both bf16")
     flags = _native.WLB_BWD_DKV_BF16 if dk.dtype == torch.bfloat16 else 0
+    if covered_only:
+        flags |= _native.WLB_BWD_COVERED_ONLY
     lib = _native.lib()
     ws = torch.empty(lib.wlb_attn_bwd_workspace(tl, T, hq, hkv, d, tiles.n_docs),
                      dtype=torch.uint8, device=q.device)

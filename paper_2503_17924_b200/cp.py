@@ -392,6 +392,9 @@ class CPStepPipeline:
         cur = torch.cuda.current_stream()
         n = len(shards)
         rdy = ready if ready is not None else [None] * n
+        # the covered pull reads only the partial rows each rank's KV tiles
+        # wrote: skip the zero fill of the rest
+        covered = bool(getattr(self.exchange, "pull_covered", False))
         outs = [None] * n
         pend = {}
         for b in range(min(self.depth, n)):
@@ -412,7 +415,9 @@ class CPStepPipeline:
                         dv_out=dv_out):
                 o, lse = attn_forward(q, k_full, v_full, sh.tiles, scale)
                 dq, dkf, dvf = attn_backward(q, k_full, v_full, o, lse, do, sh.tiles, scale,
-                                             dk_out, dv_out)
+                                             dk_out, dv_out,
+                                             covered_only=covered and dk_out is not None
+                                             and sh.tiles.n_docs > 0)
                 return o, dq, dkf, dvf
 
             o, dq, dkf, dvf = on_kernels(b, shards[b], kernels) if on_kernels else kernels()

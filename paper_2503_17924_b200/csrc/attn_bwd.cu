@@ -1291,7 +1291,7 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
                       const float* lse, void* dq, void* dk, void* dv, const int32_t* rowset_off,
                       const int32_t* doc_start, int32_t n_docs, const int32_t* positions,
                       int32_t Tl, int32_t T, int32_t Hq, int32_t Hkv, float scale, void* ws,
-                      int dkv_bf16, cudaStream_t stream) {
+                      int dkv_bf16, bool covered_only, cudaStream_t stream) {
   using C = BwdCfg<D>;
   BwdWorkspace w = carve(ws, Tl, T, Hq, D, n_docs);
   const int max_items = T / 128 + n_docs + 1;
@@ -1299,7 +1299,7 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   // dK/dV rows of every KV tile are stored whole by the kernel; only the keys
   // no KV tile covers (past a document's last local query position) are zeroed
   // here, instead of clearing 2 x T x Hkv x D x 4 bytes up front.
-  if (n_docs > 0) {
+  if (n_docs > 0 && !covered_only) {
     zero_uncovered_kernel<<<(unsigned)((T + kZeroRows - 1) / kZeroRows), 256, 0, stream>>>(
         rowset_off, positions, doc_start, n_docs, (uint4*)dk, (uint4*)dv,
         Hkv * D * (dkv_bf16 ? 2 : 4) / 16);
@@ -1436,13 +1436,15 @@ extern "C" int wlb_attn_bwd_ex(const void* q, const void* k, const void* v, cons
   WLB_REQUIRE(D == 64 || D == 128, "head dim %d unsupported (64 or 128)", D);
   WLB_REQUIRE(Hq > 0 && Hkv > 0 && Hq % Hkv == 0, "Hq must be a multiple of Hkv");
   WLB_REQUIRE(Tl >= 0 && T > 0 && n_docs >= 0 && ws != nullptr, "bad sizes");
-  WLB_REQUIRE((flags & ~WLB_BWD_DKV_BF16) == 0, "unknown backward flags 0x%x", flags);
+  WLB_REQUIRE((flags & ~(WLB_BWD_DKV_BF16 | WLB_BWD_COVERED_ONLY)) == 0,
+              "unknown backward flags 0x%x", flags);
   const int bf = (flags & WLB_BWD_DKV_BF16) != 0;
+  const bool cov = (flags & WLB_BWD_COVERED_ONLY) != 0;
   if (D == 64)
     return wlb::launch_bwd<64>(q, k, v, o, do_, lse, dq, dk, dv, rowset_off, doc_start, n_docs,
-                               positions, Tl, T, Hq, Hkv, scale, ws, bf, (cudaStream_t)stream);
+                               positions, Tl, T, Hq, Hkv, scale, ws, bf, cov, (cudaStream_t)stream);
   return wlb::launch_bwd<128>(q, k, v, o, do_, lse, dq, dk, dv, rowset_off, doc_start, n_docs,
-                              positions, Tl, T, Hq, Hkv, scale, ws, bf, (cudaStream_t)stream);
+                              positions, Tl, T, Hq, Hkv, scale, ws, bf, cov, (cudaStream_t)stream);
 }
 
 extern "C" int wlb_attn_bwd(const void* q, const void* k, const void* v, const void* o,

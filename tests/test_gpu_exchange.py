@@ -70,7 +70,8 @@ def _run_group(cp, policy, hq, hkv, d, covered=True, passes=2, seed=0):
                 o, lse = attn_forward(ql, full[r][0], full[r][1], sh.tiles)
                 dk_out, dv_out = ex[r].dkv_out(sh, b, cur)
                 dq, dkf, dvf = attn_backward(ql, full[r][0], full[r][1], o, lse, dol, sh.tiles,
-                                             dk_out=dk_out, dv_out=dv_out)
+                                             dk_out=dk_out, dv_out=dv_out,
+                                             covered_only=ex[r].pull_covered)
                 parts.append((o, dq, dkf, dvf))
             outs = []
             for r in range(cp):

@@ -1,7 +1,9 @@
 """BASELINE config 5: 64 micro-batches packed by the W(d) packer with outlier
-delay queues, padded for CP=8, adaptive per-seq / per-doc selection (one
-batched GPU launch), then CP=8 attention fwd+bwd for a sample of the packed
-micro-batches, each rank replayed on this GPU (exact per-rank kernel time).
+delay queues, padded for CP=8, per-seq / per-doc selection by the measured
+tile model (one batched GPU launch; the reference CostProfile's choices are
+reported beside it), then CP=8 attention fwd+bwd for a sample of the packed
+micro-batches, each rank replayed on this GPU (exact per-rank kernel time,
+the backward as the CP pipeline runs it: covered dK/dV partial rows only).
 
     python tools/config5.py --iters 2 --sample 6 --out r.json
 """
@@ -17,6 +19,7 @@ def main():
     ap.add_argument("--iters", type=int, default=2)
     ap.add_argument("--sample", type=int, default=6)
     ap.add_argument("--cp", type=int, default=8)
+    ap.add_argument("--policy", default="measured", choices=["measured", "adaptive"])
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     dev = torch.device("cuda")
@@ -35,13 +38,19 @@ def main():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        plan = wl.build_shard_plan(mbs, a.cp, "adaptive", prof)   # ONE launch, 64 micro-batches
+        model = wl.TileModel.for_shape(hq, hkv, d)
+        plan = wl.build_shard_plan(mbs, a.cp, a.policy, prof,    # ONE launch, 64 micro-batches
+                                   model=model if a.policy == "measured" else None)
         e1.record()
         torch.cuda.synchronize()
         plan_ms = e0.elapsed_time(e1)
         choices = [plan.strategy(b).value for b in range(plan.n_mb)]
+        ref = wl.build_shard_plan(mbs, a.cp, "adaptive", prof, with_tokens=False)
+        ref_choices = [ref.strategy(b).value for b in range(plan.n_mb)]
         rec = {"iteration": it, "docs": len(batch), "microbatches": plan.n_mb, "pack_ms": round(pack_ms, 2),
-               "plan_ms_gpu": round(plan_ms, 3), "per_document_chosen": choices.count("per_document"),
+               "plan_ms_gpu": round(plan_ms, 3), "policy": a.policy,
+               "per_document_chosen": choices.count("per_document"),
+               "reference_profile_per_document": ref_choices.count("per_document"),
                "imbalance_degree_attention": round(wl.imbalance_degree_attention(plan_h.microbatches), 4),
                "carried": len(plan_h.carried_over), "sample": []}
         # heaviest micro-batches first
@@ -58,11 +67,11 @@ def main():
                 q = q_full[g.long()]
                 tiles = build_tiles(ro, pos, lengths)
                 o, lse = attn_forward(q, k, v, tiles)
-                attn_backward(q, k, v, o, lse, q, tiles)
+                attn_backward(q, k, v, o, lse, q, tiles, covered_only=True)
                 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 s.record()
                 o, lse = attn_forward(q, k, v, tiles)
-                attn_backward(q, k, v, o, lse, q, tiles)
+                attn_backward(q, k, v, o, lse, q, tiles, covered_only=True)
                 e.record()
                 e.synchronize()
                 times.append(s.elapsed_time(e))

@@ -41,6 +41,9 @@ def main():
     ap.add_argument("--hq", type=int, default=32)
     ap.add_argument("--hkv", type=int, default=32)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--full-partials", action="store_true",
+                    help="zero-fill uncovered dK/dV rows (the single-rank API) instead of the "
+                         "CP pipeline's covered-only backward")
     a = ap.parse_args()
     dev = torch.device("cuda")
     prof = wl.CostProfile()
@@ -75,8 +78,8 @@ def main():
                     box["o"], box["lse"] = attn_forward(q, k, v, box["t"])
 
                 t_fwd = ev_ms(fwd, a.reps)
-                t_bwd = ev_ms(lambda: attn_backward(q, k, v, box["o"], box["lse"], q, box["t"]),
-                              a.reps)
+                t_bwd = ev_ms(lambda: attn_backward(q, k, v, box["o"], box["lse"], q, box["t"],
+                                                    covered_only=not a.full_partials), a.reps)
                 rp = int(plan.rank_pairs[0, r].item())
                 rec["ranks"].append({"rank": r, "rows": q.shape[0], "pairs": rp,
                                      "tiles_ms": round(t_tiles, 4), "fwd_ms": round(t_fwd, 4),
