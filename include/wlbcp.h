@@ -166,6 +166,11 @@ int32_t wlb_attn_bwd_select(int32_t v3_min_rows);
  * negative = default; returns the previous setting. */
 int32_t wlb_attn_bwd_pairs(int32_t on);
 
+/* 64-query (v2) backward scheduling: 1 = persistent (one CTA per SM taking
+ * (KV tile, KV head) units from a dynamic queue), 0 = one CTA per unit;
+ * negative = default.  Returns the previous setting.  Process-wide knob. */
+int32_t wlb_attn_bwd_persistent(int32_t on);
+
 /* Split a fused QKV projection y[Tl][Hq+2*Hkv][D] (bf16) into THD q / k / v
  * and apply rotate-half rotary embeddings at the IN-DOCUMENT positions the
  * shard builder emits (positions[Tl], TokenRange coordinates,

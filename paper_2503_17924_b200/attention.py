@@ -134,6 +134,12 @@ def set_bwd_v3_min_rows(rows: int) -> int:
     return int(_native.lib().wlb_attn_bwd_select(int(rows)))
 
 
+def set_bwd_persistent(on: int) -> int:
+    """64-query backward as a persistent kernel (1) or one CTA per work unit
+    (0); negative = default.  Returns the previous setting."""
+    return int(_native.lib().wlb_attn_bwd_persistent(int(on)))
+
+
 def set_bwd_pairs(on: int) -> int:
     """v3 backward as 2-CTA clusters sharing dQ (1 on, 0 off, negative =
     default).  Returns the previous setting."""

@@ -72,8 +72,8 @@ struct BwdCfg {
   static constexpr int OFF_VEC = OFF_DS + 2 * T_BYTES;  // QS x {lse2, delta, pos-k0}[BM]
   static constexpr int OFF_BAR = OFF_VEC + QS * 3 * BM * 4;
   // The dynamic-SMEM window starts 1024-B aligned on sm_100 (checked at run
-  // time), so no alignment slack is reserved: D = 128 uses 226.4 KB of 227.
-  static constexpr int SMEM = OFF_BAR + 256;
+  // time), so no alignment slack is reserved (D = 128: 194.8 KB).
+  static constexpr int SMEM = OFF_BAR + 512;
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr uint32_t COL_S = 0;      // S^T[b] at b*64
   static constexpr uint32_t COL_DP = 128;   // dP^T[b] at 128 + b*64 (later dQ^T[b])
@@ -85,14 +85,22 @@ struct BwdCfg {
   static constexpr int THREADS = 128 + 128 * NCW + 128;   // + dQ drain warpgroup
 };
 
-struct BwdBars {  // 188 bytes; OFF_BAR reserves 256
+// Work units reach the roles through a small ring: the producer warp takes
+// the next unit (dynamically, from a global counter, when persistent) and
+// publishes its index; every consumer warp reads it and releases the slot.
+constexpr int kUnitRing = 4;
+
+struct BwdBars {  // 268 bytes; OFF_BAR reserves 512
   uint64_t kv_full, kv_empty;
   uint64_t q_full[3], q_empty[3];
   uint64_t s_full[2], p_full[2], mma2_done[2], s_free[2];
   uint64_t vec_full[3], vec_empty[3];
   uint64_t acc_done;
+  uint64_t unit_full[kUnitRing], unit_empty[kUnitRing];
+  int unit_id[kUnitRing];
   uint32_t tmem_base;
 };
+static_assert(sizeof(BwdBars) <= 512, "barrier block");
 
 // 32 consecutive dV and dK values (dK scaled) of one key row at element offset
 // `off`: fp32, or bf16 when the partials go through the bf16 CP exchange.
@@ -127,9 +135,17 @@ __device__ __forceinline__ void store_dkv32(void* dv, void* dk, size_t off, cons
 }
 
 // kv_tiles[2i] = {kv_begin (global), kv_len, row_first, row_end}, kv_tiles[2i+1].x = k0
-// A CTA runs KV heads [g0, g0 + nh) of its KV tile back to back (hpc > 1 for
-// short row-sets); the query tiles of all its heads form one flat sequence
-// I = head * n_iter + i, so every ring and barrier phase runs on across heads.
+//
+// Work unit u = (KV tile item, KV-head group): item u % n_slots, KV heads
+// [g0, g0 + nh) with g0 = (u / n_slots) * hpc (head-major unit order, LPT
+// within a head: resident CTAs share one head's Q / dO / dQ in L2).  The query
+// tiles of a unit's heads form one flat sequence, and the sequences of all
+// the units a CTA runs are concatenated: every ring stage and barrier phase
+// runs on a CTA-global tile counter, so one unit's tail (its last dK/dV
+// epilogue, the next K/V load) overlaps the next unit's start.
+//   persistent = 0: one unit per CTA (unit = blockIdx.x);
+//   persistent = 1: one CTA per SM takes units from a global counter until
+//                   none are left (dynamic list scheduling in unit order).
 template <int D, int NCW>
 __global__ void __launch_bounds__(256 + 128 * NCW, 1)
 attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -138,26 +154,15 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 float* __restrict__ dq_acc, void* __restrict__ dk, void* __restrict__ dv,
                 const int4* __restrict__ kv_tiles, const int* __restrict__ n_kv_tiles,
                 const int* __restrict__ positions, int Tl, int Hq, int Hkv, int n_slots, int hpc,
-                float scale, float scale_log2, int dkv_bf16) {
+                int n_units, int* __restrict__ sched, int persistent, float scale,
+                float scale_log2, int dkv_bf16) {
   using C = BwdCfg<D, NCW>;
   extern __shared__ uint8_t smem_raw[];
   if (smem_u32(smem_raw) & 1023) __trap();   // SW128 tiles need 1024-B alignment
   uint8_t* smem = smem_raw;
-  // head-major order (LPT within a head): resident CTAs share one head's Q/dO/dQ in L2
-  const int item = blockIdx.x % n_slots, g0 = (blockIdx.x / n_slots) * hpc;
-  if (item >= n_kv_tiles[0]) return;
-  const int nh = min(hpc, Hkv - g0);
-  const int4 kt = kv_tiles[2 * item];
-  const int k0 = kv_tiles[2 * item + 1].x;   // in-document position of key 0 of the tile
+  const int n_items = n_kv_tiles[0];
   const int group = Hq / Hkv;
-  const int qt_per_head = (kt.w - kt.z + C::BM - 1) / C::BM;
-  const int n_iter = qt_per_head * group;    // query tiles per KV head
-  const int n_all = n_iter * nh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // flat tile I -> (KV head, query head, first row)
-  auto tile_g = [&](int I) { return g0 + I / n_iter; };
-  auto tile_h = [&](int I) { return tile_g(I) * group + (I % n_iter) / qt_per_head; };
-  auto tile_row = [&](int I) { return kt.z + ((I % n_iter) % qt_per_head) * C::BM; };
 
   BwdBars* bars = reinterpret_cast<BwdBars*>(smem + C::OFF_BAR);
   uint8_t* sK = smem + C::OFF_K;
@@ -183,6 +188,11 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       mbar_init(&bars->s_free[i], 128);
     }
     mbar_init(&bars->acc_done, 1);
+    for (int i = 0; i < kUnitRing; ++i) {
+      mbar_init(&bars->unit_full[i], 1);
+      // consumers: MMA warp, vector warp, 4 drain warps, 4 * NCW compute warps
+      mbar_init(&bars->unit_empty[i], 2 + 4 + 4 * NCW);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(&bars->tmem_base, C::TMEM_COLS);
@@ -191,26 +201,82 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
 
+  // unit geometry (every role derives the same from the unit index)
+  struct Unit {
+    int4 kt;        // {kv_begin, kv_len, row_first, row_end}
+    int k0, g0, nh, qt_per_head, n_iter, n_all;
+  };
+  auto geom = [&](int u) {
+    Unit U;
+    const int item = u % n_slots;
+    U.kt = kv_tiles[2 * item];
+    U.k0 = kv_tiles[2 * item + 1].x;   // in-document position of key 0 of the tile
+    U.g0 = (u / n_slots) * hpc;
+    U.nh = min(hpc, Hkv - U.g0);
+    U.qt_per_head = (U.kt.w - U.kt.z + C::BM - 1) / C::BM;
+    U.n_iter = U.qt_per_head * group;  // query tiles per KV head
+    U.n_all = U.n_iter * U.nh;
+    return U;
+  };
+  // unit-local flat tile I -> (KV head, query head, first row)
+  auto tile_g = [&](const Unit& U, int I) { return U.g0 + I / U.n_iter; };
+  auto tile_h = [&](const Unit& U, int I) {
+    return tile_g(U, I) * group + (I % U.n_iter) / U.qt_per_head;
+  };
+  auto tile_row = [&](const Unit& U, int I) {
+    return U.kt.z + ((I % U.n_iter) % U.qt_per_head) * C::BM;
+  };
+  // consumer side of the unit ring (whole warp; lane 0 releases the slot)
+  auto next_unit = [&](int seq) {
+    const int st = seq % kUnitRing;
+    mbar_wait(&bars->unit_full[st], (seq / kUnitRing) & 1);
+    const int u = *reinterpret_cast<volatile int*>(&bars->unit_id[st]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bars->unit_empty[st]);
+    return u;
+  };
+
   if (warp == 0) {
     // ------------------------------------------------------------ producer --
-    {   // whole warp; one elected lane issues
-      tma_prefetch(&tmQ);
-      tma_prefetch(&tmK);
-      tma_prefetch(&tmV);
-      tma_prefetch(&tmDO);
-      for (int I = 0; I < n_all; ++I) {
-        if (I % n_iter == 0) {                 // next KV head: K/V once the last reader is done
-          const int gl = I / n_iter;
-          if (gl > 0) mbar_wait(&bars->kv_empty, (gl - 1) & 1);
+    // whole warp; one elected lane issues.  I0 / G0: tiles / KV heads of the
+    // units this CTA already ran (ring stages and barrier phases run on).
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    tma_prefetch(&tmDO);
+    int I0 = 0, G0 = 0;
+    for (int seq = 0;; ++seq) {
+      int u = -1;
+      if (lane == 0) {
+        if (persistent) {
+          do {
+            u = atomicAdd(sched, 1);
+          } while (u < n_units && u % n_slots >= n_items);
+          if (u >= n_units) u = -1;
+        } else if (seq == 0 && (int)blockIdx.x % n_slots < n_items) {
+          u = blockIdx.x;
+        }
+        const int st = seq % kUnitRing;
+        mbar_wait(&bars->unit_empty[st], ((seq / kUnitRing) & 1) ^ 1);
+        bars->unit_id[st] = u;
+        mbar_arrive(&bars->unit_full[st]);
+      }
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if (u < 0) break;
+      const Unit U = geom(u);
+      for (int I = 0; I < U.n_all; ++I) {
+        if (I % U.n_iter == 0) {            // next KV head: K/V once the last reader is done
+          const int gl = I / U.n_iter, G = G0 + gl;
+          if (G > 0) mbar_wait(&bars->kv_empty, (G - 1) & 1);
           mbar_expect_tx_w(&bars->kv_full, 2 * C::KV_BYTES);
           for (int s = 0; s < C::SLABS; ++s) {
-            tma_load_3d_w(sK + s * C::KV_SLAB, &tmK, &bars->kv_full, s * 64, g0 + gl, kt.x);
-            tma_load_3d_w(sV + s * C::KV_SLAB, &tmV, &bars->kv_full, s * 64, g0 + gl, kt.x);
+            tma_load_3d_w(sK + s * C::KV_SLAB, &tmK, &bars->kv_full, s * 64, U.g0 + gl, U.kt.x);
+            tma_load_3d_w(sV + s * C::KV_SLAB, &tmV, &bars->kv_full, s * 64, U.g0 + gl, U.kt.x);
           }
         }
-        const int st = I % C::QS;
-        const int h = tile_h(I), row = tile_row(I);
-        mbar_wait(&bars->q_empty[st], ((I / C::QS) & 1) ^ 1);
+        const int Ig = I0 + I, st = Ig % C::QS;
+        const int h = tile_h(U, I), row = tile_row(U, I);
+        mbar_wait(&bars->q_empty[st], ((Ig / C::QS) & 1) ^ 1);
         mbar_expect_tx_w(&bars->q_full[st], 2 * C::Q_BYTES);
         for (int s = 0; s < C::SLABS; ++s) {
           tma_load_3d_w(sQ + st * C::Q_BYTES + s * C::Q_SLAB, &tmQ, &bars->q_full[st], s * 64, h, row);
@@ -218,17 +284,25 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                         row);
         }
       }
+      I0 += U.n_all;
+      G0 += U.nh;
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer --
-    {   // whole warp; one elected lane issues
-      const uint32_t k_b = smem_u32(sK), v_b = smem_u32(sV), q_b = smem_u32(sQ),
-                     do_b = smem_u32(sDO), ds_b = smem_u32(sDS);
+    // whole warp; one elected lane issues
+    const uint32_t k_b = smem_u32(sK), v_b = smem_u32(sV), q_b = smem_u32(sQ),
+                   do_b = smem_u32(sDO), ds_b = smem_u32(sDS);
+    int I0 = 0, G0 = 0;
+    for (int seq = 0;; ++seq) {
+      const int u = next_unit(seq);
+      if (u < 0) break;
+      const Unit U = geom(u);
       // S^T / dP^T of tile I (first MMA group)
       auto first_half = [&](int I) {
-        const int b = I & 1, st = I % C::QS;
-        mbar_wait(&bars->q_full[st], (I / C::QS) & 1);
-        TRACE(0, I);
+        const int Ig = I0 + I;
+        const int b = Ig & 1, st = Ig % C::QS;
+        mbar_wait(&bars->q_full[st], (Ig / C::QS) & 1);
+        TRACE(0, Ig);
         tc_fence_after();
         const uint32_t qs = q_b + st * C::Q_BYTES, dos = do_b + st * C::Q_BYTES;
         // S^T[b] was last read by the compute warps of tile I-2 (before p_full,
@@ -241,8 +315,8 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
           mma_ss_w(tmem + C::COL_S + b * 64, sdesc_sw128(k_b + ko, 16, 1024),
                    sdesc_sw128(qs + qo, 16, 1024), C::IDESC_ST, kk > 0);
         }
-        if (I >= 2) mbar_wait_fast(&bars->s_free[b], ((I - 2) >> 1) & 1);
-        TRACE(1, I);
+        if (Ig >= 2) mbar_wait_fast(&bars->s_free[b], ((Ig - 2) >> 1) & 1);
+        TRACE(1, Ig);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -255,9 +329,10 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       };
       // dQ^T, dV, dK of tile J (second MMA group)
       auto second_half = [&](int J) {
-        const int b = J & 1, st = J % C::QS, j = J % n_iter;
-        mbar_wait_fast(&bars->p_full[b], (J >> 1) & 1);
-        TRACE(2, J);
+        const int Jg = I0 + J;
+        const int b = Jg & 1, st = Jg % C::QS, j = J % U.n_iter;
+        mbar_wait_fast(&bars->p_full[b], (Jg >> 1) & 1);
+        TRACE(2, Jg);
         tc_fence_after();
         const uint32_t qs = q_b + st * C::Q_BYTES, dos = do_b + st * C::Q_BYTES;
         const uint32_t dss = ds_b + b * C::T_BYTES;
@@ -282,40 +357,50 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                    sdesc_sw128(qs + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
         }
         mma_commit_w(&bars->q_empty[st]);
-        if (j == n_iter - 1) {                  // last tile of this KV head
+        if (j == U.n_iter - 1) {                  // last tile of this KV head
           mma_commit_w(&bars->acc_done);
           mma_commit_w(&bars->kv_empty);
         }
       };
       // Pipelined one tile deep (S/dP of tile I before dQ/dV/dK of tile I-1),
-      // except across a KV-head boundary: tile I of the next head needs the new
-      // K/V, which may only land after the last reader of the old ones.
-      for (int I = 0; I <= n_all; ++I) {
-        const bool head_start = I < n_all && I % n_iter == 0;
-        if (I < n_all && !head_start) first_half(I);
+      // except across a KV-head (or unit) boundary: tile I of the next head
+      // needs the new K/V, which may only land after the last reader of the
+      // old ones.
+      for (int I = 0; I <= U.n_all; ++I) {
+        const bool head_start = I < U.n_all && I % U.n_iter == 0;
+        if (I < U.n_all && !head_start) first_half(I);
         if (I >= 1) second_half(I - 1);
         if (head_start) {
-          mbar_wait(&bars->kv_full, (I / n_iter) & 1);
+          mbar_wait(&bars->kv_full, (G0 + I / U.n_iter) & 1);
           first_half(I);
         }
       }
+      I0 += U.n_all;
+      G0 += U.nh;
     }
   } else if (warp == 3) {
     // ------------------------------------------------- per-query vectors --
-    for (int I = 0; I < n_all; ++I) {
-      const int b = I % C::QS;
-      const int h = tile_h(I), row0 = tile_row(I);
-      mbar_wait(&bars->vec_empty[b], ((I / C::QS) & 1) ^ 1);
-      float* vec = sVec + b * 3 * C::BM;
+    int I0 = 0;
+    for (int seq = 0;; ++seq) {
+      const int u = next_unit(seq);
+      if (u < 0) break;
+      const Unit U = geom(u);
+      for (int I = 0; I < U.n_all; ++I) {
+        const int Ig = I0 + I, b = Ig % C::QS;
+        const int h = tile_h(U, I), row0 = tile_row(U, I);
+        mbar_wait(&bars->vec_empty[b], ((Ig / C::QS) & 1) ^ 1);
+        float* vec = sVec + b * 3 * C::BM;
 #pragma unroll
-      for (int e = lane; e < C::BM; e += 32) {
-        const int row = row0 + e;
-        const bool ok = row < kt.w;
-        vec[e] = ok ? lse[(size_t)h * Tl + row] * 1.4426950408889634f : 0.f;
-        vec[C::BM + e] = ok ? delta[(size_t)h * Tl + row] : 0.f;
-        reinterpret_cast<int*>(vec)[2 * C::BM + e] = ok ? positions[row] - k0 : -1;
+        for (int e = lane; e < C::BM; e += 32) {
+          const int row = row0 + e;
+          const bool ok = row < U.kt.w;
+          vec[e] = ok ? lse[(size_t)h * Tl + row] * 1.4426950408889634f : 0.f;
+          vec[C::BM + e] = ok ? delta[(size_t)h * Tl + row] : 0.f;
+          reinterpret_cast<int*>(vec)[2 * C::BM + e] = ok ? positions[row] - U.k0 : -1;
+        }
+        mbar_arrive(&bars->vec_full[b]);
       }
-      mbar_arrive(&bars->vec_full[b]);
+      I0 += U.n_all;
     }
   } else if (warp >= 4 + 4 * NCW) {
     // ------------------------------------------------------------ dQ drain --
@@ -327,126 +412,141 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     const uint32_t lane_base = tmem + ((uint32_t)(lg * 32) << 16);
     const int d = D == 128 ? lg * 32 + lane : lg * 16 + lane;
     const size_t stride = (size_t)Hq * D;
-    for (int J = 0; J < n_all; ++J) {
-      const int b = J & 1;
-      const int h = tile_h(J), row0 = tile_row(J);
-      mbar_wait(&bars->mma2_done[b], (J >> 1) & 1);
-      TRACE(6, J);
-      tc_fence_after();
-      uint32_t u[64];
-      tmem_ld32(lane_base + C::COL_DP + b * 64, *reinterpret_cast<uint32_t(*)[32]>(u));
-      tmem_ld32(lane_base + C::COL_DP + b * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&bars->s_free[b]);
-      TRACE(7, J);
-      if (D == 128 || lane < 16) {
-        float* ptr = dq_acc + ((size_t)row0 * Hq + h) * D + d;
-        const int nvalid = min(C::BM, kt.w - row0);
-        if (nvalid == C::BM) {
+    int I0 = 0;
+    for (int seq = 0;; ++seq) {
+      const int u = next_unit(seq);
+      if (u < 0) break;
+      const Unit U = geom(u);
+      for (int J = 0; J < U.n_all; ++J) {
+        const int Jg = I0 + J, b = Jg & 1;
+        const int h = tile_h(U, J), row0 = tile_row(U, J);
+        mbar_wait(&bars->mma2_done[b], (Jg >> 1) & 1);
+        TRACE(6, Jg);
+        tc_fence_after();
+        uint32_t v[64];
+        tmem_ld32(lane_base + C::COL_DP + b * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
+        tmem_ld32(lane_base + C::COL_DP + b * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&bars->s_free[b]);
+        TRACE(7, Jg);
+        if (D == 128 || lane < 16) {
+          float* ptr = dq_acc + ((size_t)row0 * Hq + h) * D + d;
+          const int nvalid = min(C::BM, U.kt.w - row0);
+          if (nvalid == C::BM) {
 #pragma unroll
-          for (int q = 0; q < C::BM; ++q, ptr += stride) atomicAdd(ptr, __uint_as_float(u[q]) * scale);
-        } else {
+            for (int q = 0; q < C::BM; ++q, ptr += stride) atomicAdd(ptr, __uint_as_float(v[q]) * scale);
+          } else {
 #pragma unroll
-          for (int q = 0; q < C::BM; ++q, ptr += stride)
-            if (q < nvalid) atomicAdd(ptr, __uint_as_float(u[q]) * scale);
+            for (int q = 0; q < C::BM; ++q, ptr += stride)
+              if (q < nvalid) atomicAdd(ptr, __uint_as_float(v[q]) * scale);
+          }
         }
       }
+      I0 += U.n_all;
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------- compute --
     const int lg = warp & 3;                 // TMEM lane quarter
     const int ch = (warp - 4) >> 2;          // which 32-column half of the 64 queries
     const int t = lg * 32 + lane;            // key row in the tile
-    const bool key_ok = t < kt.y;
     const uint32_t lane_base = tmem + ((uint32_t)(lg * 32) << 16);
-
-    for (int I = 0; I < n_all; ++I) {
-      const int b = I & 1, vb = I % C::QS;
-      mbar_wait(&bars->vec_full[vb], (I / C::QS) & 1);
-      mbar_wait(&bars->s_full[b], (I >> 1) & 1);
-      TRACE(3, I);
-      tc_fence_after();
-      uint32_t us[32], ud[32];
-      tmem_ld32(lane_base + C::COL_S + b * 64 + ch * 32, us);
-      tmem_ld32(lane_base + C::COL_DP + b * 64 + ch * 32, ud);
-      const float* vec = sVec + vb * 3 * C::BM + ch * 32;
-      const float4* vl4 = reinterpret_cast<const float4*>(vec);
-      const float4* vd4 = reinterpret_cast<const float4*>(vec + C::BM);
-      const int4* vp4 = reinterpret_cast<const int4*>(vec + 2 * C::BM);
-      // Unmasked fast path: every query of this half sees every key of the tile
-      // (rows are position-sorted, so the first and last columns bound them).
-      const bool full = kt.y == C::BN && vp4[0].x >= C::BN - 1 && vp4[7].w >= C::BN - 1;
-      tmem_ld_wait();
-      TRACE(4, I);
-      uint32_t pk[16], dk2[16];
-#pragma unroll
-      for (int e4 = 0; e4 < 8; ++e4) {
-        const float4 l4 = vl4[e4], d4 = vd4[e4];
-        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
-        float pp[4], dd[4];
-        if (full) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            pp[u] = ex2(fmaf(__uint_as_float(us[4 * e4 + u]), scale_log2, -lv[u]));
-            dd[u] = pp[u] * (__uint_as_float(ud[4 * e4 + u]) - dv4[u]);
-          }
-        } else {
-          const int4 p4 = vp4[e4];
-          const int pv[4] = {p4.x, p4.y, p4.z, p4.w};
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const bool allowed = key_ok && pv[u] >= t;   // key position k0+t <= query position
-            const float x = fmaf(__uint_as_float(us[4 * e4 + u]), scale_log2, -lv[u]);
-            pp[u] = allowed ? ex2(x) : 0.f;
-            dd[u] = pp[u] * (__uint_as_float(ud[4 * e4 + u]) - dv4[u]);
-          }
-        }
-        pk[2 * e4] = pack_bf16(pp[0], pp[1]);
-        pk[2 * e4 + 1] = pack_bf16(pp[2], pp[3]);
-        dk2[2 * e4] = pack_bf16(dd[0], dd[1]);
-        dk2[2 * e4 + 1] = pack_bf16(dd[2], dd[3]);
-      }
-      tc_fence_before();
-      mbar_arrive(&bars->vec_empty[vb]);
-      // P^T and dS^T (packed bf16) over THIS warp's own 32 S^T columns (no
-      // other warp reads them): A operands of the TS dV / dK MMAs.  The
-      // previous readers (dV/dK of tile I-2) finished before MMA1(I)
-      // (s_full implies it).  dP^T[b] is free once loaded: dQ^T(I) goes
-      // there.  dS^T also goes to SMEM as the B operand of dQ^T = K^T dS^T.
-      tmem_st16(lane_base + C::COL_S + b * 64 + ch * 32, pk);
-      tmem_st16(lane_base + C::COL_S + b * 64 + ch * 32 + 16, dk2);
-      uint8_t* drow = sDS + b * C::T_BYTES + t * 128;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int off = (((ch * 4 + c) ^ (t & 7)) << 4);
-        *reinterpret_cast<uint4*>(drow + off) = make_uint4(dk2[4 * c], dk2[4 * c + 1], dk2[4 * c + 2], dk2[4 * c + 3]);
-      }
-      fence_proxy_async_smem();
-      tmem_st_wait();
-      tc_fence_before();
-      TRACE(5, I);
-      mbar_arrive(&bars->p_full[b]);
-      if (I % n_iter == n_iter - 1) {
-        // ---------------------------------------------------------- epilogue --
-        // the last MMA group of this KV head wrote dV / dK; the next head's
-        // first dV/dK MMA (accumulate = 0) waits for this warp's next p_full,
-        // i.e. for these TMEM loads
-        const int g = tile_g(I);
-        mbar_wait(&bars->acc_done, (I / n_iter) & 1);
+    int I0 = 0, G0 = 0;
+    for (int seq = 0;; ++seq) {
+      const int u = next_unit(seq);
+      if (u < 0) break;
+      const Unit U = geom(u);
+      const bool key_ok = t < U.kt.y;
+      for (int I = 0; I < U.n_all; ++I) {
+        const int Ig = I0 + I;
+        const int b = Ig & 1, vb = Ig % C::QS;
+        mbar_wait(&bars->vec_full[vb], (Ig / C::QS) & 1);
+        mbar_wait(&bars->s_full[b], (Ig >> 1) & 1);
+        TRACE(3, Ig);
         tc_fence_after();
-        // TMEM loads are warp-collective: issue converged, predicate the stores.
-        const size_t off = ((size_t)(kt.x + t) * Hkv + g) * D + ch * (D / 2);
+        uint32_t us[32], ud[32];
+        tmem_ld32(lane_base + C::COL_S + b * 64 + ch * 32, us);
+        tmem_ld32(lane_base + C::COL_DP + b * 64 + ch * 32, ud);
+        const float* vec = sVec + vb * 3 * C::BM + ch * 32;
+        const float4* vl4 = reinterpret_cast<const float4*>(vec);
+        const float4* vd4 = reinterpret_cast<const float4*>(vec + C::BM);
+        const int4* vp4 = reinterpret_cast<const int4*>(vec + 2 * C::BM);
+        // Unmasked fast path: every query of this half sees every key of the tile
+        // (rows are position-sorted, so the first and last columns bound them).
+        const bool full = U.kt.y == C::BN && vp4[0].x >= C::BN - 1 && vp4[7].w >= C::BN - 1;
+        tmem_ld_wait();
+        TRACE(4, Ig);
+        uint32_t pk[16], dk2[16];
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c) {
-          uint32_t a[32], bb[32];
-          tmem_ld32(lane_base + C::COL_DV + ch * (D / 2) + c * 32, a);
-          tmem_ld32(lane_base + C::COL_DK + ch * (D / 2) + c * 32, bb);
-          tmem_ld_wait();
-          if (key_ok) store_dkv32(dv, dk, off + c * 32, a, bb, scale, dkv_bf16 != 0);
+        for (int e4 = 0; e4 < 8; ++e4) {
+          const float4 l4 = vl4[e4], d4 = vd4[e4];
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
+          float pp[4], dd[4];
+          if (full) {
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+              pp[x] = ex2(fmaf(__uint_as_float(us[4 * e4 + x]), scale_log2, -lv[x]));
+              dd[x] = pp[x] * (__uint_as_float(ud[4 * e4 + x]) - dv4[x]);
+            }
+          } else {
+            const int4 p4 = vp4[e4];
+            const int pv[4] = {p4.x, p4.y, p4.z, p4.w};
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+              const bool allowed = key_ok && pv[x] >= t;   // key position k0+t <= query position
+              const float y = fmaf(__uint_as_float(us[4 * e4 + x]), scale_log2, -lv[x]);
+              pp[x] = allowed ? ex2(y) : 0.f;
+              dd[x] = pp[x] * (__uint_as_float(ud[4 * e4 + x]) - dv4[x]);
+            }
+          }
+          pk[2 * e4] = pack_bf16(pp[0], pp[1]);
+          pk[2 * e4 + 1] = pack_bf16(pp[2], pp[3]);
+          dk2[2 * e4] = pack_bf16(dd[0], dd[1]);
+          dk2[2 * e4 + 1] = pack_bf16(dd[2], dd[3]);
         }
         tc_fence_before();
+        mbar_arrive(&bars->vec_empty[vb]);
+        // P^T and dS^T (packed bf16) over THIS warp's own 32 S^T columns (no
+        // other warp reads them): A operands of the TS dV / dK MMAs.  The
+        // previous readers (dV/dK of tile I-2) finished before MMA1(I)
+        // (s_full implies it).  dP^T[b] is free once loaded: dQ^T(I) goes
+        // there.  dS^T also goes to SMEM as the B operand of dQ^T = K^T dS^T.
+        tmem_st16(lane_base + C::COL_S + b * 64 + ch * 32, pk);
+        tmem_st16(lane_base + C::COL_S + b * 64 + ch * 32 + 16, dk2);
+        uint8_t* drow = sDS + b * C::T_BYTES + t * 128;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int off = (((ch * 4 + c) ^ (t & 7)) << 4);
+          *reinterpret_cast<uint4*>(drow + off) = make_uint4(dk2[4 * c], dk2[4 * c + 1], dk2[4 * c + 2], dk2[4 * c + 3]);
+        }
+        fence_proxy_async_smem();
+        tmem_st_wait();
+        tc_fence_before();
+        TRACE(5, Ig);
+        mbar_arrive(&bars->p_full[b]);
+        if (I % U.n_iter == U.n_iter - 1) {
+          // -------------------------------------------------------- epilogue --
+          // the last MMA group of this KV head wrote dV / dK; the next head's
+          // (or unit's) first dV/dK MMA (accumulate = 0) waits for this warp's
+          // next p_full, i.e. for these TMEM loads
+          const int g = tile_g(U, I);
+          mbar_wait(&bars->acc_done, (G0 + I / U.n_iter) & 1);
+          tc_fence_after();
+          // TMEM loads are warp-collective: issue converged, predicate the stores.
+          const size_t off = ((size_t)(U.kt.x + t) * Hkv + g) * D + ch * (D / 2);
+#pragma unroll
+          for (int c = 0; c < D / 64; ++c) {
+            uint32_t a[32], bb[32];
+            tmem_ld32(lane_base + C::COL_DV + ch * (D / 2) + c * 32, a);
+            tmem_ld32(lane_base + C::COL_DK + ch * (D / 2) + c * 32, bb);
+            tmem_ld_wait();
+            if (key_ok) store_dkv32(dv, dk, off + c * 32, a, bb, scale, dkv_bf16 != 0);
+          }
+          tc_fence_before();
+        }
       }
+      I0 += U.n_all;
+      G0 += U.nh;
     }
   }
   tc_fence_before();
@@ -1227,6 +1327,11 @@ static int g_bwd_hpc_short = WLB_HPC;
 #define WLB_BWD_PAIRS 0
 #endif
 static int g_bwd_pairs = WLB_BWD_PAIRS;
+// v2 backward as a persistent kernel (one CTA per SM, dynamic unit queue)
+#ifndef WLB_BWD_PERSIST
+#define WLB_BWD_PERSIST 1
+#endif
+static int g_bwd_persistent = WLB_BWD_PERSIST;
 
 // Zero the dK/dV rows no KV tile covers: in document p, keys at in-document
 // positions >= 128 * ceil((last local position + 1) / 128) (all of p when this
@@ -1265,6 +1370,7 @@ struct BwdWorkspace {
   float* delta;
   int4* kv_tiles;   // [2*max_items] sorted + [2*max_items] scratch
   int* n_kv;
+  int* sched;       // persistent kernel's unit counter
   size_t bytes;
 };
 
@@ -1282,6 +1388,7 @@ static BwdWorkspace carve(void* base, int Tl, int T, int Hq, int D, int n_docs) 
   w.delta = (float*)take((size_t)Hq * Tl * 4);
   w.kv_tiles = (int4*)take(4 * max_items * sizeof(int4) + (n_docs + 1) * sizeof(int));
   w.n_kv = (int*)take(16);
+  w.sched = (int*)take(16);
   w.bytes = off;
   return w;
 }
@@ -1369,16 +1476,30 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   //  slower: the S/dP -> compute -> dV/dK/dQ serialisation costs more than the
   //  SMEM bandwidth it saves.)
   WLB_SMEM_ATTR((attn_bwd_kernel<D, 2>), C::SMEM);
-  // several KV heads per CTA for short row-sets (< 2048 local rows per
-  // document on average): the next head's loads overlap this head's tail
-  // (only with >= 6 waves of CTAs left: Tl/128 bounds the KV tiles from below)
-  const int hpc = (Hkv % g_bwd_hpc_short == 0 && (long long)Tl < (long long)WLB_HPC_ROWS * (n_docs > 0 ? n_docs : 1) &&
-                   (long long)(Tl / 128) * Hkv >= 6LL * 148 * g_bwd_hpc_short)
-                      ? g_bwd_hpc_short : 1;
-  attn_bwd_kernel<D, 2><<<(unsigned)max_items * ((Hkv + hpc - 1) / hpc), C::THREADS, C::SMEM,
-                          stream>>>(
-      tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq, Hkv,
-      max_items, hpc, scale, scale * 1.4426950408889634f, dkv_bf16);
+  if (g_bwd_persistent) {
+    // one CTA per SM taking (KV tile, KV head) units from a global counter:
+    // a unit's tail (dK/dV epilogue, next K/V load) overlaps the next unit
+    // instead of a CTA teardown + launch, and the SMs stay busy to the end
+    int dev = 0, sms = 148;
+    WLB_CUDA_TRY(cudaGetDevice(&dev));
+    WLB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int n_units = max_items * Hkv;
+    WLB_CUDA_TRY(cudaMemsetAsync(w.sched, 0, sizeof(int), stream));
+    attn_bwd_kernel<D, 2><<<(unsigned)std::min(n_units, sms), C::THREADS, C::SMEM, stream>>>(
+        tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
+        Hkv, max_items, 1, n_units, w.sched, 1, scale, scale * 1.4426950408889634f, dkv_bf16);
+  } else {
+    // several KV heads per CTA for short row-sets (< 2048 local rows per
+    // document on average): the next head's loads overlap this head's tail
+    // (only with >= 6 waves of CTAs left: Tl/128 bounds the KV tiles from below)
+    const int hpc = (Hkv % g_bwd_hpc_short == 0 && (long long)Tl < (long long)WLB_HPC_ROWS * (n_docs > 0 ? n_docs : 1) &&
+                     (long long)(Tl / 128) * Hkv >= 6LL * 148 * g_bwd_hpc_short)
+                        ? g_bwd_hpc_short : 1;
+    const int n_units = max_items * ((Hkv + hpc - 1) / hpc);
+    attn_bwd_kernel<D, 2><<<(unsigned)n_units, C::THREADS, C::SMEM, stream>>>(
+        tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
+        Hkv, max_items, hpc, n_units, w.sched, 0, scale, scale * 1.4426950408889634f, dkv_bf16);
+  }
   WLB_LAUNCH_CHECK();
   }
   const long long n4 = (long long)Tl * Hq * D / 4;
@@ -1412,6 +1533,12 @@ extern "C" int wlb_debug_bwd_trace(void* host) {
 extern "C" int32_t wlb_attn_bwd_pairs(int32_t on) {
   const int32_t prev = wlb::g_bwd_pairs;
   wlb::g_bwd_pairs = on < 0 ? WLB_BWD_PAIRS : (on != 0);
+  return prev;
+}
+
+extern "C" int32_t wlb_attn_bwd_persistent(int32_t on) {
+  const int32_t prev = wlb::g_bwd_persistent;
+  wlb::g_bwd_persistent = on < 0 ? WLB_BWD_PERSIST : (on != 0);
   return prev;
 }
 

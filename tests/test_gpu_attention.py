@@ -13,7 +13,8 @@ import torch
 
 import paper_2503_17924_b200 as wl
 from paper_2503_17924_b200.attention import (attn_backward, attn_forward, build_tiles,
-                                             set_bwd_pairs, set_bwd_v3_min_rows)
+                                             set_bwd_pairs, set_bwd_persistent,
+                                             set_bwd_v3_min_rows)
 from oracle import attention_oracle as ao
 from oracle import shard_oracle as so
 
@@ -112,13 +113,15 @@ def test_bwd_cp_ranks(policy):
 
 # D = 128 backward kernels: v3 (128-query tiles) is chosen for long row-sets;
 # force each one on the same cases.
-@pytest.fixture(params=["v2", "v3", "v3pair"])
+@pytest.fixture(params=["v2", "v2-per-unit", "v3", "v3pair"])
 def bwd_variant(request):
-    prev = set_bwd_v3_min_rows(1 << 30 if request.param == "v2" else 0)
+    prev = set_bwd_v3_min_rows(1 << 30 if request.param.startswith("v2") else 0)
     prev_p = set_bwd_pairs(1 if request.param == "v3pair" else 0)
+    prev_s = set_bwd_persistent(0 if request.param == "v2-per-unit" else 1)
     yield request.param
     set_bwd_v3_min_rows(prev)
     set_bwd_pairs(prev_p)
+    set_bwd_persistent(prev_s)
 
 
 @pytest.mark.parametrize("case", ["single", "multi", "gqa", "cp_doc", "cp_seq", "ragged"])
