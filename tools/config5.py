@@ -20,8 +20,11 @@ def main():
     ap.add_argument("--sample", type=int, default=6)
     ap.add_argument("--cp", type=int, default=8)
     ap.add_argument("--policy", default="measured", choices=["measured", "adaptive"])
+    ap.add_argument("--bwd-persistent", type=int, default=-1)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
+    from paper_2503_17924_b200.attention import set_bwd_persistent
+    set_bwd_persistent(a.bwd_persistent)
     dev = torch.device("cuda")
     prof = wl.CostProfile()
     spec = wl.SyntheticSpec(context_window=131072, tokens_per_global_batch=64 * 131072)
