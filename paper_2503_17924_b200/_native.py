@@ -15,8 +15,8 @@ import os
 from .errors import NativeError
 
 # WLB_LIB_PATH selects an alternative build of the SAME library (A/B experiments).
-LIB_PATH = os.environ.get("WLB_LIB_PATH",
-                          os.path.join(os.path.dirname(os.path.abspath(__file__)), "libwlbcp.so"))
+_DEFAULT_LIB = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libwlbcp.so")
+LIB_PATH = os.environ.get("WLB_LIB_PATH", _DEFAULT_LIB)
 
 WLB_OK, WLB_EINVAL, WLB_ENODEV, WLB_ECUDA = 0, 22, 19, 1000
 WLB_BWD_DKV_BF16 = 1
@@ -70,6 +70,8 @@ def lib():
             raise NativeError(f"{LIB_PATH} is missing: run `python -m paper_2503_17924_b200.build`")
         handle = C.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
+            if not hasattr(handle, name) and LIB_PATH != _DEFAULT_LIB:
+                continue      # an older build under WLB_LIB_PATH (A/B runs)
             fn = getattr(handle, name)
             fn.restype, fn.argtypes = res, args
         _lib = handle

@@ -158,8 +158,8 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 float* __restrict__ dq_acc, void* __restrict__ dk, void* __restrict__ dv,
                 const int4* __restrict__ kv_tiles, const int* __restrict__ n_kv_tiles,
                 const int* __restrict__ positions, int Tl, int Hq, int Hkv, int n_slots, int hpc,
-                int n_units, int* __restrict__ sched, int persistent, float scale,
-                float scale_log2, int dkv_bf16) {
+                int n_units, int* __restrict__ sched, int persistent, int g_begin, int g_end,
+                float scale, float scale_log2, int dkv_bf16) {
   using C = BwdCfg<D, NCW>;
   extern __shared__ uint8_t smem_raw[];
   if (smem_u32(smem_raw) & 1023) __trap();   // SW128 tiles need 1024-B alignment
@@ -219,8 +219,8 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     const int item = u % n_slots;
     U.kt = kv_tiles[2 * item];
     U.k0 = kv_tiles[2 * item + 1].x;   // in-document position of key 0 of the tile
-    U.g0 = (u / n_slots) * hpc;
-    U.nh = min(hpc, Hkv - U.g0);
+    U.g0 = g_begin + (u / n_slots) * hpc;   // KV heads [g_begin, g_end) of this launch
+    U.nh = min(hpc, g_end - U.g0);
     U.qt_per_head = (U.kt.w - U.kt.z + C::BM - 1) / C::BM;
     U.n_iter = U.qt_per_head * group;  // query tiles per KV head
     U.n_all = U.n_iter * U.nh;
@@ -732,7 +732,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                  float* __restrict__ dq_acc, void* __restrict__ dk, void* __restrict__ dv,
                  const int4* __restrict__ kv_tiles, const int* __restrict__ n_kv_tiles,
                  const int* __restrict__ positions, int Tl, int Hq, int Hkv, int n_slots,
-                 float scale, float scale_log2, int dkv_bf16) {
+                 int g_begin, float scale, float scale_log2, int dkv_bf16) {
   using C = Bwd3Cfg;
   constexpr int D = C::D;
   extern __shared__ uint8_t smem_raw[];
@@ -744,7 +744,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
   // for a lone last tile); each CTA reduces half of the pair's summed dQ.
   const int cta = PAIR ? (int)cluster_ctarank() : 0;
   const int slot = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int item = slot % n_slots, g = slot / n_slots;
+  const int item = slot % n_slots, g = g_begin + slot / n_slots;
   if (item >= n_kv_tiles[0]) return;
   int4 kt = kv_tiles[2 * item];
   int k0 = kv_tiles[2 * item + 1].x;
@@ -1179,10 +1179,11 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 template <int D>
 __global__ void __launch_bounds__(256) bwd_delta_kernel(const __nv_bfloat16* __restrict__ o,
                                                         const __nv_bfloat16* __restrict__ dout,
-                                                        float* __restrict__ delta, int Tl, int Hq) {
+                                                        float* __restrict__ delta, int Tl, int Hq,
+                                                        int h_begin, int h_count) {
   constexpr int LPR = D / 8;                 // lanes per (row, head)
   constexpr int U = 4;                       // pairs in flight per thread
-  const long long n = (long long)Tl * Hq;
+  const long long n = (long long)Tl * h_count;   // (row, head) pairs, heads [h_begin, +h_count)
   const int sub = threadIdx.x % LPR;
   const long long lanes = (long long)gridDim.x * blockDim.x / LPR;
   for (long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / LPR; w0 < n;
@@ -1192,8 +1193,9 @@ __global__ void __launch_bounds__(256) bwd_delta_kernel(const __nv_bfloat16* __r
     for (int u = 0; u < U; ++u) {
       const long long w = w0 + u * lanes;
       if (w < n) {
-        a[u] = reinterpret_cast<const uint4*>(o + w * D)[sub];
-        b[u] = reinterpret_cast<const uint4*>(dout + w * D)[sub];
+        const long long rh = (w / h_count) * Hq + h_begin + w % h_count;
+        a[u] = reinterpret_cast<const uint4*>(o + rh * D)[sub];
+        b[u] = reinterpret_cast<const uint4*>(dout + rh * D)[sub];
       } else {
         a[u] = b[u] = make_uint4(0, 0, 0, 0);
       }
@@ -1211,33 +1213,40 @@ __global__ void __launch_bounds__(256) bwd_delta_kernel(const __nv_bfloat16* __r
 #pragma unroll
       for (int off = LPR / 2; off; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
       const long long w = w0 + u * lanes;
-      if (sub == 0 && w < n) delta[(size_t)(w % Hq) * Tl + (w / Hq)] = sum;
+      if (sub == 0 && w < n) delta[(size_t)(h_begin + w % h_count) * Tl + (w / h_count)] = sum;
     }
   }
 }
 
-// v3 dQ accumulator [Hq][D/4][Tl][4] fp32 -> dq [Tl][Hq][D] bf16
+// v3 dQ accumulator [Hq][D/4][Tl][4] fp32 -> dq [Tl][Hq][D] bf16, heads
+// [h_begin, h_begin + h_count)
 __global__ void dq_convert3_kernel(const float4* __restrict__ acc, uint2* __restrict__ dq, int Tl,
-                                   int Hq, int D) {
-  const long long n = (long long)Tl * Hq * (D / 4);
+                                   int Hq, int D, int h_begin, int h_count) {
+  const long long n = (long long)Tl * h_count * (D / 4);
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     const int db = (int)(i % (D / 4));           // output-ordered: consecutive threads write
     const long long rh = i / (D / 4);            // consecutive 8-B pieces of a row
-    const int h = (int)(rh % Hq), row = (int)(rh / Hq);
+    const int h = h_begin + (int)(rh % h_count), row = (int)(rh / h_count);
     const float4 v = acc[((long long)h * (D / 4) + db) * Tl + row];
     __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
-    dq[i] = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+    dq[((long long)row * Hq + h) * (D / 4) + db] =
+        make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
   }
 }
 
+// v2 dQ accumulator [Tl][Hq][D] fp32 -> dq bf16, heads [h_begin, h_begin + h_count)
 __global__ void dq_convert_kernel(const float4* __restrict__ acc, __nv_bfloat162* __restrict__ dq,
-                                  long long n4) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+                                  int Tl, int Hq, int D, int h_begin, int h_count) {
+  const long long n = (long long)Tl * h_count * (D / 4);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
-    float4 v = acc[i];
-    dq[2 * i] = __floats2bfloat162_rn(v.x, v.y);
-    dq[2 * i + 1] = __floats2bfloat162_rn(v.z, v.w);
+    const int db = (int)(i % (D / 4));
+    const long long rh = i / (D / 4);
+    const long long j = ((rh / h_count) * Hq + h_begin + rh % h_count) * (D / 4) + db;
+    const float4 v = acc[j];
+    dq[2 * j] = __floats2bfloat162_rn(v.x, v.y);
+    dq[2 * j + 1] = __floats2bfloat162_rn(v.z, v.w);
   }
 }
 
@@ -1365,7 +1374,8 @@ __global__ void zero_uncovered_kernel(const int* __restrict__ rowset_off,
                                       const int* __restrict__ positions,
                                       const int* __restrict__ doc_start, int n_docs,
                                       uint4* __restrict__ dk, uint4* __restrict__ dv,
-                                      int row_f4) {   // row length in 16-B units
+                                      int row_f4,     // row length in 16-B units
+                                      int col_f4, int ncol_f4) {   // the KV heads' columns
   const int a0 = blockIdx.x * kZeroRows, a1 = min(a0 + kZeroRows, doc_start[n_docs]);
   int lo = 0, hi = n_docs;                   // last document with doc_start <= a0
   while (hi - lo > 1) {
@@ -1380,10 +1390,11 @@ __global__ void zero_uncovered_kernel(const int* __restrict__ rowset_off,
     const int covered = r1 > r0 ? min(len, (positions[r1 - 1] + 128) / 128 * 128) : 0;
     const int z0 = max(a0, doc_start[p] + covered), z1 = min(a1, doc_start[p + 1]);
     if (z0 >= z1) continue;
-    const long long base = (long long)z0 * row_f4, n = (long long)(z1 - z0) * row_f4;
+    const long long n = (long long)(z1 - z0) * ncol_f4;
     for (long long i = threadIdx.x; i < n; i += blockDim.x) {
-      dk[base + i] = z;
-      dv[base + i] = z;
+      const long long e = (long long)(z0 + i / ncol_f4) * row_f4 + col_f4 + i % ncol_f4;
+      dk[e] = z;
+      dv[e] = z;
     }
   }
 }
@@ -1421,33 +1432,43 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
                       const float* lse, void* dq, void* dk, void* dv, const int32_t* rowset_off,
                       const int32_t* doc_start, int32_t n_docs, const int32_t* positions,
                       int32_t Tl, int32_t T, int32_t Hq, int32_t Hkv, float scale, void* ws,
-                      int dkv_bf16, bool covered_only, cudaStream_t stream) {
+                      int dkv_bf16, bool covered_only, int g_begin, int g_count,
+                      cudaStream_t stream) {
   using C = BwdCfg<D>;
   BwdWorkspace w = carve(ws, Tl, T, Hq, D, n_docs);
   const int max_items = T / 128 + n_docs + 1;
-  WLB_CUDA_TRY(cudaMemsetAsync(w.dq_acc, 0, (size_t)Tl * Hq * D * 4, stream));
-  // dK/dV rows of every KV tile are stored whole by the kernel; only the keys
-  // no KV tile covers (past a document's last local query position) are zeroed
-  // here, instead of clearing 2 x T x Hkv x D x 4 bytes up front.
-  if (n_docs > 0 && !covered_only) {
-    zero_uncovered_kernel<<<(unsigned)((T + kZeroRows - 1) / kZeroRows), 256, 0, stream>>>(
-        rowset_off, positions, doc_start, n_docs, (uint4*)dk, (uint4*)dv,
-        Hkv * D * (dkv_bf16 ? 2 : 4) / 16);
-    WLB_LAUNCH_CHECK();
-  }
-  {
-    const long long lanes = (long long)Tl * Hq * (D / 8);
-    const unsigned blocks = (unsigned)std::min<long long>((lanes + 255) / 256, 148 * 8);
-    bwd_delta_kernel<D><<<blocks, 256, 0, stream>>>(
-        (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, w.delta, Tl, Hq);
-    WLB_LAUNCH_CHECK();
-  }
+  const int group = Hq / Hkv, h_begin = g_begin * group, h_count = g_count * group;
 #if WLB_BWD_V3
   const bool v3 = D == 128 && (long long)Tl >= (long long)g_bwd_v3_min_rows * (n_docs > 0 ? n_docs : 1);
   const bool pairs = v3 && g_bwd_pairs;
 #else
-  const bool pairs = false;
+  const bool v3 = false, pairs = false;
 #endif
+  // dQ accumulator of this launch's query heads: [Hq][D/4][Tl][4] (v3) keeps
+  // a head contiguous, [Tl][Hq][D] (v2) strides it
+  if (v3)
+    WLB_CUDA_TRY(cudaMemsetAsync(w.dq_acc + (size_t)h_begin * D * Tl, 0,
+                                 (size_t)Tl * h_count * D * 4, stream));
+  else
+    WLB_CUDA_TRY(cudaMemset2DAsync(w.dq_acc + (size_t)h_begin * D, (size_t)Hq * D * 4, 0,
+                                   (size_t)h_count * D * 4, (size_t)Tl, stream));
+  // dK/dV rows of every KV tile are stored whole by the kernel; only the keys
+  // no KV tile covers (past a document's last local query position) are zeroed
+  // here, instead of clearing 2 x T x Hkv x D x 4 bytes up front.
+  if (n_docs > 0 && !covered_only) {
+    const int hf4 = D * (dkv_bf16 ? 2 : 4) / 16;    // one KV head's columns in 16-B units
+    zero_uncovered_kernel<<<(unsigned)((T + kZeroRows - 1) / kZeroRows), 256, 0, stream>>>(
+        rowset_off, positions, doc_start, n_docs, (uint4*)dk, (uint4*)dv, Hkv * hf4,
+        g_begin * hf4, g_count * hf4);
+    WLB_LAUNCH_CHECK();
+  }
+  {
+    const long long lanes = (long long)Tl * h_count * (D / 8);
+    const unsigned blocks = (unsigned)std::min<long long>((lanes + 255) / 256, 148 * 8);
+    bwd_delta_kernel<D><<<blocks, 256, 0, stream>>>(
+        (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, w.delta, Tl, Hq, h_begin, h_count);
+    WLB_LAUNCH_CHECK();
+  }
   bwd_kv_tiles_kernel<<<1, kKvThreads, 0, stream>>>(n_docs, rowset_off, positions, doc_start,
                                                      max_items, w.kv_tiles, w.n_kv,
                                                      w.kv_tiles + 2 * max_items, pairs ? 1 : 0);
@@ -1467,7 +1488,7 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
     if (pairs) {
       // 2-CTA clusters: one pair of KV tiles per cluster
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)(2 * max_items * Hkv));
+      cfg.gridDim = dim3((unsigned)(2 * max_items * g_count));
       cfg.blockDim = dim3(C3::THREADS);
       cfg.dynamicSmemBytes = C3::SMEM;
       cfg.stream = stream;
@@ -1481,11 +1502,11 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
       WLB_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn_bwd3_kernel<true>, tq, tk, tv, tdo, lse,
                                       (const float*)w.delta, w.dq_acc, dk, dv,
                                       (const int4*)w.kv_tiles, (const int*)w.n_kv, positions, Tl,
-                                      Hq, Hkv, max_items, scale, sl2, dkv_bf16));
+                                      Hq, Hkv, max_items, g_begin, scale, sl2, dkv_bf16));
     } else {
-      attn_bwd3_kernel<false><<<(unsigned)max_items * Hkv, C3::THREADS, C3::SMEM, stream>>>(
+      attn_bwd3_kernel<false><<<(unsigned)max_items * g_count, C3::THREADS, C3::SMEM, stream>>>(
           tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
-          Hkv, max_items, scale, sl2, dkv_bf16);
+          Hkv, max_items, g_begin, scale, sl2, dkv_bf16);
     }
     WLB_LAUNCH_CHECK();
   } else
@@ -1506,36 +1527,37 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
     int dev = 0, sms = 148;
     WLB_CUDA_TRY(cudaGetDevice(&dev));
     WLB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int n_units = max_items * Hkv;
+    const int n_units = max_items * g_count;
     WLB_CUDA_TRY(cudaMemsetAsync(w.sched, 0, sizeof(int), stream));
     attn_bwd_kernel<D, 2><<<(unsigned)std::min(n_units, sms), C::THREADS, C::SMEM, stream>>>(
         tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
-        Hkv, max_items, 1, n_units, w.sched, 1, scale, scale * 1.4426950408889634f, dkv_bf16);
+        Hkv, max_items, 1, n_units, w.sched, 1, g_begin, g_begin + g_count, scale,
+        scale * 1.4426950408889634f, dkv_bf16);
   } else {
     // several KV heads per CTA for short row-sets (< 2048 local rows per
     // document on average): the next head's loads overlap this head's tail
     // (only with >= 6 waves of CTAs left: Tl/128 bounds the KV tiles from below)
-    const int hpc = (Hkv % g_bwd_hpc_short == 0 && (long long)Tl < (long long)WLB_HPC_ROWS * (n_docs > 0 ? n_docs : 1) &&
-                     (long long)(Tl / 128) * Hkv >= 6LL * 148 * g_bwd_hpc_short)
+    const int hpc = (g_count % g_bwd_hpc_short == 0 && (long long)Tl < (long long)WLB_HPC_ROWS * (n_docs > 0 ? n_docs : 1) &&
+                     (long long)(Tl / 128) * g_count >= 6LL * 148 * g_bwd_hpc_short)
                         ? g_bwd_hpc_short : 1;
-    const int n_units = max_items * ((Hkv + hpc - 1) / hpc);
+    const int n_units = max_items * ((g_count + hpc - 1) / hpc);
     attn_bwd_kernel<D, 2><<<(unsigned)n_units, C::THREADS, C::SMEM, stream>>>(
         tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
-        Hkv, max_items, hpc, n_units, w.sched, 0, scale, scale * 1.4426950408889634f, dkv_bf16);
+        Hkv, max_items, hpc, n_units, w.sched, 0, g_begin, g_begin + g_count, scale,
+        scale * 1.4426950408889634f, dkv_bf16);
   }
   WLB_LAUNCH_CHECK();
   }
-  const long long n4 = (long long)Tl * Hq * D / 4;
-#if WLB_BWD_V3
+  const long long n4 = (long long)Tl * h_count * D / 4;
+  const unsigned cblocks = (unsigned)std::min<long long>((n4 + 255) / 256, 148 * 16);
   if (v3) {
-    dq_convert3_kernel<<<(unsigned)std::min<long long>((n4 + 255) / 256, 148 * 16), 256, 0, stream>>>(
-        (const float4*)w.dq_acc, (uint2*)dq, Tl, Hq, D);
+    dq_convert3_kernel<<<cblocks, 256, 0, stream>>>((const float4*)w.dq_acc, (uint2*)dq, Tl, Hq, D,
+                                                     h_begin, h_count);
     WLB_LAUNCH_CHECK();
     return WLB_OK;
   }
-#endif
-  dq_convert_kernel<<<(unsigned)std::min<long long>((n4 + 255) / 256, 148 * 16), 256, 0, stream>>>(
-      (const float4*)w.dq_acc, (__nv_bfloat162*)dq, n4);
+  dq_convert_kernel<<<cblocks, 256, 0, stream>>>((const float4*)w.dq_acc, (__nv_bfloat162*)dq, Tl,
+                                                 Hq, D, h_begin, h_count);
   WLB_LAUNCH_CHECK();
   return WLB_OK;
 }
@@ -1577,24 +1599,41 @@ extern "C" size_t wlb_attn_bwd_workspace(int32_t Tl, int32_t T, int32_t Hq, int3
   return wlb::carve(nullptr, Tl, T, Hq, D, n_docs).bytes;
 }
 
+extern "C" int wlb_attn_bwd_heads(const void* q, const void* k, const void* v, const void* o,
+                                  const void* do_, const float* lse, void* dq, void* dk, void* dv,
+                                  const int32_t* rowset_off, const int32_t* doc_start,
+                                  int32_t n_docs, const int32_t* positions, int32_t Tl, int32_t T,
+                                  int32_t Hq, int32_t Hkv, int32_t D, float scale, void* ws,
+                                  int32_t flags, int32_t kv_head_begin, int32_t kv_head_count,
+                                  void* stream) {
+  WLB_REQUIRE(D == 64 || D == 128, "head dim %d unsupported (64 or 128)", D);
+  WLB_REQUIRE(Hq > 0 && Hkv > 0 && Hq % Hkv == 0, "Hq must be a multiple of Hkv");
+  WLB_REQUIRE(Tl >= 0 && T > 0 && n_docs >= 0 && ws != nullptr, "bad sizes");
+  WLB_REQUIRE((flags & ~(WLB_BWD_DKV_BF16 | WLB_BWD_COVERED_ONLY)) == 0,
+              "unknown backward flags 0x%x", flags);
+  WLB_REQUIRE(kv_head_begin >= 0 && kv_head_count >= 0 && kv_head_begin + kv_head_count <= Hkv,
+              "KV head range [%d, %d) outside [0, %d)", kv_head_begin,
+              kv_head_begin + kv_head_count, Hkv);
+  if (kv_head_count == 0) return WLB_OK;
+  const int bf = (flags & WLB_BWD_DKV_BF16) != 0;
+  const bool cov = (flags & WLB_BWD_COVERED_ONLY) != 0;
+  if (D == 64)
+    return wlb::launch_bwd<64>(q, k, v, o, do_, lse, dq, dk, dv, rowset_off, doc_start, n_docs,
+                               positions, Tl, T, Hq, Hkv, scale, ws, bf, cov, kv_head_begin,
+                               kv_head_count, (cudaStream_t)stream);
+  return wlb::launch_bwd<128>(q, k, v, o, do_, lse, dq, dk, dv, rowset_off, doc_start, n_docs,
+                              positions, Tl, T, Hq, Hkv, scale, ws, bf, cov, kv_head_begin,
+                              kv_head_count, (cudaStream_t)stream);
+}
+
 extern "C" int wlb_attn_bwd_ex(const void* q, const void* k, const void* v, const void* o,
                                const void* do_, const float* lse, void* dq, void* dk, void* dv,
                                const int32_t* rowset_off, const int32_t* doc_start, int32_t n_docs,
                                const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq,
                                int32_t Hkv, int32_t D, float scale, void* ws, int32_t flags,
                                void* stream) {
-  WLB_REQUIRE(D == 64 || D == 128, "head dim %d unsupported (64 or 128)", D);
-  WLB_REQUIRE(Hq > 0 && Hkv > 0 && Hq % Hkv == 0, "Hq must be a multiple of Hkv");
-  WLB_REQUIRE(Tl >= 0 && T > 0 && n_docs >= 0 && ws != nullptr, "bad sizes");
-  WLB_REQUIRE((flags & ~(WLB_BWD_DKV_BF16 | WLB_BWD_COVERED_ONLY)) == 0,
-              "unknown backward flags 0x%x", flags);
-  const int bf = (flags & WLB_BWD_DKV_BF16) != 0;
-  const bool cov = (flags & WLB_BWD_COVERED_ONLY) != 0;
-  if (D == 64)
-    return wlb::launch_bwd<64>(q, k, v, o, do_, lse, dq, dk, dv, rowset_off, doc_start, n_docs,
-                               positions, Tl, T, Hq, Hkv, scale, ws, bf, cov, (cudaStream_t)stream);
-  return wlb::launch_bwd<128>(q, k, v, o, do_, lse, dq, dk, dv, rowset_off, doc_start, n_docs,
-                              positions, Tl, T, Hq, Hkv, scale, ws, bf, cov, (cudaStream_t)stream);
+  return wlb_attn_bwd_heads(q, k, v, o, do_, lse, dq, dk, dv, rowset_off, doc_start, n_docs,
+                            positions, Tl, T, Hq, Hkv, D, scale, ws, flags, 0, Hkv, stream);
 }
 
 extern "C" int wlb_attn_bwd(const void* q, const void* k, const void* v, const void* o,

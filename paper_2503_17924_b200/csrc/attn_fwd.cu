@@ -100,7 +100,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ out,
                 float* __restrict__ lse, const int4* __restrict__ items,
                 const int* __restrict__ n_items, const int* __restrict__ positions, int Tl,
-                int Hq, int Hkv, int n_slots, int hpc, float scale_log2) {
+                int Hq, int Hkv, int n_slots, int hpc, int h_begin, int h_end, float scale_log2) {
   using C = FwdCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -108,9 +108,11 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
   // A CTA runs heads [h0, h0 + nh) of its tile pair back to back (hpc > 1 for
   // short row-sets): the next head's Q and K/V loads and its first QK overlap
   // this head's last PV and epilogue instead of a CTA teardown + launch.
-  const int item = blockIdx.x % n_slots, h0 = (blockIdx.x / n_slots) * hpc;
+  // Query heads [h_begin, h_end) of the launch (all heads, or one head group
+  // of the CP exchange's head-group pipeline).
+  const int item = blockIdx.x % n_slots, h0 = h_begin + (blockIdx.x / n_slots) * hpc;
   if (item >= n_items[0]) return;
-  const int nh = min(hpc, Hq - h0);
+  const int nh = min(hpc, h_end - h0);
   const int4 tx = items[2 * item], ty = items[2 * item + 1];
   // tile 0 = X {row0, nrows, kv_end}, tile 1 = Y
   const int kv_begin = tx.z;
@@ -420,7 +422,7 @@ template <int D>
 static int launch_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
                       const int32_t* tiles, const int32_t* n_tiles, int32_t max_tiles,
                       const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq, int32_t Hkv,
-                      float scale, cudaStream_t stream) {
+                      int32_t h_begin, int32_t h_count, float scale, cudaStream_t stream) {
   using C = FwdCfg<D>;
   CUtensorMap tq, tk, tv;
   int rc;
@@ -435,12 +437,13 @@ static int launch_fwd(const void* q, const void* k, const void* v, void* o, floa
   // Only when that still leaves >= 6 waves of CTAs (a small rank's few tiles
   // need the parallelism more: config-5 ranks of ~4K rows lost 10% with it).
   const long long docs = std::max<long long>(1, (long long)max_tiles - Tl / (2 * C::BM) - 1);
-  const int hpc = (Hq % g_fwd_hpc_short == 0 && (long long)Tl < (long long)WLB_HPC_ROWS * docs &&
-                   (long long)max_tiles * Hq >= 6LL * 148 * g_fwd_hpc_short)
+  const int hpc = (h_count % g_fwd_hpc_short == 0 && (long long)Tl < (long long)WLB_HPC_ROWS * docs &&
+                   (long long)max_tiles * h_count >= 6LL * 148 * g_fwd_hpc_short)
                       ? g_fwd_hpc_short : 1;
-  attn_fwd_kernel<D><<<(unsigned)max_tiles * ((Hq + hpc - 1) / hpc), C::THREADS, C::SMEM, stream>>>(
+  attn_fwd_kernel<D><<<(unsigned)max_tiles * ((h_count + hpc - 1) / hpc), C::THREADS, C::SMEM,
+                       stream>>>(
       tq, tk, tv, (__nv_bfloat16*)o, lse, (const int4*)tiles, n_tiles, positions, Tl, Hq, Hkv,
-      max_tiles, hpc, scale_log2);
+      max_tiles, hpc, h_begin, h_begin + h_count, scale_log2);
   WLB_LAUNCH_CHECK();
   return WLB_OK;
 }
@@ -454,17 +457,31 @@ extern "C" int wlb_debug_fwd_trace(void* host) {
 }
 #endif
 
+extern "C" int wlb_attn_fwd_heads(const void* q, const void* k, const void* v, void* o, float* lse,
+                                  const int32_t* tiles, const int32_t* n_tiles, int32_t max_tiles,
+                                  const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq,
+                                  int32_t Hkv, int32_t D, float scale, int32_t kv_head_begin,
+                                  int32_t kv_head_count, void* stream) {
+  WLB_REQUIRE(D == 64 || D == 128, "head dim %d unsupported (64 or 128)", D);
+  WLB_REQUIRE(Hq > 0 && Hkv > 0 && Hq % Hkv == 0, "Hq must be a multiple of Hkv");
+  WLB_REQUIRE(Tl >= 0 && T > 0 && max_tiles >= 0, "bad sizes");
+  WLB_REQUIRE(kv_head_begin >= 0 && kv_head_count >= 0 && kv_head_begin + kv_head_count <= Hkv,
+              "KV head range [%d, %d) outside [0, %d)", kv_head_begin,
+              kv_head_begin + kv_head_count, Hkv);
+  if (Tl == 0 || max_tiles == 0 || kv_head_count == 0) return WLB_OK;
+  const int g = Hq / Hkv;
+  if (D == 64)
+    return wlb::launch_fwd<64>(q, k, v, o, lse, tiles, n_tiles, max_tiles, positions, Tl, T, Hq,
+                               Hkv, kv_head_begin * g, kv_head_count * g, scale,
+                               (cudaStream_t)stream);
+  return wlb::launch_fwd<128>(q, k, v, o, lse, tiles, n_tiles, max_tiles, positions, Tl, T, Hq,
+                              Hkv, kv_head_begin * g, kv_head_count * g, scale, (cudaStream_t)stream);
+}
+
 extern "C" int wlb_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
                             const int32_t* tiles, const int32_t* n_tiles, int32_t max_tiles,
                             const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq,
                             int32_t Hkv, int32_t D, float scale, void* stream) {
-  WLB_REQUIRE(D == 64 || D == 128, "head dim %d unsupported (64 or 128)", D);
-  WLB_REQUIRE(Hq > 0 && Hkv > 0 && Hq % Hkv == 0, "Hq must be a multiple of Hkv");
-  WLB_REQUIRE(Tl >= 0 && T > 0 && max_tiles >= 0, "bad sizes");
-  if (Tl == 0 || max_tiles == 0) return WLB_OK;
-  if (D == 64)
-    return wlb::launch_fwd<64>(q, k, v, o, lse, tiles, n_tiles, max_tiles, positions, Tl, T, Hq,
-                               Hkv, scale, (cudaStream_t)stream);
-  return wlb::launch_fwd<128>(q, k, v, o, lse, tiles, n_tiles, max_tiles, positions, Tl, T, Hq,
-                              Hkv, scale, (cudaStream_t)stream);
+  return wlb_attn_fwd_heads(q, k, v, o, lse, tiles, n_tiles, max_tiles, positions, Tl, T, Hq, Hkv,
+                            D, scale, 0, Hkv, stream);
 }

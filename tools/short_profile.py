@@ -47,7 +47,8 @@ def main():
     ap.add_argument("--bwd-persistent", type=int, default=-1)
     a = ap.parse_args()
     from paper_2503_17924_b200.attention import set_bwd_persistent
-    set_bwd_persistent(a.bwd_persistent)
+    if a.bwd_persistent >= 0:
+        set_bwd_persistent(a.bwd_persistent)
     dev = torch.device("cuda")
     prof = wl.CostProfile()
     spec = wl.SyntheticSpec(context_window=131072, tokens_per_global_batch=64 * 131072)
