@@ -127,6 +127,15 @@ int wlb_attn_fwd(const void* q, const void* k, const void* v, void* o, float* ls
                  const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq,
                  int32_t Hkv, int32_t D, float scale, void* stream);
 
+/* wlb_attn_fwd restricted to KV heads [kv_head_begin, +kv_head_count) and
+ * their query heads (the CP exchange's head-group pipeline: attention on a
+ * head group starts as soon as that group's K/V rows have landed). */
+int wlb_attn_fwd_heads(const void* q, const void* k, const void* v, void* o, float* lse,
+                       const int32_t* tiles, const int32_t* n_tiles, int32_t max_tiles,
+                       const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq, int32_t Hkv,
+                       int32_t D, float scale, int32_t kv_head_begin, int32_t kv_head_count,
+                       void* stream);
+
 /* Backward.  do_[Tl][Hq][D] bf16, o and lse from the forward.  Writes
  * dq[Tl][Hq][D] bf16 and dK/dV partials over the full document-ordered
  * sequence, dk/dv[T][Hkv][D] fp32 (summed over ranks by the CP
@@ -155,6 +164,15 @@ int wlb_attn_bwd_ex(const void* q, const void* k, const void* v, const void* o,
                     const int32_t* rowset_off, const int32_t* doc_start, int32_t n_docs,
                     const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq,
                     int32_t Hkv, int32_t D, float scale, void* ws, int32_t flags, void* stream);
+/* wlb_attn_bwd_ex restricted to KV heads [kv_head_begin, +kv_head_count)
+ * (dQ of their query heads, dK/dV partial columns of those KV heads).
+ * Successive calls over disjoint head ranges may share one workspace. */
+int wlb_attn_bwd_heads(const void* q, const void* k, const void* v, const void* o,
+                       const void* do_, const float* lse, void* dq, void* dk, void* dv,
+                       const int32_t* rowset_off, const int32_t* doc_start, int32_t n_docs,
+                       const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq, int32_t Hkv,
+                       int32_t D, float scale, void* ws, int32_t flags, int32_t kv_head_begin,
+                       int32_t kv_head_count, void* stream);
 /* Backward kernel selection for D = 128: the 128-query-tile kernel (v3) runs
  * when Tl >= v3_min_rows * n_docs, else the 64-query kernel (v2).  Negative
  * restores the default (4096); returns the previous threshold.  Process-wide
@@ -230,6 +248,34 @@ int wlb_cp_dkv_pull_cov(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_o
                         const int32_t* rowset_all, int32_t rowset_stride,
                         const int32_t* positions_all, const int32_t* doc_start, int32_t n_docs,
                         void* stream);
+
+/* General forms of the push / pull above: columns [col_off, col_off +
+ * col_bytes) of every row only (a range of KV heads; 16-B aligned), and the
+ * covered variant when rowset_all != NULL (else every rank / every row).
+ * For the pull, row_bytes / col_* count the partial rows (bf16 with
+ * WLB_BWD_DKV_BF16), and dk / dv are fp32 rows of the full head width. */
+int wlb_cp_kv_push_part(const void* k_local, const void* v_local, const int32_t* gather_local,
+                        int64_t n_rows, int64_t row_bytes, int64_t col_off, int64_t col_bytes,
+                        const uint64_t* peer_bases, int64_t k_off, int64_t v_off, int32_t cp,
+                        const int32_t* rowset_all, int32_t rowset_stride,
+                        const int32_t* positions_all, const int32_t* doc_start, int32_t n_docs,
+                        void* stream);
+int wlb_cp_dkv_pull_part(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_off,
+                         const int32_t* gather_local, int64_t n_rows, int64_t row_bytes,
+                         int64_t col_off, int64_t col_bytes, float* dk, float* dv, int32_t cp,
+                         int32_t flags, const int32_t* rowset_all, int32_t rowset_stride,
+                         const int32_t* positions_all, const int32_t* doc_start, int32_t n_docs,
+                         void* stream);
+/* Per-peer arrival flags on symmetric memory (replace whole-slot barriers on
+ * the data path).  wlb_cp_signal: once the work before it on `stream` is
+ * complete, store `value` (system-scope release) at byte offset flag_off of
+ * every rank's flag buffer (flag_bases: device [cp] peer-mapped addresses).
+ * wlb_cp_wait: work after it on `stream` starts once all n int32 flags
+ * (device, this rank's buffer) are >= value (system-scope acquire).  Values
+ * are increasing epochs; a wait longer than 60 s traps. */
+int wlb_cp_signal(const uint64_t* flag_bases, int64_t flag_off, int32_t cp, int32_t value,
+                  void* stream);
+int wlb_cp_wait(const int32_t* flags, int32_t n, int32_t value, void* stream);
 
 #ifdef __cplusplus
 }

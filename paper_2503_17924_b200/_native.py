@@ -38,6 +38,10 @@ SIGNATURES = {
     "wlb_attn_tiles": (C.c_int, [_i32, _p, _p, _p, _i32, _i32, _p, _p, _p]),
     "wlb_attn_fwd": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, _i32, _p, _i32, _i32, _i32, _i32,
                                _i32, _f32, _p]),
+    "wlb_attn_fwd_heads": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, _i32, _p, _i32, _i32, _i32, _i32,
+                                     _i32, _f32, _i32, _i32, _p]),
+    "wlb_attn_bwd_heads": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i32, _p, _i32,
+                                     _i32, _i32, _i32, _i32, _f32, _p, _i32, _i32, _i32, _p]),
     "wlb_attn_bwd_workspace": (_sz, [_i32, _i32, _i32, _i32, _i32, _i32]),
     "wlb_attn_bwd_ex": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i32, _p, _i32,
                                   _i32, _i32, _i32, _i32, _f32, _p, _i32, _p]),
@@ -54,6 +58,12 @@ SIGNATURES = {
     "wlb_cp_dkv_pull_ex": (C.c_int, [_p, _i64, _i64, _p, _i64, _i64, _p, _p, _i32, _i32, _p]),
     "wlb_cp_kv_push_cov": (C.c_int, [_p, _p, _p, _i64, _i64, _p, _i64, _i64, _i32,
                                      _p, _i32, _p, _p, _i32, _p]),
+    "wlb_cp_kv_push_part": (C.c_int, [_p, _p, _p, _i64, _i64, _i64, _i64, _p, _i64, _i64, _i32,
+                                      _p, _i32, _p, _p, _i32, _p]),
+    "wlb_cp_dkv_pull_part": (C.c_int, [_p, _i64, _i64, _p, _i64, _i64, _i64, _i64, _p, _p, _i32,
+                                       _i32, _p, _i32, _p, _p, _i32, _p]),
+    "wlb_cp_signal": (C.c_int, [_p, _i64, _i32, _i32, _p]),
+    "wlb_cp_wait": (C.c_int, [_p, _i32, _i32, _p]),
     "wlb_cp_dkv_pull_cov": (C.c_int, [_p, _i64, _i64, _p, _i64, _i64, _p, _p, _i32, _i32,
                                       _p, _i32, _p, _p, _i32, _p]),
 }

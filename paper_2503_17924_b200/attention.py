@@ -63,34 +63,60 @@ def _check_inputs(q, k, v):
         raise ValueError("shape mismatch between q, k, v")
 
 
-def attn_forward(q, k, v, tiles: AttnTiles, scale: float | None = None):
-    """O [Tl,Hq,D] bf16 and LSE [Hq,Tl] fp32 for one rank's local queries."""
+def attn_forward(q, k, v, tiles: AttnTiles, scale: float | None = None, kv_heads=None,
+                 out=None):
+    """O [Tl,Hq,D] bf16 and LSE [Hq,Tl] fp32 for one rank's local queries.
+
+    kv_heads=(begin, count): only those KV heads and their query heads, into
+    `out` = (o, lse) from an earlier call (the CP head-group pipeline)."""
     _check_inputs(q, k, v)
     tl, hq, d = q.shape
+    hkv = k.shape[1]
     scale = 1.0 / math.sqrt(d) if scale is None else scale
-    o = torch.empty_like(q)
-    lse = torch.empty((hq, tl), dtype=torch.float32, device=q.device)
+    if out is None:
+        o = torch.empty_like(q)
+        lse = torch.empty((hq, tl), dtype=torch.float32, device=q.device)
+    else:
+        o, lse = out
     p = _native.ptr
-    _native.check(_native.lib().wlb_attn_fwd(
+    if kv_heads is None:
+        _native.check(_native.lib().wlb_attn_fwd(
+            p(q), p(k), p(v), p(o), p(lse), p(tiles.tiles), p(tiles.n_tiles), tiles.max_tiles,
+            p(tiles.positions), tl, k.shape[0], hq, hkv, d, scale, _native.stream_ptr()),
+            "wlb_attn_fwd")
+        return o, lse
+    _native.check(_native.lib().wlb_attn_fwd_heads(
         p(q), p(k), p(v), p(o), p(lse), p(tiles.tiles), p(tiles.n_tiles), tiles.max_tiles,
-        p(tiles.positions), tl, k.shape[0], hq, k.shape[1], d, scale, _native.stream_ptr()),
-        "wlb_attn_fwd")
+        p(tiles.positions), tl, k.shape[0], hq, hkv, d, scale, kv_heads[0], kv_heads[1],
+        _native.stream_ptr()), "wlb_attn_fwd_heads")
     return o, lse
 
 
+def bwd_workspace(q, k, tiles: AttnTiles):
+    """Backward workspace for one rank's micro-batch (shareable by the calls of
+    a head-group sequence)."""
+    tl, hq, d = q.shape
+    return torch.empty(_native.lib().wlb_attn_bwd_workspace(tl, k.shape[0], hq, k.shape[1], d,
+                                                            tiles.n_docs),
+                       dtype=torch.uint8, device=q.device)
+
+
 def attn_backward(q, k, v, o, lse, do, tiles: AttnTiles, scale: float | None = None,
-                  dk_out=None, dv_out=None, covered_only: bool = False):
+                  dk_out=None, dv_out=None, covered_only: bool = False, kv_heads=None,
+                  dq_out=None, ws=None):
     """dQ [Tl,Hq,D] bf16 and fp32 dK/dV partials over the full sequence
     (written into dk_out / dv_out when given, e.g. symmetric exchange buffers;
     bf16 dk_out / dv_out take bf16 partials).  covered_only: rows no KV tile
     of this rank covers are left unwritten instead of zeroed (for the covered
-    CP pull, which never reads them)."""
+    CP pull, which never reads them).  kv_heads=(begin, count): only those KV
+    heads (dK/dV columns) and their query heads (dQ), into dq_out / dk_out /
+    dv_out with workspace `ws` shared across the head groups."""
     _check_inputs(q, k, v)
     tl, hq, d = q.shape
     T, hkv = k.shape[0], k.shape[1]
     scale = 1.0 / math.sqrt(d) if scale is None else scale
     do = do.contiguous()
-    dq = torch.empty_like(q)
+    dq = torch.empty_like(q) if dq_out is None else dq_out
     dk = torch.empty((T, hkv, d), dtype=torch.float32, device=q.device) if dk_out is None else dk_out
     dv = torch.empty((T, hkv, d), dtype=torch.float32, device=q.device) if dv_out is None else dv_out
     if dk.dtype != dv.dtype or dk.dtype not in (torch.float32, torch.bfloat16):
@@ -99,14 +125,29 @@ def attn_backward(q, k, v, o, lse, do, tiles: AttnTiles, scale: float | None = N
     if covered_only:
         flags |= _native.WLB_BWD_COVERED_ONLY
     lib = _native.lib()
-    ws = torch.empty(lib.wlb_attn_bwd_workspace(tl, T, hq, hkv, d, tiles.n_docs),
-                     dtype=torch.uint8, device=q.device)
+    ws = bwd_workspace(q, k, tiles) if ws is None else ws
     p = _native.ptr
-    _native.check(lib.wlb_attn_bwd_ex(
-        p(q), p(k), p(v), p(o), p(do), p(lse), p(dq), p(dk), p(dv), p(tiles.rowset_off),
-        p(tiles.doc_start), tiles.n_docs, p(tiles.positions), tl, T, hq, hkv, d, scale, p(ws),
-        flags, _native.stream_ptr()), "wlb_attn_bwd_ex")
+    args = (p(q), p(k), p(v), p(o), p(do), p(lse), p(dq), p(dk), p(dv), p(tiles.rowset_off),
+            p(tiles.doc_start), tiles.n_docs, p(tiles.positions), tl, T, hq, hkv, d, scale,
+            p(ws), flags)
+    if kv_heads is None:
+        _native.check(lib.wlb_attn_bwd_ex(*args, _native.stream_ptr()), "wlb_attn_bwd_ex")
+    else:
+        _native.check(lib.wlb_attn_bwd_heads(*args, kv_heads[0], kv_heads[1],
+                                             _native.stream_ptr()), "wlb_attn_bwd_heads")
     return dq, dk, dv
+
+
+def head_groups(hkv: int, groups: int):
+    """Split KV heads [0, hkv) into `groups` contiguous (begin, count) ranges."""
+    groups = max(1, min(groups, hkv))
+    base, extra = divmod(hkv, groups)
+    out, b = [], 0
+    for i in range(groups):
+        c = base + (1 if i < extra else 0)
+        out.append((b, c))
+        b += c
+    return out
 
 
 def qkv_rope(y, positions, hq: int, hkv: int, d: int, base: float = 10000.0):

@@ -25,7 +25,8 @@ import torch
 import torch.distributed as dist
 
 from . import _native
-from .attention import AttnTiles, attn_backward, attn_forward, build_tiles, qkv_rope
+from .attention import (AttnTiles, attn_backward, attn_forward, build_tiles, bwd_workspace,
+                        head_groups, qkv_rope)
 from .sharding import ShardPlan, build_shard_plan
 from .workload import CostProfile
 
@@ -169,30 +170,44 @@ class NcclExchange:
         return scatter_dkv(dkf, dvf, shard, self.group)
 
 
+MAX_GROUPS = 8          # head groups per micro-batch in the flag layout
+_KV, _DKV = 0, 1         # flag kinds
+
+
 class SymmExchange:
     """CP exchange as ONE-SIDED NVLink traffic on symmetric memory.
 
     Every rank owns `slots` slots (micro-batch b uses slot b % slots) of a
     document-ordered K/V buffer and of fp32 dK/dV partial buffers
     (WLB_XCHG_DKV=bf16: bf16 partials, summed in fp32 by the pull), mapped
-    into every peer.  With more than 2 slots the pipeline pushes K/V
-    slots-1 micro-batches ahead on a stream of its own (3 slots measured
-    slower at N=4: 3748-3758 vs 3785-3791 TFLOP/s; the early pushes added
-    more interference with the attention kernels than the exposure they
-    hid):
+    into every peer, plus a small flag buffer.  With more than 2 slots the
+    pipeline pushes K/V slots-1 micro-batches ahead on a stream of its own
+    (3 slots measured slower at N=4: 3748-3758 vs 3785-3791 TFLOP/s; the early
+    pushes added more interference with the attention kernels than the
+    exposure they hid).
 
-      forward : barrier (slot free everywhere) -> wlb_cp_kv_push stores this
-                rank's rows into every rank's slot at their document positions
-                -> barrier.  The local slot then IS the gathered, un-permuted
-                K/V: no all-gather, no permutation pass.
-      backward: the attention backward writes its full-length partials
-                straight into the local dK/dV slot -> barrier ->
-                wlb_cp_dkv_pull sums every rank's partials for this rank's rows
-                -> barrier (slot reusable; the compute stream waits on it
-                before the backward of the micro-batch `slots` steps later).
+    The K/V heads are split into `groups` head groups (WLB_HEAD_GROUPS,
+    default 4), and the data path is gated by per-peer arrival flags
+    (`wlb_cp_signal` / `wlb_cp_wait`, one int per (slot, kind, group, source
+    rank)), not whole-slot barriers:
+
+      forward : barrier (slot free everywhere) -> per head group g:
+                wlb_cp_kv_push_part stores this rank's rows of g into every
+                covering rank's slot at their document positions -> signal
+                every peer's KV flag of g.  The attention of group g waits
+                (device side) until all peers' KV flags of g are set, so it
+                starts while the later groups are still in flight.  The local
+                slot IS the gathered, un-permuted K/V.
+      backward: the attention backward of group g writes its partials straight
+                into the local dK/dV slot -> signal every peer's DKV flag of
+                g; the pull of g waits for all peers' DKV flags of g and sums
+                this rank's rows while the backward of the later groups runs
+                -> barrier after the last group (slot reusable; the compute
+                stream waits on it before the backward `slots` micro-batches
+                later).
     """
 
-    def __init__(self, group, t_max, hkv, d, device, slots=2):
+    def __init__(self, group, t_max, hkv, d, device, slots=2, groups=None):
         import torch.distributed._symmetric_memory as symm
         self.group = group if group is not None else dist.group.WORLD
         cp = dist.get_world_size(self.group)
@@ -203,8 +218,12 @@ class SymmExchange:
         kv_h = symm.rendezvous(kv, self.group)
         dkv = symm.empty(2 * slots * n, dtype=self._dkv_dtype(), device=device)  # [slot][dK|dV]
         dkv_h = symm.rendezvous(dkv, self.group)
+        flags = symm.empty(slots * 2 * MAX_GROUPS * cp, dtype=torch.int32, device=device)
+        flags.zero_()
+        flags_h = symm.rendezvous(flags, self.group)
         self._setup(cp, t_max, hkv, d, device, slots, kv, dkv, list(kv_h.buffer_ptrs),
-                    list(dkv_h.buffer_ptrs))
+                    list(dkv_h.buffer_ptrs), flags, list(flags_h.buffer_ptrs),
+                    dist.get_rank(self.group), groups)
         self._kv_barrier = lambda: kv_h.barrier(channel=0)
         self._dkv_barrier = lambda: dkv_h.barrier(channel=1)
 
@@ -217,16 +236,22 @@ class SymmExchange:
         # 2.5e-2 on dK, past the 2e-2 + 1e-2|ref| bar (tests/test_gpu_exchange.py).
         return torch.bfloat16 if os.environ.get("WLB_XCHG_DKV", "fp32") == "bf16" else torch.float32
 
-    def _setup(self, cp, t_max, hkv, d, device, slots, kv, dkv, kv_ptrs, dkv_ptrs):
-        self.cp = cp
+    def _setup(self, cp, t_max, hkv, d, device, slots, kv, dkv, kv_ptrs, dkv_ptrs, flags,
+               flag_ptrs, rank, groups):
+        self.cp, self.rank = cp, rank
         self.t_max, self.hkv, self.d = t_max, hkv, d
         self.n = t_max * hkv * d
         self.slots = slots
         self.depth = slots - 1          # K/V pushed this many micro-batches ahead
-        self.kv, self.dkv = kv, dkv
+        self.kv, self.dkv, self.flags = kv, dkv, flags
         self.dkv_bf16 = dkv.dtype == torch.bfloat16
         self.kv_bases = torch.tensor(kv_ptrs, dtype=torch.int64, device=device)
         self.dkv_bases = torch.tensor(dkv_ptrs, dtype=torch.int64, device=device)
+        self.flag_bases = torch.tensor(flag_ptrs, dtype=torch.int64, device=device)
+        groups = int(os.environ.get("WLB_HEAD_GROUPS", 4)) if groups is None else groups
+        self.groups = head_groups(hkv, min(groups, MAX_GROUPS))
+        self.seq = 0                    # micro-batches pushed (flag epochs)
+        self.epoch = [0] * slots        # epoch of the micro-batch in slot s
         self.free = [None] * slots     # event: all ranks finished pulling slot s
         # The covered kernels take a warp-ballot rank mask (cp <= 32); larger
         # groups use the full push / pull, which work for any cp.
@@ -250,27 +275,48 @@ class SymmExchange:
     def _view(self, buf, idx, T):
         return buf[idx * self.n: idx * self.n + T * self.hkv * self.d].view(T, self.hkv, self.d)
 
+    def _flag_off(self, s, kind, gi, src):
+        return (((s * 2 + kind) * MAX_GROUPS + gi) * self.cp + src) * 4
+
+    def _signal(self, s, kind, gi):
+        _native.check(_native.lib().wlb_cp_signal(
+            self.flag_bases.data_ptr(), self._flag_off(s, kind, gi, self.rank), self.cp,
+            self.epoch[s], _native.stream_ptr()), "wlb_cp_signal")
+
+    def _wait(self, s, kind, gi):
+        _native.check(_native.lib().wlb_cp_wait(
+            self.flags.data_ptr() + self._flag_off(s, kind, gi, 0), self.cp, self.epoch[s],
+            _native.stream_ptr()), "wlb_cp_wait")
+
     def gather(self, k, v, shard, b):
+        """Push this rank's K/V rows of micro-batch b, group by group, each
+        followed by a signal to every peer; returns the local slot's
+        document-ordered K / V views (read them only after `wait_kv`)."""
         s, T = b % self.slots, shard.gather_all.numel()
         if T > self.t_max:
             raise ValueError(f"micro-batch of {T} tokens exceeds the exchange capacity {self.t_max}")
-        self._kv_barrier()
+        self.seq += 1
+        self.epoch[s] = self.seq
+        self._kv_barrier()                  # every rank finished reading slot s
         row = self.hkv * self.d * 2
-        if self.push_covered and shard.tiles.n_docs > 0:
-            # store each row only into the ranks whose attention reads it
-            rows, pos = self._tables(shard)
-            _native.check(_native.lib().wlb_cp_kv_push_cov(
+        covered = self.push_covered and shard.tiles.n_docs > 0
+        rows, pos = self._tables(shard) if covered else (None, None)
+        p = _native.ptr
+        for gi, (g0, ng) in enumerate(self.groups):
+            _native.check(_native.lib().wlb_cp_kv_push_part(
                 k.data_ptr(), v.data_ptr(), shard.gather_local.data_ptr(), k.shape[0], row,
-                self.kv_bases.data_ptr(), 2 * s * self.n * 2, (2 * s + 1) * self.n * 2, self.cp,
-                rows.data_ptr(), rows.shape[-1], pos.data_ptr(), shard.tiles.doc_start.data_ptr(),
-                shard.tiles.n_docs, _native.stream_ptr()), "wlb_cp_kv_push_cov")
-        else:
-            _native.check(_native.lib().wlb_cp_kv_push(
-                k.data_ptr(), v.data_ptr(), shard.gather_local.data_ptr(), k.shape[0], row,
-                self.kv_bases.data_ptr(), 2 * s * self.n * 2, (2 * s + 1) * self.n * 2, self.cp,
-                _native.stream_ptr()), "wlb_cp_kv_push")
-        self._kv_barrier()
+                g0 * self.d * 2, ng * self.d * 2, self.kv_bases.data_ptr(),
+                2 * s * self.n * 2, (2 * s + 1) * self.n * 2, self.cp, p(rows),
+                rows.shape[-1] if covered else 0, p(pos),
+                shard.tiles.doc_start.data_ptr() if covered else None,
+                shard.tiles.n_docs if covered else 0, _native.stream_ptr()), "wlb_cp_kv_push_part")
+            self._signal(s, _KV, gi)
         return self._view(self.kv, 2 * s, T), self._view(self.kv, 2 * s + 1, T)
+
+    def wait_kv(self, b, gi):
+        """On the current stream: later work waits until every peer's rows of
+        head group gi of micro-batch b have landed."""
+        self._wait(b % self.slots, _KV, gi)
 
     def dkv_out(self, shard, b, cur):
         s, T = b % self.slots, shard.gather_all.numel()
@@ -278,29 +324,34 @@ class SymmExchange:
             cur.wait_event(self.free[s])
         return self._view(self.dkv, 2 * s, T), self._view(self.dkv, 2 * s + 1, T)
 
+    def signal_dkv(self, b, gi):
+        """On the current stream, after the backward of head group gi: tell
+        every peer this rank's partials of gi are complete."""
+        self._signal(b % self.slots, _DKV, gi)
+
     def scatter(self, dkf, dvf, shard, b):
+        """Pull (on the current stream) this rank's rows of every rank's
+        partials, each head group as soon as all peers' partials of it are
+        complete; fp32 dK / dV [T/cp, Hkv, D]."""
         s = b % self.slots
         tl = shard.gather_local.numel()
         dk = torch.empty((tl, self.hkv, self.d), dtype=torch.float32, device=dkf.device)
         dv = torch.empty_like(dk)
-        self._dkv_barrier()
         es = 2 if self.dkv_bf16 else 4
         flags = _native.WLB_BWD_DKV_BF16 if self.dkv_bf16 else 0
-        if self.pull_covered and shard.tiles.n_docs > 0:
-            # read a peer's partial row only where that peer's backward wrote it
-            rows, pos = self._tables(shard)
-            _native.check(_native.lib().wlb_cp_dkv_pull_cov(
+        covered = self.pull_covered and shard.tiles.n_docs > 0
+        rows, pos = self._tables(shard) if covered else (None, None)
+        p = _native.ptr
+        for gi, (g0, ng) in enumerate(self.groups):
+            self._wait(s, _DKV, gi)
+            _native.check(_native.lib().wlb_cp_dkv_pull_part(
                 self.dkv_bases.data_ptr(), 2 * s * self.n * es, (2 * s + 1) * self.n * es,
-                shard.gather_local.data_ptr(), tl, self.hkv * self.d * es, dk.data_ptr(),
-                dv.data_ptr(), self.cp, flags, rows.data_ptr(), rows.shape[-1], pos.data_ptr(),
-                shard.tiles.doc_start.data_ptr(), shard.tiles.n_docs, _native.stream_ptr()),
-                "wlb_cp_dkv_pull_cov")
-        else:
-            _native.check(_native.lib().wlb_cp_dkv_pull_ex(
-                self.dkv_bases.data_ptr(), 2 * s * self.n * es, (2 * s + 1) * self.n * es,
-                shard.gather_local.data_ptr(), tl, self.hkv * self.d * es, dk.data_ptr(),
-                dv.data_ptr(), self.cp, flags, _native.stream_ptr()), "wlb_cp_dkv_pull_ex")
-        self._dkv_barrier()
+                shard.gather_local.data_ptr(), tl, self.hkv * self.d * es, g0 * self.d * es,
+                ng * self.d * es, dk.data_ptr(), dv.data_ptr(), self.cp, flags, p(rows),
+                rows.shape[-1] if covered else 0, p(pos),
+                shard.tiles.doc_start.data_ptr() if covered else None,
+                shard.tiles.n_docs if covered else 0, _native.stream_ptr()), "wlb_cp_dkv_pull_part")
+        self._dkv_barrier()                 # every rank finished pulling from slot s
         ev = torch.cuda.Event()
         ev.record()
         self.free[s] = ev
@@ -309,16 +360,17 @@ class SymmExchange:
 
 class LocalPeersExchange(SymmExchange):
     """One-GPU emulation of a CP group's symmetric exchange: every rank's slot
-    buffers are ordinary allocations on ONE device and `kv_bases` /
-    `dkv_bases` hold all of them, so the same push / pull kernels and the same
-    `gather` / `dkv_out` / `scatter` code run for cp = 2..8 without peers.
-    Cross-rank ordering is the caller's: run every rank's `gather` before any
-    rank's attention, and every rank's backward before any rank's `scatter`
-    (stream order on one device; the barriers are no-ops).  Used by the
+    and flag buffers are ordinary allocations on ONE device and the base
+    tables hold all of them, so the same push / pull / signal / wait kernels
+    and the same `gather` / `wait_kv` / `dkv_out` / `signal_dkv` / `scatter`
+    code run for cp = 2..8 without peers.  Cross-rank ordering is the
+    caller's: run every rank's `gather` before any rank's attention, and every
+    rank's backward (+ `signal_dkv`) before any rank's `scatter` (stream order
+    on one device; the barriers are no-ops, the flags are real).  Used by the
     exchange parity tests and tools/cp_emulate.py."""
 
     @classmethod
-    def create(cls, cp, t_max, hkv, d, device, slots=2, fill=0.0):
+    def create(cls, cp, t_max, hkv, d, device, slots=2, fill=0.0, groups=None):
         """cp exchange objects, rank r's at index r.  `fill` initialises the
         K/V slots (e.g. NaN, to prove every row a tile loads is rewritten)."""
         n = t_max * hkv * d
@@ -326,15 +378,18 @@ class LocalPeersExchange(SymmExchange):
                for _ in range(cp)]
         dkvs = [torch.full((2 * slots * n,), float("nan"), dtype=cls._dkv_dtype(), device=device)
                 for _ in range(cp)]
+        flags = [torch.zeros(slots * 2 * MAX_GROUPS * cp, dtype=torch.int32, device=device)
+                 for _ in range(cp)]
         kv_ptrs = [t.data_ptr() for t in kvs]
         dkv_ptrs = [t.data_ptr() for t in dkvs]
+        flag_ptrs = [t.data_ptr() for t in flags]
         out = []
         for r in range(cp):
             ex = cls.__new__(cls)
             ex.group = None
-            ex._setup(cp, t_max, hkv, d, device, slots, kvs[r], dkvs[r], kv_ptrs, dkv_ptrs)
+            ex._setup(cp, t_max, hkv, d, device, slots, kvs[r], dkvs[r], kv_ptrs, dkv_ptrs,
+                      flags[r], flag_ptrs, r, groups)
             ex._kv_barrier = ex._dkv_barrier = lambda: None
-            ex.rank = r
             out.append(ex)
         return out
 
@@ -343,15 +398,18 @@ class CPStepPipeline:
     """CP attention over all micro-batches of a step with the exchange overlapped.
 
     The K/V exchange of micro-batch b+1 and the dK/dV exchange of micro-batch
-    b-1 run on a dedicated communication stream while micro-batch b's
-    attention kernels run on the compute stream; CUDA events order each
-    exchange against its producer and consumer.  `exchange` is NcclExchange
-    (default) or SymmExchange (one-sided NVLink stores / loads).  Hooks:
+    b-1 run on dedicated communication streams while micro-batch b's
+    attention kernels run on the compute stream.  With NcclExchange (default)
+    CUDA events order each exchange against its producer and consumer.  With
+    SymmExchange the attention runs head group by head group, each gated on
+    the device by the peers' arrival flags of that group, and the dK/dV pull
+    of a group overlaps the backward of the later groups.  Hooks:
 
     * `ready[b]` (optional CUDA events): micro-batch b's inputs are valid once
       they fire (e.g. H2D copies); by default inputs are taken as resident.
     * `on_kernels(b, shard, fn)` wraps the attention kernels (e.g. CUDA events
-      for per-rank kernel time) without timing the exchange.
+      for per-rank kernel time; with head groups this includes the device-side
+      waits for the peers' K/V of each group).
     * `on_outputs(b, (o, dq, dk, dv), event)` is called as soon as micro-batch
       b's outputs are enqueued; `event` fires when all four are complete.
     """
@@ -360,6 +418,7 @@ class CPStepPipeline:
         self.group = group
         self.exchange = exchange if exchange is not None else NcclExchange(group)
         self.depth = getattr(self.exchange, "depth", 1)
+        self.flagged = isinstance(self.exchange, SymmExchange)
         # The exchange stream outranks the compute stream (CUDA: lower value =
         # higher priority; default streams are 0): its blocks are dispatched
         # as soon as an SM frees up, so an exchange is done before the
@@ -405,48 +464,67 @@ class CPStepPipeline:
             if nb < n:
                 pend[nb] = self._gather(inputs[nb][1], inputs[nb][2], shards[nb], nb, cur, rdy[nb])
             k_full, v_full, ev = pend.pop(b)
-            cur.wait_event(ev)
+            sh = shards[b]
+            flagged = self.flagged and sh.cp > 1
+            if not flagged:
+                cur.wait_event(ev)          # (flagged: the device-side waits gate each group)
             if rdy[b] is not None:
                 cur.wait_event(rdy[b])
             q, _, _, do = inputs[b]
-            dk_out, dv_out = self.exchange.dkv_out(shards[b], b, cur) if shards[b].cp > 1 else (None, None)
+            dk_out, dv_out = self.exchange.dkv_out(sh, b, cur) if sh.cp > 1 else (None, None)
+            cov = covered and dk_out is not None and sh.tiles.n_docs > 0
 
-            def kernels(q=q, do=do, k_full=k_full, v_full=v_full, sh=shards[b], dk_out=dk_out,
-                        dv_out=dv_out):
-                o, lse = attn_forward(q, k_full, v_full, sh.tiles, scale)
-                dq, dkf, dvf = attn_backward(q, k_full, v_full, o, lse, do, sh.tiles, scale,
-                                             dk_out, dv_out,
-                                             covered_only=covered and dk_out is not None
-                                             and sh.tiles.n_docs > 0)
-                return o, dq, dkf, dvf
+            def kernels(q=q, do=do, k_full=k_full, v_full=v_full, sh=sh, dk_out=dk_out,
+                        dv_out=dv_out, b=b, flagged=flagged, cov=cov):
+                if not flagged:
+                    o, lse = attn_forward(q, k_full, v_full, sh.tiles, scale)
+                    dq, dkf, dvf = attn_backward(q, k_full, v_full, o, lse, do, sh.tiles, scale,
+                                                 dk_out, dv_out, covered_only=cov)
+                    return o, dq, dkf, dvf
+                ex = self.exchange
+                o, lse = torch.empty_like(q), None
+                for gi, grp in enumerate(ex.groups):
+                    ex.wait_kv(b, gi)
+                    o, lse = attn_forward(q, k_full, v_full, sh.tiles, scale, kv_heads=grp,
+                                          out=None if lse is None else (o, lse))
+                dq, ws = torch.empty_like(q), bwd_workspace(q, k_full, sh.tiles)
+                for gi, grp in enumerate(ex.groups):
+                    attn_backward(q, k_full, v_full, o, lse, do, sh.tiles, scale, dk_out, dv_out,
+                                  covered_only=cov, kv_heads=grp, dq_out=dq, ws=ws)
+                    ex.signal_dkv(b, gi)
+                return o, dq, dk_out, dv_out
 
-            o, dq, dkf, dvf = on_kernels(b, shards[b], kernels) if on_kernels else kernels()
-            if shards[b].cp > 1:
+            o, dq, dkf, dvf = on_kernels(b, sh, kernels) if on_kernels else kernels()
+            if sh.cp > 1:
                 for t in (k_full, v_full):
                     t.record_stream(cur)
                     if self.push is not self.comm:
                         t.record_stream(self.push)
             done = torch.cuda.Event()
             done.record(cur)
-            self.comm.wait_event(done)
+            if not flagged:
+                self.comm.wait_event(done)  # (flagged: the pull waits on the DKV flags)
             with torch.cuda.stream(self.comm):
-                dk, dv = self.exchange.scatter(dkf, dvf, shards[b], b) if shards[b].cp > 1 \
-                    else (dkf, dvf)
-                if shards[b].cp > 1:
+                dk, dv = self.exchange.scatter(dkf, dvf, sh, b) if sh.cp > 1 else (dkf, dvf)
+                if sh.cp > 1:
                     for t in (dkf, dvf):
                         t.record_stream(self.comm)
                 fin = torch.cuda.Event()
                 fin.record(self.comm)
             tail.append(fin)
             if on_outputs is not None:
+                if flagged:                 # o, dq (compute) as well as dk, dv (comm)
+                    self.comm.wait_event(done)
+                    fin = torch.cuda.Event()
+                    fin.record(self.comm)
                 on_outputs(b, (o, dq, dk, dv), fin)
             if keep_outputs:
                 outs[b] = (o, dq, dk, dv)
             else:
                 for t in (o, dq, dk, dv):      # freed now; keep them valid for pending work
                     t.record_stream(cur)
-                    if shards[b].cp > 1:
+                    if sh.cp > 1:
                         t.record_stream(self.comm)
-        for ev in tail:
-            cur.wait_event(ev)
+        for fin in tail:
+            cur.wait_event(fin)
         return outs

@@ -372,10 +372,10 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       }
     };
     // Pipelined one tile deep: S/dP of tile I is issued before dQ/dV/dK of
-    // tile I-1, across KV-head and unit boundaries too (the next head's K is
-    // in the other buffer; its V only replaces this head's after the last
-    // dP^T).  The second group of a unit's last tile runs after the next
-    // unit's first S/dP (or at the end).
+    // tile I-1 within a KV head.  At a head (or unit) boundary the previous
+    // head's last tile completes first; the next head's K is already in the
+    // other buffer and its V load started after the previous head's last
+    // dP^T, so the boundary costs little more than the V load's tail.
     Unit P;                       // unit of the pending second group
     int pJ = -1, pJg = 0, pG = 0;
     int I0 = 0, G0 = 0;
@@ -385,7 +385,12 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       const Unit U = geom(u);
       for (int I = 0; I < U.n_all; ++I) {
         const int G = G0 + I / U.n_iter;
-        if (I % U.n_iter == 0) {              // new KV head: its K and V
+        if (I % U.n_iter == 0) {
+          // new KV head: finish the previous head's last tile first (its dQ
+          // drain and dK/dV epilogue then overlap the wait for this head's V,
+          // whose load started after the previous head's last dP^T)
+          if (pJ >= 0) second_half(P, pJ, pJg, pG);
+          pJ = -1;
           mbar_wait(&bars->k_full[G & 1], (G >> 1) & 1);
           mbar_wait(&bars->v_full, G & 1);
         }

@@ -21,85 +21,6 @@
 
 namespace wlb {
 
-__global__ void kv_push_kernel(const int4* __restrict__ k, const int4* __restrict__ v,
-                               const int* __restrict__ gidx, long long n_rows, long long row_vecs,
-                               const unsigned long long* __restrict__ bases, long long k_off,
-                               long long v_off, int cp) {
-  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  const int lane = threadIdx.x & 31;
-  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
-       r += warps) {
-    const long long g = gidx[r];
-    for (long long c = lane; c < row_vecs; c += 32) {
-      const int4 kv = k[r * row_vecs + c], vv = v[r * row_vecs + c];
-      for (int p = 0; p < cp; ++p) {
-        char* base = reinterpret_cast<char*>(bases[p]);
-        reinterpret_cast<int4*>(base + k_off)[g * row_vecs + c] = kv;
-        reinterpret_cast<int4*>(base + v_off)[g * row_vecs + c] = vv;
-      }
-    }
-  }
-}
-
-__global__ void dkv_pull_kernel(const unsigned long long* __restrict__ bases, long long dk_off,
-                                long long dv_off, const int* __restrict__ gidx, long long n_rows,
-                                long long row_vecs, float4* __restrict__ dk,
-                                float4* __restrict__ dv, int cp) {
-  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  const int lane = threadIdx.x & 31;
-  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
-       r += warps) {
-    const long long g = gidx[r];
-    for (long long c = lane; c < row_vecs; c += 32) {
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-      for (int p = 0; p < cp; ++p) {
-        const char* base = reinterpret_cast<const char*>(bases[p]);
-        const float4 x = reinterpret_cast<const float4*>(base + dk_off)[g * row_vecs + c];
-        const float4 y = reinterpret_cast<const float4*>(base + dv_off)[g * row_vecs + c];
-        a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
-        b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
-      }
-      dk[r * row_vecs + c] = a;
-      dv[r * row_vecs + c] = b;
-    }
-  }
-}
-
-// bf16 partials: each lane reads 8 bf16 (16 B) of every peer, sums in fp32
-// and writes 8 fp32 (two float4) of the local row.  row_vecs counts 16-B
-// units of the bf16 row.
-__global__ void dkv_pull_bf16_kernel(const unsigned long long* __restrict__ bases, long long dk_off,
-                                     long long dv_off, const int* __restrict__ gidx,
-                                     long long n_rows, long long row_vecs, float4* __restrict__ dk,
-                                     float4* __restrict__ dv, int cp) {
-  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  const int lane = threadIdx.x & 31;
-  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
-       r += warps) {
-    const long long g = gidx[r];
-    for (long long c = lane; c < row_vecs; c += 32) {
-      float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, b[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      for (int p = 0; p < cp; ++p) {
-        const char* base = reinterpret_cast<const char*>(bases[p]);
-        const uint4 x = reinterpret_cast<const uint4*>(base + dk_off)[g * row_vecs + c];
-        const uint4 y = reinterpret_cast<const uint4*>(base + dv_off)[g * row_vecs + c];
-        const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&x);
-        const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&y);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 xf = __bfloat1622float2(x2[e]), yf = __bfloat1622float2(y2[e]);
-          a[2 * e] += xf.x; a[2 * e + 1] += xf.y;
-          b[2 * e] += yf.x; b[2 * e + 1] += yf.y;
-        }
-      }
-      dk[(r * row_vecs + c) * 2] = make_float4(a[0], a[1], a[2], a[3]);
-      dk[(r * row_vecs + c) * 2 + 1] = make_float4(a[4], a[5], a[6], a[7]);
-      dv[(r * row_vecs + c) * 2] = make_float4(b[0], b[1], b[2], b[3]);
-      dv[(r * row_vecs + c) * 2 + 1] = make_float4(b[4], b[5], b[6], b[7]);
-    }
-  }
-}
-
 // Coverage test shared by the covered push / pull: does rank `lane` (< cp)
 // read (forward K/V) or write (backward dK/dV partials) global row g?  Rank p
 // touches document d's keys below min(len_d, roundup128(last local position
@@ -145,27 +66,30 @@ __device__ __forceinline__ unsigned covering_ranks(int g, int lane, int cp,
   return __ballot_sync(0xffffffffu, covers);
 }
 
-// Covered push: local row i goes only to the ranks whose attention reads it,
-// including the rows a rank's last tile of a document reads past that
-// document's end (SPILL).  Rows a rank never loads stay as they were.
-__global__ void kv_push_cov_kernel(const int4* __restrict__ k, const int4* __restrict__ v,
-                                   const int* __restrict__ gidx, long long n_rows,
-                                   long long row_vecs, const unsigned long long* __restrict__ bases,
-                                   long long k_off, long long v_off, int cp,
-                                   const int* __restrict__ rowset_all, int rs,
-                                   const int* __restrict__ pos_all,
-                                   const int* __restrict__ doc_start, int n_docs) {
+// Push: local row i of K and V (columns [col0, col0 + ncol) of the row, in
+// 16-B units: a range of KV heads) is stored at row gather_local[i] of the
+// document-ordered buffers of every rank (COVERED: only of the ranks whose
+// attention loads it, including a last tile's reads past its document's end).
+template <bool COVERED>
+__global__ void kv_push_kernel(const int4* __restrict__ k, const int4* __restrict__ v,
+                               const int* __restrict__ gidx, long long n_rows, long long row_vecs,
+                               long long col0, long long ncol,
+                               const unsigned long long* __restrict__ bases, long long k_off,
+                               long long v_off, int cp, const int* __restrict__ rowset_all, int rs,
+                               const int* __restrict__ pos_all, const int* __restrict__ doc_start,
+                               int n_docs) {
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   const int lane = threadIdx.x & 31;
   for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
        r += warps) {
     const long long g = gidx[r];
-    const unsigned mask =
-        covering_ranks<true>((int)g, lane, cp, rowset_all, rs, pos_all, n_rows, doc_start, n_docs);
-    for (long long c = lane; c < row_vecs; c += 32) {
+    const unsigned mask = COVERED ? covering_ranks<true>((int)g, lane, cp, rowset_all, rs, pos_all,
+                                                         n_rows, doc_start, n_docs)
+                                  : 0xffffffffu;
+    for (long long c = col0 + lane; c < col0 + ncol; c += 32) {
       const int4 kv = k[r * row_vecs + c], vv = v[r * row_vecs + c];
       for (int p = 0; p < cp; ++p) {
-        if (!((mask >> p) & 1u)) continue;
+        if (COVERED && !((mask >> p) & 1u)) continue;
         char* base = reinterpret_cast<char*>(bases[p]);
         reinterpret_cast<int4*>(base + k_off)[g * row_vecs + c] = kv;
         reinterpret_cast<int4*>(base + v_off)[g * row_vecs + c] = vv;
@@ -174,33 +98,36 @@ __global__ void kv_push_cov_kernel(const int4* __restrict__ k, const int4* __res
   }
 }
 
-// Coverage-aware pull: a peer's partial row is read only where that peer's
-// backward wrote it.  Rank p's KV tiles cover the keys of document d up to
-// its last local query position there, rounded up to the 128-key tile
-// (capped at the document length); every key past that is an exact zero
-// (zero_uncovered_kernel).  Skipping those rows gives the same fp32 sums and
-// cuts the NVLink reads, most under per-sequence shards where a short
-// document lives in one rank's chunk.  rowset_all: [cp][rs] per-rank row-set
-// offsets per document; pos_all: [cp][tl] per-rank in-document positions.
-template <bool BF16>
-__global__ void dkv_pull_cov_kernel(const unsigned long long* __restrict__ bases, long long dk_off,
-                                    long long dv_off, const int* __restrict__ gidx,
-                                    long long n_rows, long long row_vecs, float4* __restrict__ dk,
-                                    float4* __restrict__ dv, int cp,
-                                    const int* __restrict__ rowset_all, int rs,
-                                    const int* __restrict__ pos_all, long long tl,
-                                    const int* __restrict__ doc_start, int n_docs) {
+// Pull: dk[i] = sum over ranks of their dK partial row gather_local[i]
+// (columns [col0, col0 + ncol) of the partial row, 16-B units), same for dV,
+// summed in fp32 in rank order (deterministic).  BF16: the partials are bf16
+// and the fp32 outputs have twice the row bytes.  COVERED: a peer's row is
+// read only where that peer's backward wrote it; rank p covers document d's
+// keys below min(len_d, roundup128(last local position of p in d + 1)), every
+// key past that is an exact zero, so the sums are the same and fewer bytes
+// cross NVLink (most under per-sequence shards, where a short document lives
+// in one rank's chunk).  rowset_all: [cp][rs] per-rank row-set offsets per
+// document; pos_all: [cp][tl] per-rank in-document positions.
+template <bool COVERED, bool BF16>
+__global__ void dkv_pull_kernel(const unsigned long long* __restrict__ bases, long long dk_off,
+                                long long dv_off, const int* __restrict__ gidx, long long n_rows,
+                                long long row_vecs, long long col0, long long ncol,
+                                float4* __restrict__ dk, float4* __restrict__ dv, int cp,
+                                const int* __restrict__ rowset_all, int rs,
+                                const int* __restrict__ pos_all, long long tl,
+                                const int* __restrict__ doc_start, int n_docs) {
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   const int lane = threadIdx.x & 31;
   for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
        r += warps) {
     const int g = gidx[r];
-    const unsigned mask =
-        covering_ranks<false>(g, lane, cp, rowset_all, rs, pos_all, tl, doc_start, n_docs);
-    for (long long c = lane; c < row_vecs; c += 32) {
+    const unsigned mask = COVERED ? covering_ranks<false>(g, lane, cp, rowset_all, rs, pos_all, tl,
+                                                          doc_start, n_docs)
+                                  : 0xffffffffu;
+    for (long long c = col0 + lane; c < col0 + ncol; c += 32) {
       float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, b[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       for (int p = 0; p < cp; ++p) {
-        if (!((mask >> p) & 1u)) continue;
+        if (COVERED && !((mask >> p) & 1u)) continue;
         const char* base = reinterpret_cast<const char*>(bases[p]);
         if (BF16) {
           const uint4 x = reinterpret_cast<const uint4*>(base + dk_off)[g * row_vecs + c];
@@ -233,6 +160,40 @@ __global__ void dkv_pull_cov_kernel(const unsigned long long* __restrict__ bases
   }
 }
 
+// Per-peer arrival flags (one int per (slot, kind, head group, source rank) in
+// every rank's symmetric flag buffer).  signal: after this rank's stores of a
+// head group have completed (the previous kernel on the stream), publish
+// `value` into slot flag_off of every peer with a system-scope release.
+// wait: spin until the n local flags reach `value` (system-scope acquire),
+// so the next kernel on the stream sees every peer's rows.  Values are
+// monotonically increasing epochs, so no flag is ever reset.  A wait that
+// exceeds 60 s traps (a lost peer must not hang the GPU).
+__global__ void signal_kernel(const unsigned long long* __restrict__ bases, long long flag_off,
+                              int cp, int value) {
+  __threadfence_system();
+  for (int p = threadIdx.x; p < cp; p += blockDim.x) {
+    int* f = reinterpret_cast<int*>(reinterpret_cast<char*>(bases[p]) + flag_off);
+    asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(f), "r"(value) : "memory");
+  }
+}
+
+__global__ void wait_kernel(const int* __restrict__ flags, int n, int value) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+      int x;
+      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(x) : "l"(flags + i) : "memory");
+      if (x >= value) break;
+      __nanosleep(128);
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 60000000000ull) __trap();
+    }
+  }
+  __syncthreads();
+}
+
 // Push/pull blocks (256 threads) per 8 SMs.  The exchange runs on its own
 // stream beside the attention kernels, which hold one CTA per SM: a grid of
 // 8 blocks per SM took SMs from the attention for the whole exchange (N=4
@@ -260,83 +221,77 @@ static int grid_for(long long n_rows) {
 
 using namespace wlb;
 
-extern "C" int wlb_cp_kv_push(const void* k_local, const void* v_local, const int32_t* gather_local,
-                              int64_t n_rows, int64_t row_bytes, const uint64_t* peer_bases,
-                              int64_t k_off, int64_t v_off, int32_t cp, void* stream) {
-  WLB_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && k_off % 16 == 0 && v_off % 16 == 0,
-              "rows and offsets must be 16-byte aligned");
-  WLB_REQUIRE(aligned16(k_local, v_local), "k_local / v_local must be 16-byte aligned");
-  WLB_REQUIRE(cp >= 1, "cp must be >= 1");
-  if (n_rows <= 0) return WLB_OK;
-  kv_push_kernel<<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
-      (const int4*)k_local, (const int4*)v_local, gather_local, n_rows, row_bytes / 16,
-      (const unsigned long long*)peer_bases, k_off, v_off, cp);
-  WLB_LAUNCH_CHECK();
-  return WLB_OK;
-}
-
-extern "C" int wlb_cp_dkv_pull_ex(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_off,
-                                  const int32_t* gather_local, int64_t n_rows, int64_t row_bytes,
-                                  float* dk, float* dv, int32_t cp, int32_t flags, void* stream) {
-  WLB_REQUIRE((flags & ~WLB_BWD_DKV_BF16) == 0, "unknown pull flags 0x%x", flags);
-  if (!(flags & WLB_BWD_DKV_BF16))
-    return wlb_cp_dkv_pull(peer_bases, dk_off, dv_off, gather_local, n_rows, row_bytes, dk, dv,
-                           cp, stream);
-  WLB_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && dk_off % 16 == 0 && dv_off % 16 == 0,
-              "rows and offsets must be 16-byte aligned");
-  WLB_REQUIRE(aligned16(dk, dv), "dk / dv must be 16-byte aligned");
-  WLB_REQUIRE(cp >= 1, "cp must be >= 1");
-  if (n_rows <= 0) return WLB_OK;
-  // row_bytes is the bf16 partial row; the local fp32 output rows are twice as long
-  dkv_pull_bf16_kernel<<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
-      (const unsigned long long*)peer_bases, dk_off, dv_off, gather_local, n_rows, row_bytes / 16,
-      (float4*)dk, (float4*)dv, cp);
-  WLB_LAUNCH_CHECK();
-  return WLB_OK;
-}
-
-extern "C" int wlb_cp_dkv_pull(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_off,
-                               const int32_t* gather_local, int64_t n_rows, int64_t row_bytes,
-                               float* dk, float* dv, int32_t cp, void* stream) {
-  WLB_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && dk_off % 16 == 0 && dv_off % 16 == 0,
-              "rows and offsets must be 16-byte aligned");
-  WLB_REQUIRE(aligned16(dk, dv), "dk / dv must be 16-byte aligned");
-  WLB_REQUIRE(cp >= 1, "cp must be >= 1");
-  if (n_rows <= 0) return WLB_OK;
-  dkv_pull_kernel<<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
-      (const unsigned long long*)peer_bases, dk_off, dv_off, gather_local, n_rows, row_bytes / 16,
-      (float4*)dk, (float4*)dv, cp);
-  WLB_LAUNCH_CHECK();
-  return WLB_OK;
-}
-
-extern "C" int wlb_cp_dkv_pull_cov(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_off,
+extern "C" int wlb_cp_kv_push_part(const void* k_local, const void* v_local,
                                    const int32_t* gather_local, int64_t n_rows, int64_t row_bytes,
-                                   float* dk, float* dv, int32_t cp, int32_t flags,
+                                   int64_t col_off, int64_t col_bytes, const uint64_t* peer_bases,
+                                   int64_t k_off, int64_t v_off, int32_t cp,
                                    const int32_t* rowset_all, int32_t rowset_stride,
                                    const int32_t* positions_all, const int32_t* doc_start,
                                    int32_t n_docs, void* stream) {
+  WLB_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && k_off % 16 == 0 && v_off % 16 == 0,
+              "rows and offsets must be 16-byte aligned");
+  WLB_REQUIRE(col_off >= 0 && col_bytes >= 0 && col_off % 16 == 0 && col_bytes % 16 == 0 &&
+                  col_off + col_bytes <= row_bytes,
+              "column range [%lld, %lld) must be 16-byte aligned inside the %lld-byte row",
+              (long long)col_off, (long long)(col_off + col_bytes), (long long)row_bytes);
+  WLB_REQUIRE(aligned16(k_local, v_local), "k_local / v_local must be 16-byte aligned");
+  WLB_REQUIRE(cp >= 1, "cp must be >= 1");
+  const bool covered = rowset_all != nullptr;
+  if (covered) {
+    WLB_REQUIRE(cp <= 32, "the covered push needs cp in [1, 32]");
+    WLB_REQUIRE(n_docs >= 1 && rowset_stride >= n_docs + 1,
+                "bad row-set table (n_docs %d, stride %d)", n_docs, rowset_stride);
+  }
+  if (n_rows <= 0 || col_bytes == 0) return WLB_OK;
+  auto kern = covered ? kv_push_kernel<true> : kv_push_kernel<false>;
+  kern<<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
+      (const int4*)k_local, (const int4*)v_local, gather_local, n_rows, row_bytes / 16,
+      col_off / 16, col_bytes / 16, (const unsigned long long*)peer_bases, k_off, v_off, cp,
+      rowset_all, rowset_stride, positions_all, doc_start, n_docs);
+  WLB_LAUNCH_CHECK();
+  return WLB_OK;
+}
+
+extern "C" int wlb_cp_dkv_pull_part(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_off,
+                                    const int32_t* gather_local, int64_t n_rows, int64_t row_bytes,
+                                    int64_t col_off, int64_t col_bytes, float* dk, float* dv,
+                                    int32_t cp, int32_t flags, const int32_t* rowset_all,
+                                    int32_t rowset_stride, const int32_t* positions_all,
+                                    const int32_t* doc_start, int32_t n_docs, void* stream) {
   WLB_REQUIRE((flags & ~WLB_BWD_DKV_BF16) == 0, "unknown pull flags 0x%x", flags);
   WLB_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && dk_off % 16 == 0 && dv_off % 16 == 0,
               "rows and offsets must be 16-byte aligned");
+  WLB_REQUIRE(col_off >= 0 && col_bytes >= 0 && col_off % 16 == 0 && col_bytes % 16 == 0 &&
+                  col_off + col_bytes <= row_bytes,
+              "column range [%lld, %lld) must be 16-byte aligned inside the %lld-byte row",
+              (long long)col_off, (long long)(col_off + col_bytes), (long long)row_bytes);
   WLB_REQUIRE(aligned16(dk, dv), "dk / dv must be 16-byte aligned");
-  WLB_REQUIRE(cp >= 1 && cp <= 32, "cp must be in [1, 32]");
-  WLB_REQUIRE(n_docs >= 1 && rowset_stride >= n_docs + 1, "bad row-set table (n_docs %d, stride %d)",
-              n_docs, rowset_stride);
-  if (n_rows <= 0) return WLB_OK;
-  const long long tl = n_rows;   // every rank holds T / cp rows
-  if (flags & WLB_BWD_DKV_BF16)
-    dkv_pull_cov_kernel<true><<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
-        (const unsigned long long*)peer_bases, dk_off, dv_off, gather_local, n_rows,
-        row_bytes / 16, (float4*)dk, (float4*)dv, cp, rowset_all, rowset_stride, positions_all,
-        tl, doc_start, n_docs);
-  else
-    dkv_pull_cov_kernel<false><<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
-        (const unsigned long long*)peer_bases, dk_off, dv_off, gather_local, n_rows,
-        row_bytes / 16, (float4*)dk, (float4*)dv, cp, rowset_all, rowset_stride, positions_all,
-        tl, doc_start, n_docs);
+  WLB_REQUIRE(cp >= 1, "cp must be >= 1");
+  const bool covered = rowset_all != nullptr;
+  if (covered) {
+    WLB_REQUIRE(cp <= 32, "the covered pull needs cp in [1, 32]");
+    WLB_REQUIRE(n_docs >= 1 && rowset_stride >= n_docs + 1,
+                "bad row-set table (n_docs %d, stride %d)", n_docs, rowset_stride);
+  }
+  if (n_rows <= 0 || col_bytes == 0) return WLB_OK;
+  const bool bf = (flags & WLB_BWD_DKV_BF16) != 0;
+  auto kern = covered ? (bf ? dkv_pull_kernel<true, true> : dkv_pull_kernel<true, false>)
+                      : (bf ? dkv_pull_kernel<false, true> : dkv_pull_kernel<false, false>);
+  // row_bytes / col_* count the partial rows; the local fp32 outputs are
+  // twice as long for bf16 partials
+  kern<<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
+      (const unsigned long long*)peer_bases, dk_off, dv_off, gather_local, n_rows, row_bytes / 16,
+      col_off / 16, col_bytes / 16, (float4*)dk, (float4*)dv, cp, rowset_all, rowset_stride,
+      positions_all, n_rows, doc_start, n_docs);
   WLB_LAUNCH_CHECK();
   return WLB_OK;
+}
+
+extern "C" int wlb_cp_kv_push(const void* k_local, const void* v_local, const int32_t* gather_local,
+                              int64_t n_rows, int64_t row_bytes, const uint64_t* peer_bases,
+                              int64_t k_off, int64_t v_off, int32_t cp, void* stream) {
+  return wlb_cp_kv_push_part(k_local, v_local, gather_local, n_rows, row_bytes, 0, row_bytes,
+                             peer_bases, k_off, v_off, cp, nullptr, 0, nullptr, nullptr, 0, stream);
 }
 
 extern "C" int wlb_cp_kv_push_cov(const void* k_local, const void* v_local,
@@ -345,17 +300,52 @@ extern "C" int wlb_cp_kv_push_cov(const void* k_local, const void* v_local,
                                   int32_t cp, const int32_t* rowset_all, int32_t rowset_stride,
                                   const int32_t* positions_all, const int32_t* doc_start,
                                   int32_t n_docs, void* stream) {
-  WLB_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && k_off % 16 == 0 && v_off % 16 == 0,
-              "rows and offsets must be 16-byte aligned");
-  WLB_REQUIRE(aligned16(k_local, v_local), "k_local / v_local must be 16-byte aligned");
-  WLB_REQUIRE(cp >= 1 && cp <= 32, "cp must be in [1, 32]");
-  WLB_REQUIRE(n_docs >= 1 && rowset_stride >= n_docs + 1, "bad row-set table (n_docs %d, stride %d)",
-              n_docs, rowset_stride);
-  if (n_rows <= 0) return WLB_OK;
-  kv_push_cov_kernel<<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
-      (const int4*)k_local, (const int4*)v_local, gather_local, n_rows, row_bytes / 16,
-      (const unsigned long long*)peer_bases, k_off, v_off, cp, rowset_all, rowset_stride,
-      positions_all, doc_start, n_docs);
+  WLB_REQUIRE(rowset_all != nullptr, "rowset_all is required");
+  return wlb_cp_kv_push_part(k_local, v_local, gather_local, n_rows, row_bytes, 0, row_bytes,
+                             peer_bases, k_off, v_off, cp, rowset_all, rowset_stride,
+                             positions_all, doc_start, n_docs, stream);
+}
+
+extern "C" int wlb_cp_dkv_pull(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_off,
+                               const int32_t* gather_local, int64_t n_rows, int64_t row_bytes,
+                               float* dk, float* dv, int32_t cp, void* stream) {
+  return wlb_cp_dkv_pull_part(peer_bases, dk_off, dv_off, gather_local, n_rows, row_bytes, 0,
+                              row_bytes, dk, dv, cp, 0, nullptr, 0, nullptr, nullptr, 0, stream);
+}
+
+extern "C" int wlb_cp_dkv_pull_ex(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_off,
+                                  const int32_t* gather_local, int64_t n_rows, int64_t row_bytes,
+                                  float* dk, float* dv, int32_t cp, int32_t flags, void* stream) {
+  return wlb_cp_dkv_pull_part(peer_bases, dk_off, dv_off, gather_local, n_rows, row_bytes, 0,
+                              row_bytes, dk, dv, cp, flags, nullptr, 0, nullptr, nullptr, 0,
+                              stream);
+}
+
+extern "C" int wlb_cp_dkv_pull_cov(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_off,
+                                   const int32_t* gather_local, int64_t n_rows, int64_t row_bytes,
+                                   float* dk, float* dv, int32_t cp, int32_t flags,
+                                   const int32_t* rowset_all, int32_t rowset_stride,
+                                   const int32_t* positions_all, const int32_t* doc_start,
+                                   int32_t n_docs, void* stream) {
+  WLB_REQUIRE(rowset_all != nullptr, "rowset_all is required");
+  return wlb_cp_dkv_pull_part(peer_bases, dk_off, dv_off, gather_local, n_rows, row_bytes, 0,
+                              row_bytes, dk, dv, cp, flags, rowset_all, rowset_stride,
+                              positions_all, doc_start, n_docs, stream);
+}
+
+extern "C" int wlb_cp_signal(const uint64_t* flag_bases, int64_t flag_off, int32_t cp,
+                             int32_t value, void* stream) {
+  WLB_REQUIRE(cp >= 1 && flag_off >= 0 && flag_off % 4 == 0, "bad signal arguments");
+  signal_kernel<<<1, 32 * ((cp + 31) / 32 < 32 ? (cp + 31) / 32 : 32), 0, (cudaStream_t)stream>>>(
+      (const unsigned long long*)flag_bases, flag_off, cp, value);
+  WLB_LAUNCH_CHECK();
+  return WLB_OK;
+}
+
+extern "C" int wlb_cp_wait(const int32_t* flags, int32_t n, int32_t value, void* stream) {
+  WLB_REQUIRE(n >= 0 && ((uintptr_t)flags & 3) == 0, "bad wait arguments");
+  if (n == 0) return WLB_OK;
+  wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(flags, n, value);
   WLB_LAUNCH_CHECK();
   return WLB_OK;
 }
