@@ -126,29 +126,71 @@ def scatter_dkv(dk_full, dv_full, shard: CPShard, group=None):
 
 class CPDocAttention(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, shard: CPShard, group, scale):
-        k_full, v_full = gather_kv(k, v, shard, group)
-        o, lse = attn_forward(q, k_full, v_full, shard.tiles, scale)
+    def forward(ctx, q, k, v, shard: CPShard, group, scale, exchange):
+        ctx.shard, ctx.group, ctx.scale, ctx.exchange = shard, group, scale, exchange
+        if isinstance(exchange, SymmExchange) and shard.cp > 1:
+            # push K/V head group by head group on a side stream; the attention
+            # of each group starts once every peer's rows of it have landed
+            cur = torch.cuda.current_stream()
+            b = exchange.begin_microbatch()
+            side = exchange.side_stream()
+            side.wait_stream(cur)
+            with torch.cuda.stream(side):
+                k_full, v_full = exchange.gather(k, v, shard, b)
+            o = lse = None
+            for gi, grp in enumerate(exchange.groups):
+                exchange.wait_kv(b, gi)
+                o, lse = attn_forward(q, k_full, v_full, shard.tiles, scale, kv_heads=grp,
+                                      out=None if o is None else (o, lse))
+            for t in (k, v, k_full, v_full):
+                t.record_stream(side)
+            ctx.b = b
+        else:
+            k_full, v_full = gather_kv(k, v, shard, group)
+            o, lse = attn_forward(q, k_full, v_full, shard.tiles, scale)
         ctx.save_for_backward(q, k_full, v_full, o, lse)
-        ctx.shard, ctx.group, ctx.scale = shard, group, scale
         return o
 
     @staticmethod
     def backward(ctx, do):
         q, k_full, v_full, o, lse = ctx.saved_tensors
-        dq, dk_full, dv_full = attn_backward(q, k_full, v_full, o, lse, do, ctx.shard.tiles,
+        shard, ex = ctx.shard, ctx.exchange
+        if isinstance(ex, SymmExchange) and shard.cp > 1:
+            cur = torch.cuda.current_stream()
+            b = ctx.b
+            dk_out, dv_out = ex.dkv_out(shard, b, cur)
+            cov = ex.pull_covered and shard.tiles.n_docs > 0
+            dq, ws = torch.empty_like(q), bwd_workspace(q, k_full, shard.tiles)
+            do = do.contiguous()
+            for gi, grp in enumerate(ex.groups):
+                attn_backward(q, k_full, v_full, o, lse, do, shard.tiles, ctx.scale, dk_out,
+                              dv_out, covered_only=cov, kv_heads=grp, dq_out=dq, ws=ws)
+                ex.signal_dkv(b, gi)
+            # each group's pull starts once every peer's partials of it are in
+            side = ex.side_stream()
+            with torch.cuda.stream(side):
+                dk, dv = ex.scatter(dk_out, dv_out, shard, b)
+            cur.wait_stream(side)
+            ex.end_microbatch(b)
+            return dq, dk.to(torch.bfloat16), dv.to(torch.bfloat16), None, None, None, None
+        dq, dk_full, dv_full = attn_backward(q, k_full, v_full, o, lse, do, shard.tiles,
                                              ctx.scale)
-        dk, dv = scatter_dkv(dk_full, dv_full, ctx.shard, ctx.group)
-        return dq, dk.to(torch.bfloat16), dv.to(torch.bfloat16), None, None, None
+        dk, dv = scatter_dkv(dk_full, dv_full, shard, ctx.group)
+        return dq, dk.to(torch.bfloat16), dv.to(torch.bfloat16), None, None, None, None
 
 
-def cp_doc_attention(q, k, v, shard: CPShard, group=None, scale=None):
+def cp_doc_attention(q, k, v, shard: CPShard, group=None, scale=None, exchange=None):
     """Document-masked causal attention of this rank's local tokens.
 
     q [T/cp, Hq, D], k/v [T/cp, Hkv, D] bf16 in the rank's local order
     (`shard.gather_local`); returns O [T/cp, Hq, D] bf16.  Differentiable.
+
+    exchange=None: NCCL all-gather / reduce-scatter (no overlap).  A
+    `SymmExchange`: the one-sided head-group exchange with per-peer arrival
+    flags, overlapped with the attention of the groups already landed (at
+    most `exchange.slots` micro-batches between a forward and its backward).
     """
-    return CPDocAttention.apply(q, k, v, shard, group, scale)
+    return CPDocAttention.apply(q, k, v, shard, group, scale, exchange)
 
 
 class NcclExchange:
@@ -262,6 +304,28 @@ class SymmExchange:
         # tile's reads past its document's end, so no stale row is ever read);
         # WLB_XCHG_PUSH=all stores to every rank
         self.push_covered = covered_ok and os.environ.get("WLB_XCHG_PUSH", "covered") != "all"
+
+    def side_stream(self):
+        """High-priority stream for this exchange's pushes / pulls outside a
+        CPStepPipeline (cp_doc_attention)."""
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(priority=-1)
+        return self._side
+
+    def begin_microbatch(self) -> int:
+        """Index of the next micro-batch of the autograd path (slot b % slots);
+        at most `slots` micro-batches may be between forward and backward."""
+        b = self.seq
+        live = getattr(self, "_live", set())
+        if any(x % self.slots == b % self.slots for x in live):
+            raise RuntimeError(f"more than {self.slots} CP micro-batches between forward and "
+                               "backward: the K/V slot is still needed")
+        live.add(b)
+        self._live = live
+        return b
+
+    def end_microbatch(self, b: int) -> None:
+        getattr(self, "_live", set()).discard(b)
 
     @staticmethod
     def _tables(shard):

@@ -63,11 +63,8 @@ struct BwdCfg {
   static constexpr int Q_BYTES = BM * D * 2;
   static constexpr int T_BYTES = BN * BM * 2;   // P^T / dS^T tile: 128 rows x 128 B
   static constexpr int Q_SLAB = BM * 128, KV_SLAB = BN * 128;
-  // K is double-buffered (consecutive KV heads / units alternate), so the
-  // next head's K lands while this head's last dQ^T MMAs still read it; V is
-  // single-buffered but freed by the head's last dP^T MMA, a tile early.
-  static constexpr int OFF_K = 0;                       // 2 buffers
-  static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = OFF_K + KV_BYTES;
   static constexpr int QS = 3;                          // Q/dO + query-vector ring depth
   static constexpr int OFF_Q = OFF_V + KV_BYTES;        // QS stages
   static constexpr int OFF_DO = OFF_Q + QS * Q_BYTES;   // QS stages
@@ -75,7 +72,10 @@ struct BwdCfg {
   static constexpr int OFF_VEC = OFF_DS + 2 * T_BYTES;  // QS x {lse2, delta, pos-k0}[BM]
   static constexpr int OFF_BAR = OFF_VEC + QS * 3 * BM * 4;
   // The dynamic-SMEM window starts 1024-B aligned on sm_100 (checked at run
-  // time), so no alignment slack is reserved (D = 128: 226.75 KB of 227).
+  // time), so no alignment slack is reserved (D = 128: 194.75 KB).
+  // (A second K buffer, so the next KV head's K lands early, measured 3-10%
+  //  SLOWER on the same box: profiles/r02_ab_bwd_kdb.txt; the 227 KB carve-out
+  //  leaves almost no L1 for the per-query vector loads.)
   static constexpr int SMEM = OFF_BAR + 512;
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr uint32_t COL_S = 0;      // S^T[b] at b*64
@@ -93,8 +93,8 @@ struct BwdCfg {
 // publishes its index; every consumer warp reads it and releases the slot.
 constexpr int kUnitRing = 4;
 
-struct BwdBars {  // 284 bytes; OFF_BAR reserves 512
-  uint64_t k_full[2], k_empty[2], v_full, v_empty;
+struct BwdBars {  // 268 bytes; OFF_BAR reserves 512
+  uint64_t kv_full, kv_empty;
   uint64_t q_full[3], q_empty[3];
   uint64_t s_full[2], p_full[2], mma2_done[2], s_free[2];
   uint64_t vec_full[3], vec_empty[3];
@@ -177,12 +177,8 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
   float* sVec = reinterpret_cast<float*>(smem + C::OFF_VEC);
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&bars->k_full[i], 1);
-      mbar_init(&bars->k_empty[i], 1);
-    }
-    mbar_init(&bars->v_full, 1);
-    mbar_init(&bars->v_empty, 1);
+    mbar_init(&bars->kv_full, 1);
+    mbar_init(&bars->kv_empty, 1);
     for (int i = 0; i < C::QS; ++i) {
       mbar_init(&bars->q_full[i], 1);
       mbar_init(&bars->q_empty[i], 1);
@@ -273,19 +269,14 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       if (u < 0) break;
       const Unit U = geom(u);
       for (int I = 0; I < U.n_all; ++I) {
-        if (I % U.n_iter == 0) {
-          // next KV head G: K into buffer G & 1 once head G-2's dQ^T MMAs are
-          // done; V once head G-1's last dP^T MMA is
-          const int gl = I / U.n_iter, G = G0 + gl, kb = G & 1;
-          if (G >= 2) mbar_wait(&bars->k_empty[kb], ((G >> 1) - 1) & 1);
-          mbar_expect_tx_w(&bars->k_full[kb], C::KV_BYTES);
-          for (int s = 0; s < C::SLABS; ++s)
-            tma_load_3d_w(sK + kb * C::KV_BYTES + s * C::KV_SLAB, &tmK, &bars->k_full[kb], s * 64,
-                          U.g0 + gl, U.kt.x);
-          if (G >= 1) mbar_wait(&bars->v_empty, (G - 1) & 1);
-          mbar_expect_tx_w(&bars->v_full, C::KV_BYTES);
-          for (int s = 0; s < C::SLABS; ++s)
-            tma_load_3d_w(sV + s * C::KV_SLAB, &tmV, &bars->v_full, s * 64, U.g0 + gl, U.kt.x);
+        if (I % U.n_iter == 0) {            // next KV head: K/V once the last reader is done
+          const int gl = I / U.n_iter, G = G0 + gl;
+          if (G > 0) mbar_wait(&bars->kv_empty, (G - 1) & 1);
+          mbar_expect_tx_w(&bars->kv_full, 2 * C::KV_BYTES);
+          for (int s = 0; s < C::SLABS; ++s) {
+            tma_load_3d_w(sK + s * C::KV_SLAB, &tmK, &bars->kv_full, s * 64, U.g0 + gl, U.kt.x);
+            tma_load_3d_w(sV + s * C::KV_SLAB, &tmV, &bars->kv_full, s * 64, U.g0 + gl, U.kt.x);
+          }
         }
         const int Ig = I0 + I, st = Ig % C::QS;
         const int h = tile_h(U, I), row = tile_row(U, I);
@@ -305,107 +296,92 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     // whole warp; one elected lane issues
     const uint32_t k_b = smem_u32(sK), v_b = smem_u32(sV), q_b = smem_u32(sQ),
                    do_b = smem_u32(sDO), ds_b = smem_u32(sDS);
-    // S^T / dP^T of unit-local tile I (first MMA group); Ig = CTA-global tile,
-    // G = CTA-global KV head
-    auto first_half = [&](const Unit& U, int Ig, int G) {
-      const int b = Ig & 1, st = Ig % C::QS;
-      const uint32_t kbuf = k_b + (G & 1) * C::KV_BYTES;
-      mbar_wait(&bars->q_full[st], (Ig / C::QS) & 1);
-      TRACE(0, Ig);
-      tc_fence_after();
-      const uint32_t qs = q_b + st * C::Q_BYTES, dos = do_b + st * C::Q_BYTES;
-      // S^T[b] was last read by the compute warps of tile I-2 (before p_full,
-      // already waited); dP^T[b] also held dQ^T of tile I-2, so only the dP
-      // half waits for the drain warps.
-#pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {   // contract over D: K-major both
-        const uint32_t ko = (kk >> 2) * C::KV_SLAB + (kk & 3) * 32;
-        const uint32_t qo = (kk >> 2) * C::Q_SLAB + (kk & 3) * 32;
-        mma_ss_w(tmem + C::COL_S + b * 64, sdesc_sw128(kbuf + ko, 16, 1024),
-                 sdesc_sw128(qs + qo, 16, 1024), C::IDESC_ST, kk > 0);
-      }
-      if (Ig >= 2) mbar_wait_fast(&bars->s_free[b], ((Ig - 2) >> 1) & 1);
-      TRACE(1, Ig);
-      tc_fence_after();
-#pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
-        const uint32_t ko = (kk >> 2) * C::KV_SLAB + (kk & 3) * 32;
-        const uint32_t qo = (kk >> 2) * C::Q_SLAB + (kk & 3) * 32;
-        mma_ss_w(tmem + C::COL_DP + b * 64, sdesc_sw128(v_b + ko, 16, 1024),
-                 sdesc_sw128(dos + qo, 16, 1024), C::IDESC_ST, kk > 0);
-      }
-      mma_commit_w(&bars->s_full[b]);
-    };
-    // dQ^T, dV, dK of unit-local tile J (second MMA group)
-    auto second_half = [&](const Unit& U, int J, int Jg, int G) {
-      const int b = Jg & 1, st = Jg % C::QS, j = J % U.n_iter;
-      const uint32_t kbuf = k_b + (G & 1) * C::KV_BYTES;
-      mbar_wait_fast(&bars->p_full[b], (Jg >> 1) & 1);
-      TRACE(2, Jg);
-      tc_fence_after();
-      const uint32_t qs = q_b + st * C::Q_BYTES, dos = do_b + st * C::Q_BYTES;
-      const uint32_t dss = ds_b + b * C::T_BYTES;
-      // dQ^T first: it lands in the dP^T[b] columns (free once the compute
-      // warps loaded dP^T), so the drain of tile J overlaps dV/dK(J) and
-      // S(J+2) instead of stalling dP(J+2).
-#pragma unroll
-      for (int kk = 0; kk < C::BN / 16; ++kk) {   // contract over keys
-        mma_ss_w(tmem + C::COL_DP + b * 64, sdesc_sw128(kbuf + kk * 2048, C::KV_SLAB, 1024),
-                 sdesc_sw128(dss + kk * 2048, C::KV_SLAB, 1024), C::IDESC_DQT, kk > 0);
-      }
-      mma_commit_w(&bars->mma2_done[b]);
-      // P^T / dS^T (packed bf16) sit in the S^T[b] columns: queries
-      // [32c, 32c+32) at column 32c (P) and 32c+16 (dS), 8 columns per K16
-#pragma unroll
-      for (int kk = 0; kk < C::BM / 16; ++kk) {   // contract over queries (A from TMEM)
-        const uint32_t acc = (j > 0) || (kk > 0);
-        const uint32_t ca = C::COL_S + b * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
-        mma_ts_w(tmem + C::COL_DV, tmem + ca,
-                 sdesc_sw128(dos + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
-        mma_ts_w(tmem + C::COL_DK, tmem + ca + 16,
-                 sdesc_sw128(qs + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
-      }
-      mma_commit_w(&bars->q_empty[st]);
-      if (j == U.n_iter - 1) {                  // last tile of this KV head
-        mma_commit_w(&bars->acc_done);
-        mma_commit_w(&bars->k_empty[G & 1]);
-      }
-    };
-    // Pipelined one tile deep: S/dP of tile I is issued before dQ/dV/dK of
-    // tile I-1 within a KV head.  At a head (or unit) boundary the previous
-    // head's last tile completes first; the next head's K is already in the
-    // other buffer and its V load started after the previous head's last
-    // dP^T, so the boundary costs little more than the V load's tail.
-    Unit P;                       // unit of the pending second group
-    int pJ = -1, pJg = 0, pG = 0;
     int I0 = 0, G0 = 0;
     for (int seq = 0;; ++seq) {
       const int u = next_unit(seq);
       if (u < 0) break;
       const Unit U = geom(u);
-      for (int I = 0; I < U.n_all; ++I) {
-        const int G = G0 + I / U.n_iter;
-        if (I % U.n_iter == 0) {
-          // new KV head: finish the previous head's last tile first (its dQ
-          // drain and dK/dV epilogue then overlap the wait for this head's V,
-          // whose load started after the previous head's last dP^T)
-          if (pJ >= 0) second_half(P, pJ, pJg, pG);
-          pJ = -1;
-          mbar_wait(&bars->k_full[G & 1], (G >> 1) & 1);
-          mbar_wait(&bars->v_full, G & 1);
+      // S^T / dP^T of tile I (first MMA group)
+      auto first_half = [&](int I) {
+        const int Ig = I0 + I;
+        const int b = Ig & 1, st = Ig % C::QS;
+        mbar_wait(&bars->q_full[st], (Ig / C::QS) & 1);
+        TRACE(0, Ig);
+        tc_fence_after();
+        const uint32_t qs = q_b + st * C::Q_BYTES, dos = do_b + st * C::Q_BYTES;
+        // S^T[b] was last read by the compute warps of tile I-2 (before p_full,
+        // already waited); dP^T[b] also held dQ^T of tile I-2, so only the dP
+        // half waits for the drain warps.
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {   // contract over D: K-major both
+          const uint32_t ko = (kk >> 2) * C::KV_SLAB + (kk & 3) * 32;
+          const uint32_t qo = (kk >> 2) * C::Q_SLAB + (kk & 3) * 32;
+          mma_ss_w(tmem + C::COL_S + b * 64, sdesc_sw128(k_b + ko, 16, 1024),
+                   sdesc_sw128(qs + qo, 16, 1024), C::IDESC_ST, kk > 0);
         }
-        first_half(U, I0 + I, G);
-        if (I % U.n_iter == U.n_iter - 1) mma_commit_w(&bars->v_empty);   // last dP^T of head G
-        if (pJ >= 0) second_half(P, pJ, pJg, pG);
-        P = U;
-        pJ = I;
-        pJg = I0 + I;
-        pG = G;
+        if (Ig >= 2) mbar_wait_fast(&bars->s_free[b], ((Ig - 2) >> 1) & 1);
+        TRACE(1, Ig);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t ko = (kk >> 2) * C::KV_SLAB + (kk & 3) * 32;
+          const uint32_t qo = (kk >> 2) * C::Q_SLAB + (kk & 3) * 32;
+          mma_ss_w(tmem + C::COL_DP + b * 64, sdesc_sw128(v_b + ko, 16, 1024),
+                   sdesc_sw128(dos + qo, 16, 1024), C::IDESC_ST, kk > 0);
+        }
+        mma_commit_w(&bars->s_full[b]);
+      };
+      // dQ^T, dV, dK of tile J (second MMA group)
+      auto second_half = [&](int J) {
+        const int Jg = I0 + J;
+        const int b = Jg & 1, st = Jg % C::QS, j = J % U.n_iter;
+        mbar_wait_fast(&bars->p_full[b], (Jg >> 1) & 1);
+        TRACE(2, Jg);
+        tc_fence_after();
+        const uint32_t qs = q_b + st * C::Q_BYTES, dos = do_b + st * C::Q_BYTES;
+        const uint32_t dss = ds_b + b * C::T_BYTES;
+        // dQ^T first: it lands in the dP^T[b] columns (free once the compute
+        // warps loaded dP^T), so the drain of tile J overlaps dV/dK(J) and
+        // S(J+2) instead of stalling dP(J+2).
+#pragma unroll
+        for (int kk = 0; kk < C::BN / 16; ++kk) {   // contract over keys
+          mma_ss_w(tmem + C::COL_DP + b * 64, sdesc_sw128(k_b + kk * 2048, C::KV_SLAB, 1024),
+                   sdesc_sw128(dss + kk * 2048, C::KV_SLAB, 1024), C::IDESC_DQT, kk > 0);
+        }
+        mma_commit_w(&bars->mma2_done[b]);
+        // P^T / dS^T (packed bf16) sit in the S^T[b] columns: queries
+        // [32c, 32c+32) at column 32c (P) and 32c+16 (dS), 8 columns per K16
+#pragma unroll
+        for (int kk = 0; kk < C::BM / 16; ++kk) {   // contract over queries (A from TMEM)
+          const uint32_t acc = (j > 0) || (kk > 0);
+          const uint32_t ca = C::COL_S + b * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
+          mma_ts_w(tmem + C::COL_DV, tmem + ca,
+                   sdesc_sw128(dos + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
+          mma_ts_w(tmem + C::COL_DK, tmem + ca + 16,
+                   sdesc_sw128(qs + kk * 2048, C::Q_SLAB, 1024), C::IDESC_ACC, acc);
+        }
+        mma_commit_w(&bars->q_empty[st]);
+        if (j == U.n_iter - 1) {                  // last tile of this KV head
+          mma_commit_w(&bars->acc_done);
+          mma_commit_w(&bars->kv_empty);
+        }
+      };
+      // Pipelined one tile deep (S/dP of tile I before dQ/dV/dK of tile I-1),
+      // except across a KV-head (or unit) boundary: tile I of the next head
+      // needs the new K/V, which may only land after the last reader of the
+      // old ones.
+      for (int I = 0; I <= U.n_all; ++I) {
+        const bool head_start = I < U.n_all && I % U.n_iter == 0;
+        if (I < U.n_all && !head_start) first_half(I);
+        if (I >= 1) second_half(I - 1);
+        if (head_start) {
+          mbar_wait(&bars->kv_full, (G0 + I / U.n_iter) & 1);
+          first_half(I);
+        }
       }
       I0 += U.n_all;
       G0 += U.nh;
     }
-    if (pJ >= 0) second_half(P, pJ, pJg, pG);
   } else if (warp == 3) {
     // ------------------------------------------------- per-query vectors --
     int I0 = 0;

@@ -119,21 +119,26 @@ def main():
         plan = wl.build_shard_plan([lengths], world, policy)
         shard = shard_for_rank(plan, 0, rank)
         idx = shard.gather_local.long().cpu()
-        ql = q[idx].to(dev).requires_grad_(True)
-        kl = k[idx].to(dev).requires_grad_(True)
-        vl = v[idx].to(dev).requires_grad_(True)
-        o = cp_doc_attention(ql, kl, vl, shard)
-        o.backward(do[idx].to(dev))
-        torch.cuda.synchronize()
         full = [(p, 0, x) for p, x in enumerate(lengths)]
         ro, _, rdq, rdk, rdv = ao.segment_attention_fwd_bwd(q, k, v, do, lengths, full)
-        for name, got, ref in (("o", o, ro[idx]), ("dq", ql.grad, rdq[idx]),
-                               ("dk", kl.grad, rdk[idx]), ("dv", vl.grad, rdv[idx])):
-            ok, msg = check(name, got, ref)
-            tag = f"[rank {rank} {policy} {shard.strategy.value} hq={hq} hkv={hkv} d={d}] {msg}"
-            print(tag, flush=True)
-            if not ok:
-                failures.append(tag)
+        symm = SymmExchange(dist.group.WORLD, sum(lengths), hkv, d, dev)
+        for xname, xch in (("nccl", None), ("symm-groups", symm)):
+            for rep in range(3):            # slots reused (epochs advance)
+                ql = q[idx].to(dev).requires_grad_(True)
+                kl = k[idx].to(dev).requires_grad_(True)
+                vl = v[idx].to(dev).requires_grad_(True)
+                o = cp_doc_attention(ql, kl, vl, shard, exchange=xch)
+                o.backward(do[idx].to(dev))
+                torch.cuda.synchronize()
+                for name, got, ref in (("o", o, ro[idx]), ("dq", ql.grad, rdq[idx]),
+                                       ("dk", kl.grad, rdk[idx]), ("dv", vl.grad, rdv[idx])):
+                    ok, msg = check(name, got, ref)
+                    tag = (f"[rank {rank} {xname} {policy} {shard.strategy.value} hq={hq} "
+                           f"hkv={hkv} d={d} rep {rep}] {msg}")
+                    if rep == 0:
+                        print(tag, flush=True)
+                    if not ok:
+                        failures.append(tag)
     failures += pipeline_cases(rank, world, dev)
     dist.barrier()
     dist.destroy_process_group()

@@ -21,7 +21,7 @@ import pytest
 import torch
 
 import paper_2503_17924_b200 as wl
-from paper_2503_17924_b200.attention import attn_backward, attn_forward
+from paper_2503_17924_b200.attention import attn_backward, attn_forward, bwd_workspace
 from paper_2503_17924_b200.cp import LocalPeersExchange, shard_for_rank
 from oracle import attention_oracle as ao
 from oracle import shard_oracle as so
@@ -40,13 +40,13 @@ def _close(got, ref, tag):
     assert excess <= 0, f"{tag}: max abs err {err.max().item():.3e}, excess {excess:.3e}"
 
 
-def _run_group(cp, policy, hq, hkv, d, covered=True, passes=2, seed=0):
+def _run_group(cp, policy, hq, hkv, d, covered=True, passes=2, seed=0, groups=None):
     dev = torch.device("cuda")
     mbs = [so.pad_lengths_for_cp(x, cp) for x in MBS]
     plan = wl.build_shard_plan(mbs, cp, policy)
     shards = [[shard_for_rank(plan, b, r) for r in range(cp)] for b in range(len(mbs))]
     t_max = max(sum(x) for x in mbs)
-    ex = LocalPeersExchange.create(cp, t_max, hkv, d, dev, fill=float("nan"))
+    ex = LocalPeersExchange.create(cp, t_max, hkv, d, dev, fill=float("nan"), groups=groups)
     for e in ex:
         e.push_covered = e.pull_covered = covered
     g = torch.Generator(device=dev).manual_seed(seed)
@@ -65,14 +65,23 @@ def _run_group(cp, policy, hq, hkv, d, covered=True, passes=2, seed=0):
                     for r in range(cp)]
             parts = []
             for r in range(cp):
+                # the CP pipeline's head-group flow: each group's attention
+                # gated by the peers' KV flags, each group's partials signalled
                 sh = shards[b][r]
                 ql, dol = q[idx[r]].contiguous(), do[idx[r]].contiguous()
-                o, lse = attn_forward(ql, full[r][0], full[r][1], sh.tiles)
+                o = lse = None
+                for gi, grp in enumerate(ex[r].groups):
+                    ex[r].wait_kv(b, gi)
+                    o, lse = attn_forward(ql, full[r][0], full[r][1], sh.tiles, kv_heads=grp,
+                                          out=None if o is None else (o, lse))
                 dk_out, dv_out = ex[r].dkv_out(sh, b, cur)
-                dq, dkf, dvf = attn_backward(ql, full[r][0], full[r][1], o, lse, dol, sh.tiles,
-                                             dk_out=dk_out, dv_out=dv_out,
-                                             covered_only=ex[r].pull_covered)
-                parts.append((o, dq, dkf, dvf))
+                dq, ws = torch.empty_like(ql), bwd_workspace(ql, full[r][0], sh.tiles)
+                for gi, grp in enumerate(ex[r].groups):
+                    attn_backward(ql, full[r][0], full[r][1], o, lse, dol, sh.tiles,
+                                  dk_out=dk_out, dv_out=dv_out, covered_only=ex[r].pull_covered,
+                                  kv_heads=grp, dq_out=dq, ws=ws)
+                    ex[r].signal_dkv(b, gi)
+                parts.append((o, dq, dk_out, dv_out))
             outs = []
             for r in range(cp):
                 dk, dv = ex[r].scatter(parts[r][2], parts[r][3], shards[b][r], b)
@@ -94,6 +103,13 @@ def _run_group(cp, policy, hq, hkv, d, covered=True, passes=2, seed=0):
 @pytest.mark.parametrize("cp", [2, 4, 8])
 def test_local_peers_exchange_matches_oracle(cp, policy):
     _run_group(cp, policy, 4, 2, 128)
+
+
+@pytest.mark.parametrize("groups", [1, 3, 8])
+def test_head_groups(groups):
+    """Head-group exchange: KV heads split into 1, 3 (uneven) or 8 groups,
+    each pushed, signalled, attended and pulled on its own."""
+    _run_group(4, "adaptive", 16, 8, 64, passes=1, seed=5, groups=groups)
 
 
 @pytest.mark.parametrize("cp", [4, 8])
