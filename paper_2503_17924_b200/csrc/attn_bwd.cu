@@ -219,6 +219,11 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     U.nh = min(hpc, g_end - U.g0);
     U.qt_per_head = (U.kt.w - U.kt.z + C::BM - 1) / C::BM;
     U.n_iter = U.qt_per_head * group;  // query tiles per KV head
+    // unit invariants: a non-empty row suffix inside [0, Tl), 1..128 keys of
+    // one document from position k0, KV heads inside the launch's range
+    WLB_DCHECK(U.kt.z >= 0 && U.kt.z < U.kt.w && U.kt.w <= Tl);
+    WLB_DCHECK(U.kt.y >= 1 && U.kt.y <= C::BN && U.kt.x >= 0 && U.k0 >= 0);
+    WLB_DCHECK(U.g0 >= g_begin && U.nh >= 1 && U.g0 + U.nh <= g_end && g_end <= Hkv);
     U.n_all = U.n_iter * U.nh;
     return U;
   };
@@ -729,6 +734,8 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
   if (item >= n_kv_tiles[0]) return;
   int4 kt = kv_tiles[2 * item];
   int k0 = kv_tiles[2 * item + 1].x;
+  WLB_DCHECK(kt.z >= 0 && kt.z < kt.w && kt.w <= Tl && kt.y >= 1 && kt.y <= 128 && k0 >= 0);
+  WLB_DCHECK(g >= 0 && g < Hkv);
   bool paired = false;
   if (PAIR) {
     const int4 t2 = kv_tiles[2 * item + 1];
@@ -1501,27 +1508,26 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   //  slower: the S/dP -> compute -> dV/dK/dQ serialisation costs more than the
   //  SMEM bandwidth it saves.)
   WLB_SMEM_ATTR((attn_bwd_kernel<D, 2>), C::SMEM);
+  // several KV heads per unit for short row-sets (< WLB_HPC_ROWS local rows
+  // per document on average): a unit's heads run back to back (only with >= 6
+  // waves of units: Tl/128 bounds the KV tiles from below)
+  const int hpc = (g_count % g_bwd_hpc_short == 0 && (long long)Tl < (long long)WLB_HPC_ROWS * (n_docs > 0 ? n_docs : 1) &&
+                   (long long)(Tl / 128) * g_count >= 6LL * 148 * g_bwd_hpc_short)
+                      ? g_bwd_hpc_short : 1;
+  const int n_units = max_items * ((g_count + hpc - 1) / hpc);
   if (g_bwd_persistent) {
-    // one CTA per SM taking (KV tile, KV head) units from a global counter:
-    // a unit's tail (dK/dV epilogue, next K/V load) overlaps the next unit
-    // instead of a CTA teardown + launch, and the SMs stay busy to the end
+    // one CTA per SM taking units from a global counter: a unit's tail
+    // (dK/dV epilogue, next K/V load) overlaps the next unit instead of a CTA
+    // teardown + launch, and the SMs stay busy to the end
     int dev = 0, sms = 148;
     WLB_CUDA_TRY(cudaGetDevice(&dev));
     WLB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int n_units = max_items * g_count;
     WLB_CUDA_TRY(cudaMemsetAsync(w.sched, 0, sizeof(int), stream));
     attn_bwd_kernel<D, 2><<<(unsigned)std::min(n_units, sms), C::THREADS, C::SMEM, stream>>>(
         tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
-        Hkv, max_items, 1, n_units, w.sched, 1, g_begin, g_begin + g_count, scale,
+        Hkv, max_items, hpc, n_units, w.sched, 1, g_begin, g_begin + g_count, scale,
         scale * 1.4426950408889634f, dkv_bf16);
   } else {
-    // several KV heads per CTA for short row-sets (< 2048 local rows per
-    // document on average): the next head's loads overlap this head's tail
-    // (only with >= 6 waves of CTAs left: Tl/128 bounds the KV tiles from below)
-    const int hpc = (g_count % g_bwd_hpc_short == 0 && (long long)Tl < (long long)WLB_HPC_ROWS * (n_docs > 0 ? n_docs : 1) &&
-                     (long long)(Tl / 128) * g_count >= 6LL * 148 * g_bwd_hpc_short)
-                        ? g_bwd_hpc_short : 1;
-    const int n_units = max_items * ((g_count + hpc - 1) / hpc);
     attn_bwd_kernel<D, 2><<<(unsigned)n_units, C::THREADS, C::SMEM, stream>>>(
         tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
         Hkv, max_items, hpc, n_units, w.sched, 0, g_begin, g_begin + g_count, scale,

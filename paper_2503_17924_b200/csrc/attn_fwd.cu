@@ -114,6 +114,12 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
   if (item >= n_items[0]) return;
   const int nh = min(hpc, h_end - h0);
   const int4 tx = items[2 * item], ty = items[2 * item + 1];
+  // item invariants: rows inside [0, Tl), tile Y directly before X, KV
+  // extents past kv_begin
+  WLB_DCHECK(tx.x >= 0 && tx.y >= 1 && tx.y <= 128 && tx.x + tx.y <= Tl);
+  WLB_DCHECK(ty.y == 0 || (ty.y <= 128 && ty.x >= 0 && ty.x + ty.y == tx.x));
+  WLB_DCHECK(tx.w > tx.z && (ty.y == 0 || (ty.z > tx.z && ty.z <= tx.w)));
+  WLB_DCHECK(h0 >= 0 && h0 < h_end && h_end <= Hq);
   // tile 0 = X {row0, nrows, kv_end}, tile 1 = Y
   const int kv_begin = tx.z;
   const int n_kv[2] = {(tx.w - kv_begin + C::BN - 1) / C::BN,
@@ -276,6 +282,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       const bool valid = r < tt.y;
       const int row = tt.x + r;
       const int lim0 = (valid ? positions[row] : 0) + 1;   // allowed keys from kv_begin
+      WLB_DCHECK(!valid || lim0 <= nkv * C::BN);
       const uint32_t lane_base = tmem + ((uint32_t)(wq * 32) << 16);
       const uint32_t s_col = lane_base + C::COL_S + t * 128;
       const uint32_t o_col = lane_base + C::COL_O + t * D;

@@ -32,6 +32,24 @@ void set_error(const char* fmt, ...);
     }                                                                             \
   } while (0)
 
+// Device-side bounds checks, compiled in with -DWLB_DEBUG_CHECKS (the
+// checked build, tools/debug_checks.sh; compute-sanitizer is not available
+// on the GPU pool): a violated invariant traps with its location.
+#ifdef WLB_DEBUG_CHECKS
+#define WLB_DCHECK(cond)                                                          \
+  do {                                                                            \
+    if (!(cond)) {                                                                \
+      printf("WLB_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #cond,      \
+             __FILE__, __LINE__, (int)blockIdx.x, (int)threadIdx.x);              \
+      __trap();                                                                   \
+    }                                                                             \
+  } while (0)
+#else
+#define WLB_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
 // the attribute is per-device state, so the "done" flag is a bit per device
 // of the calling thread's current device (up to 64 devices).

@@ -83,6 +83,7 @@ __global__ void kv_push_kernel(const int4* __restrict__ k, const int4* __restric
   for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
        r += warps) {
     const long long g = gidx[r];
+    WLB_DCHECK(g >= 0 && g < n_rows * cp);      // every rank holds T / cp rows
     const unsigned mask = COVERED ? covering_ranks<true>((int)g, lane, cp, rowset_all, rs, pos_all,
                                                          n_rows, doc_start, n_docs)
                                   : 0xffffffffu;
@@ -121,6 +122,7 @@ __global__ void dkv_pull_kernel(const unsigned long long* __restrict__ bases, lo
   for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
        r += warps) {
     const int g = gidx[r];
+    WLB_DCHECK(g >= 0 && g < n_rows * cp);
     const unsigned mask = COVERED ? covering_ranks<false>(g, lane, cp, rowset_all, rs, pos_all, tl,
                                                           doc_start, n_docs)
                                   : 0xffffffffu;
