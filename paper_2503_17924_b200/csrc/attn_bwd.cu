@@ -1181,7 +1181,7 @@ __global__ void __launch_bounds__(256) bwd_delta_kernel(const __nv_bfloat16* __r
     for (int u = 0; u < U; ++u) {
       const long long w = w0 + u * lanes;
       if (w < n) {
-        const long long rh = (w / h_count) * Hq + h_begin + w % h_count;
+        const long long rh = h_count == Hq ? w : (w / h_count) * Hq + h_begin + w % h_count;
         a[u] = reinterpret_cast<const uint4*>(o + rh * D)[sub];
         b[u] = reinterpret_cast<const uint4*>(dout + rh * D)[sub];
       } else {
@@ -1201,37 +1201,47 @@ __global__ void __launch_bounds__(256) bwd_delta_kernel(const __nv_bfloat16* __r
 #pragma unroll
       for (int off = LPR / 2; off; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
       const long long w = w0 + u * lanes;
-      if (sub == 0 && w < n) delta[(size_t)(h_begin + w % h_count) * Tl + (w / h_count)] = sum;
+      if (sub == 0 && w < n) {
+        const unsigned uw = (unsigned)w;          // Tl * Hq < 2^31
+        delta[(size_t)(h_begin + uw % (unsigned)h_count) * Tl + uw / (unsigned)h_count] = sum;
+      }
     }
   }
 }
 
 // v3 dQ accumulator [Hq][D/4][Tl][4] fp32 -> dq [Tl][Hq][D] bf16, heads
-// [h_begin, h_begin + h_count)
+// [h_begin, h_begin + h_count).  32-bit index math with D a template
+// constant (a 64-bit division per element cost ~6% of a short rank's step).
+template <int D>
 __global__ void dq_convert3_kernel(const float4* __restrict__ acc, uint2* __restrict__ dq, int Tl,
-                                   int Hq, int D, int h_begin, int h_count) {
-  const long long n = (long long)Tl * h_count * (D / 4);
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int db = (int)(i % (D / 4));           // output-ordered: consecutive threads write
-    const long long rh = i / (D / 4);            // consecutive 8-B pieces of a row
-    const int h = h_begin + (int)(rh % h_count), row = (int)(rh / h_count);
-    const float4 v = acc[((long long)h * (D / 4) + db) * Tl + row];
+                                   int Hq, int h_begin, int h_count) {
+  constexpr unsigned DB = D / 4;
+  const unsigned n = (unsigned)Tl * (unsigned)h_count * DB;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const unsigned db = i % DB;                  // output-ordered: consecutive threads write
+    const unsigned rh = i / DB;                  // consecutive 8-B pieces of a row
+    const unsigned hh = rh % (unsigned)h_count, row = rh / (unsigned)h_count;
+    const unsigned h = h_begin + hh;
+    const float4 v = acc[((size_t)h * DB + db) * Tl + row];
     __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
-    dq[((long long)row * Hq + h) * (D / 4) + db] =
+    dq[((size_t)row * Hq + h) * DB + db] =
         make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
   }
 }
 
-// v2 dQ accumulator [Tl][Hq][D] fp32 -> dq bf16, heads [h_begin, h_begin + h_count)
+// v2 dQ accumulator [Tl][Hq][D] fp32 -> dq bf16, heads [h_begin, h_begin +
+// h_count); all heads (the common case) is one flat pass.
+template <int D>
 __global__ void dq_convert_kernel(const float4* __restrict__ acc, __nv_bfloat162* __restrict__ dq,
-                                  int Tl, int Hq, int D, int h_begin, int h_count) {
-  const long long n = (long long)Tl * h_count * (D / 4);
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int db = (int)(i % (D / 4));
-    const long long rh = i / (D / 4);
-    const long long j = ((rh / h_count) * Hq + h_begin + rh % h_count) * (D / 4) + db;
+                                  int Tl, int Hq, int h_begin, int h_count) {
+  constexpr unsigned DB = D / 4;
+  const unsigned n = (unsigned)Tl * (unsigned)h_count * DB;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    size_t j = i;
+    if (h_count != Hq) {
+      const unsigned rh = i / DB;
+      j = ((size_t)(rh / (unsigned)h_count) * Hq + h_begin + rh % (unsigned)h_count) * DB + i % DB;
+    }
     const float4 v = acc[j];
     dq[2 * j] = __floats2bfloat162_rn(v.x, v.y);
     dq[2 * j + 1] = __floats2bfloat162_rn(v.z, v.w);
@@ -1434,8 +1444,8 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
 #endif
   // dQ accumulator of this launch's query heads: [Hq][D/4][Tl][4] (v3) keeps
   // a head contiguous, [Tl][Hq][D] (v2) strides it
-  if (v3)
-    WLB_CUDA_TRY(cudaMemsetAsync(w.dq_acc + (size_t)h_begin * D * Tl, 0,
+  if (v3 || h_count == Hq)
+    WLB_CUDA_TRY(cudaMemsetAsync(w.dq_acc + (size_t)h_begin * D * (v3 ? Tl : 1), 0,
                                  (size_t)Tl * h_count * D * 4, stream));
   else
     WLB_CUDA_TRY(cudaMemset2DAsync(w.dq_acc + (size_t)h_begin * D, (size_t)Hq * D * 4, 0,
@@ -1538,13 +1548,13 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   const long long n4 = (long long)Tl * h_count * D / 4;
   const unsigned cblocks = (unsigned)std::min<long long>((n4 + 255) / 256, 148 * 16);
   if (v3) {
-    dq_convert3_kernel<<<cblocks, 256, 0, stream>>>((const float4*)w.dq_acc, (uint2*)dq, Tl, Hq, D,
-                                                     h_begin, h_count);
+    dq_convert3_kernel<D><<<cblocks, 256, 0, stream>>>((const float4*)w.dq_acc, (uint2*)dq, Tl, Hq,
+                                                        h_begin, h_count);
     WLB_LAUNCH_CHECK();
     return WLB_OK;
   }
-  dq_convert_kernel<<<cblocks, 256, 0, stream>>>((const float4*)w.dq_acc, (__nv_bfloat162*)dq, Tl,
-                                                 Hq, D, h_begin, h_count);
+  dq_convert_kernel<D><<<cblocks, 256, 0, stream>>>((const float4*)w.dq_acc, (__nv_bfloat162*)dq,
+                                                    Tl, Hq, h_begin, h_count);
   WLB_LAUNCH_CHECK();
   return WLB_OK;
 }
