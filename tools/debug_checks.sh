@@ -9,4 +9,4 @@ out=gpurun_out/debug_checks; mkdir -p $out
 export WLB_LIB_PATH=var/libdbg.so
 timeout 1500 python -m pytest tests -m gpu -q > $out/gpu_tests.txt 2>&1; echo "rc=$?" >> $out/gpu_tests.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke.txt 2>&1; echo "rc=$?" >> $out/smoke.txt
-tail -3 $out/gpu_tests.txt $out/smoke.txt
+tail -n 3 $out/gpu_tests.txt; tail -n 3 $out/smoke.txt
