@@ -370,6 +370,9 @@ def main():
     my_ms = t0.elapsed_time(t1)
     alloc_retries = torch.cuda.memory_stats(dev).get("num_alloc_retries", 0)
     kern_each = [e[0].elapsed_time(e[1]) for e, _ in recs]
+    # per micro-batch kernel time of this rank, mean over the timed steps
+    mb_ms = torch.tensor([sum(kern_each[s * N_SEQ + b] for s in range(args.steps)) / args.steps
+                          for b in range(N_SEQ)], device=dev, dtype=torch.float64)
     my_pairs = sum(sh.pairs for sh in shards)
     total_pairs = sum(sum(x * (x + 1) // 2 for x in ls) for ls in lengths)
     step_flops = 14.0 * d * hq * total_pairs
@@ -379,8 +382,12 @@ def main():
         allv = [torch.empty_like(stats) for _ in range(world)]
         dist.all_gather(allv, stats)
         allv = torch.stack(allv).cpu()
+        allmb = [torch.empty_like(mb_ms) for _ in range(world)]
+        dist.all_gather(allmb, mb_ms)
+        allmb = torch.stack(allmb).cpu()
     else:
         allv = stats.cpu()[None]
+        allmb = mb_ms.cpu()[None]
     max_ms = float(allv[:, 0].max())
     ms_step = max_ms / args.steps
     value = step_flops * args.steps / (max_ms / 1e3) / 1e12
@@ -408,24 +415,38 @@ def main():
         def e2e_step():
             shards = build_cp_shards(lengths, cp, rank, policy, model=model)
             h2d_s.wait_stream(cur)             # previous step is done reading the inputs
-            ready = []
+            ready, bwd_ready = [], []
             with torch.cuda.stream(h2d_s):
+                # k, v, q first (the forward needs them), dO behind them (only
+                # the backward does), micro-batch by micro-batch
                 for b in range(N_SEQ):
-                    for dst, src in zip(ins[b], host_in):
+                    q_d, k_d, v_d, do_d = ins[b]
+                    for dst, src in ((k_d, host_in[1]), (v_d, host_in[2]), (q_d, host_in[0])):
                         dst.copy_(src, non_blocking=True)
                     e = torch.cuda.Event()
                     e.record(h2d_s)
                     ready.append(e)
+                    do_d.copy_(host_in[3], non_blocking=True)
+                    e = torch.cuda.Event()
+                    e.record(h2d_s)
+                    bwd_ready.append(e)
+
+            def d2h_o(b, o, ev):                # O leaves during the backward
+                d2h_s.wait_event(ev)
+                with torch.cuda.stream(d2h_s):
+                    host_out[0].copy_(o, non_blocking=True)
+                    o.record_stream(d2h_s)
 
             def d2h(b, outs, fin):
-                d2h_s.wait_event(fin)           # o, dq (compute) and dk, dv (comm) complete
+                d2h_s.wait_event(fin)           # dq (compute) and dk, dv (comm) complete
                 with torch.cuda.stream(d2h_s):
-                    for src, dst in zip(outs, host_out):
+                    for src, dst in zip(outs[1:], host_out[1:]):
                         src = src if src.dtype == torch.bfloat16 else src.to(torch.bfloat16)
                         dst.copy_(src, non_blocking=True)
                         src.record_stream(d2h_s)
 
-            pipe.run(shards, ins, ready=ready, on_outputs=d2h, keep_outputs=False)
+            pipe.run(shards, ins, ready=ready, bwd_ready=bwd_ready, on_forward=d2h_o,
+                     on_outputs=d2h, keep_outputs=False)
             cur.wait_stream(d2h_s)
 
         e2e_step()
@@ -445,9 +466,9 @@ def main():
         e2e = {"value": round(step_flops * n_e2e / (float(e_ms) / 1e3) / 1e12, 2),
                "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": round(float(e_ms) / n_e2e, 2),
-               "note": "every micro-batch: H2D q,k,v,dO from pinned host, D2H o,dq,dk,dv "
-                       "(copy streams pipelined against compute); shard plan + attention "
-                       "through the public API"}
+               "note": "every micro-batch: H2D k,v,q then dO from pinned host, D2H o "
+                       "(during the backward) then dq,dk,dv (copy streams pipelined against "
+                       "compute); shard plan + attention through the public API"}
 
     if rank != 0:
         if world > 1:
@@ -484,6 +505,7 @@ def main():
         "imbalance": round(imbalance, 4),
         "pair_imbalance": round(pair_imb, 5),
         "rank_kernel_ms": [round(float(x), 3) for x in kt],
+        "rank_mb_kernel_ms": [[round(float(x), 2) for x in row] for row in allmb],
         "kernel_ms": round(kern_ms, 3),
         "roofline": {"kernel": dom[0], "bound": "tensor", "achieved": round(achieved, 1),
                      "peak": peak_sus, "unit": "TFLOP/s", "frac": round(achieved / peak_sus, 4),

@@ -469,8 +469,13 @@ class CPStepPipeline:
     the device by the peers' arrival flags of that group, and the dK/dV pull
     of a group overlaps the backward of the later groups.  Hooks:
 
-    * `ready[b]` (optional CUDA events): micro-batch b's inputs are valid once
+    * `ready[b]` (optional CUDA events): micro-batch b's q, k, v are valid once
       they fire (e.g. H2D copies); by default inputs are taken as resident.
+      `bwd_ready[b]`: the same for dO, waited for only before the backward
+      (so dO can still be in flight during the forward).
+    * `on_forward(b, o, event)` is called once micro-batch b's forward is
+      enqueued; `event` fires when O is complete (e.g. to copy it out during
+      the backward).
     * `on_kernels(b, shard, fn)` wraps the attention kernels (e.g. CUDA events
       for per-rank kernel time; with head groups this includes the device-side
       waits for the peers' K/V of each group).
@@ -508,13 +513,14 @@ class CPStepPipeline:
         return k_full, v_full, ev
 
     def run(self, shards, inputs, scale=None, ready=None, on_kernels=None, on_outputs=None,
-            keep_outputs=True):
+            keep_outputs=True, bwd_ready=None, on_forward=None):
         """inputs[b] = (q, k, v, do) local bf16 tensors.  Returns per micro-batch
         (o, dq, dk, dv) local tensors (dk/dv fp32), complete on the current stream
         (None entries when keep_outputs=False: consume them in on_outputs)."""
         cur = torch.cuda.current_stream()
         n = len(shards)
         rdy = ready if ready is not None else [None] * n
+        brdy = bwd_ready if bwd_ready is not None else [None] * n
         # the covered pull reads only the partial rows each rank's KV tiles
         # wrote: skip the zero fill of the rest
         covered = bool(getattr(self.exchange, "pull_covered", False))
@@ -540,17 +546,25 @@ class CPStepPipeline:
 
             def kernels(q=q, do=do, k_full=k_full, v_full=v_full, sh=sh, dk_out=dk_out,
                         dv_out=dv_out, b=b, flagged=flagged, cov=cov):
+                ex = self.exchange
                 if not flagged:
                     o, lse = attn_forward(q, k_full, v_full, sh.tiles, scale)
+                else:
+                    o, lse = torch.empty_like(q), None
+                    for gi, grp in enumerate(ex.groups):
+                        ex.wait_kv(b, gi)
+                        o, lse = attn_forward(q, k_full, v_full, sh.tiles, scale, kv_heads=grp,
+                                              out=None if lse is None else (o, lse))
+                if on_forward is not None:
+                    fev = torch.cuda.Event()
+                    fev.record(cur)
+                    on_forward(b, o, fev)
+                if brdy[b] is not None:
+                    cur.wait_event(brdy[b])
+                if not flagged:
                     dq, dkf, dvf = attn_backward(q, k_full, v_full, o, lse, do, sh.tiles, scale,
                                                  dk_out, dv_out, covered_only=cov)
                     return o, dq, dkf, dvf
-                ex = self.exchange
-                o, lse = torch.empty_like(q), None
-                for gi, grp in enumerate(ex.groups):
-                    ex.wait_kv(b, gi)
-                    o, lse = attn_forward(q, k_full, v_full, sh.tiles, scale, kv_heads=grp,
-                                          out=None if lse is None else (o, lse))
                 dq, ws = torch.empty_like(q), bwd_workspace(q, k_full, sh.tiles)
                 for gi, grp in enumerate(ex.groups):
                     attn_backward(q, k_full, v_full, o, lse, do, sh.tiles, scale, dk_out, dv_out,
