@@ -198,6 +198,20 @@ int32_t wlb_attn_bwd_persistent(int32_t on);
 int wlb_qkv_rope(const void* y, void* q, void* k, void* v, const int32_t* positions,
                  int32_t Tl, int32_t Hq, int32_t Hkv, int32_t D, float base, void* stream);
 
+/* The projection and RoPE fused into ONE tcgen05 GEMM (D = 128): for local
+ * row i, y = x[rows ? rows[i] : i] @ w (x [x_rows][hidden] bf16, w
+ * [hidden][(Hq + 2 Hkv) * D] bf16, the x @ W orientation), then q / k get
+ * rotate-half RoPE at positions[i] (in-document, as wlb_qkv_rope) and v is
+ * y's value heads; q [Tl][Hq][D], k / v [Tl][Hkv][D] bf16.  rows (device
+ * [Tl], may be NULL) is the rank's gather_local when x holds the
+ * micro-batch's global rows (TMA gather4 loads them).  hidden % 64 == 0,
+ * ((Hq + 2 Hkv) * D) % 256 == 0.  Replaces cuBLAS + wlb_qkv_rope (SURVEY.md
+ * 8f row 3). */
+int wlb_qkv_proj_rope(const void* x, int32_t x_rows, const int32_t* rows, const void* w,
+                      void* q, void* k, void* v, const int32_t* positions, int32_t Tl,
+                      int32_t hidden, int32_t Hq, int32_t Hkv, int32_t D, float base,
+                      void* stream);
+
 /* Row permutations for the CP exchange (rows of row_bytes, 16-B aligned).
  * scatter: dst[index[i]] = src[i];  gather: dst[i] = src[index[i]]. */
 int wlb_rows_scatter(const void* src, void* dst, const int32_t* index, int64_t n_rows,

@@ -9,7 +9,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.environ.get("WLB_LIB_OUT", os.path.join(HERE, "libwlbcp.so"))
-SOURCES = ["abi.cu", "shard_plan.cu", "attn_fwd.cu", "attn_bwd.cu", "cp_exchange.cu", "rope.cu"]
+SOURCES = ["abi.cu", "shard_plan.cu", "attn_fwd.cu", "attn_bwd.cu", "cp_exchange.cu", "rope.cu",
+           "proj_gemm.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

@@ -53,14 +53,35 @@ class CPShard:
         return self.plan.strategy(self.index)
 
 
-def project_qkv(x_local, w_qkv, shard: CPShard, hq: int, hkv: int, d: int,
-                base: float = 10000.0):
-    """The step before the path: this rank's local hidden states x [T/cp, hidden]
-    (rank-local order, `shard.gather_local`) times the fused QKV weight
-    [hidden, (hq + 2*hkv)*d] (a plain cuBLAS GEMM), then one pass that splits
-    the result into THD q, k, v and applies rotary embeddings at each row's
-    in-document position (`shard.tiles.positions`), ready for
-    `cp_doc_attention` / `CPStepPipeline`."""
+def project_qkv(x, w_qkv, shard: CPShard, hq: int, hkv: int, d: int, base: float = 10000.0,
+                gather: bool = False):
+    """The step before the path: this rank's q, k, v (THD bf16) from hidden
+    states and the fused QKV weight w_qkv [hidden, (hq + 2*hkv)*d] (x @ W),
+    with rotary embeddings at each row's in-document position
+    (`shard.tiles.positions`), ready for `cp_doc_attention` / `CPStepPipeline`.
+
+    x: this rank's local hidden states [T/cp, hidden] in local order, or with
+    gather=True the micro-batch's hidden states [T, hidden] in global order
+    (the kernel gathers the rank's rows by `shard.gather_local`).  D = 128:
+    one tcgen05 kernel (`wlb_qkv_proj_rope`: projection, gather and RoPE
+    fused); other D: a library GEMM then `wlb_qkv_rope`."""
+    tl = shard.gather_local.numel()
+    if d == 128:
+        for name, t in (("x", x), ("w_qkv", w_qkv)):
+            if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous() or t.dim() != 2:
+                raise ValueError(f"{name} must be a contiguous 2-D CUDA bf16 tensor")
+        if w_qkv.shape != (x.shape[1], (hq + 2 * hkv) * d):
+            raise ValueError("w_qkv must be [hidden, (hq + 2*hkv)*d]")
+        q = torch.empty((tl, hq, d), dtype=torch.bfloat16, device=x.device)
+        k = torch.empty((tl, hkv, d), dtype=torch.bfloat16, device=x.device)
+        v = torch.empty_like(k)
+        p = _native.ptr
+        _native.check(_native.lib().wlb_qkv_proj_rope(
+            p(x), x.shape[0], p(shard.gather_local) if gather else None, p(w_qkv), p(q), p(k),
+            p(v), p(shard.tiles.positions), tl, x.shape[1], hq, hkv, d, float(base),
+            _native.stream_ptr()), "wlb_qkv_proj_rope")
+        return q, k, v
+    x_local = x[shard.gather_local.long()] if gather else x
     y = torch.matmul(x_local, w_qkv)
     return qkv_rope(y, shard.tiles.positions, hq, hkv, d, base)
 

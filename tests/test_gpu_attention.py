@@ -175,13 +175,17 @@ def _rope_ref(x, pos, base):
     return torch.cat((a * c - b * s, b * c + a * s), dim=-1)
 
 
+@pytest.mark.parametrize("gather", [False, True])
+@pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("cp,policy", [(1, "per_document"), (2, "per_document"), (4, "per_sequence")])
-def test_project_qkv_rope_in_document_positions(cp, policy):
+def test_project_qkv_rope_in_document_positions(cp, policy, d, gather):
     """QKV projection + RoPE at in-document positions vs a torch fp32 reference:
-    every document restarts at rotary position 0 on every rank."""
+    every document restarts at rotary position 0 on every rank.  D = 128 runs
+    the fused tcgen05 kernel (projection, TMA gather4 of the rank's rows from
+    global-order x with gather=True, RoPE epilogue); D = 64 the two-step path."""
     from paper_2503_17924_b200.cp import project_qkv, shard_for_rank
     lengths = so.pad_lengths_for_cp([700, 1, 257, 3000, 64], cp)
-    hq, hkv, d, hidden = 4, 2, 128, 256
+    hq, hkv, hidden = 4, 2, 320
     plan = wl.build_shard_plan([lengths], cp, policy)
     g = torch.Generator().manual_seed(41)
     w = (torch.randn(hidden, (hq + 2 * hkv) * d, generator=g) / hidden ** 0.5).to(torch.bfloat16)
@@ -191,7 +195,8 @@ def test_project_qkv_rope_in_document_positions(cp, policy):
         sh = shard_for_rank(plan, 0, r)
         idx = sh.gather_local.long().cpu()
         xl = x_all[idx]
-        q, k, v = project_qkv(xl.to(dev), w.to(dev), sh, hq, hkv, d, base=500000.0)
+        x_in = x_all.to(dev) if gather else xl.to(dev)
+        q, k, v = project_qkv(x_in, w.to(dev), sh, hq, hkv, d, base=500000.0, gather=gather)
         y = (xl.float() @ w.float()).view(-1, hq + 2 * hkv, d)
         # in-document positions of the rank's rows, recomputed on the host
         starts = [0]
@@ -203,6 +208,35 @@ def test_project_qkv_rope_in_document_positions(cp, policy):
         _close(q, _rope_ref(y[:, :hq], pos, 500000.0), "q")
         _close(k, _rope_ref(y[:, hq:hq + hkv], pos, 500000.0), "k")
         _close(v, y[:, hq + hkv:], "v")
+
+
+def test_fused_projection_config_shape():
+    """The fused kernel at the Llama-7B projection shape (hidden 4096, 32 + 2 x 32
+    heads) on a CP=8 rank of a 128K micro-batch, gathering from global rows,
+    against fp32 (a subsample of rows checked)."""
+    from paper_2503_17924_b200.cp import project_qkv, shard_for_rank
+    lengths = _bench_lengths(131072, 3)
+    plan = wl.build_shard_plan([lengths], 8, "per_document")
+    sh = shard_for_rank(plan, 0, 0)
+    hq = hkv = 32
+    d, hidden = 128, 4096
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(7)
+    x = torch.randn(sum(lengths), hidden, generator=g, device=dev).to(torch.bfloat16)
+    w = (torch.randn(hidden, (hq + 2 * hkv) * d, generator=g, device=dev) / 64).to(torch.bfloat16)
+    q, k, v = project_qkv(x, w, sh, hq, hkv, d, base=10000.0, gather=True)
+    rows = torch.arange(0, sh.gather_local.numel(), 97, device=dev)
+    xl = x[sh.gather_local.long()[rows]].float()
+    y = (xl @ w.float()).view(-1, hq + 2 * hkv, d).cpu()
+    pos = sh.tiles.positions[rows].cpu()
+    _close(q[rows], _rope_ref(y[:, :hq], pos, 10000.0), "q")
+    _close(k[rows], _rope_ref(y[:, hq:hq + hkv], pos, 10000.0), "k")
+    _close(v[rows], y[:, hq + hkv:], "v")
+
+
+def _bench_lengths(window, index):
+    spec = wl.SyntheticSpec(context_window=window, tokens_per_global_batch=window)
+    return [doc.length for doc in wl.generate_synthetic_stream(spec, 0, index + 1)[index]]
 
 
 @pytest.mark.parametrize("d", [64, 128])
