@@ -5,7 +5,8 @@ cd "$(dirname "$0")/.."
 N=$(nvidia-smi -L | wc -l)
 out=gpurun_out/abm_n$N; mkdir -p $out
 for rep in 1 2; do
-  (cd var/r01 && timeout 900 python bench.py --gpus $N --steps 5 --warmup 3 --no-e2e > ../../$out/r01_$rep.json 2>/dev/null) || (cd var/r01 && timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr=127.0.0.1 --master-port=2960$rep bench.py --gpus $N --steps 5 --warmup 3 --no-e2e > ../../$out/r01_$rep.json 2>/dev/null)
+  # (the round-1 bench.py does not launch torchrun itself)
+  (cd var/r01 && timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr=127.0.0.1 --master-port=2960$rep bench.py --gpus $N --steps 5 --warmup 3 --no-e2e > ../../$out/r01_$rep.json 2>/dev/null)
   timeout 900 python bench.py --gpus $N --steps 5 --warmup 3 --no-e2e > $out/cur_$rep.json 2>/dev/null
   WLB_XCHG_DKV=bf16 timeout 900 python bench.py --gpus $N --steps 5 --warmup 3 --no-e2e > $out/curbf16_$rep.json 2>/dev/null
 done
