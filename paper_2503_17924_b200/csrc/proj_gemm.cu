@@ -21,9 +21,10 @@
 //               buffered in TMEM (2 x 256 columns) so tile t's epilogue overlaps
 //               tile t+1's main loop
 //   warp 2      TMEM allocator
-//   warps 4-7   epilogue: one output row per thread (TMEM lane), RoPE in fp32
-//               (accurate sincosf: angles reach 1e5 rad at 128K positions), bf16
-//               16-B stores into THD q / k / v
+//   warps 4-7   epilogue: one output row per thread (TMEM lane), RoPE with the
+//               angle pos * theta_i formed in fp64 (theta_i from a per-CTA table)
+//               and reduced mod 2 pi before an fp32 sincos (angles reach 1.3e5
+//               rad at 128K positions), bf16 16-B stores into THD q / k / v
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -43,7 +44,7 @@ constexpr int B_BYTES = (BN / 64) * B_SLAB;   // 32 KB
 constexpr int OFF_A = 0;
 constexpr int OFF_B = OFF_A + STAGES * A_BYTES;
 constexpr int OFF_BAR = OFF_B + STAGES * B_BYTES;
-constexpr int SMEM = OFF_BAR + 256;
+constexpr int SMEM = OFF_BAR + 1024;
 constexpr uint32_t IDESC = idesc_bf16(BM, BN, 0, 1);
 constexpr int THREADS = 256;
 static_assert(SMEM <= 232448, "projection GEMM exceeds the SMEM window");
@@ -53,14 +54,15 @@ struct ProjBars {
   uint64_t full[proj::STAGES], empty[proj::STAGES];
   uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem_base;
+  double theta[proj::D / 2];     // rotary frequencies base^(-2i/D)
 };
 
-__device__ __forceinline__ void tma_gather4_w(void* dst, const void* tmap, uint64_t* bar, int col,
-                                              int r0, int r1, int r2, int r3) {
+// per-thread (not elected): every lane of the producer warp gathers its own 4 rows
+__device__ __forceinline__ void tma_gather4(void* dst, const void* tmap, uint64_t* bar, int col,
+                                            int r0, int r1, int r2, int r3) {
   asm volatile(
-      "{\n\t.reg .pred P;\n\t" WLB_ELECT
-      "@P cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];\n\t}" ::"r"(smem_u32(dst)),
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1),
       "r"(r2), "r"(r3)
       : "memory");
@@ -92,7 +94,7 @@ qkv_proj_rope_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                      const int* __restrict__ rows, int gather, const int* __restrict__ positions,
                      __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ k,
                      __nv_bfloat16* __restrict__ v, int Tl, int hidden, int Hq, int Hkv,
-                     float log2_base) {
+                     double log2_base) {
   using namespace proj;
   extern __shared__ uint8_t smem_raw[];
   if (smem_u32(smem_raw) & 1023) __trap();   // SW128 tiles need 1024-B alignment
@@ -114,6 +116,8 @@ qkv_proj_rope_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(&bars->tmem_base, 512);
+  if (threadIdx.x >= 128 && threadIdx.x < 128 + D / 2)
+    bars->theta[threadIdx.x - 128] = exp2(-(double)(2 * (threadIdx.x - 128)) / D * log2_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -142,12 +146,13 @@ qkv_proj_rope_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         mbar_expect_tx_w(&bars->full[st], A_BYTES + B_BYTES);
         uint8_t* sa = smem + OFF_A + st * A_BYTES;
         if (gather) {
-          // 32 x 4 rows: lane g's rows land at rows 4g..4g+3 of the slab
-          for (int g = 0; g < 32; ++g) {
-            const int r0 = __shfl_sync(0xffffffffu, src[0], g), r1 = __shfl_sync(0xffffffffu, src[1], g);
-            const int r2 = __shfl_sync(0xffffffffu, src[2], g), r3 = __shfl_sync(0xffffffffu, src[3], g);
-            tma_gather4_w(sa + g * 4 * 128, &tmA, &bars->full[st], kb * BK, r0, r1, r2, r3);
-          }
+          // 32 x 4 rows: lane g's rows land at rows 4g..4g+3 of the slab (the
+          // SW128 swizzle follows the shared-memory address, so 512-B pieces
+          // compose into the 1024-B atoms of a K-major slab)
+          __syncwarp();
+          tma_gather4(sa + lane * 4 * 128, &tmA, &bars->full[st], kb * BK, src[0], src[1], src[2],
+                      src[3]);
+          __syncwarp();
         } else {
           tma_load_2d_w(sa, &tmA, &bars->full[st], kb * BK, m0);
         }
@@ -189,7 +194,7 @@ qkv_proj_rope_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
       const int row = m * BM + lg * 32 + lane;
       const bool valid = row < Tl;
       const int ab = tc & 1;
-      const float pos = valid ? (float)positions[row] : 0.f;
+      const int pos = valid ? positions[row] : 0;
       mbar_wait(&bars->acc_full[ab], (tc >> 1) & 1);
       tc_fence_after();
 #pragma unroll 1
@@ -214,11 +219,13 @@ qkv_proj_rope_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             float b0 = __uint_as_float(hi[2 * e]), b1 = __uint_as_float(hi[2 * e + 1]);
             if (rope) {
               // rotate-half: x'[i] = x[i] cos - x[i+D/2] sin, x'[i+D/2] = x[i+D/2] cos + x[i] sin,
-              // theta_i = base^(-2i/D) (the wlb_qkv_rope expression)
+              // theta_i = base^(-2i/D); angle pos * theta_i in fp64, reduced mod 2 pi
               const int i0 = c + 2 * e;
+              constexpr double two_pi = 6.283185307179586;
+              const double g0 = (double)pos * bars->theta[i0], g1 = (double)pos * bars->theta[i0 + 1];
               float s0, c0, s1, c1;
-              sincosf(pos * exp2f(-(float)(2 * i0) / D * log2_base), &s0, &c0);
-              sincosf(pos * exp2f(-(float)(2 * i0 + 2) / D * log2_base), &s1, &c1);
+              sincosf((float)(g0 - rint(g0 / two_pi) * two_pi), &s0, &c0);
+              sincosf((float)(g1 - rint(g1 / two_pi) * two_pi), &s1, &c1);
               const float x0 = a0 * c0 - b0 * s0, y0 = b0 * c0 + a0 * s0;
               const float x1 = a1 * c1 - b1 * s1, y1 = b1 * c1 + a1 * s1;
               a0 = x0; b0 = y0; a1 = x1; b1 = y1;
@@ -300,7 +307,7 @@ extern "C" int wlb_qkv_proj_rope(const void* x, int32_t x_rows, const int32_t* r
   const int tiles = ((Tl + proj::BM - 1) / proj::BM) * (N / proj::BN);
   qkv_proj_rope_kernel<<<std::min(tiles, sms), proj::THREADS, proj::SMEM, (cudaStream_t)stream>>>(
       ta, tw, rows, rows ? 1 : 0, positions, (__nv_bfloat16*)q, (__nv_bfloat16*)k,
-      (__nv_bfloat16*)v, Tl, hidden, Hq, Hkv, log2f(base));
+      (__nv_bfloat16*)v, Tl, hidden, Hq, Hkv, log2((double)base));
   WLB_LAUNCH_CHECK();
   return WLB_OK;
 }

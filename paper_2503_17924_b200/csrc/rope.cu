@@ -10,7 +10,8 @@
 // q [Tl][Hq][D], k/v [Tl][Hkv][D] bf16.  Rotate-half (GPT-NeoX / Llama) form:
 //   x'[i]       = x[i] cos(t w_i) - x[i + D/2] sin(t w_i)
 //   x'[i + D/2] = x[i + D/2] cos(t w_i) + x[i] sin(t w_i),  w_i = base^(-2i/D)
-// in fp32 with accurate sincosf (angles reach 1e5 rad at 128K positions).
+// with the angle formed in fp64 and reduced mod 2 pi (angles reach 1.3e5 rad
+// at 128K positions, common.cuh rope_sincos).
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -20,7 +21,7 @@ namespace wlb {
 __global__ void qkv_rope_kernel(const __nv_bfloat162* __restrict__ y, __nv_bfloat162* __restrict__ q,
                                 __nv_bfloat162* __restrict__ k, __nv_bfloat162* __restrict__ v,
                                 const int* __restrict__ positions, int Tl, int Hq, int Hkv, int D,
-                                float log2_base) {
+                                double log2_base) {
   // one thread per (row, head, pair of rotation indices {2j, 2j+1})
   const int H = Hq + 2 * Hkv, P = D / 4;     // bf16x2 pairs per half-head
   const long long n = (long long)Tl * H * P;
@@ -41,11 +42,11 @@ __global__ void qkv_rope_kernel(const __nv_bfloat162* __restrict__ y, __nv_bfloa
       dst[j + P] = b;
       continue;
     }
-    const float pos = (float)positions[row];
+    const int pos = positions[row];
     const float2 x0 = __bfloat1622float2(a), x1 = __bfloat1622float2(b);
     float s0, c0, s1, c1;
-    sincosf(pos * exp2f(-(float)(4 * j) / D * log2_base), &s0, &c0);       // i = 2j
-    sincosf(pos * exp2f(-(float)(4 * j + 2) / D * log2_base), &s1, &c1);   // i = 2j+1
+    rope_sincos(pos, 2 * j, D, log2_base, &s0, &c0);       // i = 2j
+    rope_sincos(pos, 2 * j + 1, D, log2_base, &s1, &c1);   // i = 2j+1
     dst[j] = __floats2bfloat162_rn(x0.x * c0 - x1.x * s0, x0.y * c1 - x1.y * s1);
     dst[j + P] = __floats2bfloat162_rn(x1.x * c0 + x0.x * s0, x1.y * c1 + x0.y * s1);
   }
@@ -63,7 +64,7 @@ extern "C" int wlb_qkv_rope(const void* y, void* q, void* k, void* v, const int3
   const unsigned blocks = (unsigned)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
   wlb::qkv_rope_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
       (const __nv_bfloat162*)y, (__nv_bfloat162*)q, (__nv_bfloat162*)k, (__nv_bfloat162*)v,
-      positions, Tl, Hq, Hkv, D, log2f(base));
+      positions, Tl, Hq, Hkv, D, log2((double)base));
   WLB_LAUNCH_CHECK();
   return WLB_OK;
 }
