@@ -197,17 +197,30 @@ qkv_proj_rope_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
       const int pos = valid ? positions[row] : 0;
       mbar_wait(&bars->acc_full[ab], (tc >> 1) & 1);
       tc_fence_after();
+      // the tile's two heads share every row's rotation angles: cos / sin of
+      // 32 frequencies at a time, then both heads' column pairs (i, i + D/2)
+      const int h_first = n * (BN / D);
+      const bool any_rope = h_first < Hq + Hkv;
 #pragma unroll 1
-      for (int hh = 0; hh < BN / D; ++hh) {
-        const int h = n * (BN / D) + hh;            // head among q | k | v
-        const uint32_t col = lane_base + ab * BN + hh * D;
-        __nv_bfloat16* dst;
-        if (h < Hq) dst = q + ((size_t)row * Hq + h) * D;
-        else if (h < Hq + Hkv) dst = k + ((size_t)row * Hkv + (h - Hq)) * D;
-        else dst = v + ((size_t)row * Hkv + (h - Hq - Hkv)) * D;
-        const bool rope = h < Hq + Hkv;
+      for (int c = 0; c < D / 2; c += 32) {
+        float cs[32], sn[32];
+        if (any_rope) {
+          constexpr double two_pi = 6.283185307179586, inv_two_pi = 0.15915494309189535;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const double g = (double)pos * bars->theta[c + e];
+            sincosf((float)fma(-rint(g * inv_two_pi), two_pi, g), &sn[e], &cs[e]);
+          }
+        }
 #pragma unroll 1
-        for (int c = 0; c < D / 2; c += 32) {       // columns c.. and c + D/2..
+        for (int hh = 0; hh < BN / D; ++hh) {
+          const int h = h_first + hh;               // head among q | k | v
+          const uint32_t col = lane_base + ab * BN + hh * D;
+          __nv_bfloat16* dst;
+          if (h < Hq) dst = q + ((size_t)row * Hq + h) * D;
+          else if (h < Hq + Hkv) dst = k + ((size_t)row * Hkv + (h - Hq)) * D;
+          else dst = v + ((size_t)row * Hkv + (h - Hq - Hkv)) * D;
+          const bool rope = h < Hq + Hkv;
           uint32_t lo[32], hi[32];
           tmem_ld32(col + c, lo);
           tmem_ld32(col + c + D / 2, hi);
@@ -218,14 +231,8 @@ qkv_proj_rope_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             float a0 = __uint_as_float(lo[2 * e]), a1 = __uint_as_float(lo[2 * e + 1]);
             float b0 = __uint_as_float(hi[2 * e]), b1 = __uint_as_float(hi[2 * e + 1]);
             if (rope) {
-              // rotate-half: x'[i] = x[i] cos - x[i+D/2] sin, x'[i+D/2] = x[i+D/2] cos + x[i] sin,
-              // theta_i = base^(-2i/D); angle pos * theta_i in fp64, reduced mod 2 pi
-              const int i0 = c + 2 * e;
-              constexpr double two_pi = 6.283185307179586;
-              const double g0 = (double)pos * bars->theta[i0], g1 = (double)pos * bars->theta[i0 + 1];
-              float s0, c0, s1, c1;
-              sincosf((float)(g0 - rint(g0 / two_pi) * two_pi), &s0, &c0);
-              sincosf((float)(g1 - rint(g1 / two_pi) * two_pi), &s1, &c1);
+              // rotate-half: x'[i] = x[i] cos - x[i+D/2] sin, x'[i+D/2] = x[i+D/2] cos + x[i] sin
+              const float c0 = cs[2 * e], s0 = sn[2 * e], c1 = cs[2 * e + 1], s1 = sn[2 * e + 1];
               const float x0 = a0 * c0 - b0 * s0, y0 = b0 * c0 + a0 * s0;
               const float x1 = a1 * c1 - b1 * s1, y1 = b1 * c1 + a1 * s1;
               a0 = x0; b0 = y0; a1 = x1; b1 = y1;
