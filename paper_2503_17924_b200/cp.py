@@ -54,18 +54,30 @@ class CPShard:
 
 
 def project_qkv(x, w_qkv, shard: CPShard, hq: int, hkv: int, d: int, base: float = 10000.0,
-                gather: bool = False):
+                gather: bool = False, gather_in_gemm: bool = False):
     """The step before the path: this rank's q, k, v (THD bf16) from hidden
     states and the fused QKV weight w_qkv [hidden, (hq + 2*hkv)*d] (x @ W),
     with rotary embeddings at each row's in-document position
     (`shard.tiles.positions`), ready for `cp_doc_attention` / `CPStepPipeline`.
 
     x: this rank's local hidden states [T/cp, hidden] in local order, or with
-    gather=True the micro-batch's hidden states [T, hidden] in global order
-    (the kernel gathers the rank's rows by `shard.gather_local`).  D = 128:
-    one tcgen05 kernel (`wlb_qkv_proj_rope`: projection, gather and RoPE
-    fused); other D: a library GEMM then `wlb_qkv_rope`."""
+    gather=True the micro-batch's hidden states [T, hidden] in global order,
+    whose rows `shard.gather_local` are this rank's.  D = 128: one tcgen05
+    kernel (`wlb_qkv_proj_rope`: projection and RoPE fused); other D: a
+    library GEMM then `wlb_qkv_rope`.
+
+    With gather=True the rank's rows are first packed by one `wlb_rows_gather`
+    pass (T/cp x hidden bf16).  The kernel can instead gather them itself with
+    TMA gather4 (`gather_in_gemm=True`), but it then re-gathers every row once
+    per 256-column output tile (48 times at the Llama-7B shape) and measured
+    2.5x slower than pack + tiled loads (profiles/r02_proj_bench.jsonl)."""
     tl = shard.gather_local.numel()
+    if gather and not gather_in_gemm:
+        if x.dtype != torch.bfloat16 or not x.is_cuda or not x.is_contiguous() or x.dim() != 2:
+            raise ValueError("x must be a contiguous 2-D CUDA bf16 tensor")
+        packed = torch.empty((tl, x.shape[1]), dtype=x.dtype, device=x.device)
+        _rows("wlb_rows_gather", x, packed, shard.gather_local)
+        x, gather = packed, False
     if d == 128:
         for name, t in (("x", x), ("w_qkv", w_qkv)):
             if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous() or t.dim() != 2:

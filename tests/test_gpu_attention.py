@@ -175,7 +175,7 @@ def _rope_ref(x, pos, base):
     return torch.cat((a * c - b * s, b * c + a * s), dim=-1)
 
 
-@pytest.mark.parametrize("gather", [False, True])
+@pytest.mark.parametrize("gather", [False, True, "in_gemm"])
 @pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("cp,policy", [(1, "per_document"), (2, "per_document"), (4, "per_sequence")])
 def test_project_qkv_rope_in_document_positions(cp, policy, d, gather):
@@ -196,7 +196,8 @@ def test_project_qkv_rope_in_document_positions(cp, policy, d, gather):
         idx = sh.gather_local.long().cpu()
         xl = x_all[idx]
         x_in = x_all.to(dev) if gather else xl.to(dev)
-        q, k, v = project_qkv(x_in, w.to(dev), sh, hq, hkv, d, base=500000.0, gather=gather)
+        q, k, v = project_qkv(x_in, w.to(dev), sh, hq, hkv, d, base=500000.0, gather=bool(gather),
+                              gather_in_gemm=gather == "in_gemm")
         y = (xl.float() @ w.float()).view(-1, hq + 2 * hkv, d)
         # in-document positions of the rank's rows, recomputed on the host
         starts = [0]
@@ -224,7 +225,7 @@ def test_fused_projection_config_shape():
     g = torch.Generator(device=dev).manual_seed(7)
     x = torch.randn(sum(lengths), hidden, generator=g, device=dev).to(torch.bfloat16)
     w = (torch.randn(hidden, (hq + 2 * hkv) * d, generator=g, device=dev) / 64).to(torch.bfloat16)
-    q, k, v = project_qkv(x, w, sh, hq, hkv, d, base=10000.0, gather=True)
+    q, k, v = project_qkv(x, w, sh, hq, hkv, d, base=10000.0, gather=True, gather_in_gemm=True)
     rows = torch.arange(0, sh.gather_local.numel(), 97, device=dev)
     xl = x[sh.gather_local.long()[rows]].float()
     y = (xl @ w.float()).view(-1, hq + 2 * hkv, d).cpu()

@@ -41,6 +41,7 @@ def main():
             flops = 2.0 * tl * hidden * (hq + 2 * hkv) * d
             t_fused = ev_ms(lambda: project_qkv(xl, w, sh, hq, hkv, d))
             t_gather = ev_ms(lambda: project_qkv(x, w, sh, hq, hkv, d, gather=True))
+            t_g4 = ev_ms(lambda: project_qkv(x, w, sh, hq, hkv, d, gather=True, gather_in_gemm=True))
             t_lib = ev_ms(lambda: qkv_rope(xl @ w, sh.tiles.positions, hq, hkv, d))
             print(json.dumps({"shape": name, "cp": cp, "rows": tl, "hidden": hidden,
                               "fused_ms": round(t_fused, 3), "fused_gather_ms": round(t_gather, 3),
