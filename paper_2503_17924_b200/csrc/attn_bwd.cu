@@ -673,7 +673,7 @@ static_assert(sizeof(Bwd3Bars) <= 256, "barrier block");
 // (P, then dS) and put the GQA dK (summed over 8 query heads x 32K queries)
 // past the 2e-2 + 1e-2|ref| bar; with fp16 P its error matches the 64-query
 // kernel's, which multiplies the fp32 P.
-template <bool MASK>
+template <bool MASK, bool P16>
 __device__ __forceinline__ void bwd3_p_chunk(const uint32_t (&us)[32], const float* nl,
                                              const int8_t* rp, int t, bool key_ok,
                                              float scale_log2, uint32_t (&pk)[16],
@@ -705,12 +705,16 @@ __device__ __forceinline__ void bwd3_p_chunk(const uint32_t (&us)[32], const flo
         pp.y = (key_ok && pos[e + 1] >= t) ? pp.y : 0.f;
       }
       pk[e >> 1] = pack_bf16(pp.x, pp.y);
-      ph[e >> 1] = pack_f16(pp.x, pp.y);
+      ph[e >> 1] = P16 ? pack_f16(pp.x, pp.y) : pk[e >> 1];
     }
   }
 }
 
-template <bool PAIR>
+// P16: dS from the fp16 copy of P (GQA, where dK sums over the group's query
+// heads and the bf16 double rounding of P failed the bar); otherwise from the
+// bf16 P the dV MMA reads (one conversion fewer per pair on the compute warps,
+// within the bar for Hq = Hkv: tests/test_gpu_scale.py).
+template <bool PAIR, bool P16>
 __global__ void __launch_bounds__(512, 1)
 attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -1081,7 +1085,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       mbar_wait(&bars->s_full, ph);
       if (warp == 4) TRACE3(6, i);
       tc_fence_after();
-      uint32_t p16[2][16];   // P (fp16 pairs), kept for dS
+      uint32_t p16[2][16];   // P (fp16 pairs with P16, else bf16), kept for dS
       // ---- P^T = exp2(S^T * scale * log2e - lse2), per 32-query chunk
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -1092,9 +1096,9 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 
         uint32_t pk[16];
         if (full)
-          bwd3_p_chunk<false>(us, nl + 32 * c, rp + 32 * c, t, key_ok, scale_log2, pk, p16[c]);
+          bwd3_p_chunk<false, P16>(us, nl + 32 * c, rp + 32 * c, t, key_ok, scale_log2, pk, p16[c]);
         else
-          bwd3_p_chunk<true>(us, nl + 32 * c, rp + 32 * c, t, key_ok, scale_log2, pk, p16[c]);
+          bwd3_p_chunk<true, P16>(us, nl + 32 * c, rp + 32 * c, t, key_ok, scale_log2, pk, p16[c]);
 
         // over S^T columns this warp already loaded (chunk 0's 32 columns)
         tmem_st16(lane_base + C::COL_S + 64 * hf + 16 * c, pk);
@@ -1123,7 +1127,8 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
           for (int u2 = 0; u2 < 2; ++u2) {
             const int e = 4 * e4 + 2 * u2;
             const uint32_t pp = p16[c][e >> 1];
-            const float2 pf = __half22float2(*reinterpret_cast<const __half2*>(&pp));
+            const float2 pf = P16 ? __half22float2(*reinterpret_cast<const __half2*>(&pp))
+                                  : make_float2(__uint_as_float(pp << 16), __uint_as_float(pp & 0xffff0000u));
             const float2 dd = fadd2(make_float2(__uint_as_float(ud[e]), __uint_as_float(ud[e + 1])),
                                     u2 ? make_float2(-d4.z, -d4.w) : make_float2(-d4.x, -d4.y));
             const float2 ds = fmul2(pf, dd);
@@ -1480,8 +1485,11 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
     if ((rc = make_thd_tmap(&tdo, dout, Tl, Hq, D, C3::BM))) return rc;
     if ((rc = make_thd_tmap(&tk, k, T, Hkv, D, C3::BN))) return rc;
     if ((rc = make_thd_tmap(&tv, v, T, Hkv, D, C3::BN))) return rc;
-    WLB_SMEM_ATTR(attn_bwd3_kernel<false>, C3::SMEM);
-    WLB_SMEM_ATTR(attn_bwd3_kernel<true>, C3::SMEM);
+    const bool p16 = Hq != Hkv;
+    WLB_SMEM_ATTR((attn_bwd3_kernel<false, false>), C3::SMEM);
+    WLB_SMEM_ATTR((attn_bwd3_kernel<false, true>), C3::SMEM);
+    WLB_SMEM_ATTR((attn_bwd3_kernel<true, false>), C3::SMEM);
+    WLB_SMEM_ATTR((attn_bwd3_kernel<true, true>), C3::SMEM);
     const float sl2 = scale * 1.4426950408889634f;
     if (pairs) {
       // 2-CTA clusters: one pair of KV tiles per cluster
@@ -1497,12 +1505,13 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      WLB_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn_bwd3_kernel<true>, tq, tk, tv, tdo, lse,
+      WLB_CUDA_TRY(cudaLaunchKernelEx(&cfg, p16 ? attn_bwd3_kernel<true, true> : attn_bwd3_kernel<true, false>, tq, tk, tv, tdo, lse,
                                       (const float*)w.delta, w.dq_acc, dk, dv,
                                       (const int4*)w.kv_tiles, (const int*)w.n_kv, positions, Tl,
                                       Hq, Hkv, max_items, g_begin, scale, sl2, dkv_bf16));
     } else {
-      attn_bwd3_kernel<false><<<(unsigned)max_items * g_count, C3::THREADS, C3::SMEM, stream>>>(
+      auto kern = p16 ? attn_bwd3_kernel<false, true> : attn_bwd3_kernel<false, false>;
+      kern<<<(unsigned)max_items * g_count, C3::THREADS, C3::SMEM, stream>>>(
           tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
           Hkv, max_items, g_begin, scale, sl2, dkv_bf16);
     }

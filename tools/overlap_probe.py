@@ -20,7 +20,8 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 import paper_2503_17924_b200 as wl  # noqa: E402
-from paper_2503_17924_b200.attention import attn_backward, attn_forward  # noqa: E402
+from paper_2503_17924_b200.attention import (attn_backward, attn_forward, bwd_workspace,  # noqa: E402
+                                             head_groups)
 from paper_2503_17924_b200.cp import SymmExchange, cp_doc_attention, shard_for_rank  # noqa: E402
 
 
@@ -75,6 +76,22 @@ def main():
            "strategy": sh.strategy.value, "heads": [a.hq, a.hkv]}
     res["attn_ms"] = timed(attn_only, a.reps)
     for G in a.groups:
+        # the same kernels split into G head-group launches, no exchange
+        grps = head_groups(a.hkv, G)
+
+        def attn_groups():
+            o = lse = None
+            for grp in grps:
+                o, lse = attn_forward(q, kf, vf, sh.tiles, kv_heads=grp,
+                                      out=None if o is None else (o, lse))
+            dq, ws = torch.empty_like(q), bwd_workspace(q, kf, sh.tiles)
+            dk = torch.empty((T, a.hkv, d), dtype=torch.float32, device=dev)
+            dv = torch.empty_like(dk)
+            for grp in grps:
+                attn_backward(q, kf, vf, o, lse, do, sh.tiles, dk_out=dk, dv_out=dv,
+                              covered_only=True, kv_heads=grp, dq_out=dq, ws=ws)
+
+        res[f"attn_g{G}_ms"] = timed(attn_groups, a.reps)
         ex = SymmExchange(dist.group.WORLD, T, a.hkv, d, dev, groups=G)
 
         def step():
@@ -84,6 +101,7 @@ def main():
 
         res[f"step_g{G}_ms"] = timed(step, a.reps)
         res[f"exposed_g{G}"] = round(1 - res["attn_ms"] / res[f"step_g{G}_ms"], 4)
+        res[f"exposed_vs_split_g{G}"] = round(1 - res[f"attn_g{G}_ms"] / res[f"step_g{G}_ms"], 4)
         del ex
 
     def nccl_step():
