@@ -36,6 +36,17 @@
 
 #include <algorithm>
 
+// Query-tile order inside a KV work item for GQA (Hq > Hkv): 1 = the group's
+// query heads innermost (every resident KV-tile CTA sweeps the query rows
+// once, reducing all heads of a row block back to back, so the fp32 dQ
+// accumulator lines are reused while L2-resident); 0 = head by head (each
+// CTA sweeps the rows once per head, and the second wave of CTAs restarts
+// at head 0 after the lines were evicted: the 64-head dQ accumulator, 1 GiB
+// at 32K, spilled).  No effect for Hq = Hkv.
+#ifndef WLB_BWD_HEAD_INNER
+#define WLB_BWD_HEAD_INNER 1
+#endif
+
 namespace wlb {
 using namespace sm100;
 
@@ -230,10 +241,12 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
   // unit-local flat tile I -> (KV head, query head, first row)
   auto tile_g = [&](const Unit& U, int I) { return U.g0 + I / U.n_iter; };
   auto tile_h = [&](const Unit& U, int I) {
-    return tile_g(U, I) * group + (I % U.n_iter) / U.qt_per_head;
+    return tile_g(U, I) * group + (WLB_BWD_HEAD_INNER ? (I % U.n_iter) % group
+                                                      : (I % U.n_iter) / U.qt_per_head);
   };
   auto tile_row = [&](const Unit& U, int I) {
-    return U.kt.z + ((I % U.n_iter) % U.qt_per_head) * C::BM;
+    return U.kt.z + (WLB_BWD_HEAD_INNER ? (I % U.n_iter) / group
+                                        : (I % U.n_iter) % U.qt_per_head) * C::BM;
   };
   // consumer side of the unit ring (whole warp; lane 0 releases the slot)
   auto next_unit = [&](int seq) {
@@ -809,8 +822,8 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     }
     for (int i = 0; i < n_iter; ++i) {
       const int st = i % C::QS;
-      const int h = g * group + i / qt_per_head;
-      const int row = kt.z + (i % qt_per_head) * C::BM;
+      const int h = g * group + (WLB_BWD_HEAD_INNER ? i % group : i / qt_per_head);
+      const int row = kt.z + (WLB_BWD_HEAD_INNER ? i / group : i % qt_per_head) * C::BM;
       mbar_wait(&bars->q_empty[st], ((i / C::QS) & 1) ^ 1);
       if (PAIR) {
         // dO single-buffered (its second stage is the dQ exchange buffer): it
@@ -918,8 +931,8 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     // ------------------------------------------------- per-query vectors --
     for (int i = 0; i < n_iter; ++i) {
       const int b = i % C::QS;
-      const int h = g * group + i / qt_per_head;
-      const int row0 = kt.z + (i % qt_per_head) * C::BM;
+      const int h = g * group + (WLB_BWD_HEAD_INNER ? i % group : i / qt_per_head);
+      const int row0 = kt.z + (WLB_BWD_HEAD_INNER ? i / group : i % qt_per_head) * C::BM;
       mbar_wait(&bars->vec_empty[b], ((i / C::QS) & 1) ^ 1);
       float* vec = sVec + b * 2 * C::BM;
       int8_t* rp = sPos + b * C::BM;
@@ -949,8 +962,8 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     setmaxnreg_inc<160>();
     const size_t blk = (size_t)Tl * 4;
     for (int j = 0; j < n_iter; ++j) {
-      const int h = g * group + j / qt_per_head;
-      const int row = kt.z + (j % qt_per_head) * C::BM + lg * 32 + lane;
+      const int h = g * group + (WLB_BWD_HEAD_INNER ? j % group : j / qt_per_head);
+      const int row = kt.z + (WLB_BWD_HEAD_INNER ? j / group : j % qt_per_head) * C::BM + lg * 32 + lane;
 #ifdef WLB_EXP_NORED
       const bool ok = false;   // timing experiment: no dQ reductions (wrong dQ)
 #else
