@@ -36,15 +36,14 @@
 
 #include <algorithm>
 
-// Query-tile order inside a KV work item for GQA (Hq > Hkv): 1 = the group's
-// query heads innermost (every resident KV-tile CTA sweeps the query rows
-// once, reducing all heads of a row block back to back, so the fp32 dQ
-// accumulator lines are reused while L2-resident); 0 = head by head (each
-// CTA sweeps the rows once per head, and the second wave of CTAs restarts
-// at head 0 after the lines were evicted: the 64-head dQ accumulator, 1 GiB
-// at 32K, spilled).  No effect for Hq = Hkv.
+// Query-tile order inside a KV work item for GQA (Hq > Hkv): 0 (default) =
+// head by head; 1 = the group's query heads innermost (a row block's heads
+// back to back).  1 was meant to keep the fp32 dQ accumulator lines of a row
+// block L2-resident across heads, but measured 5x the DRAM traffic of the v3
+// backward (132 vs 27 GB per GQA bench step) and 881 vs 926-932 TFLOP/s
+// (profiles/r02_ab_gqa_head_order.txt).  No effect for Hq = Hkv.
 #ifndef WLB_BWD_HEAD_INNER
-#define WLB_BWD_HEAD_INNER 1
+#define WLB_BWD_HEAD_INNER 0
 #endif
 
 namespace wlb {
