@@ -31,6 +31,31 @@ extern "C" {
 #define WLB_POLICY_MEASURED 3   /* adaptive, priced by the B200 tile model */
 #define WLB_TILE_MODEL_LEN 11
 
+/* In-kernel CP synchronisation on per-peer arrival flags (see wlb_cp_signal /
+ * wlb_cp_wait): the attention kernels can wait for, and publish, head-group
+ * completion themselves, so one launch covers all heads and each head group
+ * still starts as soon as its peers' rows have landed.
+ *   wait_flags   device [n_groups][cp] int32 flags of THIS rank (the K/V
+ *                arrival flags of one exchange slot); a forward CTA waits
+ *                until the flags of its KV head's group are >= epoch before
+ *                loading K/V.  NULL: no wait.
+ *   signal_bases device [cp] peer-mapped flag-buffer bases; when the last
+ *                work unit of a head group has stored its dK/dV partials,
+ *                the backward stores epoch at byte offset signal_off + 4*cp*g
+ *                of every peer (system-scope release).  NULL: no signal.
+ *   counters     device [n_groups] int32, zeroed before the backward launch.
+ *   kv_per_group KV heads per group (groups are contiguous, equal ranges). */
+typedef struct WlbCpSync {
+  const int32_t* wait_flags;
+  const uint64_t* signal_bases;
+  int64_t signal_off;
+  int32_t* counters;
+  int32_t cp;
+  int32_t kv_per_group;
+  int32_t epoch;
+  int32_t pad_;
+} WlbCpSync;
+
 int32_t wlb_abi_version(void);
 const char* wlb_last_error(void);
 /* 0 when a compute-capability-10.x device is visible, else WLB_ENODEV. */
@@ -136,6 +161,13 @@ int wlb_attn_fwd_heads(const void* q, const void* k, const void* v, void* o, flo
                        int32_t D, float scale, int32_t kv_head_begin, int32_t kv_head_count,
                        void* stream);
 
+/* wlb_attn_fwd, all heads in one launch, each CTA gated on sync->wait_flags
+ * of its KV head's group (sync may be NULL: plain wlb_attn_fwd). */
+int wlb_attn_fwd_sync(const void* q, const void* k, const void* v, void* o, float* lse,
+                      const int32_t* tiles, const int32_t* n_tiles, int32_t max_tiles,
+                      const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq, int32_t Hkv,
+                      int32_t D, float scale, const WlbCpSync* sync, void* stream);
+
 /* Backward.  do_[Tl][Hq][D] bf16, o and lse from the forward.  Writes
  * dq[Tl][Hq][D] bf16 and dK/dV partials over the full document-ordered
  * sequence, dk/dv[T][Hkv][D] fp32 (summed over ranks by the CP
@@ -173,6 +205,15 @@ int wlb_attn_bwd_heads(const void* q, const void* k, const void* v, const void* 
                        const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq, int32_t Hkv,
                        int32_t D, float scale, void* ws, int32_t flags, int32_t kv_head_begin,
                        int32_t kv_head_count, void* stream);
+/* wlb_attn_bwd_ex, all heads in one launch, signalling every peer per head
+ * group through sync->signal_bases once the group's partials are stored
+ * (sync may be NULL: plain wlb_attn_bwd_ex). */
+int wlb_attn_bwd_sync(const void* q, const void* k, const void* v, const void* o,
+                      const void* do_, const float* lse, void* dq, void* dk, void* dv,
+                      const int32_t* rowset_off, const int32_t* doc_start, int32_t n_docs,
+                      const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq, int32_t Hkv,
+                      int32_t D, float scale, void* ws, int32_t flags, const WlbCpSync* sync,
+                      void* stream);
 /* Backward kernel selection for D = 128: the 128-query-tile kernel (v3) runs
  * when Tl >= v3_min_rows * n_docs, else the 64-query kernel (v2).  Negative
  * restores the default (4096); returns the previous threshold.  Process-wide

@@ -24,6 +24,13 @@ WLB_BWD_COVERED_ONLY = 2
 
 _p, _i32, _i64, _f64, _f32, _sz = C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_float, C.c_size_t
 
+
+class WlbCpSync(C.Structure):
+    """`WlbCpSync` of wlbcp.h: in-kernel CP synchronisation on arrival flags."""
+    _fields_ = [("wait_flags", C.c_void_p), ("signal_bases", C.c_void_p),
+                ("signal_off", C.c_int64), ("counters", C.c_void_p), ("cp", C.c_int32),
+                ("kv_per_group", C.c_int32), ("epoch", C.c_int32), ("pad_", C.c_int32)]
+
 # name -> (restype, argtypes); must match include/wlbcp.h
 SIGNATURES = {
     "wlb_abi_version": (_i32, []),
@@ -42,6 +49,11 @@ SIGNATURES = {
                                      _i32, _f32, _i32, _i32, _p]),
     "wlb_attn_bwd_heads": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i32, _p, _i32,
                                      _i32, _i32, _i32, _i32, _f32, _p, _i32, _i32, _i32, _p]),
+    "wlb_attn_fwd_sync": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, _i32, _p, _i32, _i32, _i32, _i32,
+                                    _i32, _f32, C.POINTER(WlbCpSync), _p]),
+    "wlb_attn_bwd_sync": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i32, _p, _i32,
+                                    _i32, _i32, _i32, _i32, _f32, _p, _i32, C.POINTER(WlbCpSync),
+                                    _p]),
     "wlb_attn_bwd_workspace": (_sz, [_i32, _i32, _i32, _i32, _i32, _i32]),
     "wlb_attn_bwd_ex": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i32, _p, _i32,
                                   _i32, _i32, _i32, _i32, _f32, _p, _i32, _p]),

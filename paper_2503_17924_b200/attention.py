@@ -64,11 +64,13 @@ def _check_inputs(q, k, v):
 
 
 def attn_forward(q, k, v, tiles: AttnTiles, scale: float | None = None, kv_heads=None,
-                 out=None):
+                 out=None, sync=None):
     """O [Tl,Hq,D] bf16 and LSE [Hq,Tl] fp32 for one rank's local queries.
 
     kv_heads=(begin, count): only those KV heads and their query heads, into
-    `out` = (o, lse) from an earlier call (the CP head-group pipeline)."""
+    `out` = (o, lse) from an earlier call (the CP head-group pipeline).
+    sync (`_native.WlbCpSync`): all heads in one launch, each CTA waiting on
+    the device for its head group's K/V arrival flags."""
     _check_inputs(q, k, v)
     tl, hq, d = q.shape
     hkv = k.shape[1]
@@ -79,6 +81,12 @@ def attn_forward(q, k, v, tiles: AttnTiles, scale: float | None = None, kv_heads
     else:
         o, lse = out
     p = _native.ptr
+    if sync is not None:
+        _native.check(_native.lib().wlb_attn_fwd_sync(
+            p(q), p(k), p(v), p(o), p(lse), p(tiles.tiles), p(tiles.n_tiles), tiles.max_tiles,
+            p(tiles.positions), tl, k.shape[0], hq, hkv, d, scale, sync, _native.stream_ptr()),
+            "wlb_attn_fwd_sync")
+        return o, lse
     if kv_heads is None:
         _native.check(_native.lib().wlb_attn_fwd(
             p(q), p(k), p(v), p(o), p(lse), p(tiles.tiles), p(tiles.n_tiles), tiles.max_tiles,
@@ -103,14 +111,16 @@ def bwd_workspace(q, k, tiles: AttnTiles):
 
 def attn_backward(q, k, v, o, lse, do, tiles: AttnTiles, scale: float | None = None,
                   dk_out=None, dv_out=None, covered_only: bool = False, kv_heads=None,
-                  dq_out=None, ws=None):
+                  dq_out=None, ws=None, sync=None):
     """dQ [Tl,Hq,D] bf16 and fp32 dK/dV partials over the full sequence
     (written into dk_out / dv_out when given, e.g. symmetric exchange buffers;
     bf16 dk_out / dv_out take bf16 partials).  covered_only: rows no KV tile
     of this rank covers are left unwritten instead of zeroed (for the covered
     CP pull, which never reads them).  kv_heads=(begin, count): only those KV
     heads (dK/dV columns) and their query heads (dQ), into dq_out / dk_out /
-    dv_out with workspace `ws` shared across the head groups."""
+    dv_out with workspace `ws` shared across the head groups.  sync
+    (`_native.WlbCpSync`): all heads in one launch, publishing each head
+    group's completion to every peer's DKV arrival flags from the device."""
     _check_inputs(q, k, v)
     tl, hq, d = q.shape
     T, hkv = k.shape[0], k.shape[1]
@@ -130,7 +140,10 @@ def attn_backward(q, k, v, o, lse, do, tiles: AttnTiles, scale: float | None = N
     args = (p(q), p(k), p(v), p(o), p(do), p(lse), p(dq), p(dk), p(dv), p(tiles.rowset_off),
             p(tiles.doc_start), tiles.n_docs, p(tiles.positions), tl, T, hq, hkv, d, scale,
             p(ws), flags)
-    if kv_heads is None:
+    if sync is not None:
+        _native.check(lib.wlb_attn_bwd_sync(*args, sync, _native.stream_ptr()),
+                      "wlb_attn_bwd_sync")
+    elif kv_heads is None:
         _native.check(lib.wlb_attn_bwd_ex(*args, _native.stream_ptr()), "wlb_attn_bwd_ex")
     else:
         _native.check(lib.wlb_attn_bwd_heads(*args, kv_heads[0], kv_heads[1],

@@ -170,11 +170,15 @@ class CPDocAttention(torch.autograd.Function):
             side.wait_stream(cur)
             with torch.cuda.stream(side):
                 k_full, v_full = exchange.gather(k, v, shard, b)
-            o = lse = None
-            for gi, grp in enumerate(exchange.groups):
-                exchange.wait_kv(b, gi)
-                o, lse = attn_forward(q, k_full, v_full, shard.tiles, scale, kv_heads=grp,
-                                      out=None if o is None else (o, lse))
+            if exchange.fused_sync:
+                o, lse = attn_forward(q, k_full, v_full, shard.tiles, scale,
+                                      sync=exchange.fwd_sync(b))
+            else:
+                o = lse = None
+                for gi, grp in enumerate(exchange.groups):
+                    exchange.wait_kv(b, gi)
+                    o, lse = attn_forward(q, k_full, v_full, shard.tiles, scale, kv_heads=grp,
+                                          out=None if o is None else (o, lse))
             for t in (k, v, k_full, v_full):
                 t.record_stream(side)
             ctx.b = b
@@ -195,10 +199,14 @@ class CPDocAttention(torch.autograd.Function):
             cov = ex.pull_covered and shard.tiles.n_docs > 0
             dq, ws = torch.empty_like(q), bwd_workspace(q, k_full, shard.tiles)
             do = do.contiguous()
-            for gi, grp in enumerate(ex.groups):
+            if ex.fused_sync:
                 attn_backward(q, k_full, v_full, o, lse, do, shard.tiles, ctx.scale, dk_out,
-                              dv_out, covered_only=cov, kv_heads=grp, dq_out=dq, ws=ws)
-                ex.signal_dkv(b, gi)
+                              dv_out, covered_only=cov, dq_out=dq, ws=ws, sync=ex.bwd_sync(b))
+            else:
+                for gi, grp in enumerate(ex.groups):
+                    attn_backward(q, k_full, v_full, o, lse, do, shard.tiles, ctx.scale, dk_out,
+                                  dv_out, covered_only=cov, kv_heads=grp, dq_out=dq, ws=ws)
+                    ex.signal_dkv(b, gi)
             # each group's pull starts once every peer's partials of it are in
             side = ex.side_stream()
             with torch.cuda.stream(side):
@@ -325,6 +333,12 @@ class SymmExchange:
         self.flag_bases = torch.tensor(flag_ptrs, dtype=torch.int64, device=device)
         groups = int(os.environ.get("WLB_HEAD_GROUPS", 4)) if groups is None else groups
         self.groups = head_groups(hkv, min(groups, MAX_GROUPS))
+        # in-kernel sync (one attention launch per direction, gated / signalling
+        # per head group on the device) needs equal groups; WLB_CP_FUSED_SYNC=0
+        # launches the attention group by group with wait / signal kernels
+        self.fused_sync = (hkv % len(self.groups) == 0
+                           and os.environ.get("WLB_CP_FUSED_SYNC", "1") != "0")
+        self.counters = torch.zeros((slots, MAX_GROUPS), dtype=torch.int32, device=device)
         self.seq = 0                    # micro-batches pushed (flag epochs)
         self.epoch = [0] * slots        # epoch of the micro-batch in slot s
         self.free = [None] * slots     # event: all ranks finished pulling slot s
@@ -409,6 +423,25 @@ class SymmExchange:
                 shard.tiles.n_docs if covered else 0, _native.stream_ptr()), "wlb_cp_kv_push_part")
             self._signal(s, _KV, gi)
         return self._view(self.kv, 2 * s, T), self._view(self.kv, 2 * s + 1, T)
+
+    def fwd_sync(self, b):
+        """`WlbCpSync` for a forward that waits on the K/V arrival flags of
+        micro-batch b, head group by head group, inside the kernel."""
+        s = b % self.slots
+        return _native.WlbCpSync(
+            wait_flags=self.flags.data_ptr() + self._flag_off(s, _KV, 0, 0), signal_bases=None,
+            signal_off=0, counters=None, cp=self.cp, kv_per_group=self.hkv // len(self.groups),
+            epoch=self.epoch[s])
+
+    def bwd_sync(self, b):
+        """`WlbCpSync` for a backward that signals every peer's DKV flags of
+        micro-batch b per head group from the device."""
+        s = b % self.slots
+        return _native.WlbCpSync(
+            wait_flags=None, signal_bases=self.flag_bases.data_ptr(),
+            signal_off=self._flag_off(s, _DKV, 0, self.rank),
+            counters=self.counters[s].data_ptr(), cp=self.cp,
+            kv_per_group=self.hkv // len(self.groups), epoch=self.epoch[s])
 
     def wait_kv(self, b, gi):
         """On the current stream: later work waits until every peer's rows of
@@ -580,8 +613,11 @@ class CPStepPipeline:
             def kernels(q=q, do=do, k_full=k_full, v_full=v_full, sh=sh, dk_out=dk_out,
                         dv_out=dv_out, b=b, flagged=flagged, cov=cov):
                 ex = self.exchange
+                fused = flagged and ex.fused_sync
                 if not flagged:
                     o, lse = attn_forward(q, k_full, v_full, sh.tiles, scale)
+                elif fused:
+                    o, lse = attn_forward(q, k_full, v_full, sh.tiles, scale, sync=ex.fwd_sync(b))
                 else:
                     o, lse = torch.empty_like(q), None
                     for gi, grp in enumerate(ex.groups):
@@ -598,6 +634,10 @@ class CPStepPipeline:
                     dq, dkf, dvf = attn_backward(q, k_full, v_full, o, lse, do, sh.tiles, scale,
                                                  dk_out, dv_out, covered_only=cov)
                     return o, dq, dkf, dvf
+                if fused:
+                    dq, _, _ = attn_backward(q, k_full, v_full, o, lse, do, sh.tiles, scale, dk_out,
+                                             dv_out, covered_only=cov, sync=ex.bwd_sync(b))
+                    return o, dq, dk_out, dv_out
                 dq, ws = torch.empty_like(q), bwd_workspace(q, k_full, sh.tiles)
                 for gi, grp in enumerate(ex.groups):
                     attn_backward(q, k_full, v_full, o, lse, do, sh.tiles, scale, dk_out, dv_out,

@@ -169,7 +169,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const int4* __restrict__ kv_tiles, const int* __restrict__ n_kv_tiles,
                 const int* __restrict__ positions, int Tl, int Hq, int Hkv, int n_slots, int hpc,
                 int n_units, int* __restrict__ sched, int persistent, int g_begin, int g_end,
-                float scale, float scale_log2, int dkv_bf16) {
+                float scale, float scale_log2, int dkv_bf16, const CpSync sync) {
   using C = BwdCfg<D, NCW>;
   extern __shared__ uint8_t smem_raw[];
   if (smem_u32(smem_raw) & 1023) __trap();   // SW128 tiles need 1024-B alignment
@@ -564,6 +564,14 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             if (key_ok) store_dkv32(dv, dk, off + c * 32, a, bb, scale, dkv_bf16 != 0);
           }
           tc_fence_before();
+          if (sync.signal_bases && I == U.n_all - 1) {
+            // CP: the unit's partials are stored (all compute warps); count it
+            // toward its head group and publish the group when complete
+            named_bar_sync(1, 128 * NCW);
+            if (warp == 4 && lane == 0)
+              cp_sync_unit_done(sync, U.g0 / sync.kv_per_group,
+                                n_items * (sync.kv_per_group / hpc));
+          }
         }
       }
       I0 += U.n_all;
@@ -734,7 +742,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                  float* __restrict__ dq_acc, void* __restrict__ dk, void* __restrict__ dv,
                  const int4* __restrict__ kv_tiles, const int* __restrict__ n_kv_tiles,
                  const int* __restrict__ positions, int Tl, int Hq, int Hkv, int n_slots,
-                 int g_begin, float scale, float scale_log2, int dkv_bf16) {
+                 int g_begin, float scale, float scale_log2, int dkv_bf16, const CpSync sync) {
   using C = Bwd3Cfg;
   constexpr int D = C::D;
   extern __shared__ uint8_t smem_raw[];
@@ -1171,6 +1179,13 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       tmem_ld_wait();
       if (key_ok) store_dkv32(dv, dk, off + c * 32, a, bb, scale, dkv_bf16 != 0);
     }
+    if (!PAIR && sync.signal_bases) {
+      // CP: this (KV tile, head) unit's partials are stored; count it toward
+      // its head group and publish the group when complete
+      named_bar_sync(1, 256);
+      if (warp == 4 && lane == 0)
+        cp_sync_unit_done(sync, g / sync.kv_per_group, n_kv_tiles[0] * sync.kv_per_group);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -1448,14 +1463,14 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
                       const int32_t* doc_start, int32_t n_docs, const int32_t* positions,
                       int32_t Tl, int32_t T, int32_t Hq, int32_t Hkv, float scale, void* ws,
                       int dkv_bf16, bool covered_only, int g_begin, int g_count,
-                      cudaStream_t stream) {
+                      const CpSync& sync, cudaStream_t stream) {
   using C = BwdCfg<D>;
   BwdWorkspace w = carve(ws, Tl, T, Hq, D, n_docs);
   const int max_items = T / 128 + n_docs + 1;
   const int group = Hq / Hkv, h_begin = g_begin * group, h_count = g_count * group;
 #if WLB_BWD_V3
   const bool v3 = D == 128 && (long long)Tl >= (long long)g_bwd_v3_min_rows * (n_docs > 0 ? n_docs : 1);
-  const bool pairs = v3 && g_bwd_pairs;
+  const bool pairs = v3 && g_bwd_pairs && !sync.signal_bases;   // (pairs do not signal)
 #else
   const bool v3 = false, pairs = false;
 #endif
@@ -1484,6 +1499,8 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
         (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, w.delta, Tl, Hq, h_begin, h_count);
     WLB_LAUNCH_CHECK();
   }
+  if (sync.signal_bases)
+    WLB_CUDA_TRY(cudaMemsetAsync(sync.counters, 0, sizeof(int) * (Hkv / sync.kv_per_group), stream));
   bwd_kv_tiles_kernel<<<1, kKvThreads, 0, stream>>>(n_docs, rowset_off, positions, doc_start,
                                                      max_items, w.kv_tiles, w.n_kv,
                                                      w.kv_tiles + 2 * max_items, pairs ? 1 : 0);
@@ -1520,12 +1537,12 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
       WLB_CUDA_TRY(cudaLaunchKernelEx(&cfg, p16 ? attn_bwd3_kernel<true, true> : attn_bwd3_kernel<true, false>, tq, tk, tv, tdo, lse,
                                       (const float*)w.delta, w.dq_acc, dk, dv,
                                       (const int4*)w.kv_tiles, (const int*)w.n_kv, positions, Tl,
-                                      Hq, Hkv, max_items, g_begin, scale, sl2, dkv_bf16));
+                                      Hq, Hkv, max_items, g_begin, scale, sl2, dkv_bf16, sync));
     } else {
       auto kern = p16 ? attn_bwd3_kernel<false, true> : attn_bwd3_kernel<false, false>;
       kern<<<(unsigned)max_items * g_count, C3::THREADS, C3::SMEM, stream>>>(
           tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
-          Hkv, max_items, g_begin, scale, sl2, dkv_bf16);
+          Hkv, max_items, g_begin, scale, sl2, dkv_bf16, sync);
     }
     WLB_LAUNCH_CHECK();
   } else
@@ -1542,9 +1559,10 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   // several KV heads per unit for short row-sets (< WLB_HPC_ROWS local rows
   // per document on average): a unit's heads run back to back (only with >= 6
   // waves of units: Tl/128 bounds the KV tiles from below)
-  const int hpc = (g_count % g_bwd_hpc_short == 0 && (long long)Tl < (long long)WLB_HPC_ROWS * (n_docs > 0 ? n_docs : 1) &&
-                   (long long)(Tl / 128) * g_count >= 6LL * 148 * g_bwd_hpc_short)
-                      ? g_bwd_hpc_short : 1;
+  int hpc = (g_count % g_bwd_hpc_short == 0 && (long long)Tl < (long long)WLB_HPC_ROWS * (n_docs > 0 ? n_docs : 1) &&
+             (long long)(Tl / 128) * g_count >= 6LL * 148 * g_bwd_hpc_short)
+                ? g_bwd_hpc_short : 1;
+  if (sync.signal_bases && sync.kv_per_group % hpc) hpc = 1;   // units inside one head group
   const int n_units = max_items * ((g_count + hpc - 1) / hpc);
   if (g_bwd_persistent) {
     // one CTA per SM taking units from a global counter: a unit's tail
@@ -1557,12 +1575,12 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
     attn_bwd_kernel<D, 2><<<(unsigned)std::min(n_units, sms), C::THREADS, C::SMEM, stream>>>(
         tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
         Hkv, max_items, hpc, n_units, w.sched, 1, g_begin, g_begin + g_count, scale,
-        scale * 1.4426950408889634f, dkv_bf16);
+        scale * 1.4426950408889634f, dkv_bf16, sync);
   } else {
     attn_bwd_kernel<D, 2><<<(unsigned)n_units, C::THREADS, C::SMEM, stream>>>(
         tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
         Hkv, max_items, hpc, n_units, w.sched, 0, g_begin, g_begin + g_count, scale,
-        scale * 1.4426950408889634f, dkv_bf16);
+        scale * 1.4426950408889634f, dkv_bf16, sync);
   }
   WLB_LAUNCH_CHECK();
   }
@@ -1635,13 +1653,40 @@ extern "C" int wlb_attn_bwd_heads(const void* q, const void* k, const void* v, c
   if (kv_head_count == 0) return WLB_OK;
   const int bf = (flags & WLB_BWD_DKV_BF16) != 0;
   const bool cov = (flags & WLB_BWD_COVERED_ONLY) != 0;
+  const wlb::CpSync none = wlb::cp_sync_none();
   if (D == 64)
     return wlb::launch_bwd<64>(q, k, v, o, do_, lse, dq, dk, dv, rowset_off, doc_start, n_docs,
                                positions, Tl, T, Hq, Hkv, scale, ws, bf, cov, kv_head_begin,
-                               kv_head_count, (cudaStream_t)stream);
+                               kv_head_count, none, (cudaStream_t)stream);
   return wlb::launch_bwd<128>(q, k, v, o, do_, lse, dq, dk, dv, rowset_off, doc_start, n_docs,
                               positions, Tl, T, Hq, Hkv, scale, ws, bf, cov, kv_head_begin,
-                              kv_head_count, (cudaStream_t)stream);
+                              kv_head_count, none, (cudaStream_t)stream);
+}
+
+extern "C" int wlb_attn_bwd_sync(const void* q, const void* k, const void* v, const void* o,
+                                 const void* do_, const float* lse, void* dq, void* dk, void* dv,
+                                 const int32_t* rowset_off, const int32_t* doc_start,
+                                 int32_t n_docs, const int32_t* positions, int32_t Tl, int32_t T,
+                                 int32_t Hq, int32_t Hkv, int32_t D, float scale, void* ws,
+                                 int32_t flags, const WlbCpSync* sync, void* stream) {
+  WLB_REQUIRE(D == 64 || D == 128, "head dim %d unsupported (64 or 128)", D);
+  WLB_REQUIRE(Hq > 0 && Hkv > 0 && Hq % Hkv == 0, "Hq must be a multiple of Hkv");
+  WLB_REQUIRE(Tl >= 0 && T > 0 && n_docs >= 0 && ws != nullptr, "bad sizes");
+  WLB_REQUIRE((flags & ~(WLB_BWD_DKV_BF16 | WLB_BWD_COVERED_ONLY)) == 0,
+              "unknown backward flags 0x%x", flags);
+  WLB_REQUIRE(!sync || (sync->cp >= 1 && sync->kv_per_group >= 1 &&
+                        Hkv % sync->kv_per_group == 0 && sync->counters),
+              "bad CP sync descriptor");
+  const int bf = (flags & WLB_BWD_DKV_BF16) != 0;
+  const bool cov = (flags & WLB_BWD_COVERED_ONLY) != 0;
+  const wlb::CpSync s = wlb::cp_sync_from(sync);
+  if (D == 64)
+    return wlb::launch_bwd<64>(q, k, v, o, do_, lse, dq, dk, dv, rowset_off, doc_start, n_docs,
+                               positions, Tl, T, Hq, Hkv, scale, ws, bf, cov, 0, Hkv, s,
+                               (cudaStream_t)stream);
+  return wlb::launch_bwd<128>(q, k, v, o, do_, lse, dq, dk, dv, rowset_off, doc_start, n_docs,
+                              positions, Tl, T, Hq, Hkv, scale, ws, bf, cov, 0, Hkv, s,
+                              (cudaStream_t)stream);
 }
 
 extern "C" int wlb_attn_bwd_ex(const void* q, const void* k, const void* v, const void* o,

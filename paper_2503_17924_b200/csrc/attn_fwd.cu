@@ -100,7 +100,8 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ out,
                 float* __restrict__ lse, const int4* __restrict__ items,
                 const int* __restrict__ n_items, const int* __restrict__ positions, int Tl,
-                int Hq, int Hkv, int n_slots, int hpc, int h_begin, int h_end, float scale_log2) {
+                int Hq, int Hkv, int n_slots, int hpc, int h_begin, int h_end, float scale_log2,
+                const CpSync sync) {
   using C = FwdCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -157,8 +158,13 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
+    int waited = -1;                 // head group whose peers' K/V are known landed
     for (int hh = 0; hh < nh; ++hh) {
       const int h = h0 + hh, kvh = h / group;
+      if (kvh / sync.kv_per_group != waited) {   // CP: the group's K/V rows have landed
+        waited = kvh / sync.kv_per_group;
+        cp_sync_wait_group(sync, waited, lane);
+      }
       if (hh > 0) mbar_wait(&bars->q_empty, (hh - 1) & 1);   // last QK of head hh-1 done
       mbar_expect_tx_w(&bars->q_full, (ty.y ? 2 : 1) * C::Q_BYTES);
       for (int s = 0; s < C::SLABS; ++s) {
@@ -429,7 +435,8 @@ template <int D>
 static int launch_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
                       const int32_t* tiles, const int32_t* n_tiles, int32_t max_tiles,
                       const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq, int32_t Hkv,
-                      int32_t h_begin, int32_t h_count, float scale, cudaStream_t stream) {
+                      int32_t h_begin, int32_t h_count, float scale, const CpSync& sync,
+                      cudaStream_t stream) {
   using C = FwdCfg<D>;
   CUtensorMap tq, tk, tv;
   int rc;
@@ -450,7 +457,7 @@ static int launch_fwd(const void* q, const void* k, const void* v, void* o, floa
   attn_fwd_kernel<D><<<(unsigned)max_tiles * ((h_count + hpc - 1) / hpc), C::THREADS, C::SMEM,
                        stream>>>(
       tq, tk, tv, (__nv_bfloat16*)o, lse, (const int4*)tiles, n_tiles, positions, Tl, Hq, Hkv,
-      max_tiles, hpc, h_begin, h_begin + h_count, scale_log2);
+      max_tiles, hpc, h_begin, h_begin + h_count, scale_log2, sync);
   WLB_LAUNCH_CHECK();
   return WLB_OK;
 }
@@ -480,9 +487,30 @@ extern "C" int wlb_attn_fwd_heads(const void* q, const void* k, const void* v, v
   if (D == 64)
     return wlb::launch_fwd<64>(q, k, v, o, lse, tiles, n_tiles, max_tiles, positions, Tl, T, Hq,
                                Hkv, kv_head_begin * g, kv_head_count * g, scale,
-                               (cudaStream_t)stream);
+                               wlb::cp_sync_none(), (cudaStream_t)stream);
   return wlb::launch_fwd<128>(q, k, v, o, lse, tiles, n_tiles, max_tiles, positions, Tl, T, Hq,
-                              Hkv, kv_head_begin * g, kv_head_count * g, scale, (cudaStream_t)stream);
+                              Hkv, kv_head_begin * g, kv_head_count * g, scale,
+                              wlb::cp_sync_none(), (cudaStream_t)stream);
+}
+
+extern "C" int wlb_attn_fwd_sync(const void* q, const void* k, const void* v, void* o, float* lse,
+                                 const int32_t* tiles, const int32_t* n_tiles, int32_t max_tiles,
+                                 const int32_t* positions, int32_t Tl, int32_t T, int32_t Hq,
+                                 int32_t Hkv, int32_t D, float scale, const WlbCpSync* sync,
+                                 void* stream) {
+  WLB_REQUIRE(D == 64 || D == 128, "head dim %d unsupported (64 or 128)", D);
+  WLB_REQUIRE(Hq > 0 && Hkv > 0 && Hq % Hkv == 0, "Hq must be a multiple of Hkv");
+  WLB_REQUIRE(Tl >= 0 && T > 0 && max_tiles >= 0, "bad sizes");
+  WLB_REQUIRE(!sync || (sync->cp >= 1 && sync->kv_per_group >= 1 &&
+                        Hkv % sync->kv_per_group == 0),
+              "bad CP sync descriptor");
+  if (Tl == 0 || max_tiles == 0) return WLB_OK;
+  const wlb::CpSync s = wlb::cp_sync_from(sync);
+  if (D == 64)
+    return wlb::launch_fwd<64>(q, k, v, o, lse, tiles, n_tiles, max_tiles, positions, Tl, T, Hq,
+                               Hkv, 0, Hq, scale, s, (cudaStream_t)stream);
+  return wlb::launch_fwd<128>(q, k, v, o, lse, tiles, n_tiles, max_tiles, positions, Tl, T, Hq,
+                              Hkv, 0, Hq, scale, s, (cudaStream_t)stream);
 }
 
 extern "C" int wlb_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,

@@ -65,6 +65,62 @@ void set_error(const char* fmt, ...);
     }                                                                                  \
   } while (0)
 
+// Device-side view of WlbCpSync (wlbcp.h): per-group arrival flags waited
+// for by the forward and published by the backward.
+struct CpSync {
+  const int* wait_flags;
+  const unsigned long long* signal_bases;
+  long long signal_off;
+  int* counters;
+  int cp, kv_per_group, epoch;
+};
+
+__host__ __device__ __forceinline__ CpSync cp_sync_none() {
+  return CpSync{nullptr, nullptr, 0, nullptr, 0, 1, 0};
+}
+
+// Spin (one warp) until the cp flags of group g are >= epoch, with a
+// system-scope acquire; then order the async proxy (TMA) after it.
+__device__ __forceinline__ void cp_sync_wait_group(const CpSync& s, int g, int lane) {
+  if (!s.wait_flags) return;
+  const int* f = s.wait_flags + (size_t)g * s.cp;
+  for (int p = lane; p < s.cp; p += 32) {
+    while (true) {
+      int x;
+      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(x) : "l"(f + p) : "memory");
+      if (x >= s.epoch) break;
+      __nanosleep(64);
+    }
+  }
+  __syncwarp();
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// One work unit of head group g is complete (its partial stores issued by
+// this CTA's threads, which have all passed a barrier before this call, made
+// by one thread): count it; the unit completing the group publishes epoch to
+// every peer.
+__device__ __forceinline__ void cp_sync_unit_done(const CpSync& s, int g, int target) {
+  if (!s.signal_bases) return;
+  __threadfence();
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(s.counters + g) : "memory");
+  if (old == target - 1) {
+    __threadfence_system();
+    for (int p = 0; p < s.cp; ++p) {
+      int* f = reinterpret_cast<int*>(reinterpret_cast<char*>(s.signal_bases[p]) + s.signal_off +
+                                      4ll * s.cp * g);
+      asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(f), "r"(s.epoch) : "memory");
+    }
+  }
+}
+
+inline CpSync cp_sync_from(const WlbCpSync* s) {
+  if (!s) return CpSync{nullptr, nullptr, 0, nullptr, 0, 1, 0};
+  return CpSync{s->wait_flags, reinterpret_cast<const unsigned long long*>(s->signal_bases),
+                s->signal_off, s->counters, s->cp, s->kv_per_group, s->epoch};
+}
+
 // Rotary angle of in-document position `pos` and frequency index i (of D/2):
 // pos * base^(-2i/D) formed in fp64 and reduced to [-pi, pi] before the fp32
 // sincos.  Positions reach 1.3e5 at 128K, where an fp32 product is already

@@ -69,18 +69,27 @@ def _run_group(cp, policy, hq, hkv, d, covered=True, passes=2, seed=0, groups=No
                 # gated by the peers' KV flags, each group's partials signalled
                 sh = shards[b][r]
                 ql, dol = q[idx[r]].contiguous(), do[idx[r]].contiguous()
-                o = lse = None
-                for gi, grp in enumerate(ex[r].groups):
-                    ex[r].wait_kv(b, gi)
-                    o, lse = attn_forward(ql, full[r][0], full[r][1], sh.tiles, kv_heads=grp,
-                                          out=None if o is None else (o, lse))
                 dk_out, dv_out = ex[r].dkv_out(sh, b, cur)
                 dq, ws = torch.empty_like(ql), bwd_workspace(ql, full[r][0], sh.tiles)
-                for gi, grp in enumerate(ex[r].groups):
+                if ex[r].fused_sync:
+                    # one launch per direction, waits / signals inside the kernels
+                    o, lse = attn_forward(ql, full[r][0], full[r][1], sh.tiles,
+                                          sync=ex[r].fwd_sync(b))
                     attn_backward(ql, full[r][0], full[r][1], o, lse, dol, sh.tiles,
                                   dk_out=dk_out, dv_out=dv_out, covered_only=ex[r].pull_covered,
-                                  kv_heads=grp, dq_out=dq, ws=ws)
-                    ex[r].signal_dkv(b, gi)
+                                  dq_out=dq, ws=ws, sync=ex[r].bwd_sync(b))
+                else:
+                    o = lse = None
+                    for gi, grp in enumerate(ex[r].groups):
+                        ex[r].wait_kv(b, gi)
+                        o, lse = attn_forward(ql, full[r][0], full[r][1], sh.tiles, kv_heads=grp,
+                                              out=None if o is None else (o, lse))
+                    for gi, grp in enumerate(ex[r].groups):
+                        attn_backward(ql, full[r][0], full[r][1], o, lse, dol, sh.tiles,
+                                      dk_out=dk_out, dv_out=dv_out,
+                                      covered_only=ex[r].pull_covered, kv_heads=grp, dq_out=dq,
+                                      ws=ws)
+                        ex[r].signal_dkv(b, gi)
                 parts.append((o, dq, dk_out, dv_out))
             outs = []
             for r in range(cp):
@@ -105,11 +114,28 @@ def test_local_peers_exchange_matches_oracle(cp, policy):
     _run_group(cp, policy, 4, 2, 128)
 
 
+@pytest.mark.parametrize("fused", ["1", "0"])
 @pytest.mark.parametrize("groups", [1, 3, 8])
-def test_head_groups(groups):
-    """Head-group exchange: KV heads split into 1, 3 (uneven) or 8 groups,
-    each pushed, signalled, attended and pulled on its own."""
+def test_head_groups(groups, fused, monkeypatch):
+    """Head-group exchange: KV heads split into 1, 3 (uneven: launched group by
+    group) or 8 groups, each pushed and signalled on its own; attention either
+    in one launch per direction that waits for / signals each group inside
+    the kernels (fused, equal groups) or group by group with wait / signal
+    kernels."""
+    monkeypatch.setenv("WLB_CP_FUSED_SYNC", fused)
     _run_group(4, "adaptive", 16, 8, 64, passes=1, seed=5, groups=groups)
+
+
+def test_fused_sync_v3_and_persistent_units():
+    """In-kernel signalling from the 128-query backward (long row-sets) and from
+    the persistent 64-query backward with several KV heads per unit."""
+    from paper_2503_17924_b200.attention import set_bwd_v3_min_rows
+    prev = set_bwd_v3_min_rows(0)
+    try:
+        _run_group(2, "per_document", 8, 8, 128, passes=1, seed=6, groups=2)
+    finally:
+        set_bwd_v3_min_rows(prev)
+    _run_group(8, "per_sequence", 8, 8, 128, passes=1, seed=7, groups=4)
 
 
 @pytest.mark.parametrize("cp", [4, 8])
