@@ -99,9 +99,14 @@ def main():
             o = cp_doc_attention(qq, kk, vv, sh, exchange=ex)
             o.backward(do)
 
+        fused = ex.fused_sync
         res[f"step_g{G}_ms"] = timed(step, a.reps)
         res[f"exposed_g{G}"] = round(1 - res["attn_ms"] / res[f"step_g{G}_ms"], 4)
         res[f"exposed_vs_split_g{G}"] = round(1 - res[f"attn_g{G}_ms"] / res[f"step_g{G}_ms"], 4)
+        if fused:   # the same groups launched one by one with wait / signal kernels
+            ex.fused_sync = False
+            res[f"step_g{G}_unfused_ms"] = timed(step, a.reps)
+            res[f"exposed_g{G}_unfused"] = round(1 - res["attn_ms"] / res[f"step_g{G}_unfused_ms"], 4)
         del ex
 
     def nccl_step():
@@ -110,6 +115,7 @@ def main():
         o.backward(do)
 
     res["nccl_ms"] = timed(nccl_step, a.reps)
+    res["attn_again_ms"] = timed(attn_only, a.reps)
     res["exposed_nccl"] = round(1 - res["attn_ms"] / res["nccl_ms"], 4)
     if rank == 0:
         print(json.dumps(res), flush=True)
