@@ -333,11 +333,16 @@ class SymmExchange:
         self.flag_bases = torch.tensor(flag_ptrs, dtype=torch.int64, device=device)
         groups = int(os.environ.get("WLB_HEAD_GROUPS", 4)) if groups is None else groups
         self.groups = head_groups(hkv, min(groups, MAX_GROUPS))
-        # in-kernel sync (one attention launch per direction, gated / signalling
-        # per head group on the device) needs equal groups; WLB_CP_FUSED_SYNC=0
-        # launches the attention group by group with wait / signal kernels
+        # In-kernel sync (one attention launch per direction, each forward CTA
+        # waiting on the device for its head group's flags, the backward
+        # signalling each group itself) needs equal groups and is OPT-IN
+        # (WLB_CP_FUSED_SYNC=1): waiting forward CTAs hold their SMs, and if
+        # they occupy every SM before a peer's push kernel is resident the
+        # exchange starves (measured: a 2-GPU 128K step hung until the wait
+        # timeout).  The default launches the attention group by group behind
+        # one-warp wait kernels, which can never take all SMs.
         self.fused_sync = (hkv % len(self.groups) == 0
-                           and os.environ.get("WLB_CP_FUSED_SYNC", "1") != "0")
+                           and os.environ.get("WLB_CP_FUSED_SYNC", "0") == "1")
         self.counters = torch.zeros((slots, MAX_GROUPS), dtype=torch.int32, device=device)
         self.seq = 0                    # micro-batches pushed (flag epochs)
         self.epoch = [0] * slots        # epoch of the micro-batch in slot s

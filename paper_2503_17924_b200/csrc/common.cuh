@@ -80,16 +80,25 @@ __host__ __device__ __forceinline__ CpSync cp_sync_none() {
 }
 
 // Spin (one warp) until the cp flags of group g are >= epoch, with a
-// system-scope acquire; then order the async proxy (TMA) after it.
+// system-scope acquire; then order the async proxy (TMA) after it.  Traps
+// after 20 s: waiting CTAs hold their SMs, so a caller that lets them start
+// before the exchange kernels they wait for are resident can deadlock (see
+// SymmExchange.fused_sync).
 __device__ __forceinline__ void cp_sync_wait_group(const CpSync& s, int g, int lane) {
   if (!s.wait_flags) return;
   const int* f = s.wait_flags + (size_t)g * s.cp;
   for (int p = lane; p < s.cp; p += 32) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     while (true) {
       int x;
       asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(x) : "l"(f + p) : "memory");
       if (x >= s.epoch) break;
       __nanosleep(64);
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      // spinning CTAs can starve the exchange kernels of SMs: never hang the GPU
+      if (t - t0 > 20000000000ull) __trap();
     }
   }
   __syncwarp();

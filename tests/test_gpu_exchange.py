@@ -126,10 +126,12 @@ def test_head_groups(groups, fused, monkeypatch):
     _run_group(4, "adaptive", 16, 8, 64, passes=1, seed=5, groups=groups)
 
 
-def test_fused_sync_v3_and_persistent_units():
+def test_fused_sync_v3_and_persistent_units(monkeypatch):
     """In-kernel signalling from the 128-query backward (long row-sets) and from
-    the persistent 64-query backward with several KV heads per unit."""
+    the persistent 64-query backward with several KV heads per unit (opt-in
+    path, single-stream emulation: every push precedes every attention)."""
     from paper_2503_17924_b200.attention import set_bwd_v3_min_rows
+    monkeypatch.setenv("WLB_CP_FUSED_SYNC", "1")
     prev = set_bwd_v3_min_rows(0)
     try:
         _run_group(2, "per_document", 8, 8, 128, passes=1, seed=6, groups=2)
