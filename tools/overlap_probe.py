@@ -25,21 +25,29 @@ from paper_2503_17924_b200.attention import (attn_backward, attn_forward, bwd_wo
 from paper_2503_17924_b200.cp import SymmExchange, cp_doc_attention, shard_for_rank  # noqa: E402
 
 
-def timed(fn, reps):
-    fn()
-    ts = []
-    for _ in range(reps):
-        dist.barrier()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
+def timed_interleaved(fns, reps):
+    """min over `reps` rounds of each fn's time, the fns alternating inside a
+    round (GPU clocks drift by several % over a run under the power cap, so
+    back-to-back blocks of one fn would bias the comparison); max over ranks."""
+    for fn in fns.values():
         fn()
-        b.record()
-        b.synchronize()
-        ts.append(a.elapsed_time(b))
-    t = torch.tensor([min(ts)], device="cuda", dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t)
+    best = {k: float("inf") for k in fns}
+    for _ in range(reps):
+        for k, fn in fns.items():
+            dist.barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            b.synchronize()
+            best[k] = min(best[k], a.elapsed_time(b))
+    out = {}
+    for k, v in best.items():
+        t = torch.tensor([v], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out[k] = float(t)
+    return out
 
 
 def main():
@@ -49,7 +57,7 @@ def main():
     ap.add_argument("--hq", type=int, default=32)
     ap.add_argument("--hkv", type=int, default=32)
     ap.add_argument("--groups", type=int, nargs="+", default=[1, 2, 4, 8])
-    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--reps", type=int, default=4)
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
@@ -74,12 +82,13 @@ def main():
 
     res = {"world": world, "window": a.window, "seq": a.seq, "docs": len(lengths),
            "strategy": sh.strategy.value, "heads": [a.hq, a.hkv]}
-    res["attn_ms"] = timed(attn_only, a.reps)
+    fns = {"attn": attn_only}
+    exchanges = []
     for G in a.groups:
-        # the same kernels split into G head-group launches, no exchange
         grps = head_groups(a.hkv, G)
 
-        def attn_groups():
+        def attn_groups(grps=grps):
+            # the same kernels split into G head-group launches, no exchange
             o = lse = None
             for grp in grps:
                 o, lse = attn_forward(q, kf, vf, sh.tiles, kv_heads=grp,
@@ -91,32 +100,29 @@ def main():
                 attn_backward(q, kf, vf, o, lse, do, sh.tiles, dk_out=dk, dv_out=dv,
                               covered_only=True, kv_heads=grp, dq_out=dq, ws=ws)
 
-        res[f"attn_g{G}_ms"] = timed(attn_groups, a.reps)
         ex = SymmExchange(dist.group.WORLD, T, a.hkv, d, dev, groups=G)
+        exchanges.append(ex)
 
-        def step():
+        def step(ex=ex):
             qq, kk, vv = (x.detach().requires_grad_(True) for x in (q, k, v))
             o = cp_doc_attention(qq, kk, vv, sh, exchange=ex)
             o.backward(do)
 
-        fused = ex.fused_sync
-        res[f"step_g{G}_ms"] = timed(step, a.reps)
-        res[f"exposed_g{G}"] = round(1 - res["attn_ms"] / res[f"step_g{G}_ms"], 4)
-        res[f"exposed_vs_split_g{G}"] = round(1 - res[f"attn_g{G}_ms"] / res[f"step_g{G}_ms"], 4)
-        if fused:   # the same groups launched one by one with wait / signal kernels
-            ex.fused_sync = False
-            res[f"step_g{G}_unfused_ms"] = timed(step, a.reps)
-            res[f"exposed_g{G}_unfused"] = round(1 - res["attn_ms"] / res[f"step_g{G}_unfused_ms"], 4)
-        del ex
+        fns[f"attn_g{G}"] = attn_groups
+        fns[f"step_g{G}"] = step
 
     def nccl_step():
         qq, kk, vv = (x.detach().requires_grad_(True) for x in (q, k, v))
         o = cp_doc_attention(qq, kk, vv, sh)
         o.backward(do)
 
-    res["nccl_ms"] = timed(nccl_step, a.reps)
-    res["attn_again_ms"] = timed(attn_only, a.reps)
-    res["exposed_nccl"] = round(1 - res["attn_ms"] / res["nccl_ms"], 4)
+    fns["nccl"] = nccl_step
+    ms = timed_interleaved(fns, a.reps)
+    res["ms"] = {k: round(v, 3) for k, v in ms.items()}
+    for G in a.groups:
+        res[f"exposed_g{G}"] = round(1 - ms["attn"] / ms[f"step_g{G}"], 4)
+        res[f"exposed_vs_split_g{G}"] = round(1 - ms[f"attn_g{G}"] / ms[f"step_g{G}"], 4)
+    res["exposed_nccl"] = round(1 - ms["attn"] / ms["nccl"], 4)
     if rank == 0:
         print(json.dumps(res), flush=True)
     dist.destroy_process_group()
