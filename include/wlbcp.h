@@ -321,6 +321,18 @@ int wlb_cp_dkv_pull_part(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_
                          int32_t flags, const int32_t* rowset_all, int32_t rowset_stride,
                          const int32_t* positions_all, const int32_t* doc_start, int32_t n_docs,
                          void* stream);
+/* The K/V push on the COPY ENGINES: runs (host [n_runs][3] int64: local
+ * row, global row, rows) of this rank's local rows, columns [col_off,
+ * col_off + col_bytes) of every row, copied (2-D, pitch row_bytes) into every
+ * rank's buffer (peer_bases: HOST [cp] peer-mapped addresses) at k_off /
+ * v_off.  No SMs: the attention kernels keep every SM while K/V move, and
+ * attention CTAs waiting on the arrival flags inside the kernel
+ * (wlb_attn_fwd_sync) cannot starve the push. */
+int wlb_cp_kv_push_dma(const void* k_local, const void* v_local, const int64_t* runs,
+                       int32_t n_runs, int64_t row_bytes, int64_t col_off, int64_t col_bytes,
+                       const uint64_t* peer_bases, int64_t k_off, int64_t v_off, int32_t cp,
+                       void* stream);
+
 /* Per-peer arrival flags on symmetric memory (replace whole-slot barriers on
  * the data path).  wlb_cp_signal: once the work before it on `stream` is
  * complete, store `value` (system-scope release) at byte offset flag_off of

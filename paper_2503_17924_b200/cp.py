@@ -17,6 +17,7 @@ all-gather output order, so one index serves both permutations.
 
 from __future__ import annotations
 
+import ctypes
 import os
 
 from dataclasses import dataclass
@@ -344,6 +345,13 @@ class SymmExchange:
         self.fused_sync = (hkv % len(self.groups) == 0
                            and os.environ.get("WLB_CP_FUSED_SYNC", "0") == "1")
         self.counters = torch.zeros((slots, MAX_GROUPS), dtype=torch.int32, device=device)
+        # K/V push on the copy engines (WLB_XCHG_PUSH=dma): needs this rank's
+        # row runs on the host (the shard plan is read back once per plan)
+        self.push_dma = os.environ.get("WLB_XCHG_PUSH", "covered") == "dma"
+        self.kv_ptrs_host = (ctypes.c_uint64 * cp)(*kv_ptrs)
+        if self.push_dma and hkv % len(self.groups) == 0 and \
+                os.environ.get("WLB_CP_FUSED_SYNC", "1") != "0":
+            self.fused_sync = True   # safe: nothing the forward waits on needs an SM
         self.seq = 0                    # micro-batches pushed (flag epochs)
         self.epoch = [0] * slots        # epoch of the micro-batch in slot s
         self.free = [None] * slots     # event: all ranks finished pulling slot s
@@ -415,6 +423,15 @@ class SymmExchange:
         self.epoch[s] = self.seq
         self._kv_barrier()                  # every rank finished reading slot s
         row = self.hkv * self.d * 2
+        if self.push_dma:
+            runs = self._runs(shard)
+            for gi, (g0, ng) in enumerate(self.groups):
+                _native.check(_native.lib().wlb_cp_kv_push_dma(
+                    k.data_ptr(), v.data_ptr(), runs.ctypes.data, len(runs), row,
+                    g0 * self.d * 2, ng * self.d * 2, self.kv_ptrs_host, 2 * s * self.n * 2,
+                    (2 * s + 1) * self.n * 2, self.cp, _native.stream_ptr()), "wlb_cp_kv_push_dma")
+                self._signal(s, _KV, gi)
+            return self._view(self.kv, 2 * s, T), self._view(self.kv, 2 * s + 1, T)
         covered = self.push_covered and shard.tiles.n_docs > 0
         rows, pos = self._tables(shard) if covered else (None, None)
         p = _native.ptr
@@ -447,6 +464,20 @@ class SymmExchange:
             signal_off=self._flag_off(s, _DKV, 0, self.rank),
             counters=self.counters[s].data_ptr(), cp=self.cp,
             kv_per_group=self.hkv // len(self.groups), epoch=self.epoch[s])
+
+    def _runs(self, shard):
+        """This rank's local rows as contiguous runs (local row, global row,
+        rows) of the document-ordered buffer: its canonical ranges (host copy
+        of the shard plan, read once per plan)."""
+        import numpy as np
+        a = shard.plan.assignment(shard.index)
+        starts = np.concatenate([[0], np.cumsum(a.doc_lengths)])
+        out, local = [], 0
+        for p_, r in a.workers[self.rank]:
+            n = r.end - r.start
+            out.append((local, int(starts[p_]) + r.start, n))
+            local += n
+        return np.ascontiguousarray(np.array(out, dtype=np.int64).reshape(-1, 3))
 
     def wait_kv(self, b, gi):
         """On the current stream: later work waits until every peer's rows of

@@ -335,6 +335,32 @@ extern "C" int wlb_cp_dkv_pull_cov(const uint64_t* peer_bases, int64_t dk_off, i
                               positions_all, doc_start, n_docs, stream);
 }
 
+extern "C" int wlb_cp_kv_push_dma(const void* k_local, const void* v_local, const int64_t* runs,
+                                  int32_t n_runs, int64_t row_bytes, int64_t col_off,
+                                  int64_t col_bytes, const uint64_t* peer_bases, int64_t k_off,
+                                  int64_t v_off, int32_t cp, void* stream) {
+  WLB_REQUIRE(row_bytes > 0 && col_off >= 0 && col_bytes > 0 && col_off + col_bytes <= row_bytes,
+              "bad column range [%lld, %lld) of a %lld-byte row", (long long)col_off,
+              (long long)(col_off + col_bytes), (long long)row_bytes);
+  WLB_REQUIRE(cp >= 1 && n_runs >= 0 && (n_runs == 0 || runs) && peer_bases, "bad push arguments");
+  const char* ks = static_cast<const char*>(k_local);
+  const char* vs = static_cast<const char*>(v_local);
+  for (int32_t r = 0; r < n_runs; ++r) {
+    const int64_t lr = runs[3 * r], gr = runs[3 * r + 1], n = runs[3 * r + 2];
+    if (n <= 0) continue;
+    for (int32_t p = 0; p < cp; ++p) {
+      char* base = reinterpret_cast<char*>(peer_bases[p]);
+      WLB_CUDA_TRY(cudaMemcpy2DAsync(base + k_off + gr * row_bytes + col_off, row_bytes,
+                                     ks + lr * row_bytes + col_off, row_bytes, col_bytes, n,
+                                     cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+      WLB_CUDA_TRY(cudaMemcpy2DAsync(base + v_off + gr * row_bytes + col_off, row_bytes,
+                                     vs + lr * row_bytes + col_off, row_bytes, col_bytes, n,
+                                     cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    }
+  }
+  return WLB_OK;
+}
+
 extern "C" int wlb_cp_signal(const uint64_t* flag_bases, int64_t flag_off, int32_t cp,
                              int32_t value, void* stream) {
   WLB_REQUIRE(cp >= 1 && flag_off >= 0 && flag_off % 4 == 0, "bad signal arguments");

@@ -48,7 +48,8 @@ def _run_group(cp, policy, hq, hkv, d, covered=True, passes=2, seed=0, groups=No
     t_max = max(sum(x) for x in mbs)
     ex = LocalPeersExchange.create(cp, t_max, hkv, d, dev, fill=float("nan"), groups=groups)
     for e in ex:
-        e.push_covered = e.pull_covered = covered
+        e.pull_covered = covered
+        e.push_covered = covered and not e.push_dma
     g = torch.Generator(device=dev).manual_seed(seed)
     cur = torch.cuda.current_stream()
     results = []
@@ -124,6 +125,16 @@ def test_head_groups(groups, fused, monkeypatch):
     kernels."""
     monkeypatch.setenv("WLB_CP_FUSED_SYNC", fused)
     _run_group(4, "adaptive", 16, 8, 64, passes=1, seed=5, groups=groups)
+
+
+@pytest.mark.parametrize("groups", [1, 4])
+def test_dma_push_fused_sync(groups, monkeypatch):
+    """K/V pushed by the copy engines (WLB_XCHG_PUSH=dma: 2-D copies of this
+    rank's row runs and head-group columns into every rank), attention in one
+    launch per direction with in-kernel flag waits / signals."""
+    monkeypatch.setenv("WLB_XCHG_PUSH", "dma")
+    for cp, policy in ((2, "per_sequence"), (4, "per_document"), (8, "adaptive")):
+        _run_group(cp, policy, 8, 4, 128, passes=1, seed=10 + cp, groups=groups)
 
 
 def test_fused_sync_v3_and_persistent_units(monkeypatch):
