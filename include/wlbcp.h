@@ -343,6 +343,12 @@ int wlb_cp_kv_push_dma(const void* k_local, const void* v_local, const int64_t* 
 int wlb_cp_signal(const uint64_t* flag_bases, int64_t flag_off, int32_t cp, int32_t value,
                   void* stream);
 int wlb_cp_wait(const int32_t* flags, int32_t n, int32_t value, void* stream);
+/* The same as stream memory operations (cuStreamWriteValue32 /
+ * cuStreamWaitValue32 GEQ), executed by the GPU front end without an SM, so
+ * they make progress while kernels hold every SM (flag_bases: HOST [cp]). */
+int wlb_cp_signal_memop(const uint64_t* flag_bases, int64_t flag_off, int32_t cp, int32_t value,
+                        void* stream);
+int wlb_cp_wait_memop(const int32_t* flags, int32_t n, int32_t value, void* stream);
 
 #ifdef __cplusplus
 }

@@ -80,6 +80,8 @@ SIGNATURES = {
                                      _p]),
     "wlb_cp_signal": (C.c_int, [_p, _i64, _i32, _i32, _p]),
     "wlb_cp_wait": (C.c_int, [_p, _i32, _i32, _p]),
+    "wlb_cp_signal_memop": (C.c_int, [_p, _i64, _i32, _i32, _p]),
+    "wlb_cp_wait_memop": (C.c_int, [_p, _i32, _i32, _p]),
     "wlb_cp_dkv_pull_cov": (C.c_int, [_p, _i64, _i64, _p, _i64, _i64, _p, _p, _i32, _i32,
                                       _p, _i32, _p, _p, _i32, _p]),
 }

@@ -349,9 +349,14 @@ class SymmExchange:
         # row runs on the host (the shard plan is read back once per plan)
         self.push_dma = os.environ.get("WLB_XCHG_PUSH", "covered") == "dma"
         self.kv_ptrs_host = (ctypes.c_uint64 * cp)(*kv_ptrs)
+        self.flag_ptrs_host = (ctypes.c_uint64 * cp)(*flag_ptrs)
+        # with the copy-engine push, signals and stream-side waits are stream
+        # memory operations (GPU front end): no exchange step needs an SM, so
+        # attention CTAs waiting on flags inside the kernel cannot starve it
+        self.memops = self.push_dma
         if self.push_dma and hkv % len(self.groups) == 0 and \
                 os.environ.get("WLB_CP_FUSED_SYNC", "1") != "0":
-            self.fused_sync = True   # safe: nothing the forward waits on needs an SM
+            self.fused_sync = True
         self.seq = 0                    # micro-batches pushed (flag epochs)
         self.epoch = [0] * slots        # epoch of the micro-batch in slot s
         self.free = [None] * slots     # event: all ranks finished pulling slot s
@@ -403,14 +408,20 @@ class SymmExchange:
         return (((s * 2 + kind) * MAX_GROUPS + gi) * self.cp + src) * 4
 
     def _signal(self, s, kind, gi):
+        if self.memops:
+            _native.check(_native.lib().wlb_cp_signal_memop(
+                self.flag_ptrs_host, self._flag_off(s, kind, gi, self.rank), self.cp,
+                self.epoch[s], _native.stream_ptr()), "wlb_cp_signal_memop")
+            return
         _native.check(_native.lib().wlb_cp_signal(
             self.flag_bases.data_ptr(), self._flag_off(s, kind, gi, self.rank), self.cp,
             self.epoch[s], _native.stream_ptr()), "wlb_cp_signal")
 
     def _wait(self, s, kind, gi):
-        _native.check(_native.lib().wlb_cp_wait(
+        fn = "wlb_cp_wait_memop" if self.memops else "wlb_cp_wait"
+        _native.check(getattr(_native.lib(), fn)(
             self.flags.data_ptr() + self._flag_off(s, kind, gi, 0), self.cp, self.epoch[s],
-            _native.stream_ptr()), "wlb_cp_wait")
+            _native.stream_ptr()), fn)
 
     def gather(self, k, v, shard, b):
         """Push this rank's K/V rows of micro-batch b, group by group, each

@@ -15,6 +15,8 @@
 //
 // One warp per row, 16-byte vectors; cross-rank ordering is done by the
 // caller's symmetric-memory barriers on the same stream.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -357,6 +359,46 @@ extern "C" int wlb_cp_kv_push_dma(const void* k_local, const void* v_local, cons
                                      vs + lr * row_bytes + col_off, row_bytes, col_bytes, n,
                                      cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
     }
+  }
+  return WLB_OK;
+}
+
+// Stream memory operations (executed by the GPU front end, no SM): signal and
+// wait on the arrival flags even while attention CTAs hold every SM.
+namespace {
+typedef CUresult (*StreamValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+StreamValue32Fn memop(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<StreamValue32Fn>(p);
+}
+}  // namespace
+
+extern "C" int wlb_cp_signal_memop(const uint64_t* flag_bases, int64_t flag_off, int32_t cp,
+                                   int32_t value, void* stream) {
+  static StreamValue32Fn write = memop("cuStreamWriteValue32");
+  WLB_REQUIRE(write != nullptr, "cuStreamWriteValue32 unavailable");
+  WLB_REQUIRE(cp >= 1 && flag_off >= 0 && flag_off % 4 == 0 && flag_bases, "bad signal arguments");
+  for (int32_t p = 0; p < cp; ++p) {
+    // default flags: the write follows a memory barrier over the stream's prior work
+    const CUresult r = write((CUstream)stream, (CUdeviceptr)(flag_bases[p] + flag_off),
+                             (cuuint32_t)value, CU_STREAM_WRITE_VALUE_DEFAULT);
+    WLB_REQUIRE(r == CUDA_SUCCESS, "cuStreamWriteValue32 failed (%d)", (int)r);
+  }
+  return WLB_OK;
+}
+
+extern "C" int wlb_cp_wait_memop(const int32_t* flags, int32_t n, int32_t value, void* stream) {
+  static StreamValue32Fn wait = memop("cuStreamWaitValue32");
+  WLB_REQUIRE(wait != nullptr, "cuStreamWaitValue32 unavailable");
+  WLB_REQUIRE(n >= 0 && ((uintptr_t)flags & 3) == 0, "bad wait arguments");
+  for (int32_t i = 0; i < n; ++i) {
+    const CUresult r = wait((CUstream)stream, (CUdeviceptr)(flags + i), (cuuint32_t)value,
+                            CU_STREAM_WAIT_VALUE_GEQ);
+    WLB_REQUIRE(r == CUDA_SUCCESS, "cuStreamWaitValue32 failed (%d)", (int)r);
   }
   return WLB_OK;
 }
