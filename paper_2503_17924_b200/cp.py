@@ -353,8 +353,8 @@ class SymmExchange:
         # with the copy-engine push, signals and stream-side waits are stream
         # memory operations (GPU front end): no exchange step needs an SM, so
         # attention CTAs waiting on flags inside the kernel cannot starve it
-        self.memops = self.push_dma
-        if self.push_dma and hkv % len(self.groups) == 0 and \
+        self.memops = os.environ.get("WLB_CP_MEMOPS", "1" if self.push_dma else "0") == "1"
+        if self.push_dma and self.memops and hkv % len(self.groups) == 0 and \
                 os.environ.get("WLB_CP_FUSED_SYNC", "1") != "0":
             self.fused_sync = True
         self.seq = 0                    # micro-batches pushed (flag epochs)
