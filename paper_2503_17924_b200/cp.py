@@ -255,7 +255,8 @@ class NcclExchange:
 
 
 MAX_GROUPS = 8          # head groups per micro-batch in the flag layout
-_KV, _DKV = 0, 1         # flag kinds
+_KV, _DKV, _KV_FREE, _DKV_FREE = 0, 1, 2, 3   # flag kinds
+_KINDS = 4
 
 
 class SymmExchange:
@@ -302,7 +303,7 @@ class SymmExchange:
         kv_h = symm.rendezvous(kv, self.group)
         dkv = symm.empty(2 * slots * n, dtype=self._dkv_dtype(), device=device)  # [slot][dK|dV]
         dkv_h = symm.rendezvous(dkv, self.group)
-        flags = symm.empty(slots * 2 * MAX_GROUPS * cp, dtype=torch.int32, device=device)
+        flags = symm.empty(slots * _KINDS * MAX_GROUPS * cp, dtype=torch.int32, device=device)
         flags.zero_()
         flags_h = symm.rendezvous(flags, self.group)
         self._setup(cp, t_max, hkv, d, device, slots, kv, dkv, list(kv_h.buffer_ptrs),
@@ -405,7 +406,18 @@ class SymmExchange:
         return buf[idx * self.n: idx * self.n + T * self.hkv * self.d].view(T, self.hkv, self.d)
 
     def _flag_off(self, s, kind, gi, src):
-        return (((s * 2 + kind) * MAX_GROUPS + gi) * self.cp + src) * 4
+        return (((s * _KINDS + kind) * MAX_GROUPS + gi) * self.cp + src) * 4
+
+    def _slot_barrier(self, s, kind):
+        """Every rank has finished with slot s (kind _KV_FREE: reading its K/V;
+        _DKV_FREE: pulling its partials).  Stream memory operations in memops
+        mode (no SM: a symmetric-memory barrier is a kernel, which attention
+        CTAs waiting on flags could starve), else the symmetric barrier."""
+        if not self.memops:
+            (self._kv_barrier if kind == _KV_FREE else self._dkv_barrier)()
+            return
+        self._signal(s, kind, 0)
+        self._wait(s, kind, 0)
 
     def _signal(self, s, kind, gi):
         if self.memops:
@@ -432,7 +444,7 @@ class SymmExchange:
             raise ValueError(f"micro-batch of {T} tokens exceeds the exchange capacity {self.t_max}")
         self.seq += 1
         self.epoch[s] = self.seq
-        self._kv_barrier()                  # every rank finished reading slot s
+        self._slot_barrier(s, _KV_FREE)     # every rank finished reading slot s
         row = self.hkv * self.d * 2
         if self.push_dma:
             runs = self._runs(shard)
@@ -528,7 +540,7 @@ class SymmExchange:
                 rows.shape[-1] if covered else 0, p(pos),
                 shard.tiles.doc_start.data_ptr() if covered else None,
                 shard.tiles.n_docs if covered else 0, _native.stream_ptr()), "wlb_cp_dkv_pull_part")
-        self._dkv_barrier()                 # every rank finished pulling from slot s
+        self._slot_barrier(s, _DKV_FREE)    # every rank finished pulling from slot s
         ev = torch.cuda.Event()
         ev.record()
         self.free[s] = ev
@@ -555,7 +567,7 @@ class LocalPeersExchange(SymmExchange):
                for _ in range(cp)]
         dkvs = [torch.full((2 * slots * n,), float("nan"), dtype=cls._dkv_dtype(), device=device)
                 for _ in range(cp)]
-        flags = [torch.zeros(slots * 2 * MAX_GROUPS * cp, dtype=torch.int32, device=device)
+        flags = [torch.zeros(slots * _KINDS * MAX_GROUPS * cp, dtype=torch.int32, device=device)
                  for _ in range(cp)]
         kv_ptrs = [t.data_ptr() for t in kvs]
         dkv_ptrs = [t.data_ptr() for t in dkvs]
@@ -567,6 +579,7 @@ class LocalPeersExchange(SymmExchange):
             ex._setup(cp, t_max, hkv, d, device, slots, kvs[r], dkvs[r], kv_ptrs, dkv_ptrs,
                       flags[r], flag_ptrs, r, groups)
             ex._kv_barrier = ex._dkv_barrier = lambda: None
+            ex._slot_barrier = lambda s_, kind: None   # the caller orders the ranks
             out.append(ex)
         return out
 
