@@ -351,13 +351,16 @@ class SymmExchange:
         self.push_dma = os.environ.get("WLB_XCHG_PUSH", "covered") == "dma"
         self.kv_ptrs_host = (ctypes.c_uint64 * cp)(*kv_ptrs)
         self.flag_ptrs_host = (ctypes.c_uint64 * cp)(*flag_ptrs)
-        # with the copy-engine push, signals and stream-side waits are stream
-        # memory operations (GPU front end): no exchange step needs an SM, so
-        # attention CTAs waiting on flags inside the kernel cannot starve it
+        # with the copy-engine push, signals, stream-side waits and slot
+        # barriers are stream memory operations (GPU front end): no exchange
+        # step needs an SM.  Measured at N=4 (profiles/r02_exchange_transports.txt):
+        # the copy-engine push is 2-5x slower than the kernel push in isolation
+        # (2-D copies of 2 KB head-group rows) and leaves the single-micro-batch
+        # exposure where it was (7.1-7.5 % vs 7.9 %), so the kernel push stays
+        # the default.  The in-kernel sync (WLB_CP_FUSED_SYNC=1) on top of it
+        # passes the one- and two-GPU parity tests but trapped at N=4 on 128K
+        # micro-batches: it stays experimental.
         self.memops = os.environ.get("WLB_CP_MEMOPS", "1" if self.push_dma else "0") == "1"
-        if self.push_dma and self.memops and hkv % len(self.groups) == 0 and \
-                os.environ.get("WLB_CP_FUSED_SYNC", "1") != "0":
-            self.fused_sync = True
         self.seq = 0                    # micro-batches pushed (flag epochs)
         self.epoch = [0] * slots        # epoch of the micro-batch in slot s
         self.free = [None] * slots     # event: all ranks finished pulling slot s

@@ -133,6 +133,7 @@ def test_dma_push_fused_sync(groups, monkeypatch):
     rank's row runs and head-group columns into every rank), attention in one
     launch per direction with in-kernel flag waits / signals."""
     monkeypatch.setenv("WLB_XCHG_PUSH", "dma")
+    monkeypatch.setenv("WLB_CP_FUSED_SYNC", "1")
     for cp, policy in ((2, "per_sequence"), (4, "per_document"), (8, "adaptive")):
         _run_group(cp, policy, 8, 4, 128, passes=1, seed=10 + cp, groups=groups)
 
