@@ -1200,7 +1200,8 @@ template <int D>
 __global__ void __launch_bounds__(256) bwd_delta_kernel(const __nv_bfloat16* __restrict__ o,
                                                         const __nv_bfloat16* __restrict__ dout,
                                                         float* __restrict__ delta, int Tl, int Hq,
-                                                        int h_begin, int h_count) {
+                                                        int h_begin, int h_count,
+                                                        uint4* __restrict__ dq_zero) {
   constexpr int LPR = D / 8;                 // lanes per (row, head)
   constexpr int U = 4;                       // pairs in flight per thread
   const long long n = (long long)Tl * h_count;   // (row, head) pairs, heads [h_begin, +h_count)
@@ -1216,6 +1217,10 @@ __global__ void __launch_bounds__(256) bwd_delta_kernel(const __nv_bfloat16* __r
         const long long rh = h_count == Hq ? w : (w / h_count) * Hq + h_begin + w % h_count;
         a[u] = reinterpret_cast<const uint4*>(o + rh * D)[sub];
         b[u] = reinterpret_cast<const uint4*>(dout + rh * D)[sub];
+        if (dq_zero) {   // the (row, head)'s fp32 dQ accumulator slice, [Tl][Hq][D] layout
+          dq_zero[rh * (D / 4) + 2 * sub] = make_uint4(0, 0, 0, 0);
+          dq_zero[rh * (D / 4) + 2 * sub + 1] = make_uint4(0, 0, 0, 0);
+        }
       } else {
         a[u] = b[u] = make_uint4(0, 0, 0, 0);
       }
@@ -1476,12 +1481,12 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
 #endif
   // dQ accumulator of this launch's query heads: [Hq][D/4][Tl][4] (v3) keeps
   // a head contiguous, [Tl][Hq][D] (v2) strides it
-  if (v3 || h_count == Hq)
-    WLB_CUDA_TRY(cudaMemsetAsync(w.dq_acc + (size_t)h_begin * D * (v3 ? Tl : 1), 0,
+  // the 64-query kernel's [Tl][Hq][D] accumulator is zeroed by the Delta pass
+  // (same rows and heads, one launch fewer: ~12 us of a short rank's step);
+  // the 128-query kernel's [Hq][D/4][Tl][4] one keeps a head range contiguous
+  if (v3)
+    WLB_CUDA_TRY(cudaMemsetAsync(w.dq_acc + (size_t)h_begin * D * Tl, 0,
                                  (size_t)Tl * h_count * D * 4, stream));
-  else
-    WLB_CUDA_TRY(cudaMemset2DAsync(w.dq_acc + (size_t)h_begin * D, (size_t)Hq * D * 4, 0,
-                                   (size_t)h_count * D * 4, (size_t)Tl, stream));
   // dK/dV rows of every KV tile are stored whole by the kernel; only the keys
   // no KV tile covers (past a document's last local query position) are zeroed
   // here, instead of clearing 2 x T x Hkv x D x 4 bytes up front.
@@ -1496,7 +1501,8 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
     const long long lanes = (long long)Tl * h_count * (D / 8);
     const unsigned blocks = (unsigned)std::min<long long>((lanes + 255) / 256, 148 * 8);
     bwd_delta_kernel<D><<<blocks, 256, 0, stream>>>(
-        (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, w.delta, Tl, Hq, h_begin, h_count);
+        (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, w.delta, Tl, Hq, h_begin, h_count,
+        v3 ? nullptr : reinterpret_cast<uint4*>(w.dq_acc));
     WLB_LAUNCH_CHECK();
   }
   if (sync.signal_bases)
