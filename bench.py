@@ -320,7 +320,22 @@ def main():
     symm = args.exchange == "symm" and cp > 1
     exchange = SymmExchange(dist.group.WORLD, T, hkv, d, dev) if symm else NcclExchange(group)
     pipe = CPStepPipeline(group, exchange=exchange)
-    ex_launches = (2 if symm else 4) if cp > 1 else 0      # push+pull | 2 scatters + 2 gathers
+
+    def mb_launches():
+        """Kernel launches of this library per micro-batch (memsets excluded):
+        tile list + forward + backward (Delta, KV tiles, backward, dQ
+        conversion; + uncovered-row zero fill without the covered pull) and the
+        exchange.  Symmetric exchange, G head groups, group-by-group launches:
+        per group a flag wait + forward, backward passes + a signal, push +
+        signal, wait + pull, plus the two slot barriers."""
+        if cp == 1:
+            return 1 + 1 + 5
+        if not symm:
+            return 1 + 1 + 5 + 4                            # 2 row scatters + 2 row gathers
+        g = len(exchange.groups)
+        if exchange.fused_sync:
+            return 1 + 1 + 4 + 2 + 4 * g
+        return 1 + 2 * g + 5 * g + 2 + 4 * g
 
     # CP > 1: per-sequence vs per-document chosen by the measured-latency tile
     # model calibrated on B200 (tilemodel.py); CP = 1 has one sharding, which
@@ -330,7 +345,7 @@ def main():
 
     def step(record=None):
         shards = build_cp_shards(lengths, cp, rank, policy, model=model)
-        launches[0] += 1 + N_SEQ + N_SEQ * (5 + ex_launches)   # plan, tiles, attn, exchange
+        launches[0] += 1 + N_SEQ * mb_launches()                # plan + per micro-batch
 
         def timed(b, sh, kernels):
             if record is None:
