@@ -43,6 +43,7 @@ sys.path.insert(0, ROOT)
 
 import paper_2503_17924_b200 as wl  # noqa: E402
 from paper_2503_17924_b200.attention import attn_backward, attn_forward  # noqa: E402
+from paper_2503_17924_b200.hoststream import HostStreamedStep  # noqa: E402
 from paper_2503_17924_b200.cp import (CPStepPipeline, NcclExchange, SymmExchange,  # noqa: E402
                                       build_cp_shards)
 
@@ -426,8 +427,19 @@ def main():
                     torch.empty((tl, hkv, d), dtype=torch.bfloat16, pin_memory=True)]
         h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
         cur = torch.cuda.current_stream()
+        # head-group granularity (hoststream.HostStreamedStep): each group's
+        # columns of q, k, v, dO land and its O, dQ, dK, dV leave on their own,
+        # so one group's transfer (not one micro-batch's) is exposed at the
+        # step's start and end; the NCCL exchange keeps whole micro-batches
+        streamer = (HostStreamedStep(pipe, groups=int(os.environ.get("WLB_E2E_GROUPS", 4)),
+                                     order=os.environ.get("WLB_E2E_ORDER", "johnson"))
+                    if (symm or cp == 1) else None)
 
-        def e2e_step():
+        def e2e_step_groups():
+            shards = build_cp_shards(lengths, cp, rank, policy, model=model)
+            streamer.run(shards, [host_in] * N_SEQ, ins, [host_out] * N_SEQ)
+
+        def e2e_step_mb():
             shards = build_cp_shards(lengths, cp, rank, policy, model=model)
             h2d_s.wait_stream(cur)             # previous step is done reading the inputs
             ready, bwd_ready = [], []
@@ -464,6 +476,7 @@ def main():
                      on_outputs=d2h, keep_outputs=False)
             cur.wait_stream(d2h_s)
 
+        e2e_step = e2e_step_groups if streamer is not None else e2e_step_mb
         e2e_step()
         barrier()
         a, b_ = ev(), ev()
@@ -481,9 +494,11 @@ def main():
         e2e = {"value": round(step_flops * n_e2e / (float(e_ms) / 1e3) / 1e12, 2),
                "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": round(float(e_ms) / n_e2e, 2),
+               "granularity": "KV-head group" if streamer is not None else "micro-batch",
                "note": "every micro-batch: H2D k,v,q then dO from pinned host, D2H o "
                        "(during the backward) then dq,dk,dv (copy streams pipelined against "
-                       "compute); shard plan + attention through the public API"}
+                       "compute, per KV-head group: hoststream.HostStreamedStep); shard plan + "
+                       "attention through the public API"}
 
     if rank != 0:
         if world > 1:

@@ -438,10 +438,12 @@ class SymmExchange:
             self.flags.data_ptr() + self._flag_off(s, kind, gi, 0), self.cp, self.epoch[s],
             _native.stream_ptr()), fn)
 
-    def gather(self, k, v, shard, b):
+    def gather(self, k, v, shard, b, ready=None):
         """Push this rank's K/V rows of micro-batch b, group by group, each
         followed by a signal to every peer; returns the local slot's
-        document-ordered K / V views (read them only after `wait_kv`)."""
+        document-ordered K / V views (read them only after `wait_kv`).
+        ready: optional per-group CUDA events, group gi's push waits for
+        ready[gi] (its K / V columns copied in)."""
         s, T = b % self.slots, shard.gather_all.numel()
         if T > self.t_max:
             raise ValueError(f"micro-batch of {T} tokens exceeds the exchange capacity {self.t_max}")
@@ -452,6 +454,8 @@ class SymmExchange:
         if self.push_dma:
             runs = self._runs(shard)
             for gi, (g0, ng) in enumerate(self.groups):
+                if ready is not None:
+                    torch.cuda.current_stream().wait_event(ready[gi])
                 _native.check(_native.lib().wlb_cp_kv_push_dma(
                     k.data_ptr(), v.data_ptr(), runs.ctypes.data, len(runs), row,
                     g0 * self.d * 2, ng * self.d * 2, self.kv_ptrs_host, 2 * s * self.n * 2,
@@ -462,6 +466,8 @@ class SymmExchange:
         rows, pos = self._tables(shard) if covered else (None, None)
         p = _native.ptr
         for gi, (g0, ng) in enumerate(self.groups):
+            if ready is not None:
+                torch.cuda.current_stream().wait_event(ready[gi])
             _native.check(_native.lib().wlb_cp_kv_push_part(
                 k.data_ptr(), v.data_ptr(), shard.gather_local.data_ptr(), k.shape[0], row,
                 g0 * self.d * 2, ng * self.d * 2, self.kv_bases.data_ptr(),
@@ -521,10 +527,11 @@ class SymmExchange:
         every peer this rank's partials of gi are complete."""
         self._signal(b % self.slots, _DKV, gi)
 
-    def scatter(self, dkf, dvf, shard, b):
+    def scatter(self, dkf, dvf, shard, b, on_group=None):
         """Pull (on the current stream) this rank's rows of every rank's
         partials, each head group as soon as all peers' partials of it are
-        complete; fp32 dK / dV [T/cp, Hkv, D]."""
+        complete; fp32 dK / dV [T/cp, Hkv, D].  on_group(gi, dk, dv) is called
+        after group gi's pull is enqueued (e.g. to record an event)."""
         s = b % self.slots
         tl = shard.gather_local.numel()
         dk = torch.empty((tl, self.hkv, self.d), dtype=torch.float32, device=dkf.device)
@@ -543,6 +550,8 @@ class SymmExchange:
                 rows.shape[-1] if covered else 0, p(pos),
                 shard.tiles.doc_start.data_ptr() if covered else None,
                 shard.tiles.n_docs if covered else 0, _native.stream_ptr()), "wlb_cp_dkv_pull_part")
+            if on_group is not None:
+                on_group(gi, dk, dv)
         self._slot_barrier(s, _DKV_FREE)    # every rank finished pulling from slot s
         ev = torch.cuda.Event()
         ev.record()
@@ -610,6 +619,18 @@ class CPStepPipeline:
       waits for the peers' K/V of each group).
     * `on_outputs(b, (o, dq, dk, dv), event)` is called as soon as micro-batch
       b's outputs are enqueued; `event` fires when all four are complete.
+
+    Head-group granularity (`io_groups=G`, for streaming micro-batches from and
+    to host memory, `hoststream.HostStreamedStep`): the attention runs in the
+    KV-head groups `io_head_groups(hkv, G, cp)` returns (the exchange's groups
+    at CP > 1), `ready[b]` / `bwd_ready[b]` are then per-group event lists
+    gating that group's forward / backward, `on_group_forward(b, gi, o, ev)`
+    fires per group when its O columns are complete and
+    `on_group_outputs(b, gi, (o, dq, dk, dv), ev)` when its columns of all
+    four are (dK / dV after that group's exchange pull at CP > 1).
+    `dkv_dtype=torch.bfloat16` (grouped runs at CP = 1): the backward stores
+    dK / dV in bf16 directly (the same RNE rounding of the fp32 sums as a
+    later conversion, without a conversion pass on the copy stream).
     """
 
     def __init__(self, group=None, exchange=None):
@@ -628,21 +649,39 @@ class CPStepPipeline:
         # one-sided K/V pushes run ahead on their own stream (depth > 1)
         self.push = torch.cuda.Stream(priority=prio) if self.depth > 1 else self.comm
 
+    def io_head_groups(self, hkv: int, groups: int, cp: int):
+        """The KV-head groups a run with `io_groups=groups` uses."""
+        if cp > 1:
+            if not self.flagged or self.exchange.fused_sync:
+                raise ValueError("head-group I/O at CP > 1 needs the flagged SymmExchange")
+            return list(self.exchange.groups)
+        return head_groups(hkv, groups)
+
     def _gather(self, k, v, shard, b, cur, ready):
         # the slot being overwritten was last read by compute already enqueued
         # on `cur` (b - slots <= the last enqueued micro-batch), so wait for it
         # as well as for the inputs
         self.push.wait_stream(cur)
-        if ready is not None:
+        per_group = isinstance(ready, (list, tuple))
+        if per_group and not (self.flagged and shard.cp > 1):
+            # CP = 1 (no exchange): each group's forward waits for its own
+            # event; NCCL: the collective needs every group
+            ready = ready[-1] if shard.cp > 1 else None
+            per_group = False
+        if ready is not None and not per_group:
             self.push.wait_event(ready)
         with torch.cuda.stream(self.push):
-            k_full, v_full = self.exchange.gather(k, v, shard, b)
+            if per_group:
+                k_full, v_full = self.exchange.gather(k, v, shard, b, ready=ready)
+            else:
+                k_full, v_full = self.exchange.gather(k, v, shard, b)
             ev = torch.cuda.Event()
             ev.record(self.push)
         return k_full, v_full, ev
 
     def run(self, shards, inputs, scale=None, ready=None, on_kernels=None, on_outputs=None,
-            keep_outputs=True, bwd_ready=None, on_forward=None):
+            keep_outputs=True, bwd_ready=None, on_forward=None, io_groups=None,
+            on_group_forward=None, on_group_outputs=None, dkv_dtype=None):
         """inputs[b] = (q, k, v, do) local bf16 tensors.  Returns per micro-batch
         (o, dq, dk, dv) local tensors (dk/dv fp32), complete on the current stream
         (None entries when keep_outputs=False: consume them in on_outputs)."""
@@ -650,6 +689,7 @@ class CPStepPipeline:
         n = len(shards)
         rdy = ready if ready is not None else [None] * n
         brdy = bwd_ready if bwd_ready is not None else [None] * n
+        grouped = io_groups is not None
         # the covered pull reads only the partial rows each rank's KV tiles
         # wrote: skip the zero fill of the rest
         covered = bool(getattr(self.exchange, "pull_covered", False))
@@ -667,16 +707,23 @@ class CPStepPipeline:
             flagged = self.flagged and sh.cp > 1
             if not flagged:
                 cur.wait_event(ev)          # (flagged: the device-side waits gate each group)
-            if rdy[b] is not None:
+            if rdy[b] is not None and not grouped:
                 cur.wait_event(rdy[b])
             q, _, _, do = inputs[b]
             dk_out, dv_out = self.exchange.dkv_out(sh, b, cur) if sh.cp > 1 else (None, None)
             cov = covered and dk_out is not None and sh.tiles.n_docs > 0
 
+            gdone = []
+
             def kernels(q=q, do=do, k_full=k_full, v_full=v_full, sh=sh, dk_out=dk_out,
-                        dv_out=dv_out, b=b, flagged=flagged, cov=cov):
+                        dv_out=dv_out, b=b, flagged=flagged, cov=cov, gdone=gdone):
                 ex = self.exchange
                 fused = flagged and ex.fused_sync
+                if grouped:
+                    return self._grouped_kernels(b, sh, q, do, k_full, v_full, dk_out, dv_out, cov,
+                                                 scale, io_groups, rdy[b], brdy[b],
+                                                 on_group_forward, on_group_outputs, gdone,
+                                                 dkv_dtype)
                 if not flagged:
                     o, lse = attn_forward(q, k_full, v_full, sh.tiles, scale)
                 elif fused:
@@ -719,7 +766,15 @@ class CPStepPipeline:
             if not flagged:
                 self.comm.wait_event(done)  # (flagged: the pull waits on the DKV flags)
             with torch.cuda.stream(self.comm):
-                dk, dv = self.exchange.scatter(dkf, dvf, sh, b) if sh.cp > 1 else (dkf, dvf)
+                on_group = None
+                if grouped and sh.cp > 1 and on_group_outputs is not None:
+                    def on_group(gi, dk_, dv_, b=b, o=o, dq=dq, gdone=gdone):
+                        self.comm.wait_event(gdone[gi])     # the group's O and dQ
+                        gev = torch.cuda.Event()
+                        gev.record(self.comm)
+                        on_group_outputs(b, gi, (o, dq, dk_, dv_), gev)
+                dk, dv = (self.exchange.scatter(dkf, dvf, sh, b, on_group=on_group) if sh.cp > 1
+                          else (dkf, dvf))
                 if sh.cp > 1:
                     for t in (dkf, dvf):
                         t.record_stream(self.comm)
@@ -742,3 +797,45 @@ class CPStepPipeline:
         for fin in tail:
             cur.wait_event(fin)
         return outs
+
+    def _grouped_kernels(self, b, sh, q, do, k_full, v_full, dk_out, dv_out, cov, scale, io_groups,
+                         rdy, brdy, on_group_forward, on_group_outputs, gdone, dkv_dtype=None):
+        """One micro-batch's attention head group by head group, each group's
+        forward / backward gated on its own input events (host streaming)."""
+        cur = torch.cuda.current_stream()
+        flagged = self.flagged and sh.cp > 1
+        groups = self.io_head_groups(k_full.shape[1], io_groups, sh.cp)
+        for e in (rdy, brdy):
+            if e is not None and len(e) != len(groups):
+                raise ValueError(f"per-group events: expected {len(groups)}, got {len(e)}")
+        ex = self.exchange
+        o, lse = torch.empty_like(q), None
+        for gi, grp in enumerate(groups):
+            if flagged:
+                ex.wait_kv(b, gi)
+            if rdy is not None:
+                cur.wait_event(rdy[gi])
+            o, lse = attn_forward(q, k_full, v_full, sh.tiles, scale, kv_heads=grp,
+                                  out=None if lse is None else (o, lse))
+            if on_group_forward is not None:
+                fev = torch.cuda.Event()
+                fev.record(cur)
+                on_group_forward(b, gi, o, fev)
+        dq, ws = torch.empty_like(q), bwd_workspace(q, k_full, sh.tiles)
+        if not flagged:
+            T, hkv, d = k_full.shape
+            dk_out = torch.empty((T, hkv, d), dtype=dkv_dtype or torch.float32, device=q.device)
+            dv_out = torch.empty_like(dk_out)
+        for gi, grp in enumerate(groups):
+            if brdy is not None:
+                cur.wait_event(brdy[gi])
+            attn_backward(q, k_full, v_full, o, lse, do, sh.tiles, scale, dk_out, dv_out,
+                          covered_only=cov and flagged, kv_heads=grp, dq_out=dq, ws=ws)
+            if flagged:
+                ex.signal_dkv(b, gi)
+            gev = torch.cuda.Event()
+            gev.record(cur)
+            gdone.append(gev)
+            if not flagged and on_group_outputs is not None:
+                on_group_outputs(b, gi, (o, dq, dk_out, dv_out), gev)
+        return o, dq, dk_out, dv_out

@@ -1,0 +1,173 @@
+"""A step's CP attention streamed from and to pinned host memory.
+
+The end-to-end form of `CPStepPipeline.run`: every micro-batch's q, k, v and
+dO arrive from pinned host buffers and O, dQ, dK, dV go back, with the PCIe
+copies pipelined against the attention at KV-head-group granularity.  A
+micro-batch's group g starts its forward as soon as the q / k / v columns of
+g have landed (not the whole micro-batch), and the O / dQ / dK / dV columns
+of g leave as soon as they are complete, so the copy engines see one
+continuous stream in each direction and only one head group's transfer (not
+one micro-batch's) is exposed at the start and the end of the step.
+
+Head-group columns of a [T, H, D] tensor are strided (H*D elements per
+row), so each copy is one `cudaMemcpy2DAsync` of T rows of G*D elements: on
+B200 these run at the contiguous-copy rate down to 512-byte rows
+(`tools/pcie2d_probe.py`).  Copies use the CUDA runtime through cuda-python
+(`cuda.bindings.runtime`) on torch's streams; this is data movement only, the
+attention is the library's sm_100a kernels.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from .cp import CPStepPipeline
+
+try:
+    from cuda.bindings import runtime as _rt
+except ImportError:   # pragma: no cover - the image ships cuda-python
+    _rt = None
+
+
+# Rates used only to rank micro-batches (not reported): attention fwd+bwd
+# TFLOP/s of a B200 rank and the per-direction pinned-host copy rate with
+# both directions busy (tools/pcie2d_probe.py: 47-50 GB/s).
+_ATTN_FLOPS_EST = 900e12
+_PCIE_EST = 48e9
+
+
+def johnson_order(shards, hq: int, hkv: int, d: int):
+    """Micro-batch order for a step streamed through PCIe: Johnson's rule
+    for a two-stage flow shop (copies in, then attention): micro-batches whose
+    attention outlasts their input copies first (by increasing copy time),
+    then the rest by decreasing attention time.  The step then ends on a
+    short attention after the last input byte instead of a long one.  Uses
+    only the micro-batches' document lengths, so every CP rank gets the same
+    order."""
+    row_bytes = (2 * hq + 2 * hkv) * d * 2
+    jobs = []
+    for i, sh in enumerate(shards):
+        ls = sh.plan.lengths[sh.index]
+        attn = 14.0 * d * hq * sum(x * (x + 1) // 2 for x in ls) / sh.cp / _ATTN_FLOPS_EST
+        copy = sum(ls) / sh.cp * row_bytes / _PCIE_EST
+        jobs.append((i, copy, attn))
+    first = sorted((j for j in jobs if j[1] < j[2]), key=lambda j: j[1])
+    rest = sorted((j for j in jobs if j[1] >= j[2]), key=lambda j: -j[2])
+    return [j[0] for j in first + rest]
+
+
+def _copy_cols(dst, src, h0: int, nh: int, stream) -> None:
+    """dst[:, h0:h0+nh] = src[:, h0:h0+nh] (or the whole of a [T, nh, D]
+    side) for [T, H, D] tensors, host <-> device, on `stream`."""
+    if _rt is None:
+        raise RuntimeError("cuda-python (cuda.bindings) is required for host streaming")
+    T = dst.shape[0]
+    es = dst.element_size()
+    w = nh * dst.shape[2] * es
+
+    def side(t):
+        full = t.shape[1] != nh
+        return t.data_ptr() + (h0 * t.shape[2] * es if full else 0), t.shape[1] * t.shape[2] * es
+
+    dp, dpitch = side(dst)
+    sp, spitch = side(src)
+    err, = _rt.cudaMemcpy2DAsync(dp, dpitch, sp, spitch, w, T,
+                                 _rt.cudaMemcpyKind.cudaMemcpyDefault, stream.cuda_stream)
+    if err != _rt.cudaError_t.cudaSuccess:
+        raise RuntimeError(f"cudaMemcpy2DAsync failed: {err}")
+
+
+class HostStreamedStep:
+    """Run a step's micro-batches from pinned host inputs to pinned host
+    outputs through `pipe` (a `CPStepPipeline`), head group by head group.
+
+    run(shards, host_in, dev_in, host_out):
+      host_in[b]  = (q, k, v, do) pinned host bf16 [T/cp, H, D] (local rows)
+      dev_in[b]   = device bf16 buffers of the same shapes (overwritten)
+      host_out[b] = (o, dq, dk, dv) pinned host bf16 [T/cp, H, D]
+    Entries may repeat the same tensors (e.g. one host buffer for every
+    micro-batch).  order="johnson" (default) runs the micro-batches in
+    `johnson_order`; "given" keeps the list order.  The outputs are complete on the current stream when run
+    returns (stream-ordered; no host sync).  The step's input copies start
+    after the work already on the current stream (the previous step)."""
+
+    def __init__(self, pipe: CPStepPipeline, groups: int = 4, order: str = "johnson"):
+        if order not in ("johnson", "given"):
+            raise ValueError("order must be 'johnson' or 'given'")
+        self.pipe = pipe
+        self.groups = groups
+        self.order = order
+        self.h2d = torch.cuda.Stream()
+        self.d2h = torch.cuda.Stream()
+
+    def run(self, shards, host_in, dev_in, host_out, scale=None, on_kernels=None):
+        cur = torch.cuda.current_stream()
+        n = len(shards)
+        hkv = dev_in[0][1].shape[1]
+        hq = dev_in[0][0].shape[1]
+        for b in range(n):
+            want = [t.shape for t in dev_in[b]]
+            want = (want[0], want[0], want[1], want[1])
+            if ([t.shape for t in host_in[b]] != [t.shape for t in dev_in[b]]
+                    or [t.shape for t in host_out[b]] != list(want)):
+                raise ValueError(f"micro-batch {b}: host_in must match dev_in (q, k, v, do) and "
+                                 "host_out be (o, dq, dk, dv) shaped like (q, q, k, k)")
+            if not all(t.is_pinned() for t in host_in[b] + host_out[b]):
+                raise ValueError(f"micro-batch {b}: host buffers must be pinned")
+        if self.order == "johnson":
+            perm = johnson_order(shards, hq, hkv, dev_in[0][0].shape[2])
+            shards, host_in, dev_in, host_out = ([x[i] for i in perm]
+                                                 for x in (shards, host_in, dev_in, host_out))
+        g_of = [self.pipe.io_head_groups(hkv, self.groups, sh.cp) for sh in shards]
+        self.h2d.wait_stream(cur)            # the previous step is done with the inputs
+        ready, bwd_ready = [], []
+        for b in range(n):
+            q_h, k_h, v_h, do_h = host_in[b]
+            q_d, k_d, v_d, do_d = dev_in[b]
+            rg = hq // hkv
+            ev_f, ev_b = [], []
+            for (g0, ng) in g_of[b]:         # k, v, q of each group (the forward needs them)
+                _copy_cols(k_d, k_h, g0, ng, self.h2d)
+                _copy_cols(v_d, v_h, g0, ng, self.h2d)
+                _copy_cols(q_d, q_h, g0 * rg, ng * rg, self.h2d)
+                e = torch.cuda.Event()
+                e.record(self.h2d)
+                ev_f.append(e)
+            for (g0, ng) in g_of[b]:         # dO behind them (only the backward needs it)
+                _copy_cols(do_d, do_h, g0 * rg, ng * rg, self.h2d)
+                e = torch.cuda.Event()
+                e.record(self.h2d)
+                ev_b.append(e)
+            ready.append(ev_f)
+            bwd_ready.append(ev_b)
+
+        def on_group_forward(b, gi, o, ev):
+            g0, ng = g_of[b][gi]
+            rg = o.shape[1] // hkv
+            self.d2h.wait_event(ev)
+            _copy_cols(host_out[b][0], o, g0 * rg, ng * rg, self.d2h)
+            o.record_stream(self.d2h)
+
+        def on_group_outputs(b, gi, outs, ev):
+            g0, ng = g_of[b][gi]
+            o, dq, dk, dv = outs
+            rg = dq.shape[1] // hkv
+            self.d2h.wait_event(ev)
+            with torch.cuda.stream(self.d2h):
+                _copy_cols(host_out[b][1], dq, g0 * rg, ng * rg, self.d2h)
+                for src, dst in ((dk, host_out[b][2]), (dv, host_out[b][3])):
+                    part = src[:, g0:g0 + ng]
+                    if part.dtype != dst.dtype:      # CP > 1: fp32 sums -> the host dtype
+                        part = part.to(dst.dtype)
+                        _copy_cols(dst, part, g0, ng, self.d2h)
+                    else:
+                        _copy_cols(dst, src, g0, ng, self.d2h)
+                    part.record_stream(self.d2h)
+                for t in (dq, dk, dv):
+                    t.record_stream(self.d2h)
+
+        self.pipe.run(shards, dev_in, scale=scale, ready=ready, bwd_ready=bwd_ready,
+                      on_kernels=on_kernels, keep_outputs=False, io_groups=self.groups,
+                      on_group_forward=on_group_forward, on_group_outputs=on_group_outputs,
+                      dkv_dtype=host_out[0][2].dtype)
+        cur.wait_stream(self.d2h)

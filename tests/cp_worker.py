@@ -66,6 +66,26 @@ def _pipeline_cases(rank, world, dev, policy):
             outs = pipe.run(shards, inputs)
         torch.cuda.synchronize()
         res[name] = [[t.float().cpu() for t in o] for o in outs]
+    # the same step streamed from / to pinned host memory by KV-head group
+    # (hoststream.HostStreamedStep over the symmetric exchange)
+    from paper_2503_17924_b200.hoststream import HostStreamedStep
+    host_in = [tuple(t.cpu().pin_memory() for t in x) for x in inputs]
+    host_out = [tuple(torch.full(t.shape, float("nan"), dtype=torch.bfloat16).pin_memory()
+                      for t in x) for x in inputs]
+    dev_in = [tuple(torch.empty_like(t) for t in x) for x in inputs]
+    hs = HostStreamedStep(CPStepPipeline(exchange=SymmExchange(dist.group.WORLD, t_max, hkv, d,
+                                                               dev)))
+    for _ in range(2):
+        hs.run(shards, host_in, dev_in, host_out)
+    torch.cuda.synchronize()
+    for b in range(len(mbs)):
+        for tn, a, c in zip(("o", "dq", "dk", "dv"), host_out[b], res["symm"][b]):
+            c = c.bfloat16()
+            same = torch.equal(a, c) if tn != "dq" else \
+                (a.float() - c.float()).abs().max().item() <= 1e-2 * max(1.0, c.abs().max().item())
+            if not same:
+                failures.append(f"[rank {rank} {policy} mb{b}] host-streamed != pipeline {tn}: "
+                                f"{(a.float() - c.float()).abs().max().item():.3e}")
     for b, lengths in enumerate(mbs):
         q, k, v, do = full[b]
         idx = shards[b].gather_local.long().cpu()

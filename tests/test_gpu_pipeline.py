@@ -71,3 +71,37 @@ def test_pipeline_host_buffers_hooks():
         assert torch.equal(o, o2.cpu())
         assert (dq.float() - dq2.float().cpu()).abs().max() < 1e-2
         assert torch.allclose(dk, dk2.cpu(), atol=1e-4) and torch.allclose(dv, dv2.cpu(), atol=1e-4)
+
+
+@pytest.mark.parametrize("hq,hkv,groups", [(8, 8, 4), (8, 4, 2), (16, 4, 4), (8, 8, 3)])
+def test_host_streamed_step_cp1(hq, hkv, groups):
+    """hoststream.HostStreamedStep: per-KV-head-group H2D (2-D copies of the
+    group's columns), the attention gated group by group, per-group D2H of
+    O / dQ / dK / dV into pinned host buffers.  Host results equal the direct
+    kernels (O and dK / dV bit for bit after the bf16 rounding, dQ within the
+    fp32-atomics noise)."""
+    from paper_2503_17924_b200.hoststream import HostStreamedStep
+    lengths = [[300, 17, 1, 640, 129, 2, 959], [2048], [1000, 1048, 6]]
+    dev = torch.device("cuda")
+    g = torch.Generator().manual_seed(11)
+    host_in, host_out, dev_in = [], [], []
+    for ls in lengths:
+        T = sum(ls)
+        mk = lambda h: torch.randn((T, h, 128), generator=g).to(torch.bfloat16).pin_memory()
+        host_in.append((mk(hq), mk(hkv), mk(hkv), mk(hq)))
+        host_out.append(tuple(torch.full((T, h, 128), float("nan"), dtype=torch.bfloat16).pin_memory()
+                              for h in (hq, hq, hkv, hkv)))
+        dev_in.append(tuple(torch.empty_like(t, device=dev) for t in host_in[-1]))
+    shards = build_cp_shards(lengths, 1, 0, "adaptive")
+    step = HostStreamedStep(CPStepPipeline(), groups=groups)
+    for _ in range(2):                                   # buffers reused across steps
+        step.run(shards, host_in, dev_in, host_out)
+    torch.cuda.synchronize()
+    for hi, ho, sh in zip(host_in, host_out, shards):
+        q, k, v, do = (t.to(dev) for t in hi)
+        o2, lse = attn_forward(q, k, v, sh.tiles)
+        dq2, dk2, dv2 = attn_backward(q, k, v, o2, lse, do, sh.tiles)
+        o, dq, dk, dv = (t.to(dev) for t in ho)
+        assert torch.equal(o, o2)
+        assert (dq.float() - dq2.float()).abs().max() < 1e-2
+        assert torch.equal(dk, dk2.to(torch.bfloat16)) and torch.equal(dv, dv2.to(torch.bfloat16))
