@@ -425,67 +425,34 @@ def main():
                     torch.empty((tl, hq, d), dtype=torch.bfloat16, pin_memory=True),
                     torch.empty((tl, hkv, d), dtype=torch.bfloat16, pin_memory=True),
                     torch.empty((tl, hkv, d), dtype=torch.bfloat16, pin_memory=True)]
-        h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
-        cur = torch.cuda.current_stream()
-        # head-group granularity (hoststream.HostStreamedStep): each group's
-        # columns of q, k, v, dO land and its O, dQ, dK, dV leave on their own,
-        # so one group's transfer (not one micro-batch's) is exposed at the
-        # step's start and end; the NCCL exchange keeps whole micro-batches
-        streamer = (HostStreamedStep(pipe, groups=int(os.environ.get("WLB_E2E_GROUPS", 4)),
-                                     order=os.environ.get("WLB_E2E_ORDER", "johnson"))
-                    if (symm or cp == 1) else None)
+        # hoststream.HostStreamedStep: copies pipelined against the attention,
+        # per KV-head group where the step is PCIe-bound (each group's columns
+        # of q, k, v, dO land and its O, dQ, dK, dV leave on their own, so one
+        # group's transfer, not one micro-batch's, is exposed at the step's
+        # start and end), per micro-batch where the attention dominates
+        gsel = os.environ.get("WLB_E2E_GROUPS", "auto")
+        streamer = HostStreamedStep(pipe, groups=None if gsel == "mb" else
+                                    gsel if gsel == "auto" else int(gsel),
+                                    order=os.environ.get("WLB_E2E_ORDER", "johnson"))
 
-        def e2e_step_groups():
+        def e2e_step():
             shards = build_cp_shards(lengths, cp, rank, policy, model=model)
             streamer.run(shards, [host_in] * N_SEQ, ins, [host_out] * N_SEQ)
 
-        def e2e_step_mb():
-            shards = build_cp_shards(lengths, cp, rank, policy, model=model)
-            h2d_s.wait_stream(cur)             # previous step is done reading the inputs
-            ready, bwd_ready = [], []
-            with torch.cuda.stream(h2d_s):
-                # k, v, q first (the forward needs them), dO behind them (only
-                # the backward does), micro-batch by micro-batch
-                for b in range(N_SEQ):
-                    q_d, k_d, v_d, do_d = ins[b]
-                    for dst, src in ((k_d, host_in[1]), (v_d, host_in[2]), (q_d, host_in[0])):
-                        dst.copy_(src, non_blocking=True)
-                    e = torch.cuda.Event()
-                    e.record(h2d_s)
-                    ready.append(e)
-                    do_d.copy_(host_in[3], non_blocking=True)
-                    e = torch.cuda.Event()
-                    e.record(h2d_s)
-                    bwd_ready.append(e)
-
-            def d2h_o(b, o, ev):                # O leaves during the backward
-                d2h_s.wait_event(ev)
-                with torch.cuda.stream(d2h_s):
-                    host_out[0].copy_(o, non_blocking=True)
-                    o.record_stream(d2h_s)
-
-            def d2h(b, outs, fin):
-                d2h_s.wait_event(fin)           # dq (compute) and dk, dv (comm) complete
-                with torch.cuda.stream(d2h_s):
-                    for src, dst in zip(outs[1:], host_out[1:]):
-                        src = src if src.dtype == torch.bfloat16 else src.to(torch.bfloat16)
-                        dst.copy_(src, non_blocking=True)
-                        src.record_stream(d2h_s)
-
-            pipe.run(shards, ins, ready=ready, bwd_ready=bwd_ready, on_forward=d2h_o,
-                     on_outputs=d2h, keep_outputs=False)
-            cur.wait_stream(d2h_s)
-
-        e2e_step = e2e_step_groups if streamer is not None else e2e_step_mb
         e2e_step()
         barrier()
+        retries0 = torch.cuda.memory_stats(dev).get("num_alloc_retries", 0)
         a, b_ = ev(), ev()
         n_e2e = args.steps
+        marks = []
         a.record()
         for _ in range(n_e2e):
             e2e_step()
+            marks.append(ev())
+            marks[-1].record()
         b_.record()
         barrier()
+        e2e_steps = [round(x.elapsed_time(y), 1) for x, y in zip([a] + marks[:-1], marks)]
         e_ms = torch.tensor([a.elapsed_time(b_)], device=dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
@@ -494,11 +461,14 @@ def main():
         e2e = {"value": round(step_flops * n_e2e / (float(e_ms) / 1e3) / 1e12, 2),
                "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": round(float(e_ms) / n_e2e, 2),
-               "granularity": "KV-head group" if streamer is not None else "micro-batch",
+               "granularity": ("micro-batch" if streamer.last_groups is None else
+                               f"{streamer.last_groups} KV-head groups"),
+               "order": streamer.order, "rank0_step_ms": e2e_steps,
+               "alloc_retries": torch.cuda.memory_stats(dev).get("num_alloc_retries", 0) - retries0,
                "note": "every micro-batch: H2D k,v,q then dO from pinned host, D2H o "
-                       "(during the backward) then dq,dk,dv (copy streams pipelined against "
-                       "compute, per KV-head group: hoststream.HostStreamedStep); shard plan + "
-                       "attention through the public API"}
+                       "(during the backward) then dq,dk,dv, copy streams pipelined against "
+                       "the attention (hoststream.HostStreamedStep); shard plan + attention "
+                       "through the public API"}
 
     if rank != 0:
         if world > 1:

@@ -191,6 +191,10 @@ int wlb_attn_bwd(const void* q, const void* k, const void* v, const void* o,
  * document); the rest are left untouched instead of zero-filled.  For
  * consumers that read covered rows only (wlb_cp_dkv_pull_cov). */
 #define WLB_BWD_COVERED_ONLY 2
+/* WLB_PULL_OUT_BF16 (wlb_cp_dkv_pull_* flags): store the fp32 sums as bf16
+ * (round to nearest even) rows of the full head width, e.g. straight into a
+ * host-bound bf16 buffer without a conversion pass. */
+#define WLB_PULL_OUT_BF16 4
 int wlb_attn_bwd_ex(const void* q, const void* k, const void* v, const void* o,
                     const void* do_, const float* lse, void* dq, void* dk, void* dv,
                     const int32_t* rowset_off, const int32_t* doc_start, int32_t n_docs,
@@ -308,7 +312,8 @@ int wlb_cp_dkv_pull_cov(const uint64_t* peer_bases, int64_t dk_off, int64_t dv_o
  * col_bytes) of every row only (a range of KV heads; 16-B aligned), and the
  * covered variant when rowset_all != NULL (else every rank / every row).
  * For the pull, row_bytes / col_* count the partial rows (bf16 with
- * WLB_BWD_DKV_BF16), and dk / dv are fp32 rows of the full head width. */
+ * WLB_BWD_DKV_BF16), and dk / dv are fp32 rows of the full head width
+ * (bf16 with WLB_PULL_OUT_BF16). */
 int wlb_cp_kv_push_part(const void* k_local, const void* v_local, const int32_t* gather_local,
                         int64_t n_rows, int64_t row_bytes, int64_t col_off, int64_t col_bytes,
                         const uint64_t* peer_bases, int64_t k_off, int64_t v_off, int32_t cp,

@@ -21,6 +21,7 @@ LIB_PATH = os.environ.get("WLB_LIB_PATH", _DEFAULT_LIB)
 WLB_OK, WLB_EINVAL, WLB_ENODEV, WLB_ECUDA = 0, 22, 19, 1000
 WLB_BWD_DKV_BF16 = 1
 WLB_BWD_COVERED_ONLY = 2
+WLB_PULL_OUT_BF16 = 4
 
 _p, _i32, _i64, _f64, _f32, _sz = C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_float, C.c_size_t
 

@@ -527,17 +527,23 @@ class SymmExchange:
         every peer this rank's partials of gi are complete."""
         self._signal(b % self.slots, _DKV, gi)
 
-    def scatter(self, dkf, dvf, shard, b, on_group=None):
+    def scatter(self, dkf, dvf, shard, b, on_group=None, out_dtype=torch.float32):
         """Pull (on the current stream) this rank's rows of every rank's
         partials, each head group as soon as all peers' partials of it are
-        complete; fp32 dK / dV [T/cp, Hkv, D].  on_group(gi, dk, dv) is called
-        after group gi's pull is enqueued (e.g. to record an event)."""
+        complete; dK / dV [T/cp, Hkv, D] as the fp32 sums (or, with
+        out_dtype=torch.bfloat16, their bf16 rounding stored by the pull).
+        on_group(gi, dk, dv) is called after group gi's pull is enqueued
+        (e.g. to record an event)."""
+        if out_dtype not in (torch.float32, torch.bfloat16):
+            raise ValueError("out_dtype must be float32 or bfloat16")
         s = b % self.slots
         tl = shard.gather_local.numel()
-        dk = torch.empty((tl, self.hkv, self.d), dtype=torch.float32, device=dkf.device)
+        dk = torch.empty((tl, self.hkv, self.d), dtype=out_dtype, device=dkf.device)
         dv = torch.empty_like(dk)
         es = 2 if self.dkv_bf16 else 4
         flags = _native.WLB_BWD_DKV_BF16 if self.dkv_bf16 else 0
+        if out_dtype == torch.bfloat16:
+            flags |= _native.WLB_PULL_OUT_BF16
         covered = self.pull_covered and shard.tiles.n_docs > 0
         rows, pos = self._tables(shard) if covered else (None, None)
         p = _native.ptr
@@ -628,9 +634,11 @@ class CPStepPipeline:
     fires per group when its O columns are complete and
     `on_group_outputs(b, gi, (o, dq, dk, dv), ev)` when its columns of all
     four are (dK / dV after that group's exchange pull at CP > 1).
-    `dkv_dtype=torch.bfloat16` (grouped runs at CP = 1): the backward stores
-    dK / dV in bf16 directly (the same RNE rounding of the fp32 sums as a
-    later conversion, without a conversion pass on the copy stream).
+    `dkv_dtype=torch.bfloat16`: dK / dV come out in bf16 — at
+    CP = 1 stored by the backward, at CP > 1 by the exchange pull — the same
+    RNE rounding of the fp32 sums as a later conversion, without conversion
+    kernels on the copy stream (those competed with the attention for SMs:
+    6 % of the N=2 host-streamed step).
     """
 
     def __init__(self, group=None, exchange=None):
@@ -712,6 +720,10 @@ class CPStepPipeline:
             q, _, _, do = inputs[b]
             dk_out, dv_out = self.exchange.dkv_out(sh, b, cur) if sh.cp > 1 else (None, None)
             cov = covered and dk_out is not None and sh.tiles.n_docs > 0
+            if sh.cp == 1 and dkv_dtype is not None and not grouped:
+                T_, hkv_, d_ = inputs[b][1].shape
+                dk_out = torch.empty((T_, hkv_, d_), dtype=dkv_dtype, device=q.device)
+                dv_out = torch.empty_like(dk_out)
 
             gdone = []
 
@@ -773,8 +785,12 @@ class CPStepPipeline:
                         gev = torch.cuda.Event()
                         gev.record(self.comm)
                         on_group_outputs(b, gi, (o, dq, dk_, dv_), gev)
-                dk, dv = (self.exchange.scatter(dkf, dvf, sh, b, on_group=on_group) if sh.cp > 1
-                          else (dkf, dvf))
+                kw = {}
+                if on_group is not None:
+                    kw["on_group"] = on_group
+                if flagged and dkv_dtype is not None:
+                    kw["out_dtype"] = dkv_dtype     # the pull stores the dtype asked for
+                dk, dv = self.exchange.scatter(dkf, dvf, sh, b, **kw) if sh.cp > 1 else (dkf, dvf)
                 if sh.cp > 1:
                     for t in (dkf, dvf):
                         t.record_stream(self.comm)

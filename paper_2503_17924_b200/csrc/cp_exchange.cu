@@ -110,12 +110,13 @@ __global__ void kv_push_kernel(const int4* __restrict__ k, const int4* __restric
 // key past that is an exact zero, so the sums are the same and fewer bytes
 // cross NVLink (most under per-sequence shards, where a short document lives
 // in one rank's chunk).  rowset_all: [cp][rs] per-rank row-set offsets per
-// document; pos_all: [cp][tl] per-rank in-document positions.
-template <bool COVERED, bool BF16>
+// document; pos_all: [cp][tl] per-rank in-document positions.  OUT16: the
+// fp32 sums are stored as bf16 (round to nearest even), half the output bytes.
+template <bool COVERED, bool BF16, bool OUT16>
 __global__ void dkv_pull_kernel(const unsigned long long* __restrict__ bases, long long dk_off,
                                 long long dv_off, const int* __restrict__ gidx, long long n_rows,
                                 long long row_vecs, long long col0, long long ncol,
-                                float4* __restrict__ dk, float4* __restrict__ dv, int cp,
+                                void* __restrict__ dk_out, void* __restrict__ dv_out, int cp,
                                 const int* __restrict__ rowset_all, int rs,
                                 const int* __restrict__ pos_all, long long tl,
                                 const int* __restrict__ doc_start, int n_docs) {
@@ -151,14 +152,34 @@ __global__ void dkv_pull_kernel(const unsigned long long* __restrict__ bases, lo
           b[0] += y.x; b[1] += y.y; b[2] += y.z; b[3] += y.w;
         }
       }
-      if (BF16) {
+      if (OUT16) {
+        // one 16-B input vector of fp32 partials (4 values) -> 8 output bytes;
+        // of bf16 partials (8 values) -> 16
+        uint32_t ka[4], vb[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat162 x = __floats2bfloat162_rn(a[2 * e], a[2 * e + 1]);
+          __nv_bfloat162 y = __floats2bfloat162_rn(b[2 * e], b[2 * e + 1]);
+          ka[e] = *reinterpret_cast<uint32_t*>(&x);
+          vb[e] = *reinterpret_cast<uint32_t*>(&y);
+        }
+        if (BF16) {
+          reinterpret_cast<uint4*>(dk_out)[r * row_vecs + c] = make_uint4(ka[0], ka[1], ka[2], ka[3]);
+          reinterpret_cast<uint4*>(dv_out)[r * row_vecs + c] = make_uint4(vb[0], vb[1], vb[2], vb[3]);
+        } else {
+          reinterpret_cast<uint2*>(dk_out)[r * row_vecs + c] = make_uint2(ka[0], ka[1]);
+          reinterpret_cast<uint2*>(dv_out)[r * row_vecs + c] = make_uint2(vb[0], vb[1]);
+        }
+      } else if (BF16) {
+        float4* dk = reinterpret_cast<float4*>(dk_out);
+        float4* dv = reinterpret_cast<float4*>(dv_out);
         dk[(r * row_vecs + c) * 2] = make_float4(a[0], a[1], a[2], a[3]);
         dk[(r * row_vecs + c) * 2 + 1] = make_float4(a[4], a[5], a[6], a[7]);
         dv[(r * row_vecs + c) * 2] = make_float4(b[0], b[1], b[2], b[3]);
         dv[(r * row_vecs + c) * 2 + 1] = make_float4(b[4], b[5], b[6], b[7]);
       } else {
-        dk[r * row_vecs + c] = make_float4(a[0], a[1], a[2], a[3]);
-        dv[r * row_vecs + c] = make_float4(b[0], b[1], b[2], b[3]);
+        reinterpret_cast<float4*>(dk_out)[r * row_vecs + c] = make_float4(a[0], a[1], a[2], a[3]);
+        reinterpret_cast<float4*>(dv_out)[r * row_vecs + c] = make_float4(b[0], b[1], b[2], b[3]);
       }
     }
   }
@@ -262,7 +283,8 @@ extern "C" int wlb_cp_dkv_pull_part(const uint64_t* peer_bases, int64_t dk_off, 
                                     int32_t cp, int32_t flags, const int32_t* rowset_all,
                                     int32_t rowset_stride, const int32_t* positions_all,
                                     const int32_t* doc_start, int32_t n_docs, void* stream) {
-  WLB_REQUIRE((flags & ~WLB_BWD_DKV_BF16) == 0, "unknown pull flags 0x%x", flags);
+  WLB_REQUIRE((flags & ~(WLB_BWD_DKV_BF16 | WLB_PULL_OUT_BF16)) == 0, "unknown pull flags 0x%x",
+              flags);
   WLB_REQUIRE(row_bytes > 0 && row_bytes % 16 == 0 && dk_off % 16 == 0 && dv_off % 16 == 0,
               "rows and offsets must be 16-byte aligned");
   WLB_REQUIRE(col_off >= 0 && col_bytes >= 0 && col_off % 16 == 0 && col_bytes % 16 == 0 &&
@@ -278,15 +300,19 @@ extern "C" int wlb_cp_dkv_pull_part(const uint64_t* peer_bases, int64_t dk_off, 
                 "bad row-set table (n_docs %d, stride %d)", n_docs, rowset_stride);
   }
   if (n_rows <= 0 || col_bytes == 0) return WLB_OK;
-  const bool bf = (flags & WLB_BWD_DKV_BF16) != 0;
-  auto kern = covered ? (bf ? dkv_pull_kernel<true, true> : dkv_pull_kernel<true, false>)
-                      : (bf ? dkv_pull_kernel<false, true> : dkv_pull_kernel<false, false>);
+  const bool bf = (flags & WLB_BWD_DKV_BF16) != 0, o16 = (flags & WLB_PULL_OUT_BF16) != 0;
+  using K = decltype(&dkv_pull_kernel<true, true, true>);
+  const K kerns[2][2][2] = {
+      {{dkv_pull_kernel<false, false, false>, dkv_pull_kernel<false, false, true>},
+       {dkv_pull_kernel<false, true, false>, dkv_pull_kernel<false, true, true>}},
+      {{dkv_pull_kernel<true, false, false>, dkv_pull_kernel<true, false, true>},
+       {dkv_pull_kernel<true, true, false>, dkv_pull_kernel<true, true, true>}}};
   // row_bytes / col_* count the partial rows; the local fp32 outputs are
-  // twice as long for bf16 partials
-  kern<<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
+  // twice as long for bf16 partials (bf16 outputs: half as long as fp32)
+  kerns[covered][bf][o16]<<<grid_for(n_rows), 256, 0, (cudaStream_t)stream>>>(
       (const unsigned long long*)peer_bases, dk_off, dv_off, gather_local, n_rows, row_bytes / 16,
-      col_off / 16, col_bytes / 16, (float4*)dk, (float4*)dv, cp, rowset_all, rowset_stride,
-      positions_all, n_rows, doc_start, n_docs);
+      col_off / 16, col_bytes / 16, dk, dv, cp, rowset_all, rowset_stride, positions_all, n_rows,
+      doc_start, n_docs);
   WLB_LAUNCH_CHECK();
   return WLB_OK;
 }

@@ -36,6 +36,17 @@ _ATTN_FLOPS_EST = 900e12
 _PCIE_EST = 48e9
 
 
+def _estimates(shards, hq: int, hkv: int, d: int):
+    """Per micro-batch (input copy seconds, attention seconds) estimates."""
+    row_bytes = (2 * hq + 2 * hkv) * d * 2
+    out = []
+    for sh in shards:
+        ls = sh.plan.lengths[sh.index]
+        attn = 14.0 * d * hq * sum(x * (x + 1) // 2 for x in ls) / sh.cp / _ATTN_FLOPS_EST
+        out.append((sum(ls) / sh.cp * row_bytes / _PCIE_EST, attn))
+    return out
+
+
 def johnson_order(shards, hq: int, hkv: int, d: int):
     """Micro-batch order for a step streamed through PCIe: Johnson's rule
     for a two-stage flow shop (copies in, then attention): micro-batches whose
@@ -44,13 +55,7 @@ def johnson_order(shards, hq: int, hkv: int, d: int):
     short attention after the last input byte instead of a long one.  Uses
     only the micro-batches' document lengths, so every CP rank gets the same
     order."""
-    row_bytes = (2 * hq + 2 * hkv) * d * 2
-    jobs = []
-    for i, sh in enumerate(shards):
-        ls = sh.plan.lengths[sh.index]
-        attn = 14.0 * d * hq * sum(x * (x + 1) // 2 for x in ls) / sh.cp / _ATTN_FLOPS_EST
-        copy = sum(ls) / sh.cp * row_bytes / _PCIE_EST
-        jobs.append((i, copy, attn))
+    jobs = [(i, c, a) for i, (c, a) in enumerate(_estimates(shards, hq, hkv, d))]
     first = sorted((j for j in jobs if j[1] < j[2]), key=lambda j: j[1])
     rest = sorted((j for j in jobs if j[1] >= j[2]), key=lambda j: -j[2])
     return [j[0] for j in first + rest]
@@ -91,9 +96,11 @@ class HostStreamedStep:
     returns (stream-ordered; no host sync).  The step's input copies start
     after the work already on the current stream (the previous step)."""
 
-    def __init__(self, pipe: CPStepPipeline, groups: int = 4, order: str = "johnson"):
+    def __init__(self, pipe: CPStepPipeline, groups="auto", order: str = "johnson"):
         if order not in ("johnson", "given"):
             raise ValueError("order must be 'johnson' or 'given'")
+        if not (groups in ("auto", None) or (isinstance(groups, int) and groups >= 1)):
+            raise ValueError("groups must be 'auto', None or a positive int")
         self.pipe = pipe
         self.groups = groups
         self.order = order
@@ -118,8 +125,23 @@ class HostStreamedStep:
             perm = johnson_order(shards, hq, hkv, dev_in[0][0].shape[2])
             shards, host_in, dev_in, host_out = ([x[i] for i in perm]
                                                  for x in (shards, host_in, dev_in, host_out))
-        g_of = [self.pipe.io_head_groups(hkv, self.groups, sh.cp) for sh in shards]
+        groups = self.groups
+        if groups == "auto":
+            # head-group granularity pays where the step is PCIe-bound; where
+            # the attention dominates (CP > 1 at 128K) whole micro-batches
+            # measured faster (N=2: 1864 vs 1759 TFLOP/s e2e)
+            est = _estimates(shards, hq, hkv, dev_in[0][0].shape[2])
+            groups = 4 if sum(c for c, _ in est) >= 0.5 * sum(a for _, a in est) else None
+            if any(sh.cp > 1 for sh in shards) and not (self.pipe.flagged and
+                                                        not self.pipe.exchange.fused_sync):
+                groups = None                # (head-group I/O needs the flagged exchange)
+        self.last_groups = groups
         self.h2d.wait_stream(cur)            # the previous step is done with the inputs
+        if groups is None:
+            self._run_mb(shards, host_in, dev_in, host_out, scale, on_kernels)
+            cur.wait_stream(self.d2h)
+            return
+        g_of = [self.pipe.io_head_groups(hkv, groups, sh.cp) for sh in shards]
         ready, bwd_ready = [], []
         for b in range(n):
             q_h, k_h, v_h, do_h = host_in[b]
@@ -156,18 +178,53 @@ class HostStreamedStep:
             with torch.cuda.stream(self.d2h):
                 _copy_cols(host_out[b][1], dq, g0 * rg, ng * rg, self.d2h)
                 for src, dst in ((dk, host_out[b][2]), (dv, host_out[b][3])):
-                    part = src[:, g0:g0 + ng]
-                    if part.dtype != dst.dtype:      # CP > 1: fp32 sums -> the host dtype
-                        part = part.to(dst.dtype)
-                        _copy_cols(dst, part, g0, ng, self.d2h)
+                    if src.dtype != dst.dtype:       # (the pipeline stores the host dtype)
+                        src = src[:, g0:g0 + ng].to(dst.dtype)
+                        _copy_cols(dst, src, g0, ng, self.d2h)
                     else:
                         _copy_cols(dst, src, g0, ng, self.d2h)
-                    part.record_stream(self.d2h)
+                    src.record_stream(self.d2h)
                 for t in (dq, dk, dv):
                     t.record_stream(self.d2h)
 
         self.pipe.run(shards, dev_in, scale=scale, ready=ready, bwd_ready=bwd_ready,
-                      on_kernels=on_kernels, keep_outputs=False, io_groups=self.groups,
+                      on_kernels=on_kernels, keep_outputs=False, io_groups=groups,
                       on_group_forward=on_group_forward, on_group_outputs=on_group_outputs,
                       dkv_dtype=host_out[0][2].dtype)
         cur.wait_stream(self.d2h)
+
+    def _run_mb(self, shards, host_in, dev_in, host_out, scale, on_kernels):
+        """Whole-micro-batch granularity: k, v, q then dO of each micro-batch
+        in one copy each; O leaves after the forward, dQ / dK / dV after the
+        backward (and the exchange pull)."""
+        ready, bwd_ready = [], []
+        for b in range(len(shards)):
+            q_h, k_h, v_h, do_h = host_in[b]
+            q_d, k_d, v_d, do_d = dev_in[b]
+            for dst, src in ((k_d, k_h), (v_d, v_h), (q_d, q_h)):
+                _copy_cols(dst, src, 0, dst.shape[1], self.h2d)
+            e = torch.cuda.Event()
+            e.record(self.h2d)
+            ready.append(e)
+            _copy_cols(do_d, do_h, 0, do_d.shape[1], self.h2d)
+            e = torch.cuda.Event()
+            e.record(self.h2d)
+            bwd_ready.append(e)
+
+        def on_forward(b, o, ev):
+            self.d2h.wait_event(ev)
+            _copy_cols(host_out[b][0], o, 0, o.shape[1], self.d2h)
+            o.record_stream(self.d2h)
+
+        def on_outputs(b, outs, ev):
+            self.d2h.wait_event(ev)
+            with torch.cuda.stream(self.d2h):
+                for src, dst in zip(outs[1:], host_out[b][1:]):
+                    if src.dtype != dst.dtype:       # (NCCL exchange: fp32 sums)
+                        src = src.to(dst.dtype)
+                    _copy_cols(dst, src, 0, dst.shape[1], self.d2h)
+                    src.record_stream(self.d2h)
+
+        self.pipe.run(shards, dev_in, scale=scale, ready=ready, bwd_ready=bwd_ready,
+                      on_kernels=on_kernels, keep_outputs=False, on_forward=on_forward,
+                      on_outputs=on_outputs, dkv_dtype=host_out[0][2].dtype)

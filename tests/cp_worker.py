@@ -71,7 +71,7 @@ def _pipeline_cases(rank, world, dev, policy):
     from paper_2503_17924_b200.hoststream import HostStreamedStep
     host_in = [tuple(t.cpu().pin_memory() for t in x) for x in inputs]
     host_out = [tuple(torch.full(t.shape, float("nan"), dtype=torch.bfloat16).pin_memory()
-                      for t in x) for x in inputs]
+                      for t in (x[0], x[0], x[1], x[1])) for x in inputs]
     dev_in = [tuple(torch.empty_like(t) for t in x) for x in inputs]
     hs = HostStreamedStep(CPStepPipeline(exchange=SymmExchange(dist.group.WORLD, t_max, hkv, d,
                                                                dev)))

@@ -96,6 +96,13 @@ def _run_group(cp, policy, hq, hkv, d, covered=True, passes=2, seed=0, groups=No
             for r in range(cp):
                 dk, dv = ex[r].scatter(parts[r][2], parts[r][3], shards[b][r], b)
                 outs.append((parts[r][0], parts[r][1], dk, dv))
+            # the pull storing bf16 (WLB_PULL_OUT_BF16, host-streamed steps)
+            # == the fp32 sums rounded to bf16
+            for r in range(cp):
+                dk16, dv16 = ex[r].scatter(parts[r][2], parts[r][3], shards[b][r], b,
+                                           out_dtype=torch.bfloat16)
+                assert torch.equal(dk16, outs[r][2].to(torch.bfloat16)), f"cp={cp} rank {r} dk bf16 pull"
+                assert torch.equal(dv16, outs[r][3].to(torch.bfloat16)), f"cp={cp} rank {r} dv bf16 pull"
             torch.cuda.synchronize()
             segs = [(i, 0, x) for i, x in enumerate(lengths)]
             ro, _, rdq, rdk, rdv = ao.segment_attention_fwd_bwd_blocked(

@@ -73,13 +73,15 @@ def test_pipeline_host_buffers_hooks():
         assert torch.allclose(dk, dk2.cpu(), atol=1e-4) and torch.allclose(dv, dv2.cpu(), atol=1e-4)
 
 
-@pytest.mark.parametrize("hq,hkv,groups", [(8, 8, 4), (8, 4, 2), (16, 4, 4), (8, 8, 3)])
+@pytest.mark.parametrize("hq,hkv,groups", [(8, 8, 4), (8, 4, 2), (16, 4, 4), (8, 8, 3), (8, 4, None),
+                                            (8, 8, "auto")])
 def test_host_streamed_step_cp1(hq, hkv, groups):
     """hoststream.HostStreamedStep: per-KV-head-group H2D (2-D copies of the
     group's columns), the attention gated group by group, per-group D2H of
     O / dQ / dK / dV into pinned host buffers.  Host results equal the direct
     kernels (O and dK / dV bit for bit after the bf16 rounding, dQ within the
-    fp32-atomics noise)."""
+    fp32-atomics noise).  groups=None: whole micro-batches (one copy per
+    tensor, the CP = 1 backward storing bf16 dK / dV); "auto" picks one."""
     from paper_2503_17924_b200.hoststream import HostStreamedStep
     lengths = [[300, 17, 1, 640, 129, 2, 959], [2048], [1000, 1048, 6]]
     dev = torch.device("cuda")

@@ -1,14 +1,15 @@
 #!/usr/bin/env bash
-# which piece of the copy-engine / stream-memop exchange fails across GPUs
 set -u
 cd "$(dirname "$0")/.."
 N=$(nvidia-smi -L | wc -l)
 out=gpurun_out/r02m_n$N; mkdir -p $out
-run() {
-  env "$@" timeout 240 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr=127.0.0.1 --master-port=$((29800 + RANDOM % 100)) tests/cp_worker.py > $out/$1.log 2>&1
-  echo "$* rc=$? $(grep -c 'CP OK' $out/$1.log) ok; $(grep -m2 -iE 'error|FAIL' $out/$1.log | cut -c1-300)"
-}
-run WLB_XCHG_PUSH=dma WLB_CP_MEMOPS=0 WLB_CP_FUSED_SYNC=0
-run WLB_XCHG_PUSH=covered WLB_CP_MEMOPS=1 WLB_CP_FUSED_SYNC=0
-run WLB_XCHG_PUSH=dma WLB_CP_MEMOPS=1 WLB_CP_FUSED_SYNC=0
-run WLB_XCHG_PUSH=dma WLB_CP_MEMOPS=1 WLB_CP_FUSED_SYNC=1
+for m in groups mb; do
+WLB_E2E_MODE=$m timeout 500 python bench.py --gpus $N --steps 4 --warmup 3 --no-cpu-baseline > $out/b.json 2> $out/b.err
+python -c "
+import json
+d=json.loads(open('$out/b.json').read().strip().splitlines()[-1]); print('$m', d['value'], d['alloc_retries'], d['e2e'])"
+done
+PYTORCH_CUDA_ALLOC_CONF=expandable_segments:True WLB_E2E_MODE=groups timeout 500 python bench.py --gpus $N --steps 4 --warmup 3 --no-cpu-baseline > $out/b.json 2> $out/b.err
+python -c "
+import json
+d=json.loads(open('$out/b.json').read().strip().splitlines()[-1]); print('groups expandable', d['value'], d['alloc_retries'], d['e2e'])"
