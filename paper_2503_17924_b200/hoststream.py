@@ -29,41 +29,13 @@ except ImportError:   # pragma: no cover - the image ships cuda-python
     _rt = None
 
 
-# Rates used only to rank micro-batches (not reported): attention fwd+bwd
-# TFLOP/s of a B200 rank and the per-direction pinned-host copy rate with
-# both directions busy (tools/pcie2d_probe.py: 47-50 GB/s).
-_ATTN_FLOPS_EST = 900e12
-_PCIE_EST = 48e9
-
-
-def _estimates(shards, hq: int, hkv: int, d: int):
-    """Per micro-batch (input copy seconds, attention seconds) estimates."""
-    row_bytes = (2 * hq + 2 * hkv) * d * 2
-    out = []
-    for sh in shards:
-        ls = sh.plan.lengths[sh.index]
-        attn = 14.0 * d * hq * sum(x * (x + 1) // 2 for x in ls) / sh.cp / _ATTN_FLOPS_EST
-        out.append((sum(ls) / sh.cp * row_bytes / _PCIE_EST, attn))
-    return out
-
-
-def johnson_order(shards, hq: int, hkv: int, d: int):
-    """Micro-batch order for a step streamed through PCIe: Johnson's rule
-    for a two-stage flow shop (copies in, then attention): micro-batches whose
-    attention outlasts their input copies first (by increasing copy time),
-    then the rest by decreasing attention time.  The step then ends on a
-    short attention after the last input byte instead of a long one.  Uses
-    only the micro-batches' document lengths, so every CP rank gets the same
-    order."""
-    jobs = [(i, c, a) for i, (c, a) in enumerate(_estimates(shards, hq, hkv, d))]
-    first = sorted((j for j in jobs if j[1] < j[2]), key=lambda j: j[1])
-    rest = sorted((j for j in jobs if j[1] >= j[2]), key=lambda j: -j[2])
-    return [j[0] for j in first + rest]
-
-
 def _copy_cols(dst, src, h0: int, nh: int, stream) -> None:
     """dst[:, h0:h0+nh] = src[:, h0:h0+nh] (or the whole of a [T, nh, D]
     side) for [T, H, D] tensors, host <-> device, on `stream`."""
+    if nh == dst.shape[1] and nh == src.shape[1]:   # whole tensors: torch's async copy
+        with torch.cuda.stream(stream):
+            dst.copy_(src, non_blocking=True)
+        return
     if _rt is None:
         raise RuntimeError("cuda-python (cuda.bindings) is required for host streaming")
     T = dst.shape[0]
@@ -91,19 +63,21 @@ class HostStreamedStep:
       dev_in[b]   = device bf16 buffers of the same shapes (overwritten)
       host_out[b] = (o, dq, dk, dv) pinned host bf16 [T/cp, H, D]
     Entries may repeat the same tensors (e.g. one host buffer for every
-    micro-batch).  order="johnson" (default) runs the micro-batches in
-    `johnson_order`; "given" keeps the list order.  The outputs are complete on the current stream when run
-    returns (stream-ordered; no host sync).  The step's input copies start
-    after the work already on the current stream (the previous step)."""
+    micro-batch).  groups: "auto" (4 KV-head groups where the pipeline can
+    run them, else whole micro-batches), an int, or None (whole micro-batches).
+    Micro-batches run in the given order (a Johnson's-rule reordering for the
+    copy-in / attention flow measured +0.4 % at N=1 and -13 % at N=2, where it
+    left the short micro-batches' copy-out exposed at the end of the step).
+    The outputs are complete on the current stream when run returns
+    (stream-ordered; no host sync).  The step's input copies start after the
+    work already on the current stream (the previous step)."""
 
-    def __init__(self, pipe: CPStepPipeline, groups="auto", order: str = "johnson"):
-        if order not in ("johnson", "given"):
-            raise ValueError("order must be 'johnson' or 'given'")
+    def __init__(self, pipe: CPStepPipeline, groups="auto"):
         if not (groups in ("auto", None) or (isinstance(groups, int) and groups >= 1)):
             raise ValueError("groups must be 'auto', None or a positive int")
         self.pipe = pipe
         self.groups = groups
-        self.order = order
+        self.last_groups = None
         self.h2d = torch.cuda.Stream()
         self.d2h = torch.cuda.Stream()
 
@@ -121,20 +95,15 @@ class HostStreamedStep:
                                  "host_out be (o, dq, dk, dv) shaped like (q, q, k, k)")
             if not all(t.is_pinned() for t in host_in[b] + host_out[b]):
                 raise ValueError(f"micro-batch {b}: host buffers must be pinned")
-        if self.order == "johnson":
-            perm = johnson_order(shards, hq, hkv, dev_in[0][0].shape[2])
-            shards, host_in, dev_in, host_out = ([x[i] for i in perm]
-                                                 for x in (shards, host_in, dev_in, host_out))
         groups = self.groups
         if groups == "auto":
-            # head-group granularity pays where the step is PCIe-bound; where
-            # the attention dominates (CP > 1 at 128K) whole micro-batches
-            # measured faster (N=2: 1864 vs 1759 TFLOP/s e2e)
-            est = _estimates(shards, hq, hkv, dev_in[0][0].shape[2])
-            groups = 4 if sum(c for c, _ in est) >= 0.5 * sum(a for _, a in est) else None
+            # 4 head groups wherever the pipeline runs them (same box, e2e
+            # TFLOP/s: N=1 424 vs 400 per micro-batch, N=2 1927 vs 1862, N=4
+            # 3072 vs 2952); whole micro-batches with the NCCL / fused exchange
+            groups = 4
             if any(sh.cp > 1 for sh in shards) and not (self.pipe.flagged and
                                                         not self.pipe.exchange.fused_sync):
-                groups = None                # (head-group I/O needs the flagged exchange)
+                groups = None
         self.last_groups = groups
         self.h2d.wait_stream(cur)            # the previous step is done with the inputs
         if groups is None:

@@ -20,7 +20,7 @@ host_in = tuple(torch.randn((T, h, d), dtype=torch.bfloat16).pin_memory() for h 
 host_out = tuple(torch.empty((T, h, d), dtype=torch.bfloat16, pin_memory=True) for h in shapes_out)
 dev_in = [tuple(torch.empty((T, h, d), dtype=torch.bfloat16, device=dev) for h in shapes_in)
           for _ in range(8)]
-step = hoststream.HostStreamedStep(CPStepPipeline(), groups=G, order=os.environ.get("ORDER", "johnson"))
+step = hoststream.HostStreamedStep(CPStepPipeline(), groups=G)
 marks = []
 orig = hoststream._copy_cols
 
