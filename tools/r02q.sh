@@ -1,7 +1,5 @@
 #!/usr/bin/env bash
-set -u
 cd "$(dirname "$0")/.."
-out=gpurun_out/r02q; mkdir -p $out
-timeout 900 python -m pytest tests/test_gpu_attention.py tests/test_gpu_exchange.py -q -x > $out/tests.txt 2>&1; echo "rc=$?" >> $out/tests.txt
-tail -2 $out/tests.txt
-bash tools/ab_run.sh ab7 G2 K
+N=$(nvidia-smi -L | wc -l)
+nvidia-smi topo -m 2>&1 | head -12
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr=127.0.0.1 --master-port=29751 tools/pcie_multi.py 2>&1 | grep world | tee gpurun_out/pcie_multi_n$N.txt
