@@ -12,7 +12,8 @@ from paper_2503_17924_b200 import hoststream  # noqa: E402
 from paper_2503_17924_b200.cp import CPStepPipeline, build_cp_shards  # noqa: E402
 
 G = int(sys.argv[1]) if len(sys.argv) > 1 else 4
-hq, hkv, T, d = 32, 32, 32768, 128
+hq, hkv = (int(sys.argv[2]), int(sys.argv[3])) if len(sys.argv) > 3 else (32, 32)
+T, d = 32768, 128
 lengths = [[x.length for x in s] for s in wl.generate_synthetic_stream(wl.SyntheticSpec(T, T), 0, 8)]
 dev = torch.device("cuda")
 shapes_in, shapes_out = (hq, hkv, hkv, hq), (hq, hq, hkv, hkv)
@@ -53,7 +54,7 @@ for it in range(3):
     t1 = torch.cuda.Event(enable_timing=True)
     t1.record()
     t1.synchronize()
-print(f"groups {G}: step {t0.elapsed_time(t1):.1f} ms")
+print(f"hq {hq} hkv {hkv} groups {G}: step {t0.elapsed_time(t1):.1f} ms")
 h = [t0.elapsed_time(e) for k, e in marks if k == "h2d"]
 dd = [t0.elapsed_time(e) for k, e in marks if k == "d2h"]
 print(f"h2d: {len(h)} copies, last ends {max(h):.1f} ms; d2h: {len(dd)} copies, first ends "
