@@ -657,14 +657,14 @@ static_assert(sizeof(Bwd3Bars) <= 256, "barrier block");
 #ifndef WLB_BWD_V3
 #define WLB_BWD_V3 1     // 0: D = 128 always uses the v2 (64-query) kernel
 #endif
-// v3 wins on long row-sets (+2-3% at 22K-32K documents) and loses on short
-// ones (-7% on 2-3K documents: its serial first/last tile and 128-row tiles
-// cost more per work item), so it is used when the rank's mean local rows per
-// document reach this many.  Re-checked on the final code with the N=1 bench
-// (profiles/r01c_ab_bwd_v3_min_rows.txt): 4096 935-939, 2048 921-931, 8192
-// 929-933 TFLOP/s.
+// v3 wins on long row-sets and, since its dQ partials leave by TMA
+// reduce-adds (TRED), from ~1024 local rows per document (2048-row documents:
+// 625 vs 579 TFLOP/s, 3072: 753 vs 675; 256-512: v2 4-5 % faster; N=1 bench
+// 1024 / 512 / always within noise, 4096 0.5-1.5 % slower:
+// profiles/r02_ab_tred.txt).  Used when the rank's mean local rows per
+// document reach this many.
 #ifndef WLB_BWD_V3_MIN_ROWS
-#define WLB_BWD_V3_MIN_ROWS 4096
+#define WLB_BWD_V3_MIN_ROWS 1024
 #endif
 #ifndef WLB_RED_B0          // dQ reduction batches (v4 REDs per thread, of 32)
 #define WLB_RED_B0 8
@@ -680,6 +680,9 @@ static_assert(sizeof(Bwd3Bars) <= 256, "barrier block");
 #endif
 #ifndef WLB_RED_SLEEP
 #define WLB_RED_SLEEP 150
+#endif
+#ifndef WLB_TRED_PACE
+#define WLB_TRED_PACE 1   // TMA dQ reduces paced by the next tile's barriers (0: at once)
 #endif
 #ifndef WLB_BWD_POLY
 #define WLB_BWD_POLY 0   // column pairs (of every 8) whose exp2 runs on the FMA pipe
@@ -734,10 +737,16 @@ __device__ __forceinline__ void bwd3_p_chunk(const uint32_t (&us)[32], const flo
 // heads and the bf16 double rounding of P failed the bar); otherwise from the
 // bf16 P the dV MMA reads (one conversion fewer per pair on the compute warps,
 // within the bar for Hq = Hkv: tests/test_gpu_scale.py).
-template <bool PAIR, bool P16>
+// TRED: the dQ drain stages each warp's 32 x 128 fp32 partial in shared memory
+// (the second dO stage: dO is single-buffered as in PAIR) and reduces it into
+// dq_acc with TMA tile reduce-adds (4 boxes of 32 rows x 32 head-dims per
+// warp and tile) instead of 32 per-thread RED.v4, taking the reduction off the
+// SM's load/store queues that the compute warps' TMEM loads share.
+template <bool PAIR, bool P16, bool TRED = false>
 __global__ void __launch_bounds__(512, 1)
 attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                 const __grid_constant__ CUtensorMap tmDQ,
                  const float* __restrict__ lse, const float* __restrict__ delta,
                  float* __restrict__ dq_acc, void* __restrict__ dk, void* __restrict__ dv,
                  const int4* __restrict__ kv_tiles, const int* __restrict__ n_kv_tiles,
@@ -832,7 +841,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       const int h = g * group + (WLB_BWD_HEAD_INNER ? i % group : i / qt_per_head);
       const int row = kt.z + (WLB_BWD_HEAD_INNER ? i / group : i % qt_per_head) * C::BM;
       mbar_wait(&bars->q_empty[st], ((i / C::QS) & 1) ^ 1);
-      if (PAIR) {
+      if (PAIR || TRED) {
         // dO single-buffered (its second stage is the dQ exchange buffer): it
         // is read by dP(i) and dV(i) only, and dO(i+1) has S(i+1), dQ(i) and
         // dK(i) to land in
@@ -904,9 +913,9 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       }
       if (i < n_iter) {
         const int st = i % C::QS;
-        const uint32_t dos = PAIR ? do_b : do_b + st * C::Q_BYTES;
+        const uint32_t dos = (PAIR || TRED) ? do_b : do_b + st * C::Q_BYTES;
         const uint32_t ph = i & 1;
-        if (PAIR) mbar_wait(&bars->do_full, ph);
+        if (PAIR || TRED) mbar_wait(&bars->do_full, ph);
         // dP^T = V dO^T into the columns dQ(i-1) occupied: wait for the drain
         if (i >= 1) mbar_wait_fast(&bars->s_free, (i - 1) & 1);
         TRACE3(1, i);
@@ -931,7 +940,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                        (i > 0) || (c | hf | sub));
             }
         }
-        if (PAIR) mma_commit_w(&bars->do_empty);   // single dO buffer: dV(i) was its last reader
+        if (PAIR || TRED) mma_commit_w(&bars->do_empty);   // single dO buffer: dV(i) was its last reader
       }
     }
   } else if (warp == 3) {
@@ -977,6 +986,11 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       const bool ok = row < kt.w;
 #endif
       float* base = dq_acc + (size_t)h * (D / 4) * blk + (size_t)row * 4;
+#ifdef WLB_EXP_NORED
+      const bool ok_tile = false;
+#else
+      const bool ok_tile = true;
+#endif
       mbar_wait(&bars->dq_full, j & 1);
       if (warp == 12) TRACE3(12, j);
       tc_fence_after();
@@ -1050,6 +1064,40 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         }
         fence_proxy_async_smem();           // loads done before the peer's next st.async
         mbar_arrive_remote(mapa_shared(smem_u32(&bars->peer_free), peer));
+        continue;
+      }
+      if (TRED) {
+        // 4 rounds of 8 column blocks (32 head-dims): staging [8][32 rows][4]
+        // fp32 = 4 KB, two buffers per warp in the unused second dO stage;
+        // rounds paced like the reductions below.  Rows past the document
+        // (masked: exact zeros) add 0; rows past Tl are clipped by the map.
+        uint8_t* stg = sDO + C::Q_BYTES + (warp - 12) * 8192;
+        const int row0 = row - lane;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (!last && WLB_TRED_PACE) {
+            if (r == 1) mbar_wait(&bars->dp_full, nph);
+            if (r == 2) mbar_wait(&bars->ds_full[0], nph);
+            if (r == 3) mbar_wait(&bars->ds_full[1], nph);
+          }
+          uint8_t* buf = stg + (r & 1) * 4096;
+          if (lane == 0) bulk_wait_group_read<1>();   // this buffer's previous reduce has read it
+          __syncwarp();
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int q = 8 * r + e;
+            *reinterpret_cast<float4*>(buf + e * 512 + lane * 16) =
+                make_float4(__uint_as_float(u[4 * q]) * scale, __uint_as_float(u[4 * q + 1]) * scale,
+                            __uint_as_float(u[4 * q + 2]) * scale,
+                            __uint_as_float(u[4 * q + 3]) * scale);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0 && ok_tile) {
+            tma_reduce_add_3d(&tmDQ, buf, 4 * row0, 8 * r, h);
+            bulk_commit_group();
+          }
+        }
         continue;
       }
 #if WLB_RED_PACE == 0
@@ -1187,6 +1235,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         cp_sync_unit_done(sync, g / sync.kv_per_group, n_kv_tiles[0] * sync.kv_per_group);
     }
   }
+  if (TRED && warp >= 12 && lane == 0) bulk_wait_group<0>();   // reduces done with the staging
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc(tmem, C::TMEM_COLS);
@@ -1394,6 +1443,12 @@ static int g_bwd_hpc_short = WLB_HPC;
 #define WLB_BWD_PAIRS 0
 #endif
 static int g_bwd_pairs = WLB_BWD_PAIRS;
+// 128-query backward: dQ partials reduced by TMA tile reduce-adds from shared
+// memory (1) or by per-thread RED.v4 (0)
+#ifndef WLB_BWD_TRED
+#define WLB_BWD_TRED 1
+#endif
+static int g_bwd_tred = WLB_BWD_TRED;
 // v2 backward as a persistent kernel (one CTA per SM, dynamic unit queue)
 #ifndef WLB_BWD_PERSIST
 #define WLB_BWD_PERSIST 1
@@ -1511,11 +1566,12 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
                                                      max_items, w.kv_tiles, w.n_kv,
                                                      w.kv_tiles + 2 * max_items, pairs ? 1 : 0);
   WLB_LAUNCH_CHECK();
-  CUtensorMap tq, tk, tv, tdo;
+  CUtensorMap tq, tk, tv, tdo, tdq;
   int rc;
 #if WLB_BWD_V3
   if (v3) {
     using C3 = Bwd3Cfg;
+    if ((rc = make_dq_acc_tmap(&tdq, w.dq_acc, Tl, Hq, D))) return rc;
     if ((rc = make_thd_tmap(&tq, q, Tl, Hq, D, C3::BM))) return rc;
     if ((rc = make_thd_tmap(&tdo, dout, Tl, Hq, D, C3::BM))) return rc;
     if ((rc = make_thd_tmap(&tk, k, T, Hkv, D, C3::BN))) return rc;
@@ -1525,6 +1581,8 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
     WLB_SMEM_ATTR((attn_bwd3_kernel<false, true>), C3::SMEM);
     WLB_SMEM_ATTR((attn_bwd3_kernel<true, false>), C3::SMEM);
     WLB_SMEM_ATTR((attn_bwd3_kernel<true, true>), C3::SMEM);
+    WLB_SMEM_ATTR((attn_bwd3_kernel<false, false, true>), C3::SMEM);
+    WLB_SMEM_ATTR((attn_bwd3_kernel<false, true, true>), C3::SMEM);
     const float sl2 = scale * 1.4426950408889634f;
     if (pairs) {
       // 2-CTA clusters: one pair of KV tiles per cluster
@@ -1540,14 +1598,16 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      WLB_CUDA_TRY(cudaLaunchKernelEx(&cfg, p16 ? attn_bwd3_kernel<true, true> : attn_bwd3_kernel<true, false>, tq, tk, tv, tdo, lse,
+      WLB_CUDA_TRY(cudaLaunchKernelEx(&cfg, p16 ? attn_bwd3_kernel<true, true> : attn_bwd3_kernel<true, false>, tq, tk, tv, tdo, tdq, lse,
                                       (const float*)w.delta, w.dq_acc, dk, dv,
                                       (const int4*)w.kv_tiles, (const int*)w.n_kv, positions, Tl,
                                       Hq, Hkv, max_items, g_begin, scale, sl2, dkv_bf16, sync));
     } else {
-      auto kern = p16 ? attn_bwd3_kernel<false, true> : attn_bwd3_kernel<false, false>;
+      auto kern = g_bwd_tred ? (p16 ? attn_bwd3_kernel<false, true, true>
+                                    : attn_bwd3_kernel<false, false, true>)
+                             : (p16 ? attn_bwd3_kernel<false, true> : attn_bwd3_kernel<false, false>);
       kern<<<(unsigned)max_items * g_count, C3::THREADS, C3::SMEM, stream>>>(
-          tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
+          tq, tk, tv, tdo, tdq, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
           Hkv, max_items, g_begin, scale, sl2, dkv_bf16, sync);
     }
     WLB_LAUNCH_CHECK();

@@ -48,4 +48,32 @@ inline int make_thd_tmap(CUtensorMap* map, const void* base, int rows, int heads
   return WLB_OK;
 }
 
+// 3-D map over the 128-query backward's fp32 dQ accumulator [H][D/4][rows][4]:
+// dims {rows*4, D/4, H}, box {128, 8, 1} = 32 rows x 32 head-dims (4 KB, laid
+// out [8][32][4] in shared memory), no swizzle; the drain warps reduce into it
+// with TMA tile reduce-adds (rows past `rows` are clipped).
+inline int make_dq_acc_tmap(CUtensorMap* map, void* base, int rows, int heads, int dim) {
+  auto enc = tmap_encoder();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return WLB_ECUDA;
+  }
+  // (rows, 4) flattened: each box row is 32 query rows x 4 floats = 512
+  // contiguous bytes (a 16-B inner box dimension made 256 separate 16-B
+  // requests per box and measured 1.8x slower)
+  cuuint64_t gdim[3] = {(cuuint64_t)rows * 4, (cuuint64_t)dim / 4, (cuuint64_t)heads};
+  cuuint64_t gstride[2] = {(cuuint64_t)rows * 16, (cuuint64_t)rows * 16 * (dim / 4)};
+  cuuint32_t box[3] = {128, 8, 1};
+  cuuint32_t estride[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, gdim, gstride, box, estride,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (dQ accumulator) failed (%d) rows=%d heads=%d", (int)r,
+              rows, heads);
+    return WLB_ECUDA;
+  }
+  return WLB_OK;
+}
+
 }  // namespace wlb
