@@ -64,6 +64,14 @@ __device__ long long g_bwd_trace[2][8][128];
   } while (0)
 #endif
 
+#ifndef WLB_BWD_TRED_V2
+// 64-query backward (D = 128): dQ by TMA reduce-adds of a staged [64][128]
+// tile instead of per-lane atomics.  Measured neutral where this kernel runs
+// (256-row documents 124 vs 128 TFLOP/s, 512-row 244 vs 235, config-5 short
+// ranks within 1 %: its cost is per-item latency, not the dQ stream;
+// profiles/r02_ab_tred.txt), so off.
+#define WLB_BWD_TRED_V2 0
+#endif
 template <int D, int NCW = 2>
 struct BwdCfg {
   static_assert(NCW == 2, "two compute warpgroups (one 32-query half each)");
@@ -86,7 +94,11 @@ struct BwdCfg {
   // (A second K buffer, so the next KV head's K lands early, measured 3-10%
   //  SLOWER on the same box: profiles/r02_ab_bwd_kdb.txt; the 227 KB carve-out
   //  leaves almost no L1 for the per-query vector loads.)
-  static constexpr int SMEM = OFF_BAR + 512;
+  static constexpr int SMEM_RED = OFF_BAR + 512;     // with per-thread dQ reductions
+  // D = 128: dQ^T tile staging [BM rows][D] fp32 for the TMA reduce-add drain
+  static constexpr int OFF_STG = SMEM_RED;
+  static constexpr bool TRED = D == 128 && WLB_BWD_TRED_V2;
+  static constexpr int SMEM = TRED ? OFF_STG + BM * D * 4 : SMEM_RED;
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr uint32_t COL_S = 0;      // S^T[b] at b*64
   static constexpr uint32_t COL_DP = 128;   // dP^T[b] at 128 + b*64 (later dQ^T[b])
@@ -115,6 +127,7 @@ struct BwdBars {  // 268 bytes; OFF_BAR reserves 512
 };
 static_assert(sizeof(BwdBars) <= 512, "barrier block");
 static_assert(BwdCfg<128>::SMEM <= 232448, "bwd v2 exceeds the 227 KB SMEM window");
+static_assert(BwdCfg<128>::OFF_STG % 128 == 0, "TMA source must be 128-B aligned");
 
 // 32 consecutive dV and dK values (dK scaled) of one key row at element offset
 // `off`: fp32, or bf16 when the partials go through the bf16 CP exchange.
@@ -164,6 +177,7 @@ template <int D, int NCW>
 __global__ void __launch_bounds__(256 + 128 * NCW, 1)
 attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                const __grid_constant__ CUtensorMap tmDQ,
                 const float* __restrict__ lse, const float* __restrict__ delta,
                 float* __restrict__ dq_acc, void* __restrict__ dk, void* __restrict__ dv,
                 const int4* __restrict__ kv_tiles, const int* __restrict__ n_kv_tiles,
@@ -451,7 +465,26 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         tc_fence_before();
         mbar_arrive(&bars->s_free[b]);
         TRACE(7, Jg);
-        if (D == 128 || lane < 16) {
+        if (C::TRED) {
+          // the four drain warps stage the tile's dQ rows [64][128] fp32 (warp
+          // lg writes head-dims [32lg, 32lg+32) of every row: 128-B,
+          // conflict-free stores) and one thread reduces the box into dq_acc
+          // with a TMA reduce-add (512-B rows); rows past the document add
+          // exact zeros, rows past Tl are clipped
+          float* stg = reinterpret_cast<float*>(smem + C::OFF_STG);
+          if (warp == 4 + 4 * NCW && lane == 0) bulk_wait_group_read<0>();   // last box read
+          named_bar_sync(2, 128);
+#pragma unroll
+          for (int q = 0; q < C::BM; ++q) stg[q * D + d] = __uint_as_float(v[q]) * scale;
+          fence_proxy_async_smem();
+          named_bar_sync(2, 128);
+#ifndef WLB_EXP_NORED
+          if (warp == 4 + 4 * NCW && lane == 0) {
+            tma_reduce_add_3d(&tmDQ, stg, 0, h, row0);
+            bulk_commit_group();
+          }
+#endif
+        } else if (D == 128 || lane < 16) {
           float* ptr = dq_acc + ((size_t)row0 * Hq + h) * D + d;
           const int nvalid = min(C::BM, U.kt.w - row0);
           if (nvalid == C::BM) {
@@ -578,6 +611,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       G0 += U.nh;
     }
   }
+  if (C::TRED && warp == 4 + 4 * NCW && lane == 0) bulk_wait_group<0>();
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc(tmem, C::TMEM_COLS);
@@ -1616,6 +1650,7 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   {
   if ((rc = make_thd_tmap(&tq, q, Tl, Hq, D, C::BM))) return rc;
   if ((rc = make_thd_tmap(&tdo, dout, Tl, Hq, D, C::BM))) return rc;
+  if (C::TRED && (rc = make_dq_rows_tmap(&tdq, w.dq_acc, Tl, Hq, D, C::BM))) return rc;
   if ((rc = make_thd_tmap(&tk, k, T, Hkv, D, C::BN))) return rc;
   if ((rc = make_thd_tmap(&tv, v, T, Hkv, D, C::BN))) return rc;
   // (A 128-query, single-buffered variant with all-N=128 MMAs measured 1.5x
@@ -1639,12 +1674,12 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
     WLB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     WLB_CUDA_TRY(cudaMemsetAsync(w.sched, 0, sizeof(int), stream));
     attn_bwd_kernel<D, 2><<<(unsigned)std::min(n_units, sms), C::THREADS, C::SMEM, stream>>>(
-        tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
+        tq, tk, tv, tdo, tdq, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
         Hkv, max_items, hpc, n_units, w.sched, 1, g_begin, g_begin + g_count, scale,
         scale * 1.4426950408889634f, dkv_bf16, sync);
   } else {
     attn_bwd_kernel<D, 2><<<(unsigned)n_units, C::THREADS, C::SMEM, stream>>>(
-        tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
+        tq, tk, tv, tdo, tdq, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
         Hkv, max_items, hpc, n_units, w.sched, 0, g_begin, g_begin + g_count, scale,
         scale * 1.4426950408889634f, dkv_bf16, sync);
   }
