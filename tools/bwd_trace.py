@@ -25,13 +25,15 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--doc", type=int, default=32768)
 ap.add_argument("--hq", type=int, default=32)
 ap.add_argument("--hkv", type=int, default=32)
+ap.add_argument("--ndocs", type=int, default=1, help="documents of --doc rows each")
+ap.add_argument("--show", type=int, default=40)
 a = ap.parse_args()
-lengths = [a.doc]
+lengths = [a.doc] * a.ndocs
 plan = wl.build_shard_plan([lengths], 1, "per_document")
 g, pos, ro = plan.rank_local(0, 0)
 tiles = build_tiles(ro, pos, lengths)
 dev = torch.device("cuda")
-T, d = a.doc, 128
+T, d = a.doc * a.ndocs, 128
 q = torch.randn(T, a.hq, d, device=dev, dtype=torch.bfloat16)
 k = torch.randn(T, a.hkv, d, device=dev, dtype=torch.bfloat16)
 v = torch.randn_like(k)
@@ -48,10 +50,12 @@ t = buf[0].astype(np.float64)
 t0 = t[0, 0]
 names = ["mma_q", "mma_sfree", "mma_pfull", "cmp_sfull", "cmp_regs", "cmp_done", "drn_mma2", "drn_ld"]
 print("iter " + " ".join(f"{n:>9s}" for n in names) + "   per-iter(mma_q delta)")
-for i in range(2, 40):
+for i in range(2, min(a.show, 128)):
     row = " ".join(f"{t[e, i] - t0:9.0f}" for e in range(8))
     print(f"{i:4d} {row}   {t[0, i] - t[0, i - 1]:7.0f}")
 it = np.arange(10, 100)
+if a.ndocs > 1:
+    sys.exit(0)
 per = np.diff(t[0, 10:101]).mean()
 print(f"steady-state cycles per q-tile (MMA warp): {per:.0f}")
 print("mean waits (cycles), iters 10..99:")
