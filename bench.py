@@ -432,7 +432,8 @@ def main():
         # start and end), per micro-batch where the attention dominates
         gsel = os.environ.get("WLB_E2E_GROUPS", "auto")
         streamer = HostStreamedStep(pipe, groups=None if gsel == "mb" else
-                                    gsel if gsel == "auto" else int(gsel))
+                                    gsel if gsel == "auto" else int(gsel),
+                                    order=os.environ.get("WLB_E2E_ORDER", "given"))
 
         def e2e_step():
             shards = build_cp_shards(lengths, cp, rank, policy, model=model)
@@ -462,7 +463,7 @@ def main():
                "ms_per_step": round(float(e_ms) / n_e2e, 2),
                "granularity": ("micro-batch" if streamer.last_groups is None else
                                f"{streamer.last_groups} KV-head groups"),
-               "rank0_step_ms": e2e_steps,
+               "order": streamer.last_order, "rank0_step_ms": e2e_steps,
                "alloc_retries": torch.cuda.memory_stats(dev).get("num_alloc_retries", 0) - retries0,
                "note": "every micro-batch: H2D k,v,q then dO from pinned host, D2H o "
                        "(during the backward) then dq,dk,dv, copy streams pipelined against "

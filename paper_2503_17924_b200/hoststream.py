@@ -29,6 +29,36 @@ except ImportError:   # pragma: no cover - the image ships cuda-python
     _rt = None
 
 
+# Rates used only to order micro-batches (not reported): attention fwd+bwd
+# TFLOP/s of a B200 rank and the per-direction pinned-host copy rate of one
+# GPU with both directions busy (tools/pcie2d_probe.py: 47-50 GB/s).
+_ATTN_FLOPS_EST = 950e12
+_PCIE_EST = 48e9
+
+
+def _estimates(shards, hq: int, hkv: int, d: int):
+    """Per micro-batch (input copy seconds, attention seconds) estimates."""
+    row_bytes = (2 * hq + 2 * hkv) * d * 2
+    out = []
+    for sh in shards:
+        ls = sh.plan.lengths[sh.index]
+        attn = 14.0 * d * hq * sum(x * (x + 1) // 2 for x in ls) / sh.cp / _ATTN_FLOPS_EST
+        out.append((sum(ls) / sh.cp * row_bytes / _PCIE_EST, attn))
+    return out
+
+
+def johnson_order(shards, hq: int, hkv: int, d: int):
+    """Johnson's rule for the two-stage flow copy-in -> attention: micro-
+    batches whose attention outlasts their copies first (by increasing copy
+    time), then the rest by decreasing attention time, so a PCIe-bound step
+    does not end on a long attention after its last input byte.  Uses only
+    document lengths, so every CP rank gets the same order."""
+    jobs = [(i, c, a) for i, (c, a) in enumerate(_estimates(shards, hq, hkv, d))]
+    first = sorted((j for j in jobs if j[1] < j[2]), key=lambda j: j[1])
+    rest = sorted((j for j in jobs if j[1] >= j[2]), key=lambda j: -j[2])
+    return [j[0] for j in first + rest]
+
+
 def _copy_cols(dst, src, h0: int, nh: int, stream) -> None:
     """dst[:, h0:h0+nh] = src[:, h0:h0+nh] (or the whole of a [T, nh, D]
     side) for [T, H, D] tensors, host <-> device, on `stream`."""
@@ -65,19 +95,22 @@ class HostStreamedStep:
     Entries may repeat the same tensors (e.g. one host buffer for every
     micro-batch).  groups: "auto" (4 KV-head groups where the pipeline can
     run them, else whole micro-batches), an int, or None (whole micro-batches).
-    Micro-batches run in the given order (a Johnson's-rule reordering for the
-    copy-in / attention flow measured +0.4 % at N=1 and -13 % at N=2, where it
-    left the short micro-batches' copy-out exposed at the end of the step).
+    order: "given" (default), "johnson" (`johnson_order`) or "auto"
+    (Johnson where the estimated copies outlast the attention).
     The outputs are complete on the current stream when run returns
     (stream-ordered; no host sync).  The step's input copies start after the
     work already on the current stream (the previous step)."""
 
-    def __init__(self, pipe: CPStepPipeline, groups="auto"):
+    def __init__(self, pipe: CPStepPipeline, groups="auto", order: str = "given"):
         if not (groups in ("auto", None) or (isinstance(groups, int) and groups >= 1)):
             raise ValueError("groups must be 'auto', None or a positive int")
+        if order not in ("auto", "given", "johnson"):
+            raise ValueError("order must be 'auto', 'given' or 'johnson'")
         self.pipe = pipe
         self.groups = groups
+        self.order = order
         self.last_groups = None
+        self.last_order = None
         self.h2d = torch.cuda.Stream()
         self.d2h = torch.cuda.Stream()
 
@@ -95,6 +128,19 @@ class HostStreamedStep:
                                  "host_out be (o, dq, dk, dv) shaped like (q, q, k, k)")
             if not all(t.is_pinned() for t in host_in[b] + host_out[b]):
                 raise ValueError(f"micro-batch {b}: host buffers must be pinned")
+        order = self.order
+        if order == "auto":
+            # Johnson's rule only where the estimated copies outlast the
+            # attention.  Measured (same box, e2e): 7B N=1 +1.2 %, but 70B GQA
+            # N=1 -11 % and N=2 -13 %: the flow has a third stage (copy-out)
+            # that the rule ignores, so "given" is the default
+            est = _estimates(shards, hq, hkv, dev_in[0][0].shape[2])
+            order = "johnson" if sum(c for c, _ in est) >= sum(a for _, a in est) else "given"
+        self.last_order = order
+        if order == "johnson":
+            perm = johnson_order(shards, hq, hkv, dev_in[0][0].shape[2])
+            shards, host_in, dev_in, host_out = ([x[i] for i in perm]
+                                                 for x in (shards, host_in, dev_in, host_out))
         groups = self.groups
         if groups == "auto":
             # 4 head groups wherever the pipeline runs them (same box, e2e
