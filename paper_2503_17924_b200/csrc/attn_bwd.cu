@@ -64,14 +64,6 @@ __device__ long long g_bwd_trace[2][8][128];
   } while (0)
 #endif
 
-#ifndef WLB_BWD_TRED_V2
-// 64-query backward (D = 128): dQ by TMA reduce-adds of a staged [64][128]
-// tile instead of per-lane atomics.  Measured neutral where this kernel runs
-// (256-row documents 124 vs 128 TFLOP/s, 512-row 244 vs 235, config-5 short
-// ranks within 1 %: its cost is per-item latency, not the dQ stream;
-// profiles/r02_ab_tred.txt), so off.
-#define WLB_BWD_TRED_V2 0
-#endif
 template <int D, int NCW = 2>
 struct BwdCfg {
   static_assert(NCW == 2, "two compute warpgroups (one 32-query half each)");
@@ -94,11 +86,10 @@ struct BwdCfg {
   // (A second K buffer, so the next KV head's K lands early, measured 3-10%
   //  SLOWER on the same box: profiles/r02_ab_bwd_kdb.txt; the 227 KB carve-out
   //  leaves almost no L1 for the per-query vector loads.)
-  static constexpr int SMEM_RED = OFF_BAR + 512;     // with per-thread dQ reductions
-  // D = 128: dQ^T tile staging [BM rows][D] fp32 for the TMA reduce-add drain
-  static constexpr int OFF_STG = SMEM_RED;
-  static constexpr bool TRED = D == 128 && WLB_BWD_TRED_V2;
-  static constexpr int SMEM = TRED ? OFF_STG + BM * D * 4 : SMEM_RED;
+  // (the dK/dV epilogue transposes through the dS^T buffers, 4 KB per compute
+  //  warp: a separate 32 KB region left almost no L1 and cost the vector
+  //  loads of short per-sequence ranks 4-8 %)
+  static constexpr int SMEM = OFF_BAR + 512;
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr uint32_t COL_S = 0;      // S^T[b] at b*64
   static constexpr uint32_t COL_DP = 128;   // dP^T[b] at 128 + b*64 (later dQ^T[b])
@@ -127,38 +118,65 @@ struct BwdBars {  // 268 bytes; OFF_BAR reserves 512
 };
 static_assert(sizeof(BwdBars) <= 512, "barrier block");
 static_assert(BwdCfg<128>::SMEM <= 232448, "bwd v2 exceeds the 227 KB SMEM window");
-static_assert(BwdCfg<128>::OFF_STG % 128 == 0, "TMA source must be 128-B aligned");
+static_assert(2 * BwdCfg<128>::T_BYTES >= 8 * 4096, "epilogue staging fits the dS^T buffers");
 
-// 32 consecutive dV and dK values (dK scaled) of one key row at element offset
-// `off`: fp32, or bf16 when the partials go through the bf16 CP exchange.
-__device__ __forceinline__ void store_dkv32(void* dv, void* dk, size_t off, const uint32_t (&a)[32],
-                                            const uint32_t (&bb)[32], float scale, bool bf16) {
-  if (bf16) {
-    uint4* v4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dv) + off);
-    uint4* k4 = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dk) + off);
+// dV and dK (scaled) of a warp's 32 key rows x 32 head-dims (one TMEM load
+// each, lane = key row) stored through a 4 KB per-warp shared-memory
+// transpose, so every store instruction writes whole 128-B lines (fp32: 8
+// lanes per row, 4 rows per instruction; bf16: 4 lanes per row, 8 rows).
+// Storing straight from the TMEM layout put 32 rows into each instruction,
+// 16 B per line: the per-KV-head epilogue of short documents then took more
+// SM time than their query tiles.  `off0` is the element offset of head-dim
+// 0 of key row 0 of the block, `ld` the row stride in elements; rows at or
+// past `n_rows` (keys past the tile) are not stored.
+__device__ __forceinline__ void store_dkv_block(void* dv, void* dk, size_t off0, size_t ld,
+                                                int n_rows, const uint32_t (&a)[32],
+                                                const uint32_t (&bb)[32], float scale, bool bf16,
+                                                uint4* stg) {
+  const int lane = threadIdx.x & 31;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      v4[e] = make_uint4(pack_bf16(__uint_as_float(a[8 * e]), __uint_as_float(a[8 * e + 1])),
-                         pack_bf16(__uint_as_float(a[8 * e + 2]), __uint_as_float(a[8 * e + 3])),
-                         pack_bf16(__uint_as_float(a[8 * e + 4]), __uint_as_float(a[8 * e + 5])),
-                         pack_bf16(__uint_as_float(a[8 * e + 6]), __uint_as_float(a[8 * e + 7])));
-      k4[e] = make_uint4(
-          pack_bf16(__uint_as_float(bb[8 * e]) * scale, __uint_as_float(bb[8 * e + 1]) * scale),
-          pack_bf16(__uint_as_float(bb[8 * e + 2]) * scale, __uint_as_float(bb[8 * e + 3]) * scale),
-          pack_bf16(__uint_as_float(bb[8 * e + 4]) * scale, __uint_as_float(bb[8 * e + 5]) * scale),
-          pack_bf16(__uint_as_float(bb[8 * e + 6]) * scale, __uint_as_float(bb[8 * e + 7]) * scale));
-    }
-  } else {
-    float4* v4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(dv) + off);
-    float4* k4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(dk) + off);
+  for (int tsel = 0; tsel < 2; ++tsel) {
+    const uint32_t(&v)[32] = tsel ? bb : a;
+    const float sc = tsel ? scale : 1.f;
+    void* dst = tsel ? dk : dv;
+    __syncwarp();
+    if (bf16) {
+      // row = 16 packed bf16 pairs = 4 x 16 B chunks, chunk j at j ^ (row & 3)
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      v4[e] = make_float4(__uint_as_float(a[4 * e]), __uint_as_float(a[4 * e + 1]),
-                          __uint_as_float(a[4 * e + 2]), __uint_as_float(a[4 * e + 3]));
-      k4[e] = make_float4(__uint_as_float(bb[4 * e]) * scale, __uint_as_float(bb[4 * e + 1]) * scale,
-                          __uint_as_float(bb[4 * e + 2]) * scale, __uint_as_float(bb[4 * e + 3]) * scale);
+      for (int j = 0; j < 4; ++j)
+        stg[lane * 4 + (j ^ (lane & 3))] =
+            make_uint4(pack_bf16(__uint_as_float(v[8 * j]) * sc, __uint_as_float(v[8 * j + 1]) * sc),
+                       pack_bf16(__uint_as_float(v[8 * j + 2]) * sc, __uint_as_float(v[8 * j + 3]) * sc),
+                       pack_bf16(__uint_as_float(v[8 * j + 4]) * sc, __uint_as_float(v[8 * j + 5]) * sc),
+                       pack_bf16(__uint_as_float(v[8 * j + 6]) * sc, __uint_as_float(v[8 * j + 7]) * sc));
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int r = 8 * k + (lane >> 2), c = lane & 3;
+        const uint4 x = stg[r * 4 + (c ^ (r & 3))];
+        if (r < n_rows)
+          *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dst) + off0 + r * ld + 8 * c) = x;
+      }
+    } else {
+      // row = 8 x 16 B chunks, chunk j at j ^ (row & 7)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        stg[lane * 8 + (j ^ (lane & 7))] =
+            make_uint4(__float_as_uint(__uint_as_float(v[4 * j]) * sc),
+                       __float_as_uint(__uint_as_float(v[4 * j + 1]) * sc),
+                       __float_as_uint(__uint_as_float(v[4 * j + 2]) * sc),
+                       __float_as_uint(__uint_as_float(v[4 * j + 3]) * sc));
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int r = 4 * k + (lane >> 3), c = lane & 7;
+        const uint4 x = stg[r * 8 + (c ^ (r & 7))];
+        if (r < n_rows)
+          *reinterpret_cast<uint4*>(reinterpret_cast<float*>(dst) + off0 + r * ld + 4 * c) = x;
+      }
     }
   }
+  __syncwarp();
 }
 
 // kv_tiles[2i] = {kv_begin (global), kv_len, row_first, row_end}, kv_tiles[2i+1].x = k0
@@ -177,7 +195,6 @@ template <int D, int NCW>
 __global__ void __launch_bounds__(256 + 128 * NCW, 1)
 attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                const __grid_constant__ CUtensorMap tmDQ,
                 const float* __restrict__ lse, const float* __restrict__ delta,
                 float* __restrict__ dq_acc, void* __restrict__ dk, void* __restrict__ dv,
                 const int4* __restrict__ kv_tiles, const int* __restrict__ n_kv_tiles,
@@ -465,26 +482,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         tc_fence_before();
         mbar_arrive(&bars->s_free[b]);
         TRACE(7, Jg);
-        if (C::TRED) {
-          // the four drain warps stage the tile's dQ rows [64][128] fp32 (warp
-          // lg writes head-dims [32lg, 32lg+32) of every row: 128-B,
-          // conflict-free stores) and one thread reduces the box into dq_acc
-          // with a TMA reduce-add (512-B rows); rows past the document add
-          // exact zeros, rows past Tl are clipped
-          float* stg = reinterpret_cast<float*>(smem + C::OFF_STG);
-          if (warp == 4 + 4 * NCW && lane == 0) bulk_wait_group_read<0>();   // last box read
-          named_bar_sync(2, 128);
-#pragma unroll
-          for (int q = 0; q < C::BM; ++q) stg[q * D + d] = __uint_as_float(v[q]) * scale;
-          fence_proxy_async_smem();
-          named_bar_sync(2, 128);
-#ifndef WLB_EXP_NORED
-          if (warp == 4 + 4 * NCW && lane == 0) {
-            tma_reduce_add_3d(&tmDQ, stg, 0, h, row0);
-            bulk_commit_group();
-          }
-#endif
-        } else if (D == 128 || lane < 16) {
+        if (D == 128 || lane < 16) {
           float* ptr = dq_acc + ((size_t)row0 * Hq + h) * D + d;
           const int nvalid = min(C::BM, U.kt.w - row0);
           if (nvalid == C::BM) {
@@ -587,14 +585,20 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
           mbar_wait(&bars->acc_done, (G0 + I / U.n_iter) & 1);
           tc_fence_after();
           // TMEM loads are warp-collective: issue converged, predicate the stores.
-          const size_t off = ((size_t)(U.kt.x + t) * Hkv + g) * D + ch * (D / 2);
+          // the warp's 32 key rows from the block's first (lg * 32)
+          const size_t off = ((size_t)(U.kt.x + lg * 32) * Hkv + g) * D + ch * (D / 2);
+          // staging: the dS^T buffers (their last reader, this head's last dQ^T
+          // MMA, completed before acc_done; the next tile's dS^T is written
+          // after this epilogue, by these warps)
+          uint4* stg = reinterpret_cast<uint4*>(sDS + (warp - 4) * 4096);
 #pragma unroll
           for (int c = 0; c < D / 64; ++c) {
             uint32_t a[32], bb[32];
             tmem_ld32(lane_base + C::COL_DV + ch * (D / 2) + c * 32, a);
             tmem_ld32(lane_base + C::COL_DK + ch * (D / 2) + c * 32, bb);
             tmem_ld_wait();
-            if (key_ok) store_dkv32(dv, dk, off + c * 32, a, bb, scale, dkv_bf16 != 0);
+            store_dkv_block(dv, dk, off + c * 32, (size_t)Hkv * D, U.kt.y - lg * 32, a, bb, scale,
+                            dkv_bf16 != 0, stg);
           }
           tc_fence_before();
           if (sync.signal_bases && I == U.n_all - 1) {
@@ -611,7 +615,6 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
       G0 += U.nh;
     }
   }
-  if (C::TRED && warp == 4 + 4 * NCW && lane == 0) bulk_wait_group<0>();
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc(tmem, C::TMEM_COLS);
@@ -1252,14 +1255,17 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     mbar_wait(&bars->acc_done, n_iter > 0 ? 0 : 1);   // the last MMA group wrote dV / dK
     tc_fence_after();
     // ------------------------------------------------------------ epilogue --
-    const size_t off = ((size_t)(kt.x + t) * Hkv + g) * D + hf * 64;
+    // (the dS^T buffer is free: acc_done follows the last dK MMA, its last reader)
+    const size_t off = ((size_t)(kt.x + lg * 32) * Hkv + g) * D + hf * 64;
+    uint4* stg = reinterpret_cast<uint4*>(sDS + (warp - 4) * 4096);
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       uint32_t a[32], bb[32];
       tmem_ld32(lane_base + C::COL_DV + hf * 64 + c * 32, a);
       tmem_ld32(lane_base + C::COL_DK + hf * 64 + c * 32, bb);
       tmem_ld_wait();
-      if (key_ok) store_dkv32(dv, dk, off + c * 32, a, bb, scale, dkv_bf16 != 0);
+      store_dkv_block(dv, dk, off + c * 32, (size_t)Hkv * D, kt.y - lg * 32, a, bb, scale,
+                      dkv_bf16 != 0, stg);
     }
     if (!PAIR && sync.signal_bases) {
       // CP: this (KV tile, head) unit's partials are stored; count it toward
@@ -1650,7 +1656,6 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   {
   if ((rc = make_thd_tmap(&tq, q, Tl, Hq, D, C::BM))) return rc;
   if ((rc = make_thd_tmap(&tdo, dout, Tl, Hq, D, C::BM))) return rc;
-  if (C::TRED && (rc = make_dq_rows_tmap(&tdq, w.dq_acc, Tl, Hq, D, C::BM))) return rc;
   if ((rc = make_thd_tmap(&tk, k, T, Hkv, D, C::BN))) return rc;
   if ((rc = make_thd_tmap(&tv, v, T, Hkv, D, C::BN))) return rc;
   // (A 128-query, single-buffered variant with all-N=128 MMAs measured 1.5x
@@ -1674,12 +1679,12 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
     WLB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     WLB_CUDA_TRY(cudaMemsetAsync(w.sched, 0, sizeof(int), stream));
     attn_bwd_kernel<D, 2><<<(unsigned)std::min(n_units, sms), C::THREADS, C::SMEM, stream>>>(
-        tq, tk, tv, tdo, tdq, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
+        tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
         Hkv, max_items, hpc, n_units, w.sched, 1, g_begin, g_begin + g_count, scale,
         scale * 1.4426950408889634f, dkv_bf16, sync);
   } else {
     attn_bwd_kernel<D, 2><<<(unsigned)n_units, C::THREADS, C::SMEM, stream>>>(
-        tq, tk, tv, tdo, tdq, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
+        tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
         Hkv, max_items, hpc, n_units, w.sched, 0, g_begin, g_begin + g_count, scale,
         scale * 1.4426950408889634f, dkv_bf16, sync);
   }

@@ -76,29 +76,4 @@ inline int make_dq_acc_tmap(CUtensorMap* map, void* base, int rows, int heads, i
   return WLB_OK;
 }
 
-// 3-D map over the 64-query backward's fp32 dQ accumulator [rows][H][D]:
-// dims {D, H, rows}, box {D, 1, box_rows} (512-B rows for D = 128), no
-// swizzle; the drain reduces a staged [box_rows][D] tile into it.
-inline int make_dq_rows_tmap(CUtensorMap* map, void* base, int rows, int heads, int dim,
-                             int box_rows) {
-  auto enc = tmap_encoder();
-  if (!enc) {
-    set_error("cuTensorMapEncodeTiled unavailable");
-    return WLB_ECUDA;
-  }
-  cuuint64_t gdim[3] = {(cuuint64_t)dim, (cuuint64_t)heads, (cuuint64_t)rows};
-  cuuint64_t gstride[2] = {(cuuint64_t)dim * 4, (cuuint64_t)heads * dim * 4};
-  cuuint32_t box[3] = {(cuuint32_t)dim, 1, (cuuint32_t)box_rows};
-  cuuint32_t estride[3] = {1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, gdim, gstride, box, estride,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    set_error("cuTensorMapEncodeTiled (dQ rows) failed (%d) rows=%d heads=%d", (int)r, rows,
-              heads);
-    return WLB_ECUDA;
-  }
-  return WLB_OK;
-}
-
 }  // namespace wlb
