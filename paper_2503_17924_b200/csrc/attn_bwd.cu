@@ -695,13 +695,13 @@ static_assert(sizeof(Bwd3Bars) <= 256, "barrier block");
 #define WLB_BWD_V3 1     // 0: D = 128 always uses the v2 (64-query) kernel
 #endif
 // v3 wins on long row-sets and, since its dQ partials leave by TMA
-// reduce-adds (TRED), from ~1024 local rows per document (2048-row documents:
-// 625 vs 579 TFLOP/s, 3072: 753 vs 675; 256-512: v2 4-5 % faster; N=1 bench
-// 1024 / 512 / always within noise, 4096 0.5-1.5 % slower:
-// profiles/r02_ab_tred.txt).  Used when the rank's mean local rows per
-// document reach this many.
+// reduce-adds (TRED) and both kernels store dK/dV as whole lines, from ~320
+// local rows per document (384-row documents: 223 vs 216 TFLOP/s, 1024: 475
+// vs 430, 2048: 708 vs 608; 256: equal; 128: v2 93 vs 81;
+// profiles/r02_ab_tred.txt, profiles/r02_ab_dkv_epilogue.txt).  Used when
+// the rank's mean local rows per document reach this many.
 #ifndef WLB_BWD_V3_MIN_ROWS
-#define WLB_BWD_V3_MIN_ROWS 1024
+#define WLB_BWD_V3_MIN_ROWS 320
 #endif
 #ifndef WLB_RED_B0          // dQ reduction batches (v4 REDs per thread, of 32)
 #define WLB_RED_B0 8

@@ -54,7 +54,7 @@ class TileModel:
     bwd_item_s: float = 4.0e-6
     bwd_step64_s: float = 1.5e-6
     bwd_step128_s: float = 2.75e-6
-    v3_min_rows: int = 1024
+    v3_min_rows: int = 320
     const_s: float = 3.0e-5
     source: str = "defaults (pre-calibration estimates from the kernel traces)"
 
