@@ -176,8 +176,13 @@ def fit_tile_model(rows, hq, hkv, d, sms=148, v3_min_rows=320):
         af.append([f["fwd_items"] * hq / sms, f["fwd_steps"] * hq / sms, 1.0])
         yf.append(r["fwd_ms"] * 1e-3)
         v3 = d == 128 and r["tl"] >= v3_min_rows * max(1, r["n_docs"])
-        ab.append([f["bwd_items"] * hkv / sms, 0.0 if v3 else f["bwd_q64"] * hq / sms,
-                   f["bwd_q128"] * hq / sms if v3 else 0.0, 1.0])
+        items = f["bwd_items"] * hkv / sms
+        # per-item costs split by kernel: the persistent 64-query kernel's
+        # items are far cheaper than the 128-query kernel's CTAs (one shared
+        # item cost picked the wrong strategy for 3 of 72 7B micro-batches)
+        ab.append([0.0 if v3 else items, items if v3 else 0.0,
+                   0.0 if v3 else f["bwd_q64"] * hq / sms, f["bwd_q128"] * hq / sms if v3 else 0.0,
+                   1.0])
         yb.append(r["bwd_ms"] * 1e-3)
     # relative least squares: every workload weighs the same whatever its size
     wf = 1.0 / np.asarray(yf)
@@ -185,9 +190,9 @@ def fit_tile_model(rows, hq, hkv, d, sms=148, v3_min_rows=320):
     xf, _ = nnls(np.asarray(af) * wf[:, None], np.asarray(yf) * wf)
     xb, _ = nnls(np.asarray(ab) * wb[:, None], np.asarray(yb) * wb)
     return TileModel(hq=hq, hkv=hkv, d=d, sms=sms, fwd_item_s=float(xf[0]),
-                     fwd_step_s=float(xf[1]), bwd_item_s=float(xb[0]),
-                     bwd_step64_s=float(xb[1]), bwd_step128_s=float(xb[2]),
-                     v3_min_rows=v3_min_rows, const_s=float(xf[2] + xb[3]),
+                     fwd_step_s=float(xf[1]), bwd_item_s=float(xb[0]), bwd_item128_s=float(xb[1]),
+                     bwd_step64_s=float(xb[2]), bwd_step128_s=float(xb[3]),
+                     v3_min_rows=v3_min_rows, const_s=float(xf[2] + xb[4]),
                      source=f"least squares over {len(rows)} measured rank workloads on "
                             f"{torch.cuda.get_device_name()}")
 

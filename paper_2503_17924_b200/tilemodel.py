@@ -23,7 +23,8 @@ and predicts
     t = max((fi*items_f + fs*steps_f) * Hq / SMs,  fi + fs*max_f)
       + max((bi*items_b*Hkv + bs*steps_b*Hq) / SMs, bi + bs*max_b*Hq/Hkv) + c0
 
-with the five per-unit costs fitted by least squares to kernel times
+(bi, bs: the per-item and per-step costs of the backward kernel the library
+picks for that rank) with the six per-unit costs fitted by least squares to kernel times
 measured on B200 (`calibrate.fit_tile_model`).  The selector keeps the
 reference's rule: per-sequence when its slowest rank is predicted no slower.
 The reference `CostProfile` path stays available, bit-exact, for parity.
@@ -57,20 +58,29 @@ class TileModel:
     v3_min_rows: int = 320
     const_s: float = 3.0e-5
     source: str = "defaults (pre-calibration estimates from the kernel traces)"
+    # per-item cost of the 128-query backward (bwd_item_s is the 64-query
+    # kernel's; its persistent unit queue makes an item much cheaper); None:
+    # same as bwd_item_s (models calibrated before the split)
+    bwd_item128_s: float | None = None
 
     def __post_init__(self):
         if self.hq <= 0 or self.hkv <= 0 or self.hq % self.hkv:
             raise ConfigError("hq must be a positive multiple of hkv")
         costs = (self.fwd_item_s, self.fwd_step_s, self.bwd_item_s, self.bwd_step64_s,
-                 self.bwd_step128_s, self.const_s)
+                 self.bwd_step128_s, self.const_s, self.item128)
         if min(costs) < 0 or self.sms < 1:
             raise ConfigError("tile-model costs must be >= 0 and sms >= 1")
+
+    @property
+    def item128(self) -> float:
+        return self.bwd_item_s if self.bwd_item128_s is None else self.bwd_item128_s
 
     def array(self) -> list[float]:
         """The WLB_TILE_MODEL_LEN doubles `wlb_shard_plan_measured` reads."""
         return [float(self.sms), float(self.hq), float(self.hkv), self.fwd_item_s,
                 self.fwd_step_s, self.bwd_item_s, self.bwd_step64_s, self.bwd_step128_s,
-                float(self.v3_min_rows), self.const_s, 1.0 if self.d == 128 else 0.0]
+                float(self.v3_min_rows), self.const_s, 1.0 if self.d == 128 else 0.0,
+                self.item128]
 
     def predict(self, f, tl: int, n_docs: int) -> float:
         """Host restatement of the kernel's prediction for one feature row
@@ -80,10 +90,11 @@ class TileModel:
         v3 = self.d == 128 and tl >= self.v3_min_rows * max(1, n_docs)
         bq, bm = (f["bwd_q128"], f["bwd_max128"]) if v3 else (f["bwd_q64"], f["bwd_max64"])
         bs = self.bwd_step128_s if v3 else self.bwd_step64_s
+        bi = self.item128 if v3 else self.bwd_item_s
         tf = max((self.fwd_item_s * f["fwd_items"] + self.fwd_step_s * f["fwd_steps"]) * self.hq
                  / self.sms, self.fwd_item_s + self.fwd_step_s * f["fwd_max"])
-        tb = max((self.bwd_item_s * f["bwd_items"] * self.hkv + bs * bq * self.hq) / self.sms,
-                 self.bwd_item_s + bs * bm * self.hq / self.hkv)
+        tb = max((bi * f["bwd_items"] * self.hkv + bs * bq * self.hq) / self.sms,
+                 bi + bs * bm * self.hq / self.hkv)
         return tf + tb + self.const_s
 
     def to_dict(self) -> dict:
