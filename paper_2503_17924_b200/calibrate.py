@@ -154,8 +154,12 @@ def measure_tile_workloads(workloads, hq, hkv, d, reps=2, model=None):
                         box["o"], box["lse"] = attn_forward(q, kk, vv, tiles)
 
                     t_f = _time_ms(fwd, reps)
-                    t_b = _time_ms(lambda: attn_backward(q, kk, vv, box["o"], box["lse"], q, tiles),
-                                   reps)
+                    # as the CP pipeline runs it: covered dK/dV partial rows
+                    # only (the symmetric exchange's covered pull; zero-filling
+                    # the rest made per-sequence ranks of short documents look
+                    # up to 25 % slower than they run)
+                    t_b = _time_ms(lambda: attn_backward(q, kk, vv, box["o"], box["lse"], q, tiles,
+                                                         covered_only=cp > 1), reps)
                     rows.append({"tag": tag, "cp": cp, "mb": b, "strategy": strat, "rank": r,
                                  "tl": T // cp, "n_docs": len(lengths),
                                  "features": dict(zip(FEATURES, feats[b, s_idx, r].tolist())),
