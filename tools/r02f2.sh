@@ -4,7 +4,7 @@
 # capture of the 128-query backward, config-5 replay.
 set -u
 cd "$(dirname "$0")/.."
-out=gpurun_out/final5; mkdir -p $out
+out=gpurun_out/final6; mkdir -p $out
 timeout 1500 python -m pytest tests -m gpu -q > $out/gpu_tests.txt 2>&1; echo "all rc=$?" >> $out/gpu_tests.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke.txt 2>&1; echo "smoke rc=$?" >> $out/smoke.txt
 timeout 600 python bench.py --steps 20 --warmup 5 > $out/bench_n1.json 2> $out/bench_n1.err
@@ -21,3 +21,4 @@ import json
 d=json.loads(open('$out/$f.json').read().strip().splitlines()[-1]); e=d.get('e2e') or {}; print('$f', d['value'], e.get('value'), e.get('ms_per_step'), (d.get('clocks') or {}).get('reasons'), (d.get('roofline') or {}).get('frac'))"; done
 tail -5 $out/config5.txt
 timeout 300 python tools/short_profile.py > $out/short_profile.jsonl 2>&1
+timeout 120 python tools/pcie_probe.py > $out/pcie.txt 2>&1
