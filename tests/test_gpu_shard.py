@@ -183,14 +183,17 @@ def test_tile_model_features_match_kernel_work_lists(cp):
                 assert feats[b, s, r].tolist() == _work_list_features(plan, b, r), (strat, b, r)
 
 
-def test_measured_policy_selects_by_predicted_latency():
+@pytest.mark.parametrize("shape", [None, (32, 32), (64, 8)])
+def test_measured_policy_selects_by_predicted_latency(shape):
     """policy="measured": per-sequence iff its slowest rank's predicted time is
     <= per-document's (ties -> per-sequence, the reference's rule); the
-    prediction equals TileModel.predict on the returned features."""
+    prediction equals TileModel.predict on the returned features (defaults,
+    and the shipped B200 calibrations, whose two backward kernels have their
+    own per-item costs)."""
     cp = 4
     mbs = [so.pad_lengths_for_cp(x, cp) for x in
            ([30000, 100, 2000], [512] * 32, [8192], [100] * 40 + [20000])]
-    model = wl.TileModel()
+    model = wl.TileModel() if shape is None else wl.TileModel.for_shape(*shape, 128)
     plan = wl.build_shard_plan(mbs, cp, "measured", model=model)
     lat, feats = plan.rank_latency.cpu(), plan.features.cpu()
     for b, ls in enumerate(mbs):

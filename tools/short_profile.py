@@ -45,7 +45,12 @@ def main():
                     help="zero-fill uncovered dK/dV rows (the single-rank API) instead of the "
                          "CP pipeline's covered-only backward")
     ap.add_argument("--bwd-persistent", type=int, default=-1)
+    ap.add_argument("--v3-min-rows", type=int, default=-1,
+                    help="backward kernel threshold override (0: always the 128-query kernel)")
     a = ap.parse_args()
+    from paper_2503_17924_b200.attention import set_bwd_v3_min_rows
+    if a.v3_min_rows >= 0:
+        set_bwd_v3_min_rows(a.v3_min_rows)
     from paper_2503_17924_b200.attention import set_bwd_persistent
     if a.bwd_persistent >= 0:
         set_bwd_persistent(a.bwd_persistent)
