@@ -1339,19 +1339,38 @@ __global__ void __launch_bounds__(256) bwd_delta_kernel(const __nv_bfloat16* __r
 // [h_begin, h_begin + h_count).  32-bit index math with D a template
 // constant (a 64-bit division per element cost ~6% of a short rank's step).
 template <int D>
-__global__ void dq_convert3_kernel(const float4* __restrict__ acc, uint2* __restrict__ dq, int Tl,
-                                   int Hq, int h_begin, int h_count) {
-  constexpr unsigned DB = D / 4;
-  const unsigned n = (unsigned)Tl * (unsigned)h_count * DB;
-  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const unsigned db = i % DB;                  // output-ordered: consecutive threads write
-    const unsigned rh = i / DB;                  // consecutive 8-B pieces of a row
-    const unsigned hh = rh % (unsigned)h_count, row = rh / (unsigned)h_count;
-    const unsigned h = h_begin + hh;
-    const float4 v = acc[((size_t)h * DB + db) * Tl + row];
-    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
-    dq[((size_t)row * Hq + h) * DB + db] =
-        make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+__global__ void __launch_bounds__(256) dq_convert3_kernel(const float4* __restrict__ acc,
+                                                          uint2* __restrict__ dq, int Tl, int Hq,
+                                                          int h_begin, int h_count) {
+  // one block per (32 rows, head): coalesced 512-B reads along rows of each
+  // 4-float column block, a shared-memory transpose, coalesced row writes
+  // (the flat output-ordered loop read 16 B per 32-B sector: ~3.9 TB/s)
+  constexpr int DB = D / 4, R = 32;
+  __shared__ float4 tile[R][DB + 1];
+  const int row0 = (int)(blockIdx.x % (unsigned)((Tl + R - 1) / R)) * R;
+  const int h = h_begin + (int)(blockIdx.x / (unsigned)((Tl + R - 1) / R));
+  const float4* src = acc + (size_t)h * DB * Tl;
+#pragma unroll
+  for (int k = 0; k < (R * DB + 255) / 256; ++k) {
+    const int idx = k * 256 + (int)threadIdx.x;
+    if (idx < R * DB) {
+      const int db = idx / R, r = idx % R;
+      tile[r][db] = row0 + r < Tl ? src[(size_t)db * Tl + row0 + r] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < (R * DB + 255) / 256; ++k) {
+    const int idx = k * 256 + (int)threadIdx.x;
+    if (idx < R * DB) {
+      const int r = idx / DB, db = idx % DB;
+      if (row0 + r < Tl) {
+        const float4 v = tile[r][db];
+        __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+        dq[((size_t)(row0 + r) * Hq + h) * DB + db] =
+            make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+      }
+    }
   }
 }
 
@@ -1693,7 +1712,8 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
   const long long n4 = (long long)Tl * h_count * D / 4;
   const unsigned cblocks = (unsigned)std::min<long long>((n4 + 255) / 256, 148 * 16);
   if (v3) {
-    dq_convert3_kernel<D><<<cblocks, 256, 0, stream>>>((const float4*)w.dq_acc, (uint2*)dq, Tl, Hq,
+    const unsigned tblocks = (unsigned)((Tl + 31) / 32) * (unsigned)h_count;
+    dq_convert3_kernel<D><<<tblocks, 256, 0, stream>>>((const float4*)w.dq_acc, (uint2*)dq, Tl, Hq,
                                                         h_begin, h_count);
     WLB_LAUNCH_CHECK();
     return WLB_OK;
