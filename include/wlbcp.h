@@ -221,7 +221,7 @@ int wlb_attn_bwd_sync(const void* q, const void* k, const void* v, const void* o
                       void* stream);
 /* Backward kernel selection for D = 128: the 128-query-tile kernel (v3) runs
  * when Tl >= v3_min_rows * n_docs, else the 64-query kernel (v2).  Negative
- * restores the default (320); returns the previous threshold.  Process-wide
+ * restores the default (1: always for D = 128); returns the previous threshold.  Process-wide
  * tuning knob (no reference analogue). */
 int32_t wlb_attn_bwd_select(int32_t v3_min_rows);
 /* v3 as 2-CTA clusters (KV tiles 2q, 2q+1 of a document share query tiles and

@@ -183,7 +183,7 @@ def qkv_rope(y, positions, hq: int, hkv: int, d: int, base: float = 10000.0):
 
 def set_bwd_v3_min_rows(rows: int) -> int:
     """Backward kernel choice for D = 128: the 128-query-tile kernel runs when a
-    rank's local rows >= rows * n_docs (default 320; negative restores it).
+    rank's local rows >= rows * n_docs (default 1, i.e. always for D = 128; negative restores it).
     Returns the previous threshold."""
     return int(_native.lib().wlb_attn_bwd_select(int(rows)))
 

@@ -168,7 +168,7 @@ def measure_tile_workloads(workloads, hq, hkv, d, reps=2, model=None):
     return rows
 
 
-def fit_tile_model(rows, hq, hkv, d, sms=148, v3_min_rows=320):
+def fit_tile_model(rows, hq, hkv, d, sms=148, v3_min_rows=1):
     """Least-squares fit of the tile model's per-unit costs to measured rows
     (forward and backward separately; non-negative), returning a TileModel."""
     import numpy as np

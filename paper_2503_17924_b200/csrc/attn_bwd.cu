@@ -672,7 +672,7 @@ struct Bwd3Cfg {
   static constexpr int OFF_VEC = OFF_DS + T_BYTES;                  // QS x {-lse2, delta}[BM] f32
   static constexpr int OFF_POS = OFF_VEC + QS * 2 * BM * 4;         // QS x rel. position[BM] i8
   static constexpr int OFF_BAR = OFF_POS + QS * BM;
-  static constexpr int SMEM = OFF_BAR + 256;
+  static constexpr int SMEM = OFF_BAR + 512;
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 384;
   static constexpr uint32_t IDESC_ST = idesc_bf16(BN, BM, 0, 0);    // S^T, dP^T
@@ -683,25 +683,28 @@ struct Bwd3Cfg {
 static_assert(Bwd3Cfg::SMEM <= 232448, "bwd v3 exceeds the 227 KB SMEM window");
 
 struct Bwd3Bars {
-  uint64_t kv_full;
+  uint64_t kv_full, kv_empty;
+  uint64_t unit_full[kUnitRing], unit_empty[kUnitRing];
+  int unit_id[kUnitRing];
   uint64_t q_full[2], q_empty[2], vec_full[2], vec_empty[2];
   uint64_t s_full, dp_full, p_full[2], ds_full[2], dq_full, s_free, acc_done;
   uint64_t do_full, do_empty, rx_full[4], peer_free;   // PAIR: single dO buffer, dQ exchange
   uint32_t tmem_base;
 };
-static_assert(sizeof(Bwd3Bars) <= 256, "barrier block");
+static_assert(sizeof(Bwd3Bars) <= 512, "barrier block");
 
 #ifndef WLB_BWD_V3
 #define WLB_BWD_V3 1     // 0: D = 128 always uses the v2 (64-query) kernel
 #endif
 // v3 wins on long row-sets and, since its dQ partials leave by TMA
-// reduce-adds (TRED) and both kernels store dK/dV as whole lines, from ~320
-// local rows per document (384-row documents: 223 vs 216 TFLOP/s, 1024: 475
-// vs 430, 2048: 708 vs 608; 256: equal; 128: v2 93 vs 81;
-// profiles/r02_ab_tred.txt, profiles/r02_ab_dkv_epilogue.txt).  Used when
-// the rank's mean local rows per document reach this many.
+// reduce-adds (TRED), both kernels store dK/dV as whole lines and v3 runs as a
+// persistent kernel, on every document length measured (128-row documents 98
+// vs 93 TFLOP/s, 256: 189 vs 156, 384: 271 vs 216; GQA 256: 254 vs 203;
+// config-5 short ranks +15 %: profiles/r02_ab_bwd3_persistent.txt), so D = 128
+// always uses it (threshold 1 local row per document); the 64-query kernel
+// serves D = 64 and remains selectable (wlb_attn_bwd_select).
 #ifndef WLB_BWD_V3_MIN_ROWS
-#define WLB_BWD_V3_MIN_ROWS 320
+#define WLB_BWD_V3_MIN_ROWS 1
 #endif
 #ifndef WLB_RED_B0          // dQ reduction batches (v4 REDs per thread, of 32)
 #define WLB_RED_B0 8
@@ -788,7 +791,8 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                  float* __restrict__ dq_acc, void* __restrict__ dk, void* __restrict__ dv,
                  const int4* __restrict__ kv_tiles, const int* __restrict__ n_kv_tiles,
                  const int* __restrict__ positions, int Tl, int Hq, int Hkv, int n_slots,
-                 int g_begin, float scale, float scale_log2, int dkv_bf16, const CpSync sync) {
+                 int g_begin, float scale, float scale_log2, int dkv_bf16, int n_units,
+                 int* __restrict__ sched, int persistent, const CpSync sync) {
   using C = Bwd3Cfg;
   constexpr int D = C::D;
   extern __shared__ uint8_t smem_raw[];
@@ -799,28 +803,53 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
   // row_end} of tile 2q, then {k0, kv_begin', kv_len', k0'} with kv_begin' < 0
   // for a lone last tile); each CTA reduces half of the pair's summed dQ.
   const int cta = PAIR ? (int)cluster_ctarank() : 0;
-  const int slot = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int item = slot % n_slots, g = g_begin + slot / n_slots;
-  if (item >= n_kv_tiles[0]) return;
-  int4 kt = kv_tiles[2 * item];
-  int k0 = kv_tiles[2 * item + 1].x;
-  WLB_DCHECK(kt.z >= 0 && kt.z < kt.w && kt.w <= Tl && kt.y >= 1 && kt.y <= 128 && k0 >= 0);
-  WLB_DCHECK(g >= 0 && g < Hkv);
+  const int n_items = n_kv_tiles[0];
+  const int group = Hq / Hkv;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Work unit u = (KV tile item u % n_slots, KV head g_begin + u / n_slots):
+  // one per CTA (blockIdx.x; PAIR: per cluster), or, persistent, one CTA per
+  // SM taking units from a global counter (dynamic list scheduling in unit
+  // order, LPT within a head) and publishing them to its warps through a
+  // ring; every ring stage and barrier phase runs on CTA-global tile / unit
+  // counters, so a unit's epilogue overlaps the next unit's loads and first
+  // MMAs instead of a CTA teardown and launch.
   bool paired = false;
   if (PAIR) {
-    const int4 t2 = kv_tiles[2 * item + 1];
-    paired = t2.y >= 0;
+    const int item = (int)(blockIdx.x >> 1) % n_slots;
+    if (item >= n_items) return;
+    paired = kv_tiles[2 * item + 1].y >= 0;
     if (!paired && cta == 1) return;         // lone tile: CTA 1 idles, CTA 0 runs solo
-    if (cta == 1) {
-      kt.x = t2.y;
-      kt.y = t2.z;
-      k0 = t2.w;
-    }
+  } else if (!persistent && (int)blockIdx.x % n_slots >= n_items) {
+    return;
   }
-  const int group = Hq / Hkv;
-  const int qt_per_head = (kt.w - kt.z + C::BM - 1) / C::BM;
-  const int n_iter = qt_per_head * group;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  struct Unit3 {
+    int4 kt;   // {kv_begin, kv_len, row_first, row_end}
+    int k0, g, qt, n_iter;
+  };
+  // PAIR: a 2-CTA cluster runs KV tiles 2q and 2q+1 of one document over the
+  // same query tiles (kv_tiles holds pair items: {kv_begin, kv_len, row_first,
+  // row_end} of tile 2q, then {k0, kv_begin', kv_len', k0'} with kv_begin' < 0
+  // for a lone last tile); each CTA reduces half of the pair's summed dQ.
+  auto geom = [&](int u) {
+    Unit3 U;
+    const int item = u % n_slots;
+    U.g = g_begin + u / n_slots;
+    U.kt = kv_tiles[2 * item];
+    U.k0 = kv_tiles[2 * item + 1].x;
+    if (PAIR && cta == 1) {
+      const int4 t2 = kv_tiles[2 * item + 1];
+      U.kt.x = t2.y;
+      U.kt.y = t2.z;
+      U.k0 = t2.w;
+    }
+    WLB_DCHECK(U.kt.z >= 0 && U.kt.z < U.kt.w && U.kt.w <= Tl && U.kt.y >= 1 && U.kt.y <= 128 &&
+               U.k0 >= 0);
+    WLB_DCHECK(U.g >= 0 && U.g < Hkv);
+    U.qt = (U.kt.w - U.kt.z + C::BM - 1) / C::BM;
+    U.n_iter = U.qt * group;
+    return U;
+  };
+  const int first_unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
 
   Bwd3Bars* bars = reinterpret_cast<Bwd3Bars*>(smem + C::OFF_BAR);
   uint8_t* sK = smem + C::OFF_K;
@@ -852,6 +881,12 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     mbar_init(&bars->do_empty, 1);
     for (int c = 0; c < 4; ++c) mbar_init(&bars->rx_full[c], 128);
     mbar_init(&bars->peer_free, 128);
+    mbar_init(&bars->kv_empty, 1);
+    for (int i = 0; i < kUnitRing; ++i) {
+      mbar_init(&bars->unit_full[i], 1);
+      // consumers: MMA warp, vector warp, 4 drain warps, 8 compute warps
+      mbar_init(&bars->unit_empty[i], 14);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(&bars->tmem_base, C::TMEM_COLS);
@@ -861,6 +896,15 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
   const uint32_t tmem = bars->tmem_base;
   if (PAIR && paired) cluster_sync();       // peer barriers initialised before remote use
 
+  // consumer side of the unit ring (whole warp; lane 0 releases the slot)
+  auto next_unit = [&](int seq) {
+    const int st = seq % kUnitRing;
+    mbar_wait(&bars->unit_full[st], (seq / kUnitRing) & 1);
+    const int u = *reinterpret_cast<volatile int*>(&bars->unit_id[st]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bars->unit_empty[st]);
+    return u;
+  };
   if (warp < 4) setmaxnreg_dec<80>();   // TMA / MMA / alloc / vector warps
   if (warp == 0) {
     // ------------------------------------------------------------ producer --
@@ -868,16 +912,41 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
     tma_prefetch(&tmDO);
+    int I0 = 0;
+    for (int seq = 0;; ++seq) {
+    int u = -1;
+    if (lane == 0) {
+      if (persistent) {
+        do {
+          u = atomicAdd(sched, 1);
+        } while (u < n_units && u % n_slots >= n_items);
+        if (u >= n_units) u = -1;
+      } else if (seq == 0) {
+        u = first_unit;
+      }
+      const int st = seq % kUnitRing;
+      mbar_wait(&bars->unit_empty[st], ((seq / kUnitRing) & 1) ^ 1);
+      bars->unit_id[st] = u;
+      mbar_arrive(&bars->unit_full[st]);
+    }
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u < 0) break;
+    const Unit3 U = geom(u);
+    const int4 kt = U.kt;
+    const int g = U.g, qt_per_head = U.qt, n_iter = U.n_iter;
+    // K/V of this unit once the previous unit's last MMAs have read the old
+    if (seq > 0) mbar_wait(&bars->kv_empty, (seq - 1) & 1);
     mbar_expect_tx_w(&bars->kv_full, 2 * C::KV_BYTES);
     for (int s = 0; s < 2; ++s) {
       tma_load_3d_w(sK + s * C::SLAB, &tmK, &bars->kv_full, s * 64, g, kt.x);
       tma_load_3d_w(sV + s * C::SLAB, &tmV, &bars->kv_full, s * 64, g, kt.x);
     }
     for (int i = 0; i < n_iter; ++i) {
-      const int st = i % C::QS;
+      const int Ig = I0 + i;
+      const int st = Ig % C::QS;
       const int h = g * group + (WLB_BWD_HEAD_INNER ? i % group : i / qt_per_head);
       const int row = kt.z + (WLB_BWD_HEAD_INNER ? i / group : i % qt_per_head) * C::BM;
-      mbar_wait(&bars->q_empty[st], ((i / C::QS) & 1) ^ 1);
+      mbar_wait(&bars->q_empty[st], ((Ig / C::QS) & 1) ^ 1);
       if (PAIR || TRED) {
         // dO single-buffered (its second stage is the dQ exchange buffer): it
         // is read by dP(i) and dV(i) only, and dO(i+1) has S(i+1), dQ(i) and
@@ -885,7 +954,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         mbar_expect_tx_w(&bars->q_full[st], C::Q_BYTES);
         for (int s = 0; s < 2; ++s)
           tma_load_3d_w(sQ + st * C::Q_BYTES + s * C::SLAB, &tmQ, &bars->q_full[st], s * 64, h, row);
-        mbar_wait(&bars->do_empty, (i & 1) ^ 1);
+        mbar_wait(&bars->do_empty, (Ig & 1) ^ 1);
         mbar_expect_tx_w(&bars->do_full, C::Q_BYTES);
         for (int s = 0; s < 2; ++s)
           tma_load_3d_w(sDO + s * C::SLAB, &tmDO, &bars->do_full, s * 64, h, row);
@@ -896,6 +965,8 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
           tma_load_3d_w(sDO + st * C::Q_BYTES + s * C::SLAB, &tmDO, &bars->q_full[st], s * 64, h, row);
         }
       }
+    }
+    I0 += n_iter;
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer --
@@ -915,12 +986,18 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       kmaj_off[kk] = ((kk >> 2) * C::SLAB + (kk & 3) * 32) >> 4;
       mn_off[kk] = (kk * 2048) >> 4;
     }
-    mbar_wait(&bars->kv_full, 0);
+    int I0 = 0;
+    for (int seq = 0;; ++seq) {
+    const int u = next_unit(seq);
+    if (u < 0) break;
+    const int n_iter = geom(u).n_iter;
+    mbar_wait(&bars->kv_full, seq & 1);
     for (int i = 0; i <= n_iter; ++i) {
+      const int Ig = I0 + i;
       if (i < n_iter) {
-        const int st = i % C::QS;
+        const int st = Ig % C::QS;
         const uint32_t qs = q_b + st * C::Q_BYTES;
-        mbar_wait(&bars->q_full[st], (i / C::QS) & 1);
+        mbar_wait(&bars->q_full[st], (Ig / C::QS) & 1);
         TRACE3(0, i);
         tc_fence_after();
         // S^T = K Q^T (contract over D; K-major both); 8-MMA chains under one
@@ -930,10 +1007,10 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         mma_commit_w(&bars->s_full);
       }
       if (i >= 1) {
-        const int j = i - 1, st = j % C::QS;
+        const int j = i - 1, Jg = Ig - 1, st = Jg % C::QS;
         const uint32_t qs = q_b + st * C::Q_BYTES;
-        mbar_wait_fast(&bars->ds_full[0], j & 1);
-        mbar_wait_fast(&bars->ds_full[1], j & 1);
+        mbar_wait_fast(&bars->ds_full[0], Jg & 1);
+        mbar_wait_fast(&bars->ds_full[1], Jg & 1);
         TRACE3(5, j);
         tc_fence_after();
         const uint32_t dsb = ds_b;
@@ -949,12 +1026,13 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         if (j == n_iter - 1) mma_commit_w(&bars->acc_done);
       }
       if (i < n_iter) {
-        const int st = i % C::QS;
+        const int st = Ig % C::QS;
         const uint32_t dos = (PAIR || TRED) ? do_b : do_b + st * C::Q_BYTES;
-        const uint32_t ph = i & 1;
+        const uint32_t ph = Ig & 1;
         if (PAIR || TRED) mbar_wait(&bars->do_full, ph);
-        // dP^T = V dO^T into the columns dQ(i-1) occupied: wait for the drain
-        if (i >= 1) mbar_wait_fast(&bars->s_free, (i - 1) & 1);
+        // dP^T = V dO^T into the columns dQ(i-1) (or the previous unit's last
+        // dQ) occupied: wait for the drain
+        if (Ig >= 1) mbar_wait_fast(&bars->s_free, (Ig - 1) & 1);
         TRACE3(1, i);
         tc_fence_after();
         mma_ss8_w(tmem + C::COL_DP, sdesc_sw128(v_b, 16, 1024), sdesc_sw128(dos, 16, 1024), kmaj_off,
@@ -980,13 +1058,24 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         if (PAIR || TRED) mma_commit_w(&bars->do_empty);   // single dO buffer: dV(i) was its last reader
       }
     }
+    mma_commit_w(&bars->kv_empty);   // this unit's last K / V readers issued
+    I0 += n_iter;
+    }
   } else if (warp == 3) {
     // ------------------------------------------------- per-query vectors --
+    int I0 = 0;
+    for (int seq = 0;; ++seq) {
+    const int u = next_unit(seq);
+    if (u < 0) break;
+    const Unit3 U = geom(u);
+    const int4 kt = U.kt;
+    const int k0 = U.k0, g = U.g, qt_per_head = U.qt, n_iter = U.n_iter;
     for (int i = 0; i < n_iter; ++i) {
-      const int b = i % C::QS;
+      const int Ig = I0 + i;
+      const int b = Ig % C::QS;
       const int h = g * group + (WLB_BWD_HEAD_INNER ? i % group : i / qt_per_head);
       const int row0 = kt.z + (WLB_BWD_HEAD_INNER ? i / group : i % qt_per_head) * C::BM;
-      mbar_wait(&bars->vec_empty[b], ((i / C::QS) & 1) ^ 1);
+      mbar_wait(&bars->vec_empty[b], ((Ig / C::QS) & 1) ^ 1);
       float* vec = sVec + b * 2 * C::BM;
       int8_t* rp = sPos + b * C::BM;
 #pragma unroll
@@ -998,6 +1087,8 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         rp[e] = (int8_t)(ok ? min(positions[row] - k0, 127) : -1);
       }
       mbar_arrive(&bars->vec_full[b]);
+    }
+    I0 += n_iter;
     }
   } else if (warp >= 12) {
     // ------------------------------------------------------------ dQ drain --
@@ -1014,7 +1105,15 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     // so those waits cannot alias a later phase.)
     setmaxnreg_inc<160>();
     const size_t blk = (size_t)Tl * 4;
+    int I0 = 0;
+    for (int seq = 0;; ++seq) {
+    const int u = next_unit(seq);
+    if (u < 0) break;
+    const Unit3 U = geom(u);
+    const int4 kt = U.kt;
+    const int g = U.g, qt_per_head = U.qt, n_iter = U.n_iter;
     for (int j = 0; j < n_iter; ++j) {
+      const int Jg = I0 + j;
       const int h = g * group + (WLB_BWD_HEAD_INNER ? j % group : j / qt_per_head);
       const int row = kt.z + (WLB_BWD_HEAD_INNER ? j / group : j % qt_per_head) * C::BM + lg * 32 + lane;
 #ifdef WLB_EXP_NORED
@@ -1028,7 +1127,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 #else
       const bool ok_tile = true;
 #endif
-      mbar_wait(&bars->dq_full, j & 1);
+      mbar_wait(&bars->dq_full, Jg & 1);
       if (warp == 12) TRACE3(12, j);
       tc_fence_after();
       uint32_t u[128];
@@ -1039,8 +1138,8 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       tc_fence_before();
       mbar_arrive(&bars->s_free);
       if (warp == 12) TRACE3(13, j);
-      const bool last = j + 1 == n_iter;
-      const uint32_t nph = (j + 1) & 1;
+      const bool last = j + 1 == n_iter;   // (no pacing across units)
+      const uint32_t nph = (Jg + 1) & 1;
       if (PAIR && paired) {
         // Exchange halves with the peer CTA: keep head-dims [64*cta, 64*cta+64),
         // send the other 64 (st.async into the peer's exchange buffer, row q,
@@ -1067,7 +1166,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         //  every completion; the peer's loads of its buffer are complete before
         //  its release-arrive, and st.async data is visible through the
         //  rx_full transaction counts)
-        mbar_wait_fast(&bars->peer_free, (j & 1) ^ 1);     // peer consumed tile j-1
+        mbar_wait_fast(&bars->peer_free, (Jg & 1) ^ 1);     // peer consumed tile j-1
         if (warp == 12) TRACE3(4, j);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -1084,7 +1183,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                         u[64 + 16 * c + 4 * e + 1], u[64 + 16 * c + 4 * e + 2],
                         u[64 + 16 * c + 4 * e + 3]);
           // (no suspend hint: a remote completion wakes a suspended waiter late)
-          mbar_wait_fast(&bars->rx_full[c], j & 1);
+          mbar_wait_fast(&bars->rx_full[c], Jg & 1);
           if (warp == 12 && c == 0) TRACE3(14, j);
           if (warp == 12 && c == 3) TRACE3(15, j);
 #pragma unroll
@@ -1171,22 +1270,32 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       }
 #endif
     }
+    I0 += n_iter;
+    }
   } else if (warp >= 4) {
     // ------------------------------------------------------------- compute --
     setmaxnreg_inc<136>();
     const int lg = warp & 3;                 // TMEM lane quarter
     const int hf = (warp - 4) >> 2;          // query half [64hf, 64hf+64)
     const int t = lg * 32 + lane;            // key row in the tile
-    const bool key_ok = t < kt.y;
     const uint32_t lane_base = tmem + ((uint32_t)(lg * 32) << 16);
+    int I0 = 0;
+    for (int seq = 0;; ++seq) {
+    const int u = next_unit(seq);
+    if (u < 0) break;
+    const Unit3 U = geom(u);
+    const int4 kt = U.kt;
+    const int g = U.g, n_iter = U.n_iter;
+    const bool key_ok = t < kt.y;
     for (int i = 0; i < n_iter; ++i) {
-      const int vb = i % C::QS;
-      const uint32_t ph = i & 1;
+      const int Ig = I0 + i;
+      const int vb = Ig % C::QS;
+      const uint32_t ph = Ig & 1;
       uint8_t* drow = sDS + hf * C::SLAB + t * 128;
       const float* nl = sVec + vb * 2 * C::BM + 64 * hf;
       const float* dl = nl + C::BM;
       const int8_t* rp = sPos + vb * C::BM + 64 * hf;
-      mbar_wait(&bars->vec_full[vb], (i / C::QS) & 1);
+      mbar_wait(&bars->vec_full[vb], (Ig / C::QS) & 1);
       mbar_wait(&bars->s_full, ph);
       if (warp == 4) TRACE3(6, i);
       tc_fence_after();
@@ -1252,7 +1361,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       }
       mbar_arrive(&bars->vec_empty[vb]);
     }
-    mbar_wait(&bars->acc_done, n_iter > 0 ? 0 : 1);   // the last MMA group wrote dV / dK
+    mbar_wait(&bars->acc_done, seq & 1);   // this unit's last MMA group wrote dV / dK
     tc_fence_after();
     // ------------------------------------------------------------ epilogue --
     // (the dS^T buffer is free: acc_done follows the last dK MMA, its last reader)
@@ -1273,6 +1382,8 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       named_bar_sync(1, 256);
       if (warp == 4 && lane == 0)
         cp_sync_unit_done(sync, g / sync.kv_per_group, n_kv_tiles[0] * sync.kv_per_group);
+    }
+    I0 += n_iter;
     }
   }
   if (TRED && warp >= 12 && lane == 0) bulk_wait_group<0>();   // reduces done with the staging
@@ -1508,6 +1619,11 @@ static int g_bwd_pairs = WLB_BWD_PAIRS;
 #define WLB_BWD_TRED 1
 #endif
 static int g_bwd_tred = WLB_BWD_TRED;
+// 128-query backward as a persistent kernel (one CTA per SM, unit queue)
+#ifndef WLB_BWD3_PERSIST
+#define WLB_BWD3_PERSIST 1
+#endif
+static int g_bwd3_persistent = WLB_BWD3_PERSIST;
 // v2 backward as a persistent kernel (one CTA per SM, dynamic unit queue)
 #ifndef WLB_BWD_PERSIST
 #define WLB_BWD_PERSIST 1
@@ -1660,14 +1776,26 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
       WLB_CUDA_TRY(cudaLaunchKernelEx(&cfg, p16 ? attn_bwd3_kernel<true, true> : attn_bwd3_kernel<true, false>, tq, tk, tv, tdo, tdq, lse,
                                       (const float*)w.delta, w.dq_acc, dk, dv,
                                       (const int4*)w.kv_tiles, (const int*)w.n_kv, positions, Tl,
-                                      Hq, Hkv, max_items, g_begin, scale, sl2, dkv_bf16, sync));
+                                      Hq, Hkv, max_items, g_begin, scale, sl2, dkv_bf16,
+                                      max_items * g_count, w.sched, 0, sync));
     } else {
       auto kern = g_bwd_tred ? (p16 ? attn_bwd3_kernel<false, true, true>
                                     : attn_bwd3_kernel<false, false, true>)
                              : (p16 ? attn_bwd3_kernel<false, true> : attn_bwd3_kernel<false, false>);
-      kern<<<(unsigned)max_items * g_count, C3::THREADS, C3::SMEM, stream>>>(
+      const int n_units = max_items * g_count;
+      unsigned grid = (unsigned)n_units;
+      if (g_bwd3_persistent) {
+        // one CTA per SM over the unit queue (a unit's epilogue overlaps the
+        // next unit's K/V load and first MMAs)
+        int dev = 0, sms = 148;
+        WLB_CUDA_TRY(cudaGetDevice(&dev));
+        WLB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        WLB_CUDA_TRY(cudaMemsetAsync(w.sched, 0, sizeof(int), stream));
+        grid = (unsigned)std::min(n_units, sms);
+      }
+      kern<<<grid, C3::THREADS, C3::SMEM, stream>>>(
           tq, tk, tv, tdo, tdq, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
-          Hkv, max_items, g_begin, scale, sl2, dkv_bf16, sync);
+          Hkv, max_items, g_begin, scale, sl2, dkv_bf16, n_units, w.sched, g_bwd3_persistent, sync);
     }
     WLB_LAUNCH_CHECK();
   } else

@@ -55,7 +55,7 @@ class TileModel:
     bwd_item_s: float = 4.0e-6
     bwd_step64_s: float = 1.5e-6
     bwd_step128_s: float = 2.75e-6
-    v3_min_rows: int = 320
+    v3_min_rows: int = 1
     const_s: float = 3.0e-5
     source: str = "defaults (pre-calibration estimates from the kernel traces)"
     # per-item cost of the 128-query backward (bwd_item_s is the 64-query
