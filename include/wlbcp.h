@@ -29,7 +29,7 @@ extern "C" {
 #define WLB_STRATEGY_PER_DOCUMENT 1
 #define WLB_POLICY_ADAPTIVE 2
 #define WLB_POLICY_MEASURED 3   /* adaptive, priced by the B200 tile model */
-#define WLB_TILE_MODEL_LEN 12
+#define WLB_TILE_MODEL_LEN 14
 
 /* In-kernel CP synchronisation on per-peer arrival flags (see wlb_cp_signal /
  * wlb_cp_wait): the attention kernels can wait for, and publish, head-group
@@ -109,7 +109,8 @@ int wlb_shard_plan(int32_t n_mb, const int32_t* mb_doc_off, const int64_t* doc_l
  *   is predicted no slower, else per-document).
  * model (device) [WLB_TILE_MODEL_LEN] fp64: {SMs, Hq, Hkv, fwd_item_s,
  *   fwd_step_s, bwd_item_s (64-query kernel), bwd_step64_s, bwd_step128_s,
- *   v3_min_rows, const_s, d_is_128, bwd_item128_s (128-query kernel)},
+ *   v3_min_rows, const_s, d_is_128, bwd_item128_s (128-query kernel),
+ *   fwd_tail, bwd_tail (list-scheduling tail weights)},
  *   calibrated on B200 (paper_2503_17924_b200/calibrate.py).
  * rank_latency receives the predicted seconds [n_mb][2][cp]; features (may
  *   be NULL) [n_mb][2][cp][8] int64: fwd items, fwd steps, max fwd item

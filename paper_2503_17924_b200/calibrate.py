@@ -168,37 +168,64 @@ def measure_tile_workloads(workloads, hq, hkv, d, reps=2, model=None):
     return rows
 
 
-def fit_tile_model(rows, hq, hkv, d, sms=148, v3_min_rows=1):
-    """Least-squares fit of the tile model's per-unit costs to measured rows
-    (forward and backward separately; non-negative), returning a TileModel."""
+def fit_tile_model(rows, hq, hkv, d, sms=148, v3_min_rows=1, device_name=None):
+    """Least-squares fit of the tile model to measured rows, forward and
+    backward separately, relative residuals (every workload weighs the same
+    whatever its size): non-negative per-unit costs, tail weights in [0, 1].
+    The costs of the pre-tail linear form (NNLS) seed the non-linear fit."""
     import numpy as np
-    from scipy.optimize import nnls
+    from scipy.optimize import least_squares, nnls
     from .tilemodel import TileModel
-    af, yf, ab, yb = [], [], [], []
-    for r in rows:
-        f = r["features"]
-        af.append([f["fwd_items"] * hq / sms, f["fwd_steps"] * hq / sms, 1.0])
-        yf.append(r["fwd_ms"] * 1e-3)
-        v3 = d == 128 and r["tl"] >= v3_min_rows * max(1, r["n_docs"])
-        items = f["bwd_items"] * hkv / sms
+    f = {k: np.array([r["features"][k] for r in rows], dtype=float)
+         for k in rows[0]["features"]}
+    v3 = np.array([d == 128 and r["tl"] >= v3_min_rows * max(1, r["n_docs"]) for r in rows])
+    yf = np.array([r["fwd_ms"] for r in rows]) * 1e-3
+    yb = np.array([r["bwd_ms"] for r in rows]) * 1e-3
+    bq = np.where(v3, f["bwd_q128"], f["bwd_q64"])
+    bm = np.where(v3, f["bwd_max128"], f["bwd_max64"])
+
+    def t_fwd(x):                       # x = fi, fs, gf, c
+        s = (x[0] * f["fwd_items"] + x[1] * f["fwd_steps"]) * hq / sms
+        m = x[0] + x[1] * f["fwd_max"]
+        return np.maximum(s, m) + x[2] * np.minimum(s, m) + x[3]
+
+    def t_bwd(x):                       # x = bi64, bi128, bs64, bs128, gb, c
         # per-item costs split by kernel: the persistent 64-query kernel's
-        # items are far cheaper than the 128-query kernel's CTAs (one shared
-        # item cost picked the wrong strategy for 3 of 72 7B micro-batches)
-        ab.append([0.0 if v3 else items, items if v3 else 0.0,
-                   0.0 if v3 else f["bwd_q64"] * hq / sms, f["bwd_q128"] * hq / sms if v3 else 0.0,
-                   1.0])
-        yb.append(r["bwd_ms"] * 1e-3)
-    # relative least squares: every workload weighs the same whatever its size
-    wf = 1.0 / np.asarray(yf)
-    wb = 1.0 / np.asarray(yb)
-    xf, _ = nnls(np.asarray(af) * wf[:, None], np.asarray(yf) * wf)
-    xb, _ = nnls(np.asarray(ab) * wb[:, None], np.asarray(yb) * wb)
+        # items are far cheaper than the 128-query kernel's
+        bi = np.where(v3, x[1], x[0])
+        bs = np.where(v3, x[3], x[2])
+        s = (bi * f["bwd_items"] * hkv + bs * bq * hq) / sms
+        m = bi + bs * bm * hq / hkv
+        return np.maximum(s, m) + x[4] * np.minimum(s, m) + x[5]
+
+    def seed(cols, y):
+        a = np.stack(cols, 1) / y[:, None]
+        return nnls(a, np.ones_like(y))[0]
+
+    sf = seed([f["fwd_items"] * hq / sms, f["fwd_steps"] * hq / sms, np.ones_like(yf)], yf)
+    items = f["bwd_items"] * hkv / sms
+    sb = seed([np.where(v3, 0, items), np.where(v3, items, 0), np.where(v3, 0, bq * hq / sms),
+               np.where(v3, bq * hq / sms, 0), np.ones_like(yb)], yb)
+    inf = np.inf
+    xf = least_squares(lambda x: t_fwd(x) / yf - 1, [sf[0], sf[1], 0.0, sf[2]],
+                       bounds=([0, 0, 0, 0], [inf, inf, 1, inf]), x_scale="jac").x
+    # a kernel no row ran keeps its seed costs (no data moves them)
+    xb = np.array([*sb[:4], 0.0, sb[4]])
+    act = [i for i in range(6) if not ((i in (0, 2) and v3.all()) or (i in (1, 3) and not v3.any()))]
+
+    def rb(x):
+        xb[act] = x
+        return t_bwd(xb) / yb - 1
+
+    hi = np.array([inf, inf, inf, inf, 1, inf])[act]
+    xb[act] = least_squares(rb, xb[act], bounds=(np.zeros(len(act)), hi), x_scale="jac").x
     return TileModel(hq=hq, hkv=hkv, d=d, sms=sms, fwd_item_s=float(xf[0]),
                      fwd_step_s=float(xf[1]), bwd_item_s=float(xb[0]), bwd_item128_s=float(xb[1]),
                      bwd_step64_s=float(xb[2]), bwd_step128_s=float(xb[3]),
-                     v3_min_rows=v3_min_rows, const_s=float(xf[2] + xb[4]),
+                     v3_min_rows=v3_min_rows, const_s=float(xf[3] + xb[5]),
+                     fwd_tail=float(xf[2]), bwd_tail=float(xb[4]),
                      source=f"least squares over {len(rows)} measured rank workloads on "
-                            f"{torch.cuda.get_device_name()}")
+                            f"{device_name or torch.cuda.get_device_name()}")
 
 
 def selection_report(rows, model, profile_choices=None):

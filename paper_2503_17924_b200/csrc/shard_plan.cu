@@ -97,9 +97,12 @@ __device__ __forceinline__ double range_latency(long long q, long long kv, long 
 //             (v2) or 128-query (v3) tile of the rows that can see it
 // Integer features per (strategy, rank), kFeat of them:
 enum { kF_ITEMS = 0, kF_STEPS, kF_MAX, kB_ITEMS, kB_Q64, kB_Q128, kB_MAX64, kB_MAX128, kFeat };
-// and model[WLB_TILE_MODEL_LEN] (seconds): predicted rank time =
-//   max((fi*F_ITEMS + fs*F_STEPS) * Hq / SMs, fi + fs*F_MAX)
-// + max((bi*B_ITEMS*Hkv + bs*B_Q*Hq) / SMs, bi + bs*B_MAX*(Hq/Hkv)) + c0,
+// and model[WLB_TILE_MODEL_LEN] (seconds): per direction, with the even
+// spread S and the largest item M,
+//   Sf = (fi*F_ITEMS + fs*F_STEPS) * Hq / SMs,   Mf = fi + fs*F_MAX
+//   Sb = (bi*B_ITEMS*Hkv + bs*B_Q*Hq) / SMs,     Mb = bi + bs*B_MAX*(Hq/Hkv)
+//   t = max(Sf, Mf) + gf*min(Sf, Mf) + max(Sb, Mb) + gb*min(Sb, Mb) + c0
+// (g: the list-scheduling tail the largest item adds; tilemodel.py),
 // bi / B_Q / B_MAX / bs of the backward kernel the library will pick (v3 when
 // the rank's rows per document reach v3_min_rows and D = 128).
 constexpr int kMaxModelCp = 64;
@@ -172,15 +175,18 @@ __device__ void tile_model_select(int b, int nd, const long long* L, const long 
     const double sms = model[0], hq = model[1], hkv = model[2];
     const double fi = model[3], fs = model[4], bi = model[5], bs64 = model[6], bs128 = model[7];
     const double v3_rows = model[8], c0 = model[9], d128 = model[10], bi128 = model[11];
+    const double gf = model[12], gb = model[13];
     const long long T = dstart[nd];
     const bool v3 = d128 != 0.0 && (double)(T / cp) >= v3_rows * (double)(nd > 0 ? nd : 1);
     const double bq = (double)(v3 ? f[kB_Q128] : f[kB_Q64]);
     const double bm = (double)(v3 ? f[kB_MAX128] : f[kB_MAX64]);
     const double bs = v3 ? bs128 : bs64, bi_k = v3 ? bi128 : bi;
-    const double tf = fmax((fi * (double)f[kF_ITEMS] + fs * (double)f[kF_STEPS]) * hq / sms,
-                           fi + fs * (double)f[kF_MAX]);
-    const double tb = fmax((bi_k * (double)f[kB_ITEMS] * hkv + bs * bq * hq) / sms,
-                           bi_k + bs * bm * (hq / hkv));
+    const double sf = (fi * (double)f[kF_ITEMS] + fs * (double)f[kF_STEPS]) * hq / sms;
+    const double mf = fi + fs * (double)f[kF_MAX];
+    const double sb = (bi_k * (double)f[kB_ITEMS] * hkv + bs * bq * hq) / sms;
+    const double mb = bi_k + bs * bm * (hq / hkv);
+    const double tf = fmax(sf, mf) + gf * fmin(sf, mf);
+    const double tb = fmax(sb, mb) + gb * fmin(sb, mb);
     rank_latency[((long long)b * 2 + strat) * cp + w] = tf + tb + c0;
   }
   __syncthreads();

@@ -18,14 +18,18 @@ per (strategy, rank):
 * backward: 128-key KV tiles (items) and their 64-query (v2) / 128-query
   (v3) steps; the largest item;
 
-and predicts
+and predicts, per direction, from the even-spread time S = (item and step
+costs summed) / SMs and the largest item M,
 
-    t = max((fi*items_f + fs*steps_f) * Hq / SMs,  fi + fs*max_f)
-      + max((bi*items_b*Hkv + bs*steps_b*Hq) / SMs, bi + bs*max_b*Hq/Hkv) + c0
+    t_dir = max(S, M) + g_dir * min(S, M)
+    t     = t_fwd + t_bwd + c0
 
-(bi, bs: the per-item and per-step costs of the backward kernel the library
-picks for that rank) with the six per-unit costs fitted by least squares to kernel times
-measured on B200 (`calibrate.fit_tile_model`).  The selector keeps the
+max(S, M) is the ideal makespan; the tail term g * min(S, M) is the part of
+the largest item that list scheduling cannot hide behind the others (Graham's
+bound S + M is g = 1).  Without it the model under-priced per-sequence ranks
+of few, long KV tiles by 1.3-1.7x (GQA 32K at cp 2-4).  The per-unit costs of
+the backward kernel the library picks for that rank, the two tail weights and
+c0 are fitted to kernel times measured on B200 (`calibrate.fit_tile_model`).  The selector keeps the
 reference's rule: per-sequence when its slowest rank is predicted no slower.
 The reference `CostProfile` path stays available, bit-exact, for parity.
 """
@@ -62,12 +66,15 @@ class TileModel:
     # kernel's; its persistent unit queue makes an item much cheaper); None:
     # same as bwd_item_s (models calibrated before the split)
     bwd_item128_s: float | None = None
+    # list-scheduling tail weights (0: the pre-tail model, max(S, M) only)
+    fwd_tail: float = 0.0
+    bwd_tail: float = 0.0
 
     def __post_init__(self):
         if self.hq <= 0 or self.hkv <= 0 or self.hq % self.hkv:
             raise ConfigError("hq must be a positive multiple of hkv")
         costs = (self.fwd_item_s, self.fwd_step_s, self.bwd_item_s, self.bwd_step64_s,
-                 self.bwd_step128_s, self.const_s, self.item128)
+                 self.bwd_step128_s, self.const_s, self.item128, self.fwd_tail, self.bwd_tail)
         if min(costs) < 0 or self.sms < 1:
             raise ConfigError("tile-model costs must be >= 0 and sms >= 1")
 
@@ -80,7 +87,7 @@ class TileModel:
         return [float(self.sms), float(self.hq), float(self.hkv), self.fwd_item_s,
                 self.fwd_step_s, self.bwd_item_s, self.bwd_step64_s, self.bwd_step128_s,
                 float(self.v3_min_rows), self.const_s, 1.0 if self.d == 128 else 0.0,
-                self.item128]
+                self.item128, self.fwd_tail, self.bwd_tail]
 
     def predict(self, f, tl: int, n_docs: int) -> float:
         """Host restatement of the kernel's prediction for one feature row
@@ -91,10 +98,12 @@ class TileModel:
         bq, bm = (f["bwd_q128"], f["bwd_max128"]) if v3 else (f["bwd_q64"], f["bwd_max64"])
         bs = self.bwd_step128_s if v3 else self.bwd_step64_s
         bi = self.item128 if v3 else self.bwd_item_s
-        tf = max((self.fwd_item_s * f["fwd_items"] + self.fwd_step_s * f["fwd_steps"]) * self.hq
-                 / self.sms, self.fwd_item_s + self.fwd_step_s * f["fwd_max"])
-        tb = max((bi * f["bwd_items"] * self.hkv + bs * bq * self.hq) / self.sms,
-                 bi + bs * bm * self.hq / self.hkv)
+        sf = (self.fwd_item_s * f["fwd_items"] + self.fwd_step_s * f["fwd_steps"]) * self.hq / self.sms
+        mf = self.fwd_item_s + self.fwd_step_s * f["fwd_max"]
+        sb = (bi * f["bwd_items"] * self.hkv + bs * bq * self.hq) / self.sms
+        mb = bi + bs * bm * self.hq / self.hkv
+        tf = max(sf, mf) + self.fwd_tail * min(sf, mf)
+        tb = max(sb, mb) + self.bwd_tail * min(sb, mb)
         return tf + tb + self.const_s
 
     def to_dict(self) -> dict:

@@ -183,7 +183,7 @@ def test_tile_model_features_match_kernel_work_lists(cp):
                 assert feats[b, s, r].tolist() == _work_list_features(plan, b, r), (strat, b, r)
 
 
-@pytest.mark.parametrize("shape", [None, (32, 32), (64, 8)])
+@pytest.mark.parametrize("shape", [None, "tail", (32, 32), (64, 8)])
 def test_measured_policy_selects_by_predicted_latency(shape):
     """policy="measured": per-sequence iff its slowest rank's predicted time is
     <= per-document's (ties -> per-sequence, the reference's rule); the
@@ -193,7 +193,12 @@ def test_measured_policy_selects_by_predicted_latency(shape):
     cp = 4
     mbs = [so.pad_lengths_for_cp(x, cp) for x in
            ([30000, 100, 2000], [512] * 32, [8192], [100] * 40 + [20000])]
-    model = wl.TileModel() if shape is None else wl.TileModel.for_shape(*shape, 128)
+    if shape is None:
+        model = wl.TileModel()
+    elif shape == "tail":           # list-scheduling tail weights on both directions
+        model = wl.TileModel(fwd_tail=0.4, bwd_tail=0.9)
+    else:
+        model = wl.TileModel.for_shape(*shape, 128)
     plan = wl.build_shard_plan(mbs, cp, "measured", model=model)
     lat, feats = plan.rank_latency.cpu(), plan.features.cpu()
     for b, ls in enumerate(mbs):

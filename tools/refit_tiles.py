@@ -25,9 +25,7 @@ def main():
     a = ap.parse_args()
     old = json.load(open(a.inp))
     rows = old["rows"]
-    import torch
-    torch.cuda.get_device_name = lambda *x: old.get("gpu", "NVIDIA B200")   # (fit source label)
-    model = cal.fit_tile_model(rows, a.hq, a.hkv, a.d)
+    model = cal.fit_tile_model(rows, a.hq, a.hkv, a.d, device_name=old.get("gpu", "NVIDIA B200"))
     prev = {(r["tag"], r["cp"], r["mb"]): r for r in old["selection"]}
     rep = cal.selection_report(rows, model, {k: v["profile_choice"] for k, v in prev.items()})
     for r in rep:
