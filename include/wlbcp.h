@@ -236,6 +236,12 @@ int32_t wlb_attn_bwd_pairs(int32_t on);
  * negative = default.  Returns the previous setting.  Process-wide knob. */
 int32_t wlb_attn_bwd_persistent(int32_t on);
 
+/* SMs the persistent backward kernels leave free for concurrent kernels on
+ * other streams (the CP exchange's push / pull): grid = SMs - n (n >= 0;
+ * negative = 0, the default).  Returns the previous value.  No reference
+ * analogue (a B200 scheduling knob). */
+int32_t wlb_attn_bwd_reserve_sms(int32_t n);
+
 /* Split a fused QKV projection y[Tl][Hq+2*Hkv][D] (bf16) into THD q / k / v
  * and apply rotate-half rotary embeddings at the IN-DOCUMENT positions the
  * shard builder emits (positions[Tl], TokenRange coordinates,

@@ -194,6 +194,13 @@ def set_bwd_persistent(on: int) -> int:
     return int(_native.lib().wlb_attn_bwd_persistent(int(on)))
 
 
+def set_bwd_reserve_sms(n: int) -> int:
+    """SMs the persistent backward kernels leave free for the CP exchange's
+    kernels on the communication stream (0 = none, the default; negative
+    restores it).  Returns the previous value."""
+    return int(_native.lib().wlb_attn_bwd_reserve_sms(int(n)))
+
+
 def set_bwd_pairs(on: int) -> int:
     """v3 backward as 2-CTA clusters sharing dQ (1 on, 0 off, negative =
     default).  Returns the previous setting."""

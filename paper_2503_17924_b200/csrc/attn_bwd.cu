@@ -1624,6 +1624,10 @@ static int g_bwd_tred = WLB_BWD_TRED;
 #define WLB_BWD3_PERSIST 1
 #endif
 static int g_bwd3_persistent = WLB_BWD3_PERSIST;
+// SMs the persistent backward kernels leave free (grid = SMs - reserve), so
+// the CP exchange's pull / push kernels on the communication stream find SMs
+// while a head group's backward runs (0: every SM; set by the CP pipeline)
+static int g_bwd_reserve_sms = 0;
 // v2 backward as a persistent kernel (one CTA per SM, dynamic unit queue)
 #ifndef WLB_BWD_PERSIST
 #define WLB_BWD_PERSIST 1
@@ -1791,7 +1795,7 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
         WLB_CUDA_TRY(cudaGetDevice(&dev));
         WLB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         WLB_CUDA_TRY(cudaMemsetAsync(w.sched, 0, sizeof(int), stream));
-        grid = (unsigned)std::min(n_units, sms);
+        grid = (unsigned)std::min(n_units, std::max(1, sms - g_bwd_reserve_sms));
       }
       kern<<<grid, C3::THREADS, C3::SMEM, stream>>>(
           tq, tk, tv, tdo, tdq, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
@@ -1825,7 +1829,8 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
     WLB_CUDA_TRY(cudaGetDevice(&dev));
     WLB_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     WLB_CUDA_TRY(cudaMemsetAsync(w.sched, 0, sizeof(int), stream));
-    attn_bwd_kernel<D, 2><<<(unsigned)std::min(n_units, sms), C::THREADS, C::SMEM, stream>>>(
+    attn_bwd_kernel<D, 2><<<(unsigned)std::min(n_units, std::max(1, sms - g_bwd_reserve_sms)),
+                            C::THREADS, C::SMEM, stream>>>(
         tq, tk, tv, tdo, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
         Hkv, max_items, hpc, n_units, w.sched, 1, g_begin, g_begin + g_count, scale,
         scale * 1.4426950408889634f, dkv_bf16, sync);
@@ -1874,6 +1879,12 @@ extern "C" int32_t wlb_attn_bwd_pairs(int32_t on) {
 extern "C" int32_t wlb_attn_bwd_persistent(int32_t on) {
   const int32_t prev = wlb::g_bwd_persistent;
   wlb::g_bwd_persistent = on < 0 ? WLB_BWD_PERSIST : (on != 0);
+  return prev;
+}
+
+extern "C" int32_t wlb_attn_bwd_reserve_sms(int32_t n) {
+  const int32_t prev = wlb::g_bwd_reserve_sms;
+  wlb::g_bwd_reserve_sms = n < 0 ? 0 : n;
   return prev;
 }
 

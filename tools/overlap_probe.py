@@ -20,7 +20,7 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 import paper_2503_17924_b200 as wl  # noqa: E402
-from paper_2503_17924_b200.attention import (attn_backward, attn_forward, bwd_workspace,  # noqa: E402
+from paper_2503_17924_b200.attention import (attn_backward, attn_forward, bwd_workspace, set_bwd_reserve_sms,  # noqa: E402
                                              head_groups)
 from paper_2503_17924_b200.cp import SymmExchange, cp_doc_attention, shard_for_rank  # noqa: E402
 
@@ -58,6 +58,8 @@ def main():
     ap.add_argument("--hkv", type=int, default=32)
     ap.add_argument("--groups", type=int, nargs="+", default=[1, 2, 4, 8])
     ap.add_argument("--reps", type=int, default=4)
+    ap.add_argument("--reserve", type=int, nargs="+", default=[0],
+                    help="SMs the persistent backward leaves to the exchange (set_bwd_reserve_sms)")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
@@ -103,13 +105,16 @@ def main():
         ex = SymmExchange(dist.group.WORLD, T, a.hkv, d, dev, groups=G)
         exchanges.append(ex)
 
-        def step(ex=ex):
+        def step(ex=ex, r=0):
+            prev = set_bwd_reserve_sms(r)
             qq, kk, vv = (x.detach().requires_grad_(True) for x in (q, k, v))
             o = cp_doc_attention(qq, kk, vv, sh, exchange=ex)
             o.backward(do)
+            set_bwd_reserve_sms(prev)
 
         fns[f"attn_g{G}"] = attn_groups
-        fns[f"step_g{G}"] = step
+        for r in a.reserve:
+            fns[f"step_g{G}" + (f"_r{r}" if r else "")] = (lambda ex=ex, r=r: step(ex, r))
 
     def nccl_step():
         qq, kk, vv = (x.detach().requires_grad_(True) for x in (q, k, v))
@@ -120,6 +125,11 @@ def main():
     ms = timed_interleaved(fns, a.reps)
     res["ms"] = {k: round(v, 3) for k, v in ms.items()}
     for G in a.groups:
+        for r in a.reserve:
+            if r:
+                res[f"exposed_g{G}_r{r}"] = round(1 - ms["attn"] / ms[f"step_g{G}_r{r}"], 4)
+        if f"step_g{G}" not in ms:
+            continue
         res[f"exposed_g{G}"] = round(1 - ms["attn"] / ms[f"step_g{G}"], 4)
         res[f"exposed_vs_split_g{G}"] = round(1 - ms[f"attn_g{G}"] / ms[f"step_g{G}"], 4)
     res["exposed_nccl"] = round(1 - ms["attn"] / ms["nccl"], 4)
