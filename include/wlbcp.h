@@ -242,6 +242,11 @@ int32_t wlb_attn_bwd_persistent(int32_t on);
  * analogue (a B200 scheduling knob). */
 int32_t wlb_attn_bwd_reserve_sms(int32_t n);
 
+/* Persistent 128-query backward: L2 prefetch of the next work unit's K / V
+ * tile and first Q / dO tile while the current unit drains (1 on, 0 off,
+ * negative = build default).  Returns the previous setting. */
+int32_t wlb_attn_bwd_l2_prefetch(int32_t on);
+
 /* Split a fused QKV projection y[Tl][Hq+2*Hkv][D] (bf16) into THD q / k / v
  * and apply rotate-half rotary embeddings at the IN-DOCUMENT positions the
  * shard builder emits (positions[Tl], TokenRange coordinates,

@@ -62,6 +62,7 @@ SIGNATURES = {
     "wlb_attn_bwd_pairs": (_i32, [_i32]),
     "wlb_attn_bwd_persistent": (_i32, [_i32]),
     "wlb_attn_bwd_reserve_sms": (_i32, [_i32]),
+    "wlb_attn_bwd_l2_prefetch": (_i32, [_i32]),
     "wlb_qkv_rope": (C.c_int, [_p, _p, _p, _p, _p, _i32, _i32, _i32, _i32, _f32, _p]),
     "wlb_attn_bwd": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i32, _p, _i32, _i32,
                                _i32, _i32, _i32, _f32, _p, _p]),

@@ -201,6 +201,13 @@ def set_bwd_reserve_sms(n: int) -> int:
     return int(_native.lib().wlb_attn_bwd_reserve_sms(int(n)))
 
 
+def set_bwd_l2_prefetch(on: int) -> int:
+    """Persistent 128-query backward: L2 prefetch of the next unit's K / V and
+    first Q / dO tile (1 on, 0 off, negative = default).  Returns the previous
+    setting."""
+    return int(_native.lib().wlb_attn_bwd_l2_prefetch(int(on)))
+
+
 def set_bwd_pairs(on: int) -> int:
     """v3 backward as 2-CTA clusters sharing dQ (1 on, 0 off, negative =
     default).  Returns the previous setting."""

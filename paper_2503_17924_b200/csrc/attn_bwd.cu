@@ -934,6 +934,17 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     const Unit3 U = geom(u);
     const int4 kt = U.kt;
     const int g = U.g, qt_per_head = U.qt, n_iter = U.n_iter;
+    // (persistent & 2) this unit is taken ~2 query tiles before the previous
+    // one ends: warm L2 with its K / V tile and first Q / dO tile, so the loads
+    // issued after kv_empty hit L2 instead of HBM at the unit boundary
+    if (seq > 0 && (persistent & 2)) {
+      for (int s = 0; s < 2; ++s) {
+        tma_prefetch_3d_w(&tmK, s * 64, g, kt.x);
+        tma_prefetch_3d_w(&tmV, s * 64, g, kt.x);
+        tma_prefetch_3d_w(&tmQ, s * 64, g * group, kt.z);
+        tma_prefetch_3d_w(&tmDO, s * 64, g * group, kt.z);
+      }
+    }
     // K/V of this unit once the previous unit's last MMAs have read the old
     if (seq > 0) mbar_wait(&bars->kv_empty, (seq - 1) & 1);
     mbar_expect_tx_w(&bars->kv_full, 2 * C::KV_BYTES);
@@ -1628,6 +1639,12 @@ static int g_bwd3_persistent = WLB_BWD3_PERSIST;
 // the CP exchange's pull / push kernels on the communication stream find SMs
 // while a head group's backward runs (0: every SM; set by the CP pipeline)
 static int g_bwd_reserve_sms = 0;
+// persistent 128-query backward: L2 prefetch of the next unit's K / V and
+// first Q / dO tile while the current unit drains
+#ifndef WLB_BWD3_L2PF
+#define WLB_BWD3_L2PF 0
+#endif
+static int g_bwd3_l2pf = WLB_BWD3_L2PF;
 // v2 backward as a persistent kernel (one CTA per SM, dynamic unit queue)
 #ifndef WLB_BWD_PERSIST
 #define WLB_BWD_PERSIST 1
@@ -1799,7 +1816,8 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
       }
       kern<<<grid, C3::THREADS, C3::SMEM, stream>>>(
           tq, tk, tv, tdo, tdq, lse, w.delta, w.dq_acc, dk, dv, w.kv_tiles, w.n_kv, positions, Tl, Hq,
-          Hkv, max_items, g_begin, scale, sl2, dkv_bf16, n_units, w.sched, g_bwd3_persistent, sync);
+          Hkv, max_items, g_begin, scale, sl2, dkv_bf16, n_units, w.sched,
+          g_bwd3_persistent ? (1 | (g_bwd3_l2pf ? 2 : 0)) : 0, sync);
     }
     WLB_LAUNCH_CHECK();
   } else
@@ -1879,6 +1897,12 @@ extern "C" int32_t wlb_attn_bwd_pairs(int32_t on) {
 extern "C" int32_t wlb_attn_bwd_persistent(int32_t on) {
   const int32_t prev = wlb::g_bwd_persistent;
   wlb::g_bwd_persistent = on < 0 ? WLB_BWD_PERSIST : (on != 0);
+  return prev;
+}
+
+extern "C" int32_t wlb_attn_bwd_l2_prefetch(int32_t on) {
+  const int32_t prev = wlb::g_bwd3_l2pf;
+  wlb::g_bwd3_l2pf = on < 0 ? WLB_BWD3_L2PF : (on != 0);
   return prev;
 }
 

@@ -153,6 +153,16 @@ __device__ __forceinline__ void tma_load_3d_w(void* dst, const void* tmap, uint6
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// L2 prefetch of a 3-D TMA box (no shared memory, no barrier): warms L2 for a
+// later tma_load_3d_w of the same box
+__device__ __forceinline__ void tma_prefetch_3d_w(const void* tmap, int c0, int c1, int c2) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t" WLB_ELECT
+      "@P cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n\t}" ::"l"(
+          reinterpret_cast<uint64_t>(tmap)),
+      "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
 // TMA tile reduce-add (fp32 by the tensor map's type) of a 3-D box from
 // shared memory into global memory, tracked by the issuing thread's bulk group
 __device__ __forceinline__ void tma_reduce_add_3d(const void* tmap, const void* src, int c0, int c1,
