@@ -247,3 +247,29 @@ def test_bwd_bf16_partials(d):
     _rank_case([1000, 3, 250, 777, 40], 4, "per_document", 4, 2, d, seed=51, with_bwd=True,
                dkv_dtype=torch.bfloat16)
     _rank_case([6144], 1, "per_document", 2, 2, d, seed=52, with_bwd=True, dkv_dtype=torch.bfloat16)
+
+
+@pytest.mark.parametrize("knob", ["l2_prefetch", "reserve_sms"])
+def test_bwd3_scheduling_switches_keep_results(knob):
+    """The persistent 128-query backward's scheduling switches (L2 prefetch of
+    the next unit; fewer CTAs than SMs) change only timing: dK/dV (one CTA per
+    KV tile, fixed order) are bit-identical, dQ (TMA reduce-adds, order-free
+    fp32 sums) within the oracle tolerance of the default run."""
+    from paper_2503_17924_b200.attention import set_bwd_l2_prefetch, set_bwd_reserve_sms
+    lengths = [1000, 3, 2200, 129, 700]
+    T, hq, hkv, d = sum(lengths), 8, 2, 128
+    q, k, v, do = (x.cuda() for x in _inputs(T, T, hq, hkv, d, 5))
+    plan = wl.build_shard_plan([lengths], 1, "per_document")
+    _, pos, ro = plan.rank_local(0, 0)
+    tiles = build_tiles(ro, pos, lengths)
+    o, lse = attn_forward(q, k, v, tiles)
+    base = attn_backward(q, k, v, o, lse, do, tiles)
+    setter, val = ((set_bwd_l2_prefetch, 1) if knob == "l2_prefetch"
+                   else (set_bwd_reserve_sms, 140))
+    prev = setter(val)
+    try:
+        got = attn_backward(q, k, v, o, lse, do, tiles)
+    finally:
+        setter(prev)
+    assert torch.equal(got[1], base[1]) and torch.equal(got[2], base[2])
+    _close(got[0], base[0].float(), "dq")
