@@ -3,8 +3,8 @@
 set -u
 cd "$(dirname "$0")/.."
 N=$(nvidia-smi -L | wc -l)
-out=gpurun_out/finalm8_n$N; mkdir -p $out
-timeout 900 python -m pytest tests/test_cp_multi.py -m gpu -q > $out/cp_tests.txt 2>&1; echo "rc=$?" >> $out/cp_tests.txt
+out=gpurun_out/finalm9_n$N; mkdir -p $out
+timeout 900 python -m pytest tests/test_cp_multi.py tests/test_gpu_attention.py -k "cp or switches" -m gpu -q > $out/cp_tests.txt 2>&1; echo "rc=$?" >> $out/cp_tests.txt
 timeout 700 python bench.py --gpus $N --steps 5 --warmup 3 > $out/bench.json 2> $out/bench.err
 timeout 700 python bench.py --gpus $N --steps 5 --warmup 3 --shape llama70b-gqa > $out/bench_gqa.json 2> $out/bench_gqa.err
 tail -2 $out/cp_tests.txt
