@@ -1009,7 +1009,8 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         const int st = Ig % C::QS;
         const uint32_t qs = q_b + st * C::Q_BYTES;
         mbar_wait(&bars->q_full[st], (Ig / C::QS) & 1);
-        TRACE3(0, i);
+        TRACE3(0, Ig);
+        if (!PAIR && i == 0) TRACE3(4, Ig);   // unit start (trace builds)
         tc_fence_after();
         // S^T = K Q^T (contract over D; K-major both); 8-MMA chains under one
         // elect.sync keep the MMA warp's issue slots off its SMSP's compute warps
@@ -1022,7 +1023,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         const uint32_t qs = q_b + st * C::Q_BYTES;
         mbar_wait_fast(&bars->ds_full[0], Jg & 1);
         mbar_wait_fast(&bars->ds_full[1], Jg & 1);
-        TRACE3(5, j);
+        TRACE3(5, Jg);
         tc_fence_after();
         const uint32_t dsb = ds_b;
         // dQ = dS K (contract over keys; A = dS from the dS^T buffer and B = K,
@@ -1044,7 +1045,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         // dP^T = V dO^T into the columns dQ(i-1) (or the previous unit's last
         // dQ) occupied: wait for the drain
         if (Ig >= 1) mbar_wait_fast(&bars->s_free, (Ig - 1) & 1);
-        TRACE3(1, i);
+        TRACE3(1, Ig);
         tc_fence_after();
         mma_ss8_w(tmem + C::COL_DP, sdesc_sw128(v_b, 16, 1024), sdesc_sw128(dos, 16, 1024), kmaj_off,
                   kmaj_off, C::IDESC_ST, 0);
@@ -1054,7 +1055,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           mbar_wait_fast(&bars->p_full[c], ph);
-          TRACE3(2 + c, i);
+          TRACE3(2 + c, Ig);
           tc_fence_after();
 #pragma unroll
           for (int hf = 0; hf < 2; ++hf)
@@ -1139,7 +1140,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       const bool ok_tile = true;
 #endif
       mbar_wait(&bars->dq_full, Jg & 1);
-      if (warp == 12) TRACE3(12, j);
+      if (warp == 12) TRACE3(12, Jg);
       tc_fence_after();
       uint32_t u[128];
 #pragma unroll
@@ -1148,7 +1149,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&bars->s_free);
-      if (warp == 12) TRACE3(13, j);
+      if (warp == 12) TRACE3(13, Jg);
       const bool last = j + 1 == n_iter;   // (no pacing across units)
       const uint32_t nph = (Jg + 1) & 1;
       if (PAIR && paired) {
@@ -1178,7 +1179,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         //  its release-arrive, and st.async data is visible through the
         //  rx_full transaction counts)
         mbar_wait_fast(&bars->peer_free, (Jg & 1) ^ 1);     // peer consumed tile j-1
-        if (warp == 12) TRACE3(4, j);
+        if (warp == 12) TRACE3(4, Jg);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           if (!last) {
@@ -1195,8 +1196,8 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                         u[64 + 16 * c + 4 * e + 3]);
           // (no suspend hint: a remote completion wakes a suspended waiter late)
           mbar_wait_fast(&bars->rx_full[c], Jg & 1);
-          if (warp == 12 && c == 0) TRACE3(14, j);
-          if (warp == 12 && c == 3) TRACE3(15, j);
+          if (warp == 12 && c == 0) TRACE3(14, Jg);
+          if (warp == 12 && c == 3) TRACE3(15, Jg);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const uint4 r = *reinterpret_cast<const uint4*>(rx + c * 8192 + q * 64 + ((e ^ sw) << 4));
@@ -1308,7 +1309,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       const int8_t* rp = sPos + vb * C::BM + 64 * hf;
       mbar_wait(&bars->vec_full[vb], (Ig / C::QS) & 1);
       mbar_wait(&bars->s_full, ph);
-      if (warp == 4) TRACE3(6, i);
+      if (warp == 4) TRACE3(6, Ig);
       tc_fence_after();
       uint32_t p16[2][16];   // P (fp16 pairs with P16, else bf16), kept for dS
       // ---- P^T = exp2(S^T * scale * log2e - lse2), per 32-query chunk
@@ -1330,13 +1331,13 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&bars->p_full[c]);
-        if (warp == 4) TRACE3(7 + c, i);
+        if (warp == 4) TRACE3(7 + c, Ig);
       }
       // ---- dS^T = P^T (dP^T - Delta), per chunk, into SMEM (for dQ and dK)
       // (the buffer's previous readers, dQ(i-1) and dK(i-1), were issued
       //  before dP(i): dp_full(i) implies they completed)
       mbar_wait(&bars->dp_full, ph);
-      if (warp == 4) TRACE3(9, i);
+      if (warp == 4) TRACE3(9, Ig);
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -1368,7 +1369,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         }
         fence_proxy_async_smem();
         mbar_arrive(&bars->ds_full[c]);
-        if (warp == 4) TRACE3(10 + c, i);
+        if (warp == 4) TRACE3(10 + c, Ig);
       }
       mbar_arrive(&bars->vec_empty[vb]);
     }

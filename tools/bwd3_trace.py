@@ -1,4 +1,7 @@
-"""Development aid: per-tile timeline of the v3 backward kernel's first CTA.
+"""Development aid: per-tile timeline of the v3 backward kernel's first CTA
+(indexed by the CTA's global tile counter, so a persistent CTA's units follow
+each other; --units summarises the S-issue interval across unit boundaries
+against the interval inside units).
 
     WLB_NVCC_EXTRA=-DWLB_TRACE WLB_LIB_OUT=var/libT.so python -m paper_2503_17924_b200.build
     WLB_LIB_PATH=var/libT.so python tools/bwd3_trace.py [--doc 32768]
@@ -20,13 +23,15 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--doc", type=int, default=32768)
 ap.add_argument("--hq", type=int, default=32)
 ap.add_argument("--hkv", type=int, default=32)
+ap.add_argument("--ndocs", type=int, default=1, help="documents of --doc rows each")
+ap.add_argument("--units", action="store_true")
 a = ap.parse_args()
-lengths = [a.doc]
+lengths = [a.doc] * a.ndocs
 plan = wl.build_shard_plan([lengths], 1, "per_document")
 g, pos, ro = plan.rank_local(0, 0)
 tiles = build_tiles(ro, pos, lengths)
 dev = torch.device("cuda")
-T, d = a.doc, 128
+T, d = a.doc * a.ndocs, 128
 q = torch.randn(T, a.hq, d, device=dev, dtype=torch.bfloat16)
 k = torch.randn(T, a.hkv, d, device=dev, dtype=torch.bfloat16)
 v = torch.randn_like(k)
@@ -41,6 +46,21 @@ lib.wlb_debug_bwd3_trace.argtypes = [ctypes.c_void_p]
 assert lib.wlb_debug_bwd3_trace(buf.ctypes.data) == 0
 t2 = buf.astype(np.float64)
 t = t2[0]
+if a.units:
+    s_issue = t[0]
+    n_tr = int((s_issue > 0).sum())
+    starts = sorted(int(x) for x in np.nonzero(t[4][:n_tr])[0])
+    dt = np.diff(s_issue[:n_tr])
+    inside = [dt[i - 1] for i in range(1, n_tr) if i not in starts]
+    across = [dt[i - 1] for i in starts if i > 0]
+    print(f"doc {a.doc} x {a.ndocs}: {len(starts)} unit starts in the first {n_tr} tiles; "
+          f"tiles per unit {n_tr / max(1, len(starts)):.1f}")
+    print(f"S-issue interval inside units: median {np.median(inside):.0f} mean {np.mean(inside):.0f} cycles")
+    print(f"S-issue interval across unit boundaries: median {np.median(across):.0f} "
+          f"mean {np.mean(across):.0f} cycles")
+    extra = (np.sum(across) - len(across) * np.median(inside)) / max(1.0, np.sum(dt))
+    print(f"boundary excess share of the traced time: {extra:.3f}")
+    sys.exit(0)
 names = ["m_qfull", "m_sfree", "m_p0", "m_p1", "d_pfree", "m_ds1", "c_sfull", "c_p0", "c_p1",
          "c_dpfull", "c_ds0", "c_ds1", "d_dqfull", "d_sfree", "d_rx0", "d_rx3"]
 n = len(names)
