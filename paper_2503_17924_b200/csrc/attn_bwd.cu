@@ -928,6 +928,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       mbar_wait(&bars->unit_empty[st], ((seq / kUnitRing) & 1) ^ 1);
       bars->unit_id[st] = u;
       mbar_arrive(&bars->unit_full[st]);
+      if (!PAIR) TRACE3(14, I0);   // unit fetched (trace builds)
     }
     u = __shfl_sync(0xffffffffu, u, 0);
     if (u < 0) break;
@@ -947,6 +948,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     }
     // K/V of this unit once the previous unit's last MMAs have read the old
     if (seq > 0) mbar_wait(&bars->kv_empty, (seq - 1) & 1);
+    if (!PAIR) TRACE3(12, I0);   // K / V buffers free (trace builds)
     mbar_expect_tx_w(&bars->kv_full, 2 * C::KV_BYTES);
     for (int s = 0; s < 2; ++s) {
       tma_load_3d_w(sK + s * C::SLAB, &tmK, &bars->kv_full, s * 64, g, kt.x);
@@ -1003,6 +1005,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     if (u < 0) break;
     const int n_iter = geom(u).n_iter;
     mbar_wait(&bars->kv_full, seq & 1);
+    if (!PAIR) TRACE3(15, I0);   // K / V of this unit landed (trace builds)
     for (int i = 0; i <= n_iter; ++i) {
       const int Ig = I0 + i;
       if (i < n_iter) {
@@ -1140,7 +1143,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       const bool ok_tile = true;
 #endif
       mbar_wait(&bars->dq_full, Jg & 1);
-      if (warp == 12) TRACE3(12, Jg);
+      // (trace event 12 is the producer's kv_empty, above)
       tc_fence_after();
       uint32_t u[128];
 #pragma unroll
@@ -1149,7 +1152,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&bars->s_free);
-      if (warp == 12) TRACE3(13, Jg);
+      // (trace event 13 is the compute warps' dK / dV epilogue end, below)
       const bool last = j + 1 == n_iter;   // (no pacing across units)
       const uint32_t nph = (Jg + 1) & 1;
       if (PAIR && paired) {
@@ -1388,6 +1391,7 @@ attn_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       store_dkv_block(dv, dk, off + c * 32, (size_t)Hkv * D, kt.y - lg * 32, a, bb, scale,
                       dkv_bf16 != 0, stg);
     }
+    if (warp == 4 && !PAIR) TRACE3(13, I0 + n_iter);   // epilogue issued (trace builds)
     if (!PAIR && sync.signal_bases) {
       // CP: this (KV tile, head) unit's partials are stored; count it toward
       // its head group and publish the group when complete

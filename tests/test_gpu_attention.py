@@ -264,8 +264,8 @@ def test_bwd3_scheduling_switches_keep_results(knob):
     tiles = build_tiles(ro, pos, lengths)
     o, lse = attn_forward(q, k, v, tiles)
     base = attn_backward(q, k, v, o, lse, do, tiles)
-    setter, val = ((set_bwd_l2_prefetch, 1) if knob == "l2_prefetch"
-                   else (set_bwd_reserve_sms, 140))
+    setter, val = {"l2_prefetch": (set_bwd_l2_prefetch, 1),
+                   "reserve_sms": (set_bwd_reserve_sms, 140)}[knob]
     prev = setter(val)
     try:
         got = attn_backward(q, k, v, o, lse, do, tiles)

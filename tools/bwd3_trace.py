@@ -49,7 +49,10 @@ t = t2[0]
 if a.units:
     s_issue = t[0]
     n_tr = int((s_issue > 0).sum())
-    starts = sorted(int(x) for x in np.nonzero(t[4][:n_tr])[0])
+    # unit-start markers left by earlier launches (dynamic scheduling differs)
+    # are dropped: a real start's fetch (14) lies within this launch's trace
+    starts = sorted(int(x) for x in np.nonzero(t[4][:n_tr])[0]
+                    if x == 0 or t[14][x] >= s_issue[0])
     dt = np.diff(s_issue[:n_tr])
     inside = [dt[i - 1] for i in range(1, n_tr) if i not in starts]
     across = [dt[i - 1] for i in starts if i > 0]
@@ -60,6 +63,14 @@ if a.units:
           f"mean {np.mean(across):.0f} cycles")
     extra = (np.sum(across) - len(across) * np.median(inside)) / max(1.0, np.sum(dt))
     print(f"boundary excess share of the traced time: {extra:.3f}")
+    # per boundary (unit starting at tile I): cycles from the previous tile's S
+    # issue to the unit fetch (14), to its K / V landing (15) and to its S (0);
+    # the previous tile's dS done (c_ds1, 11) and dQ drained (d_sfree, 13)
+    print("boundary   fetch  kv_free   kv_land   S_issue  prev_ds1  epi_end  P0_done  (cycles after the previous S)")
+    for I in starts[1:]:
+        b = s_issue[I - 1]
+        print(f"{I:8d} {t[14][I] - b:8.0f} {t[12][I] - b:8.0f} {t[15][I] - b:9.0f} {s_issue[I] - b:9.0f} "
+              f"{t[11][I - 1] - b:9.0f} {t[13][I] - b:8.0f} {t[7][I] - b:8.0f}")
     sys.exit(0)
 names = ["m_qfull", "m_sfree", "m_p0", "m_p1", "d_pfree", "m_ds1", "c_sfull", "c_p0", "c_p1",
          "c_dpfull", "c_ds0", "c_ds1", "d_dqfull", "d_sfree", "d_rx0", "d_rx3"]

@@ -1,7 +1,8 @@
 """A/B of persistent 128-query backward switches, interleaved on the same
 inputs: uniform documents of several lengths and the bench's 8 synthetic 32K
 sequences (CP=1).  --knob l2pf: L2 prefetch of the next unit
-(`set_bwd_l2_prefetch` 0 vs 1).  (--knob red timed a hybrid dQ drain, RED.v4
+(`set_bwd_l2_prefetch` 0 vs 1).  (Knobs "defer" and "qfirst" timed two
+removed unit-boundary variants: profiles/r02_bwd3_unit_boundary_trace.txt.)  (--knob red timed a hybrid dQ drain, RED.v4
 for --value of the 4 rounds, since removed: profiles/r02_ab_bwd3_hybrid_drain.txt.)
 
     python tools/l2pf_ab.py [--knob l2pf|red] [--value 2] [--hq 32 --hkv 32] [--reps 5]
