@@ -8,6 +8,8 @@ off).  Covers what the toy-shape tests cannot reach:
   the 17-document synthetic 32K sequence, all 32 heads;
 * config 4: Llama-70B GQA 64 q / 8 kv (8:1), both backward kernels (v2, v3),
   at 32K CP=1 and one rank of a 128K sequence at CP=4;
+* config 4 at CP=8: the first and last ranks of a 22-document 128K sequence
+  under both strategies;
 * config 3: one CP=8 rank of 128K sequences with pre-gathered K/V under
   per-document and per-sequence sharding, including a single 128K document
   (1024 KV tiles of forward rescaling).
@@ -133,3 +135,12 @@ def test_config3_single_128k_document_cp8():
     """1024 KV tiles of forward lazy rescaling and of backward dQ accumulation
     for the rank holding chunks 0 and 15 of one 128K document."""
     _run([131072], 8, "per_document", 32, 32, [0], "v3", seed=7)
+
+
+@pytest.mark.parametrize("policy", ["per_document", "per_sequence"])
+def test_config4_gqa_128k_cp8_rank(policy):
+    """Config 4 at CP=8 (BASELINE.json names CP=4 and CP=8): 64 q / 8 kv heads,
+    the first and last ranks of a 22-document 128K sequence under both
+    strategies."""
+    lengths = _synthetic(131072, 0)
+    _run(lengths, 8, policy, 64, 8, [0, 7], "default", seed=8)
