@@ -2,7 +2,7 @@
 # Last-commit check on one B200: whole GPU suite, smoke, N=1 bench.
 set -u
 cd "$(dirname "$0")/.."
-out=gpurun_out/final10; mkdir -p $out
+out=gpurun_out/final11; mkdir -p $out
 timeout 1500 python -m pytest tests -m gpu -q > $out/gpu_tests.txt 2>&1; echo "all rc=$?" >> $out/gpu_tests.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke.txt 2>&1; echo "smoke rc=$?" >> $out/smoke.txt
 timeout 600 python bench.py --steps 20 --warmup 5 > $out/bench_n1.json 2> $out/bench_n1.err
